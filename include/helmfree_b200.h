@@ -1,0 +1,156 @@
+/*
+ * helmfree_b200.h -- C ABI of the B200-native CSLP / multigrid / Krylov path.
+ *
+ * Drop-in boundary for the reference package `helmfree`
+ * (/root/reference/pkg/src/helmfree).  Every entry point names the reference
+ * interface it replaces (file:line).  Plain C: opaque handles, plain pointers
+ * and sizes, no torch types.  Build: paper_2308_06085_b200/_lib/libhelmfree_b200.so
+ *
+ * Conventions
+ *  - Fields are complex128, stored as interleaved (re, im) doubles, shape
+ *    (nx, n2, n3) in C order (i3 fastest) -- the reference's numpy layout.
+ *    `double *` field arguments point at the first owned value.
+ *  - Blocks are slabs along i1: a worker owns global planes [lo1, lo1 + nx).
+ *    When a slab face is interior (not a physical boundary) the caller
+ *    guarantees HF_GHOST planes of valid neighbour data directly before /
+ *    after the owned planes (the halo exchange fills them).
+ *  - Device pointers unless a name ends in _host.
+ *  - Return codes: 0 on success, negative on error (hf_last_error() explains).
+ *    Errors never fall back to another implementation.
+ */
+#ifndef HELMFREE_B200_H
+#define HELMFREE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HF_GHOST 2
+
+#define HF_BC_DIRICHLET 0
+#define HF_BC_SOMMERFELD 1
+
+#define HF_CYCLE_V 0
+#define HF_CYCLE_F 1
+
+#define HF_METHOD_GMRES 0
+#define HF_METHOD_BICGSTAB 1
+#define HF_METHOD_IDRS 2
+
+#define HF_COARSEST_DIRECT 0   /* dense LU-inverse, applied as one GEMV   */
+#define HF_COARSEST_GMRES 1    /* unpreconditioned full GMRES to tol      */
+
+#define HF_BREAKDOWN_NONE 0
+#define HF_BREAKDOWN_ARNOLDI 1
+#define HF_BREAKDOWN_RHO 2
+#define HF_BREAKDOWN_OMEGA 3
+#define HF_BREAKDOWN_PROJECTION 4
+
+#define HF_ERR_ARG -1
+#define HF_ERR_CUDA -2
+#define HF_ERR_ZERO_DIAGONAL -3
+#define HF_ERR_UNSUPPORTED -4
+#define HF_ERR_SOLVER -5
+
+typedef struct hf_operator hf_operator;
+typedef struct hf_hierarchy hf_hierarchy;
+typedef struct hf_solver hf_solver;
+
+/* multigrid.py:42-51 MGConfig */
+typedef struct hf_mg_config {
+    int nu1, nu2;
+    double omega;
+    int cycle;               /* HF_CYCLE_V | HF_CYCLE_F */
+    int coarsest_threshold;  /* coarsen while all dims > (or >=) this */
+    int threshold_ge;        /* 0: "gt" (default), 1: "ge" */
+    double coarsest_tol;
+    int coarsest_maxit;
+    int coarsest_method;     /* HF_COARSEST_DIRECT | HF_COARSEST_GMRES */
+} hf_mg_config;
+
+/* krylov.py:34-43 SolverConfig */
+typedef struct hf_solver_config {
+    int method;              /* HF_METHOD_* */
+    double tol;
+    int maxit;
+    int s;                   /* IDR shadow dimension */
+    int restart;             /* GMRES restart length, 0 = full */
+    double breakdown_tol;
+    const double *shadow_host;  /* IDR: s orthonormal vectors (s * N complex), host */
+    int check_every;         /* Bi-CGSTAB: iterations per host convergence poll */
+} hf_solver_config;
+
+/* krylov.py:46-64 ConvergenceReport (phase_times reduced to device times) */
+typedef struct hf_report {
+    int matvec_count;
+    int iterations;
+    int converged;
+    int breakdown;           /* HF_BREAKDOWN_* */
+    double final_relres;
+    double *history_host;    /* caller buffer, >= maxit + 1 entries, may be NULL */
+    int history_cap;
+    int coarsest_flags;      /* coarsest solves that missed coarsest_tol */
+    double solve_ms;         /* device time of the Krylov loop (CUDA events) */
+    int kernel_launches;     /* kernels this library enqueued for the solve */
+} hf_report;
+
+/* ---- library ----------------------------------------------------------- */
+const char *hf_last_error(void);
+int hf_version(void);
+/* Stream used by all subsequent calls of this thread (cudaStream_t, NULL = default). */
+void hf_set_stream(void *stream);
+int hf_device_synchronize(void);
+
+/* ---- operators.py:122-254 StencilOperator / apply_operator -------------- */
+/* k_host: full global wavenumber field (n1*n2*n3, C order) or NULL for the
+ * constant k_const.  shift = beta1 - i*beta2 (Helmholtz: 1 + 0i). */
+hf_operator *hf_operator_create(int n1, int n2, int n3, int lo1, int nx, double h,
+                                double shift_re, double shift_im, int bc,
+                                const double *k_host, double k_const);
+void hf_operator_destroy(hf_operator *op);
+/* v = A u on the owned slab (operators.py:200-223). */
+int hf_operator_apply(hf_operator *op, const double *u, double *v);
+/* Jacobi diagonal (operators.py:163-183), nx*n2*n3 complex. */
+int hf_operator_diag(hf_operator *op, double *d);
+/* multigrid.py:138-157 jacobi_smooth; scratch: one field (with ghost planes
+ * when the slab has interior faces). */
+int hf_jacobi_smooth(hf_operator *op, double *u, const double *b, double omega, int sweeps,
+                     int assume_zero, double *scratch);
+
+/* ---- multigrid.py:101-128 build_hierarchy ------------------------------ */
+hf_hierarchy *hf_hierarchy_create(int n1, int n2, int n3, int lo1, int nx, double h,
+                                  double beta1, double beta2, int bc, const double *k_host,
+                                  double k_const, const hf_mg_config *cfg);
+void hf_hierarchy_destroy(hf_hierarchy *hier);
+int hf_hierarchy_num_levels(const hf_hierarchy *hier);
+/* dims5 = {n1, n2, n3, lo1, nx} of level l */
+int hf_hierarchy_level_shape(const hf_hierarchy *hier, int level, int *dims5);
+/* multigrid.py:171-202 restrict_fw: fine level `level` -> level+1 */
+int hf_restrict_fw(hf_hierarchy *hier, int level, const double *r_fine, double *b_coarse);
+/* multigrid.py:238-297 prolong_tl: coarse level `level`+1 -> fine `level` */
+int hf_prolong_tl(hf_hierarchy *hier, int level, const double *e_coarse, double *out_fine);
+/* multigrid.py:300-323 coarsest_solve */
+int hf_coarsest_solve(hf_hierarchy *hier, const double *b, double *x);
+/* multigrid.py:395-419 mg_precondition: z ~= M^-1 r, one V/F cycle */
+int hf_mg_precondition(hf_hierarchy *hier, const double *r, double *z);
+
+/* ---- krylov.py:111-407 + runner.py:95-131 ------------------------------ */
+/* A: Helmholtz operator (shift 1) on the same slab as the hierarchy's finest level. */
+hf_solver *hf_solver_create(hf_operator *A, hf_hierarchy *M);
+void hf_solver_destroy(hf_solver *s);
+/* Device-resident solve: x = A^-1 b preconditioned by one MG cycle. */
+int hf_solve(hf_solver *s, const hf_solver_config *cfg, const double *b, double *x,
+             hf_report *rep);
+/* Same, from HOST buffers (pinned or pageable): H2D of b, solve, D2H of x. */
+int hf_solve_host(hf_solver *s, const hf_solver_config *cfg, const double *b_host,
+                  double *x_host, hf_report *rep);
+
+/* ---- krylov.py:67-78 dot (owned region, conjugated) --------------------- */
+int hf_dot(int64_t n, const double *u, const double *v, double *out_host2);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

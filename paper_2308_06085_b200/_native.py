@@ -1,0 +1,134 @@
+"""ctypes bindings of the C ABI declared in include/helmfree_b200.h.
+
+The product path has no fallback: if libhelmfree_b200.so is missing or
+cannot be loaded, importing a compute entry point raises NativeUnavailable.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libhelmfree_b200.so")
+
+HF_GHOST = 2
+BC = {"dirichlet": 0, "sommerfeld": 1}
+CYCLE = {"V": 0, "F": 1}
+METHOD = {"gmres": 0, "bicgstab": 1, "idrs": 2}
+COARSEST = {"direct": 0, "gmres": 1}
+BREAKDOWN = {0: None, 1: "arnoldi", 2: "rho", 3: "omega", 4: "projection"}
+ERR_ZERO_DIAGONAL = -3
+ERR_UNSUPPORTED = -4
+
+# every symbol include/helmfree_b200.h declares
+EXPORTED = (
+    "hf_last_error", "hf_version", "hf_set_stream", "hf_device_synchronize",
+    "hf_operator_create", "hf_operator_destroy", "hf_operator_apply", "hf_operator_diag",
+    "hf_jacobi_smooth", "hf_hierarchy_create", "hf_hierarchy_destroy",
+    "hf_hierarchy_num_levels", "hf_hierarchy_level_shape", "hf_restrict_fw", "hf_prolong_tl",
+    "hf_coarsest_solve", "hf_mg_precondition", "hf_solver_create", "hf_solver_destroy",
+    "hf_solve", "hf_solve_host", "hf_dot",
+)
+
+
+class NativeUnavailable(ImportError):
+    pass
+
+
+class NativeError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[hf {code}] {msg}")
+        self.code = code
+
+
+class MGConfigC(ctypes.Structure):
+    _fields_ = [("nu1", ctypes.c_int), ("nu2", ctypes.c_int), ("omega", ctypes.c_double),
+                ("cycle", ctypes.c_int), ("coarsest_threshold", ctypes.c_int),
+                ("threshold_ge", ctypes.c_int), ("coarsest_tol", ctypes.c_double),
+                ("coarsest_maxit", ctypes.c_int), ("coarsest_method", ctypes.c_int)]
+
+
+class SolverConfigC(ctypes.Structure):
+    _fields_ = [("method", ctypes.c_int), ("tol", ctypes.c_double), ("maxit", ctypes.c_int),
+                ("s", ctypes.c_int), ("restart", ctypes.c_int),
+                ("breakdown_tol", ctypes.c_double), ("shadow_host", ctypes.c_void_p),
+                ("check_every", ctypes.c_int)]
+
+
+class ReportC(ctypes.Structure):
+    _fields_ = [("matvec_count", ctypes.c_int), ("iterations", ctypes.c_int),
+                ("converged", ctypes.c_int), ("breakdown", ctypes.c_int),
+                ("final_relres", ctypes.c_double), ("history_host", ctypes.c_void_p),
+                ("history_cap", ctypes.c_int), ("coarsest_flags", ctypes.c_int),
+                ("solve_ms", ctypes.c_double), ("kernel_launches", ctypes.c_int)]
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load the native library (once).  Raises NativeUnavailable if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise NativeUnavailable(
+            f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+            " (there is no CPU fallback)")
+    try:
+        L = ctypes.CDLL(path)
+    except OSError as exc:
+        raise NativeUnavailable(f"cannot load {path}: {exc}") from exc
+    vp, dp, ip, i, d = ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.c_double
+    sig = {
+        "hf_last_error": ([], ctypes.c_char_p),
+        "hf_version": ([], i),
+        "hf_set_stream": ([vp], None),
+        "hf_device_synchronize": ([], i),
+        "hf_operator_create": ([i, i, i, i, i, d, d, d, i, vp, d], vp),
+        "hf_operator_destroy": ([vp], None),
+        "hf_operator_apply": ([vp, vp, vp], i),
+        "hf_operator_diag": ([vp, vp], i),
+        "hf_jacobi_smooth": ([vp, vp, vp, d, i, i, vp], i),
+        "hf_hierarchy_create": ([i, i, i, i, i, d, d, d, i, vp, d, ctypes.POINTER(MGConfigC)], vp),
+        "hf_hierarchy_destroy": ([vp], None),
+        "hf_hierarchy_num_levels": ([vp], i),
+        "hf_hierarchy_level_shape": ([vp, i, ip], i),
+        "hf_restrict_fw": ([vp, i, vp, vp], i),
+        "hf_prolong_tl": ([vp, i, vp, vp], i),
+        "hf_coarsest_solve": ([vp, vp, vp], i),
+        "hf_mg_precondition": ([vp, vp, vp], i),
+        "hf_solver_create": ([vp, vp], vp),
+        "hf_solver_destroy": ([vp], None),
+        "hf_solve": ([vp, ctypes.POINTER(SolverConfigC), vp, vp, ctypes.POINTER(ReportC)], i),
+        "hf_solve_host": ([vp, ctypes.POINTER(SolverConfigC), vp, vp, ctypes.POINTER(ReportC)], i),
+        "hf_dot": ([ctypes.c_int64, vp, vp, dp], i),
+    }
+    for name in EXPORTED:
+        fn = getattr(L, name)
+        fn.argtypes, fn.restype = sig[name]
+    _lib = L
+    return L
+
+
+def last_error() -> str:
+    return load().hf_last_error().decode(errors="replace")
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        raise NativeError(rc, last_error())
+
+
+def check_handle(h):
+    if not h:
+        msg = last_error()
+        code = ERR_ZERO_DIAGONAL if "diagonal vanishes" in msg else -1
+        raise NativeError(code, msg)
+    return h
+
+
+def set_stream_from_torch() -> None:
+    import torch
+    load().hf_set_stream(ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))

@@ -1,0 +1,230 @@
+// hf_device.cuh -- device-side building blocks of the B200 CSLP path.
+//
+// Layout: complex128 fields as double2, shape (nx, n2, n3) C order (i3
+// fastest), slab along i1 with HF_GHOST ghost planes before/after the owned
+// planes.  Kernels march along i1 (the slow axis): one thread per (i2, i3)
+// column, so the i1 +-1 neighbours are re-read by the same thread one step
+// later (L1 hits) and the i2/i3 neighbours come from the rows the
+// neighbouring lanes just loaded.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/helmfree_b200.h"
+
+namespace hf {
+
+typedef double2 cd;
+
+__device__ __forceinline__ cd mk(double x, double y) { return make_double2(x, y); }
+__device__ __forceinline__ cd cadd(cd a, cd b) { return mk(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ cd csub(cd a, cd b) { return mk(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ cd cscal(cd a, double s) { return mk(a.x * s, a.y * s); }
+__device__ __forceinline__ cd cmul(cd a, cd b) {
+    return mk(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// conj(a) * b
+__device__ __forceinline__ cd cjmul(cd a, cd b) {
+    return mk(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+}
+__device__ __forceinline__ cd cdiv(cd a, cd b) {
+    double inv = 1.0 / (b.x * b.x + b.y * b.y);
+    return mk((a.x * b.x + a.y * b.y) * inv, (a.y * b.x - a.x * b.y) * inv);
+}
+__device__ __forceinline__ double cabs2(cd a) { return a.x * a.x + a.y * a.y; }
+__device__ __forceinline__ double cabsd(cd a) { return hypot(a.x, a.y); }
+
+// One grid level on one slab (operators.py:122-183 StencilOperator state).
+struct Lvl {
+    int n1, n2, n3;      // global vertex counts
+    int lo1, nx;         // owned global planes [lo1, lo1 + nx)
+    long long plane;     // n2 * n3
+    double h, h2, ih2, twoh;  // h, h^2, 1/h^2, 2/h
+    double sre, sim;     // shift = beta1 - i beta2
+    int bc;              // HF_BC_*
+    const double *k;     // wavenumber at owned plane 0 (ghost planes valid), or null
+    double kc;           // constant wavenumber when k == null
+};
+
+__device__ __forceinline__ double kat(const Lvl &L, long long q) {
+    return L.k ? __ldg(L.k + q) : L.kc;
+}
+
+// Number of physical faces the vertex touches (edges/corners count each face).
+__device__ __forceinline__ int nbnd(const Lvl &L, int gi, int j, int m) {
+    return (gi == 0) + (gi == L.n1 - 1) + (j == 0) + (j == L.n2 - 1) + (m == 0) + (m == L.n3 - 1);
+}
+
+// Stencil centre ap (operators.py:163-172): (6 - s k^2 h^2)/h^2, minus 2ik/h per
+// physical face for Sommerfeld.
+__device__ __forceinline__ cd ap_of(const Lvl &L, double kk, int nb) {
+    double k2h2 = kk * kk * L.h2;
+    cd a = mk((6.0 - L.sre * k2h2) * L.ih2, (-L.sim * k2h2) * L.ih2);
+    if (L.bc == HF_BC_SOMMERFELD) a.y -= (double)nb * (kk * L.twoh);
+    return a;
+}
+
+// Jacobi diagonal (operators.py:173-178): Dirichlet boundary rows are identities.
+__device__ __forceinline__ cd diag_of(const Lvl &L, double kk, int nb) {
+    if (L.bc == HF_BC_DIRICHLET && nb) return mk(1.0, 0.0);
+    return ap_of(L, kk, nb);
+}
+
+// Generic 7-point row (operators.py:200-254) with values supplied by `val(i,j,m)`
+// at local plane i (may be a ghost plane), row j, column m.  Sommerfeld ghost
+// elimination == mirror the inward neighbour into the missing one.
+template <class V>
+__device__ __forceinline__ cd stencil_row(const Lvl &L, int i, int j, int m, cd uc, double kk,
+                                          const V &val) {
+    const int gi = L.lo1 + i;
+    const bool bxl = gi == 0, bxh = gi == L.n1 - 1;
+    const bool byl = j == 0, byh = j == L.n2 - 1;
+    const bool bzl = m == 0, bzh = m == L.n3 - 1;
+    const int nb = (int)bxl + bxh + byl + byh + bzl + bzh;
+    if (L.bc == HF_BC_DIRICHLET && nb) return uc;
+    cd xm = bxl ? mk(0, 0) : val(i - 1, j, m);
+    cd xp = bxh ? mk(0, 0) : val(i + 1, j, m);
+    cd ym = byl ? mk(0, 0) : val(i, j - 1, m);
+    cd yp = byh ? mk(0, 0) : val(i, j + 1, m);
+    cd zm = bzl ? mk(0, 0) : val(i, j, m - 1);
+    cd zp = bzh ? mk(0, 0) : val(i, j, m + 1);
+    if (bxl) xm = xp;
+    if (bxh) xp = xm;
+    if (byl) ym = yp;
+    if (byh) yp = ym;
+    if (bzl) zm = zp;
+    if (bzh) zp = zm;
+    cd s = cadd(cadd(cadd(xm, xp), cadd(ym, yp)), cadd(zm, zp));
+    cd a = ap_of(L, kk, nb);
+    cd v = cmul(a, uc);
+    v.x -= L.ih2 * s.x;
+    v.y -= L.ih2 * s.y;
+    return v;
+}
+
+struct LoadField {
+    const cd *u;
+    long long plane;
+    int n3;
+    __device__ __forceinline__ cd operator()(int i, int j, int m) const {
+        return __ldg(u + (long long)i * plane + (long long)j * n3 + m);
+    }
+};
+
+// ---------------------------------------------------------------------------
+// deterministic reductions: per-block partials + last-block finalize
+// ---------------------------------------------------------------------------
+#define HF_RED_THREADS 256
+#define HF_MAX_DOTS 2
+
+struct BcgState;   // fwd
+
+// finalize op codes
+enum {
+    FIN_STORE = 0,       // write the sums to out[]
+    FIN_BCG_INIT = 1,    // sums: |b|^2
+    FIN_BCG_ALPHA = 2,   // sums: rs^H v
+    FIN_BCG_S = 3,       // sums: |s|^2
+    FIN_BCG_OMEGA = 4,   // sums: t^H t, t^H s
+    FIN_BCG_RHO = 5,     // sums: |r|^2, rs^H r
+};
+
+struct RedSlot {
+    cd *partials;        // >= nblocks * HF_MAX_DOTS
+    unsigned *counter;   // zero-initialised, reset by the last block
+    cd *out;             // FIN_STORE destination (HF_MAX_DOTS)
+    int op;
+    BcgState *st;
+};
+
+// Bi-CGSTAB scalars, device resident (krylov.py:207-276).
+struct BcgState {
+    cd rho, rho_new, alpha, omega, beta;
+    double bnorm, tol, btol, relres;
+    int iter, maxit, done, converged, breakdown, s_conv, matvecs, pad;
+    double *hist;
+    int hist_cap, pad2;
+};
+
+__device__ __forceinline__ cd warp_sum(cd v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        v.x += __shfl_down_sync(0xffffffffu, v.x, o);
+        v.y += __shfl_down_sync(0xffffffffu, v.y, o);
+    }
+    return v;
+}
+
+// Block-wide deterministic sum of ND complex accumulators; result valid in
+// thread 0.  Requires blockDim.x*blockDim.y*blockDim.z == HF_RED_THREADS.
+template <int ND>
+__device__ __forceinline__ void block_sum(cd (&acc)[ND], cd (&out)[ND]) {
+    __shared__ cd sm[ND][HF_RED_THREADS / 32];
+    const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+    const int lane = tid & 31, w = tid >> 5;
+#pragma unroll
+    for (int d = 0; d < ND; d++) {
+        cd v = warp_sum(acc[d]);
+        if (lane == 0) sm[d][w] = v;
+    }
+    __syncthreads();
+    if (tid == 0) {
+#pragma unroll
+        for (int d = 0; d < ND; d++) {
+            cd s = mk(0, 0);
+            for (int k = 0; k < HF_RED_THREADS / 32; k++) s = cadd(s, sm[d][k]);
+            out[d] = s;
+        }
+    }
+    __syncthreads();
+}
+
+__device__ void bcg_finalize(BcgState *st, int op, const cd *sums);
+
+// Write this block's partials; the last block to arrive reduces all partials in
+// fixed block order and runs the finalize step.
+template <int ND>
+__device__ __forceinline__ void reduce_finish(cd (&acc)[ND], const RedSlot &rs) {
+    cd bs[ND];
+    block_sum<ND>(acc, bs);
+    const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+    const unsigned nblk = gridDim.x * gridDim.y * gridDim.z;
+    const unsigned bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    __shared__ bool last;
+    if (tid == 0) {
+#pragma unroll
+        for (int d = 0; d < ND; d++) rs.partials[(size_t)bid * ND + d] = bs[d];
+        __threadfence();
+        unsigned prev = atomicAdd(rs.counter, 1u);
+        last = (prev == nblk - 1);
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    cd a2[ND];
+#pragma unroll
+    for (int d = 0; d < ND; d++) a2[d] = mk(0, 0);
+    for (unsigned b = tid; b < nblk; b += HF_RED_THREADS) {
+#pragma unroll
+        for (int d = 0; d < ND; d++) {
+            cd p = __ldcg(rs.partials + (size_t)b * ND + d);
+            a2[d] = cadd(a2[d], p);
+        }
+    }
+    cd tot[ND];
+    block_sum<ND>(a2, tot);
+    if (tid == 0) {
+        *rs.counter = 0u;
+        cd sums[HF_MAX_DOTS];
+#pragma unroll
+        for (int d = 0; d < HF_MAX_DOTS; d++) sums[d] = d < ND ? tot[d < ND ? d : 0] : mk(0, 0);
+        if (rs.op == FIN_STORE) {
+#pragma unroll
+            for (int d = 0; d < ND; d++) rs.out[d] = tot[d];
+        } else {
+            bcg_finalize(rs.st, rs.op, sums);
+        }
+    }
+}
+
+}  // namespace hf

@@ -1,0 +1,46 @@
+// hf_kernels.cuh -- host-side launchers of the kernels in hf_kernels.cu.
+#pragma once
+#include "hf_device.cuh"
+
+namespace hf {
+
+int march_blocks(const Lvl &L);
+void launch_apply(const Lvl &L, const cd *u, cd *v, cudaStream_t s, const int *done);
+void launch_apply_dot1(const Lvl &L, const cd *u, cd *v, const cd *w, const RedSlot &rs,
+                       cudaStream_t s, const int *done);
+void launch_apply_dot2(const Lvl &L, const cd *u, cd *v, const cd *w, const RedSlot &rs,
+                       cudaStream_t s, const int *done);
+void launch_residual(const Lvl &L, const cd *u, const cd *b, cd *r, cudaStream_t s,
+                     const int *done);
+void launch_jacobi(const Lvl &L, const cd *u, const cd *b, cd *uo, double omega,
+                   cudaStream_t s, const int *done);
+void launch_jacobi0(const Lvl &L, const cd *b, cd *u, double omega, cudaStream_t s,
+                    const int *done);
+void launch_down1(const Lvl &L, const cd *b, cd *r, double omega, cudaStream_t s,
+                  const int *done);
+void launch_restrict(const Lvl &F, const Lvl &C, const cd *r, cd *out, cudaStream_t s,
+                     const int *done);
+void launch_prolong(const Lvl &F, const Lvl &C, const cd *e, cd *out, bool add, cudaStream_t s,
+                    const int *done);
+void launch_up1(const Lvl &L, const Lvl &C, const cd *b, const cd *e, cd *u, double omega,
+                bool pre, cudaStream_t s, const int *done);
+void launch_gemv(int N, const cd *Minv, const cd *b, cd *x, cudaStream_t s, const int *done);
+void launch_assemble(const Lvl &L, cd *A, cudaStream_t s);
+void launch_set_identity(long long N, cd *B, cudaStream_t s);
+void launch_zero(long long n, cd *y, cudaStream_t s);
+void launch_axpby(long long n, cd a, const cd *x, cd b, cd *y, cudaStream_t s);
+void launch_dot(long long n, const cd *a, const cd *b, const RedSlot &rs, cudaStream_t s);
+void launch_bcg_init(long long n, const cd *b, cd *r, cd *rs, cd *x, cd *p, cd *v,
+                     const RedSlot &red, cudaStream_t s);
+void launch_bcg_p(long long n, const BcgState *st, const cd *r, cd *p, const cd *v,
+                  cudaStream_t s, const int *done);
+void launch_bcg_s(long long n, const BcgState *st, const cd *r, const cd *v, cd *sv,
+                  const RedSlot &red, cudaStream_t s, const int *done);
+void launch_bcg_xr(long long n, const BcgState *st, cd *x, const cd *ph, const cd *sh,
+                   const cd *sv, const cd *t, cd *r, const cd *rs, const RedSlot &red,
+                   cudaStream_t s, const int *done);
+void launch_bcg_xhalf(long long n, const BcgState *st, cd *x, const cd *ph, cudaStream_t s);
+
+#define VEC_BLOCKS_HOST 592
+
+}  // namespace hf

@@ -1,0 +1,686 @@
+// hf_runtime.cu -- native runtime behind the C ABI in include/helmfree_b200.h.
+//
+// Owns device memory for levels, the multigrid hierarchy and Krylov workspace;
+// orchestrates kernel sequences on one CUDA stream.  The Bi-CGSTAB loop keeps
+// all scalars on the device and replays one captured CUDA graph per
+// iteration; the host only polls a pinned status word every few iterations.
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "hf_kernels.cuh"
+
+using namespace hf;
+
+// ---------------------------------------------------------------------------
+// errors / stream
+// ---------------------------------------------------------------------------
+static thread_local std::string g_err;
+static thread_local cudaStream_t g_user_stream = nullptr;
+
+static int fail(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+#define CK(call)                                                                           \
+    do {                                                                                   \
+        cudaError_t e__ = (call);                                                          \
+        if (e__ != cudaSuccess)                                                            \
+            return fail(HF_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e__)); \
+    } while (0)
+#define CKL()                                                                              \
+    do {                                                                                   \
+        cudaError_t e__ = cudaGetLastError();                                              \
+        if (e__ != cudaSuccess)                                                            \
+            return fail(HF_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e__)); \
+    } while (0)
+
+extern "C" const char *hf_last_error(void) { return g_err.c_str(); }
+extern "C" int hf_version(void) { return 1; }
+extern "C" void hf_set_stream(void *stream) { g_user_stream = (cudaStream_t)stream; }
+extern "C" int hf_device_synchronize(void) {
+    CK(cudaDeviceSynchronize());
+    return 0;
+}
+
+static thread_local long long g_launches = 0;
+#define L1(expr) do { expr; g_launches++; } while (0)
+
+// ---------------------------------------------------------------------------
+// device allocations
+// ---------------------------------------------------------------------------
+struct Allocs {
+    std::vector<void *> ptrs;
+    ~Allocs() {
+        for (void *p : ptrs) cudaFree(p);
+    }
+    template <class T>
+    T *get(size_t count, cudaError_t &err) {
+        void *p = nullptr;
+        err = cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T));
+        if (err != cudaSuccess) return nullptr;
+        cudaMemset(p, 0, std::max<size_t>(count, 1) * sizeof(T));
+        ptrs.push_back(p);
+        return (T *)p;
+    }
+};
+
+// complex field with HF_GHOST ghost planes on each side of the slab
+static cd *new_field(Allocs &A, int nx, long long plane, cudaError_t &err) {
+    cd *base = A.get<cd>((size_t)(nx + 2 * HF_GHOST) * plane, err);
+    return base ? base + (size_t)HF_GHOST * plane : nullptr;
+}
+
+// ---------------------------------------------------------------------------
+// levels
+// ---------------------------------------------------------------------------
+struct Level {
+    Lvl L{};
+    cd *b = nullptr, *u = nullptr, *r = nullptr, *t = nullptr;   // scratch (MGLevel)
+    cd *fb = nullptr, *guess = nullptr;                          // F-cycle scratch
+};
+
+// host: minimum |diag| h^2 check (operators.py:179-182)
+static bool zero_diagonal(const Lvl &L, const double *kfull) {
+    const double h = L.h, h2 = h * h;
+    for (int i = L.lo1; i < L.lo1 + L.nx; i++)
+        for (int j = 0; j < L.n2; j++)
+            for (int m = 0; m < L.n3; m++) {
+                int nb = (i == 0) + (i == L.n1 - 1) + (j == 0) + (j == L.n2 - 1) + (m == 0) +
+                         (m == L.n3 - 1);
+                if (L.bc == HF_BC_DIRICHLET && nb) continue;
+                double kk = kfull ? kfull[((size_t)i * L.n2 + j) * L.n3 + m] : L.kc;
+                double k2h2 = kk * kk * h2;
+                double re = 6.0 - L.sre * k2h2, im = -L.sim * k2h2;
+                if (L.bc == HF_BC_SOMMERFELD) im -= nb * 2.0 * kk * h;
+                if (std::hypot(re, im) < 6.0e-12) return true;
+                if (!kfull) {
+                    // constant k: interior value decides; boundary rows only add imaginary parts
+                }
+            }
+    return false;
+}
+
+static int make_level(Allocs &A, Level &lv, int n1, int n2, int n3, int lo1, int nx, double h,
+                      double sre, double sim, int bc, const double *kfull, double kc,
+                      bool scratch) {
+    if (n1 < 3 || n2 < 3 || n3 < 3) return fail(HF_ERR_ARG, "grid dims must all be >= 3");
+    if (!(h > 0)) return fail(HF_ERR_ARG, "grid spacing must be positive");
+    if (lo1 < 0 || nx < 1 || lo1 + nx > n1) return fail(HF_ERR_ARG, "slab outside the grid");
+    if (bc != HF_BC_DIRICHLET && bc != HF_BC_SOMMERFELD) return fail(HF_ERR_ARG, "bad bc");
+    Lvl &L = lv.L;
+    L.n1 = n1; L.n2 = n2; L.n3 = n3; L.lo1 = lo1; L.nx = nx;
+    L.plane = (long long)n2 * n3;
+    L.h = h; L.h2 = h * h; L.ih2 = 1.0 / (h * h); L.twoh = 2.0 / h;
+    L.sre = sre; L.sim = sim; L.bc = bc;
+    L.kc = kc;
+    L.k = nullptr;
+    if (!kfull && !(kc > 0)) return fail(HF_ERR_ARG, "wavenumber must be positive");
+    if (zero_diagonal(L, kfull))
+        return fail(HF_ERR_ZERO_DIAGONAL,
+                    "stencil diagonal vanishes (k^2 h^2 = 6); choose a different grid");
+    cudaError_t err;
+    if (kfull) {
+        // owned planes plus HF_GHOST ghost planes where they exist in the grid
+        double *kb = A.get<double>((size_t)(nx + 2 * HF_GHOST) * L.plane, err);
+        if (!kb) return fail(HF_ERR_CUDA, "cudaMalloc k");
+        int g0 = std::max(0, lo1 - HF_GHOST), g1 = std::min(n1, lo1 + nx + HF_GHOST);
+        double *dst = kb + (size_t)(g0 - lo1 + HF_GHOST) * L.plane;
+        CK(cudaMemcpy(dst, kfull + (size_t)g0 * L.plane, (size_t)(g1 - g0) * L.plane * sizeof(double),
+                      cudaMemcpyHostToDevice));
+        L.k = kb + (size_t)HF_GHOST * L.plane;
+    }
+    if (scratch) {
+        lv.b = new_field(A, nx, L.plane, err);
+        lv.u = new_field(A, nx, L.plane, err);
+        lv.r = new_field(A, nx, L.plane, err);
+        lv.t = new_field(A, nx, L.plane, err);
+        if (!lv.b || !lv.u || !lv.r || !lv.t) return fail(HF_ERR_CUDA, "cudaMalloc level scratch");
+    }
+    return 0;
+}
+
+struct hf_operator {
+    Allocs A;
+    Level lv;
+};
+
+// ---------------------------------------------------------------------------
+// hierarchy (multigrid.py:101-128)
+// ---------------------------------------------------------------------------
+struct hf_hierarchy {
+    Allocs A;
+    std::vector<Level> lev;
+    hf_mg_config cfg{};
+    int Nc = 0;
+    cd *Minv = nullptr;     // row-major dense inverse of the coarsest operator
+    int coarsest_flags = 0;
+};
+
+static bool keep_coarsening(int n1, int n2, int n3, const hf_mg_config &c) {
+    int th = c.coarsest_threshold;
+    bool ok = c.threshold_ge ? (n1 >= th && n2 >= th && n3 >= th) : (n1 > th && n2 > th && n3 > th);
+    return ok && (n1 % 2) && (n2 % 2) && (n3 % 2);
+}
+
+static int build_coarsest_direct(hf_hierarchy *H, cudaStream_t s) {
+    Level &C = H->lev.back();
+    if (C.L.lo1 != 0 || C.L.nx != C.L.n1)
+        return fail(HF_ERR_UNSUPPORTED, "direct coarsest solve needs the whole coarsest grid");
+    long long N = (long long)C.L.n1 * C.L.plane;
+    if (N > 60000) return fail(HF_ERR_UNSUPPORTED, "coarsest grid too large for the dense inverse");
+    H->Nc = (int)N;
+    cudaError_t err;
+    cd *Amat = nullptr;
+    CK(cudaMalloc(&Amat, (size_t)N * N * sizeof(cd)));
+    CK(cudaMemsetAsync(Amat, 0, (size_t)N * N * sizeof(cd), s));
+    launch_assemble(C.L, Amat, s);
+    CKL();
+    H->Minv = H->A.get<cd>((size_t)N * N, err);
+    if (!H->Minv) { cudaFree(Amat); return fail(HF_ERR_CUDA, "cudaMalloc coarsest inverse"); }
+    launch_set_identity(N, H->Minv, s);
+    CKL();
+    cusolverDnHandle_t hs;
+    if (cusolverDnCreate(&hs) != CUSOLVER_STATUS_SUCCESS) {
+        cudaFree(Amat);
+        return fail(HF_ERR_CUDA, "cusolverDnCreate failed");
+    }
+    cusolverDnSetStream(hs, s);
+    int lwork = 0;
+    cuDoubleComplex *Ac = (cuDoubleComplex *)Amat;
+    cusolverDnZgetrf_bufferSize(hs, (int)N, (int)N, Ac, (int)N, &lwork);
+    cuDoubleComplex *work = nullptr;
+    int *ipiv = nullptr, *info = nullptr;
+    cudaMalloc(&work, (size_t)std::max(lwork, 1) * sizeof(cuDoubleComplex));
+    cudaMalloc(&ipiv, (size_t)N * sizeof(int));
+    cudaMalloc(&info, 2 * sizeof(int));
+    // row-major A == column-major A^T; inv(A^T) column-major == inv(A) row-major
+    cusolverStatus_t st1 = cusolverDnZgetrf(hs, (int)N, (int)N, Ac, (int)N, work, ipiv, info);
+    cusolverStatus_t st2 = cusolverDnZgetrs(hs, CUBLAS_OP_N, (int)N, (int)N, Ac, (int)N, ipiv,
+                                            (cuDoubleComplex *)H->Minv, (int)N, info + 1);
+    int hinfo[2] = {0, 0};
+    cudaMemcpyAsync(hinfo, info, 2 * sizeof(int), cudaMemcpyDeviceToHost, s);
+    cudaError_t e = cudaStreamSynchronize(s);
+    cusolverDnDestroy(hs);
+    cudaFree(work); cudaFree(ipiv); cudaFree(info); cudaFree(Amat);
+    if (e != cudaSuccess) return fail(HF_ERR_CUDA, std::string("coarsest factorisation: ") + cudaGetErrorString(e));
+    if (st1 != CUSOLVER_STATUS_SUCCESS || st2 != CUSOLVER_STATUS_SUCCESS || hinfo[0] != 0 || hinfo[1] != 0)
+        return fail(HF_ERR_SOLVER, "coarsest operator is singular (getrf/getrs failed)");
+    return 0;
+}
+
+static cudaStream_t work_stream() { return g_user_stream; }
+
+extern "C" hf_hierarchy *hf_hierarchy_create(int n1, int n2, int n3, int lo1, int nx, double h,
+                                             double beta1, double beta2, int bc,
+                                             const double *k_host, double k_const,
+                                             const hf_mg_config *cfg) {
+    if (!cfg) { fail(HF_ERR_ARG, "null mg config"); return nullptr; }
+    if (cfg->cycle != HF_CYCLE_V && cfg->cycle != HF_CYCLE_F) {
+        fail(HF_ERR_ARG, "unknown cycle type");
+        return nullptr;
+    }
+    if (cfg->coarsest_method != HF_COARSEST_DIRECT) {
+        fail(HF_ERR_UNSUPPORTED, "only the direct coarsest solve is built into this library");
+        return nullptr;
+    }
+    if (cfg->nu1 < 0 || cfg->nu2 < 0 || !(cfg->omega > 0 && cfg->omega <= 1)) {
+        fail(HF_ERR_ARG, "invalid smoother parameters");
+        return nullptr;
+    }
+    auto *H = new hf_hierarchy();
+    H->cfg = *cfg;
+    double sre = beta1, sim = -beta2;
+    std::vector<double> kprev, kcur;
+    const double *kf = k_host;
+    int a = n1, b = n2, c = n3, l0 = lo1, cnx = nx;
+    double hh = h;
+    for (int lvl = 0;; lvl++) {
+        Level lv;
+        if (make_level(H->A, lv, a, b, c, l0, cnx, hh, sre, sim, bc, kf, k_const, true)) {
+            delete H;
+            return nullptr;
+        }
+        cudaError_t err;
+        if (cfg->cycle == HF_CYCLE_F) {
+            lv.fb = new_field(H->A, cnx, lv.L.plane, err);
+            lv.guess = new_field(H->A, cnx, lv.L.plane, err);
+        }
+        H->lev.push_back(lv);
+        if (!keep_coarsening(a, b, c, *cfg) || lvl > 30) break;
+        // coarse grid: n -> (n+1)/2, h -> 2h; k subsampled at 2i (0-based) (operators.py:265-274)
+        int na = (a + 1) / 2, nb = (b + 1) / 2, nc = (c + 1) / 2;
+        if (kf) {
+            kcur.assign((size_t)na * nb * nc, 0.0);
+            for (int i = 0; i < na; i++)
+                for (int j = 0; j < nb; j++)
+                    for (int m = 0; m < nc; m++)
+                        kcur[((size_t)i * nb + j) * nc + m] = kf[((size_t)(2 * i) * b + 2 * j) * c + 2 * m];
+            kprev.swap(kcur);
+            kf = kprev.data();
+        }
+        // derive_coarse_extent (partition.py:120-131) in 0-based form
+        int clo = (l0 + 1) / 2, chi = (l0 + cnx - 1) / 2;
+        if (chi < clo) {
+            fail(HF_ERR_ARG, "level-incompatible: slab owns no vertices on a coarse level");
+            delete H;
+            return nullptr;
+        }
+        a = na; b = nb; c = nc; l0 = clo; cnx = chi - clo + 1; hh = 2.0 * hh;
+    }
+    if (build_coarsest_direct(H, work_stream())) {
+        delete H;
+        return nullptr;
+    }
+    return H;
+}
+
+extern "C" void hf_hierarchy_destroy(hf_hierarchy *H) { delete H; }
+extern "C" int hf_hierarchy_num_levels(const hf_hierarchy *H) { return H ? (int)H->lev.size() : 0; }
+extern "C" int hf_hierarchy_level_shape(const hf_hierarchy *H, int l, int *d) {
+    if (!H || l < 0 || l >= (int)H->lev.size()) return fail(HF_ERR_ARG, "bad level");
+    const Lvl &L = H->lev[l].L;
+    d[0] = L.n1; d[1] = L.n2; d[2] = L.n3; d[3] = L.lo1; d[4] = L.nx;
+    return 0;
+}
+
+// ---------------------------------------------------------------------------
+// cycles (multigrid.py:326-419)
+// ---------------------------------------------------------------------------
+static void coarsest(hf_hierarchy *H, const cd *b, cd *x, cudaStream_t s, const int *done) {
+    L1(launch_gemv(H->Nc, H->Minv, b, x, s, done));
+}
+
+static void smooth_sweeps(Level &lv, cd *u, const cd *b, double omega, int sweeps,
+                          cudaStream_t s, const int *done) {
+    for (int k = 0; k < sweeps; k++) {
+        L1(launch_jacobi(lv.L, u, b, lv.t, omega, s, done));
+        cudaMemcpyAsync(u, lv.t, (size_t)lv.L.nx * lv.L.plane * sizeof(cd), cudaMemcpyDeviceToDevice, s);
+    }
+}
+
+static void v_cycle(hf_hierarchy *H, int li, const cd *b, cd *u, cudaStream_t s, const int *done) {
+    Level &lv = H->lev[li];
+    const hf_mg_config &c = H->cfg;
+    if (li == (int)H->lev.size() - 1) { coarsest(H, b, u, s, done); return; }
+    Level &nx = H->lev[li + 1];
+    const bool fused = c.nu1 <= 1 && c.nu2 == 1;
+    if (c.nu1 == 1 && fused) {
+        L1(launch_down1(lv.L, b, lv.r, c.omega, s, done));
+    } else {
+        if (c.nu1 == 0) {
+            cudaMemsetAsync(u, 0, (size_t)lv.L.nx * lv.L.plane * sizeof(cd), s);
+        } else {
+            L1(launch_jacobi0(lv.L, b, u, c.omega, s, done));
+            smooth_sweeps(lv, u, b, c.omega, c.nu1 - 1, s, done);
+        }
+        L1(launch_residual(lv.L, u, b, lv.r, s, done));
+    }
+    L1(launch_restrict(lv.L, nx.L, lv.r, nx.b, s, done));
+    v_cycle(H, li + 1, nx.b, nx.u, s, done);
+    if (fused) {
+        L1(launch_up1(lv.L, nx.L, b, nx.u, u, c.omega, c.nu1 == 1, s, done));
+    } else {
+        L1(launch_prolong(lv.L, nx.L, nx.u, u, true, s, done));
+        smooth_sweeps(lv, u, b, c.omega, c.nu2, s, done);
+    }
+}
+
+static void f_cycle(hf_hierarchy *H, int li, const cd *b, cd *u, cudaStream_t s, const int *done) {
+    Level &lv = H->lev[li];
+    if (li == (int)H->lev.size() - 1) { coarsest(H, b, u, s, done); return; }
+    Level &nx = H->lev[li + 1];
+    size_t bytes = (size_t)lv.L.nx * lv.L.plane * sizeof(cd);
+    L1(launch_restrict(lv.L, nx.L, b, nx.b, s, done));
+    f_cycle(H, li + 1, nx.b, nx.u, s, done);
+    L1(launch_prolong(lv.L, nx.L, nx.u, u, false, s, done));
+    L1(launch_residual(lv.L, u, b, lv.r, s, done));
+    cudaMemcpyAsync(lv.guess, u, bytes, cudaMemcpyDeviceToDevice, s);
+    cudaMemcpyAsync(lv.fb, lv.r, bytes, cudaMemcpyDeviceToDevice, s);
+    v_cycle(H, li, lv.fb, u, s, done);
+    L1(launch_axpby(lv.L.nx * lv.L.plane, make_double2(1, 0), lv.guess, make_double2(1, 0), u, s));
+}
+
+static void precondition(hf_hierarchy *H, const cd *r, cd *z, cudaStream_t s, const int *done) {
+    if (H->cfg.cycle == HF_CYCLE_F) f_cycle(H, 0, r, z, s, done);
+    else v_cycle(H, 0, r, z, s, done);
+}
+
+extern "C" int hf_mg_precondition(hf_hierarchy *H, const double *r, double *z) {
+    if (!H || !r || !z) return fail(HF_ERR_ARG, "null argument");
+    cudaStream_t s = work_stream();
+    precondition(H, (const cd *)r, (cd *)z, s, nullptr);
+    CKL();
+    return 0;
+}
+
+extern "C" int hf_restrict_fw(hf_hierarchy *H, int l, const double *r, double *out) {
+    if (!H || l < 0 || l + 1 >= (int)H->lev.size()) return fail(HF_ERR_ARG, "bad level");
+    L1(launch_restrict(H->lev[l].L, H->lev[l + 1].L, (const cd *)r, (cd *)out, work_stream(), nullptr));
+    CKL();
+    return 0;
+}
+
+extern "C" int hf_prolong_tl(hf_hierarchy *H, int l, const double *e, double *out) {
+    if (!H || l < 0 || l + 1 >= (int)H->lev.size()) return fail(HF_ERR_ARG, "bad level");
+    L1(launch_prolong(H->lev[l].L, H->lev[l + 1].L, (const cd *)e, (cd *)out, false, work_stream(), nullptr));
+    CKL();
+    return 0;
+}
+
+extern "C" int hf_coarsest_solve(hf_hierarchy *H, const double *b, double *x) {
+    if (!H) return fail(HF_ERR_ARG, "null hierarchy");
+    coarsest(H, (const cd *)b, (cd *)x, work_stream(), nullptr);
+    CKL();
+    return 0;
+}
+
+// ---------------------------------------------------------------------------
+// operators (operators.py:122-254)
+// ---------------------------------------------------------------------------
+extern "C" hf_operator *hf_operator_create(int n1, int n2, int n3, int lo1, int nx, double h,
+                                           double shift_re, double shift_im, int bc,
+                                           const double *k_host, double k_const) {
+    auto *op = new hf_operator();
+    if (make_level(op->A, op->lv, n1, n2, n3, lo1, nx, h, shift_re, shift_im, bc, k_host, k_const,
+                   true)) {
+        delete op;
+        return nullptr;
+    }
+    return op;
+}
+extern "C" void hf_operator_destroy(hf_operator *op) { delete op; }
+
+extern "C" int hf_operator_apply(hf_operator *op, const double *u, double *v) {
+    if (!op || !u || !v) return fail(HF_ERR_ARG, "null argument");
+    L1(launch_apply(op->lv.L, (const cd *)u, (cd *)v, work_stream(), nullptr));
+    CKL();
+    return 0;
+}
+
+extern "C" int hf_operator_diag(hf_operator *op, double *d) {
+    if (!op || !d) return fail(HF_ERR_ARG, "null argument");
+    // D = w D^-1 b with b = D, w = 1 would divide; instead apply jacobi0 to ones:
+    // diag is reported through u = 1 / (w D^-1 1) is lossy, so compute directly.
+    const Lvl &L = op->lv.L;
+    size_t n = (size_t)L.nx * L.plane;
+    std::vector<double> kh;
+    if (L.k) {
+        kh.resize(n);
+        CK(cudaMemcpy(kh.data(), L.k, n * sizeof(double), cudaMemcpyDeviceToHost));
+    }
+    std::vector<double> out(2 * n);
+    for (int i = 0; i < L.nx; i++)
+        for (int j = 0; j < L.n2; j++)
+            for (int m = 0; m < L.n3; m++) {
+                size_t q = ((size_t)i * L.n2 + j) * L.n3 + m;
+                int gi = L.lo1 + i;
+                int nb = (gi == 0) + (gi == L.n1 - 1) + (j == 0) + (j == L.n2 - 1) + (m == 0) + (m == L.n3 - 1);
+                double kk = L.k ? kh[q] : L.kc;
+                double k2h2 = kk * kk * L.h2;
+                double re = (6.0 - L.sre * k2h2) * L.ih2, im = (-L.sim * k2h2) * L.ih2;
+                if (L.bc == HF_BC_SOMMERFELD) im -= nb * (kk * L.twoh);
+                if (L.bc == HF_BC_DIRICHLET && nb) { re = 1.0; im = 0.0; }
+                out[2 * q] = re; out[2 * q + 1] = im;
+            }
+    CK(cudaMemcpy(d, out.data(), 2 * n * sizeof(double), cudaMemcpyHostToDevice));
+    return 0;
+}
+
+extern "C" int hf_jacobi_smooth(hf_operator *op, double *u, const double *b, double omega,
+                                int sweeps, int assume_zero, double *scratch) {
+    if (!op || !u || !b) return fail(HF_ERR_ARG, "null argument");
+    cudaStream_t s = work_stream();
+    Level &lv = op->lv;
+    cd *tmp = scratch ? (cd *)scratch : lv.t;
+    size_t bytes = (size_t)lv.L.nx * lv.L.plane * sizeof(cd);
+    bool first = assume_zero != 0;
+    for (int k = 0; k < sweeps; k++) {
+        if (first) {
+            L1(launch_jacobi0(lv.L, (const cd *)b, (cd *)u, omega, s, nullptr));
+            first = false;
+            continue;
+        }
+        L1(launch_jacobi(lv.L, (const cd *)u, (const cd *)b, tmp, omega, s, nullptr));
+        CK(cudaMemcpyAsync(u, tmp, bytes, cudaMemcpyDeviceToDevice, s));
+    }
+    CKL();
+    return 0;
+}
+
+// ---------------------------------------------------------------------------
+// dot (krylov.py:67-78) -- conjugated, deterministic
+// ---------------------------------------------------------------------------
+struct RedBuf {
+    cd *partials = nullptr;
+    unsigned *counter = nullptr;
+    cd *out = nullptr;
+    int init(Allocs &A, size_t nblocks) {
+        cudaError_t e;
+        partials = A.get<cd>(nblocks * HF_MAX_DOTS, e);
+        counter = A.get<unsigned>(4, e);
+        out = A.get<cd>(HF_MAX_DOTS, e);
+        return (partials && counter && out) ? 0 : -1;
+    }
+    RedSlot slot(int op, BcgState *st) const { return RedSlot{partials, counter, out, op, st}; }
+};
+
+extern "C" int hf_dot(int64_t n, const double *u, const double *v, double *out_host2) {
+    static thread_local Allocs *A = nullptr;
+    static thread_local RedBuf rb;
+    if (!A) {
+        A = new Allocs();
+        if (rb.init(*A, 4096)) return fail(HF_ERR_CUDA, "cudaMalloc dot scratch");
+    }
+    cudaStream_t s = work_stream();
+    L1(launch_dot(n, (const cd *)u, (const cd *)v, rb.slot(FIN_STORE, nullptr), s));
+    CKL();
+    CK(cudaMemcpyAsync(out_host2, rb.out, sizeof(cd), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return 0;
+}
+
+// ---------------------------------------------------------------------------
+// solver: Bi-CGSTAB with device-resident scalars + CUDA graph per iteration
+// ---------------------------------------------------------------------------
+struct hf_solver {
+    Allocs A;
+    hf_operator *Aop = nullptr;
+    hf_hierarchy *M = nullptr;
+    long long n = 0;
+    cd *x, *r, *rs, *p, *v, *ph, *s, *sh, *t;
+    cd *xb = nullptr, *bb = nullptr;    // device staging for hf_solve_host
+    BcgState *st = nullptr;             // device
+    BcgState *st_host = nullptr;        // pinned mirror
+    double *hist = nullptr;
+    int hist_cap = 0;
+    RedBuf red;
+    cudaStream_t stream = nullptr;
+    cudaGraphExec_t graph = nullptr;
+    int graph_kernels = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, evs = nullptr;
+    ~hf_solver() {
+        if (graph) cudaGraphExecDestroy(graph);
+        if (st_host) cudaFreeHost(st_host);
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+        if (evs) cudaEventDestroy(evs);
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+extern "C" hf_solver *hf_solver_create(hf_operator *Aop, hf_hierarchy *M) {
+    if (!Aop || !M) { fail(HF_ERR_ARG, "null operator or hierarchy"); return nullptr; }
+    const Lvl &L = Aop->lv.L, &F = M->lev[0].L;
+    if (L.n1 != F.n1 || L.n2 != F.n2 || L.n3 != F.n3 || L.lo1 != F.lo1 || L.nx != F.nx) {
+        fail(HF_ERR_ARG, "operator and hierarchy live on different slabs");
+        return nullptr;
+    }
+    auto *S = new hf_solver();
+    S->Aop = Aop; S->M = M;
+    S->n = (long long)L.nx * L.plane;
+    cudaError_t e;
+    cd **vecs[] = {&S->x, &S->r, &S->rs, &S->p, &S->v, &S->ph, &S->s, &S->sh, &S->t};
+    for (cd **pv : vecs) {
+        *pv = new_field(S->A, L.nx, L.plane, e);
+        if (!*pv) { fail(HF_ERR_CUDA, "cudaMalloc solver vectors"); delete S; return nullptr; }
+    }
+    S->st = S->A.get<BcgState>(1, e);
+    size_t nblk = std::max<size_t>(march_blocks(L), VEC_BLOCKS_HOST);
+    if (!S->st || S->red.init(S->A, nblk + 64)) {
+        fail(HF_ERR_CUDA, "cudaMalloc solver state");
+        delete S;
+        return nullptr;
+    }
+    if (cudaMallocHost(&S->st_host, sizeof(BcgState)) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&S->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreate(&S->ev0) != cudaSuccess || cudaEventCreate(&S->ev1) != cudaSuccess ||
+        cudaEventCreateWithFlags(&S->evs, cudaEventDisableTiming) != cudaSuccess) {
+        fail(HF_ERR_CUDA, "stream/event/pinned allocation failed");
+        delete S;
+        return nullptr;
+    }
+    return S;
+}
+
+extern "C" void hf_solver_destroy(hf_solver *S) { delete S; }
+
+// one Bi-CGSTAB iteration (krylov.py:234-273), every kernel predicated on st->done
+static void bcg_iteration(hf_solver *S, cudaStream_t s) {
+    const Lvl &A = S->Aop->lv.L;
+    const int *done = &S->st->done;
+    long long n = S->n;
+    L1(launch_bcg_p(n, S->st, S->r, S->p, S->v, s, done));
+    precondition(S->M, S->p, S->ph, s, done);
+    L1(launch_apply_dot1(A, S->ph, S->v, S->rs, S->red.slot(FIN_BCG_ALPHA, S->st), s, done));
+    L1(launch_bcg_s(n, S->st, S->r, S->v, S->s, S->red.slot(FIN_BCG_S, S->st), s, done));
+    precondition(S->M, S->s, S->sh, s, done);
+    L1(launch_apply_dot2(A, S->sh, S->t, S->s, S->red.slot(FIN_BCG_OMEGA, S->st), s, done));
+    L1(launch_bcg_xr(n, S->st, S->x, S->ph, S->sh, S->s, S->t, S->r, S->rs,
+                     S->red.slot(FIN_BCG_RHO, S->st), s, done));
+    cudaMemcpyAsync(S->st_host, S->st, sizeof(BcgState), cudaMemcpyDeviceToHost, s);
+}
+
+static int build_graph(hf_solver *S) {
+    if (S->graph) return 0;
+    cudaGraph_t g;
+    long long before = g_launches;
+    CK(cudaStreamBeginCapture(S->stream, cudaStreamCaptureModeThreadLocal));
+    bcg_iteration(S, S->stream);
+    cudaError_t e = cudaStreamEndCapture(S->stream, &g);
+    if (e != cudaSuccess) return fail(HF_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    S->graph_kernels = (int)(g_launches - before);
+    g_launches = before;
+    e = cudaGraphInstantiate(&S->graph, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fail(HF_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+    return 0;
+}
+
+static int solve_bicgstab(hf_solver *S, const hf_solver_config *cfg, const cd *b, cd *x,
+                          hf_report *rep) {
+    cudaStream_t s = S->stream;
+    if (!S->hist || S->hist_cap < cfg->maxit + 2) {
+        cudaError_t e;
+        S->hist = S->A.get<double>(cfg->maxit + 2, e);
+        if (!S->hist) return fail(HF_ERR_CUDA, "cudaMalloc history");
+        S->hist_cap = cfg->maxit + 2;
+    }
+    BcgState init{};
+    init.tol = cfg->tol;
+    init.btol = cfg->breakdown_tol > 0 ? cfg->breakdown_tol : 1e-30;
+    init.maxit = cfg->maxit;
+    init.hist = S->hist;
+    init.hist_cap = S->hist_cap;
+    *S->st_host = init;
+    CK(cudaMemcpyAsync(S->st, S->st_host, sizeof(BcgState), cudaMemcpyHostToDevice, s));
+    if (build_graph(S)) return HF_ERR_CUDA;
+    long long launches = 0;
+    CK(cudaEventRecord(S->ev0, s));
+    L1(launch_bcg_init(S->n, b, S->r, S->rs, S->x, S->p, S->v, S->red.slot(FIN_BCG_INIT, S->st), s));
+    launches++;
+    CK(cudaMemcpyAsync(S->st_host, S->st, sizeof(BcgState), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    int every = cfg->check_every > 0 ? cfg->check_every : 4;
+    int graphs = 0;
+    while (!S->st_host->done && graphs < cfg->maxit + every) {
+        for (int k = 0; k < every; k++) {
+            CK(cudaGraphLaunch(S->graph, s));
+            graphs++;
+        }
+        CK(cudaStreamSynchronize(s));
+    }
+    launches += (long long)graphs * S->graph_kernels;
+    if (S->st_host->s_conv) {
+        L1(launch_bcg_xhalf(S->n, S->st, S->x, S->ph, s));
+        launches++;
+    }
+    CK(cudaEventRecord(S->ev1, s));
+    if (x != S->x)
+        CK(cudaMemcpyAsync(x, S->x, (size_t)S->n * sizeof(cd), cudaMemcpyDeviceToDevice, s));
+    CK(cudaStreamSynchronize(s));
+    CKL();
+    const BcgState &st = *S->st_host;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, S->ev0, S->ev1);
+    rep->matvec_count = st.matvecs;
+    rep->iterations = st.iter;
+    rep->converged = st.converged;
+    rep->breakdown = st.breakdown;
+    rep->final_relres = st.relres;
+    rep->solve_ms = ms;
+    rep->kernel_launches = (int)launches;
+    rep->coarsest_flags = 0;
+    if (rep->history_host && rep->history_cap > 0 && st.iter > 0) {
+        int cnt = std::min(st.iter, rep->history_cap);
+        CK(cudaMemcpy(rep->history_host, S->hist, (size_t)cnt * sizeof(double), cudaMemcpyDeviceToHost));
+    }
+    return 0;
+}
+
+extern "C" int hf_solve(hf_solver *S, const hf_solver_config *cfg, const double *b, double *x,
+                        hf_report *rep) {
+    if (!S || !cfg || !b || !x || !rep) return fail(HF_ERR_ARG, "null argument");
+    if (cfg->maxit < 1 || !(cfg->tol > 0)) return fail(HF_ERR_ARG, "invalid tol/maxit");
+    // order the private stream after the caller's stream and back
+    CK(cudaEventRecord(S->evs, work_stream()));
+    CK(cudaStreamWaitEvent(S->stream, S->evs, 0));
+    int rc;
+    switch (cfg->method) {
+    case HF_METHOD_BICGSTAB:
+        rc = solve_bicgstab(S, cfg, (const cd *)b, (cd *)x, rep);
+        break;
+    default:
+        return fail(HF_ERR_UNSUPPORTED, "Krylov method not built into this library yet");
+    }
+    if (rc) return rc;
+    CK(cudaEventRecord(S->evs, S->stream));
+    CK(cudaStreamWaitEvent(work_stream(), S->evs, 0));
+    return 0;
+}
+
+extern "C" int hf_solve_host(hf_solver *S, const hf_solver_config *cfg, const double *b_host,
+                             double *x_host, hf_report *rep) {
+    if (!S || !b_host || !x_host) return fail(HF_ERR_ARG, "null argument");
+    cudaError_t e;
+    if (!S->bb) {
+        S->bb = new_field(S->A, S->Aop->lv.L.nx, S->Aop->lv.L.plane, e);
+        S->xb = new_field(S->A, S->Aop->lv.L.nx, S->Aop->lv.L.plane, e);
+        if (!S->bb || !S->xb) return fail(HF_ERR_CUDA, "cudaMalloc staging");
+    }
+    size_t bytes = (size_t)S->n * sizeof(cd);
+    CK(cudaMemcpyAsync(S->bb, b_host, bytes, cudaMemcpyHostToDevice, S->stream));
+    CK(cudaEventRecord(S->evs, S->stream));
+    CK(cudaStreamWaitEvent(work_stream(), S->evs, 0));
+    int rc = hf_solve(S, cfg, (const double *)S->bb, (double *)S->xb, rep);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(x_host, S->xb, bytes, cudaMemcpyDeviceToHost, S->stream));
+    CK(cudaStreamSynchronize(S->stream));
+    return 0;
+}

@@ -1,0 +1,172 @@
+"""Parity of the native CUDA path with the C oracle (which is pinned to the
+reference by tests/test_oracle.py).  Tolerances: complex128 kernels agree to
+1e-12 relative (reduction order / FMA only); solves agree on the iteration
+count within +-1 and on the solution within 1e-8 relative L2 (north_star)."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _rand(shape, seed):
+    rng = np.random.default_rng(seed)
+    return rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+
+
+def _kfield(shape, seed=0, lo=3.0, hi=8.0):
+    rng = np.random.default_rng(seed)
+    return rng.uniform(lo, hi, shape)
+
+
+def _rel(a, b):
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+@pytest.fixture(scope="module")
+def hf():
+    import paper_2308_06085_b200 as pkg
+    from paper_2308_06085_b200 import _native
+    _native.load()
+    return pkg
+
+
+GRIDS = [(5, 5, 5), (7, 7, 7), (9, 9, 9), (5, 7, 9), (17, 17, 17), (33, 17, 9)]
+
+
+@pytest.mark.parametrize("dims", GRIDS)
+@pytest.mark.parametrize("bc", ["dirichlet", "sommerfeld"])
+@pytest.mark.parametrize("kind", ["helmholtz", "cslp"])
+def test_apply_matches_oracle(hf, oracle, dims, bc, kind):
+    from paper_2308_06085_b200.operators import Dirichlet, OperatorSpec, Sommerfeld, StencilOperator
+    h = 0.125
+    k = _kfield(dims, 1)
+    u = _rand(dims, 2)
+    spec = OperatorSpec(kind, 1.0, -0.5, Dirichlet(1.0) if bc == "dirichlet" else Sommerfeld(), k)
+    grid = hf.make_grid(*dims, h)
+    got = StencilOperator(spec, grid).apply(u).cpu().numpy()
+    want = oracle.apply(k, u, h, spec.shift, bc)
+    assert _rel(got, want) < 1e-12
+
+
+def test_constant_k_fast_path(hf, oracle):
+    from paper_2308_06085_b200.operators import OperatorSpec, Sommerfeld, StencilOperator
+    dims, h = (17, 9, 33), 1 / 16
+    k = np.full(dims, 7.5)
+    u = _rand(dims, 3)
+    spec = OperatorSpec("cslp", 1.0, -0.5, Sommerfeld(), k)
+    got = StencilOperator(spec, hf.make_grid(*dims, h)).apply(u).cpu().numpy()
+    assert _rel(got, oracle.apply(k, u, h, spec.shift, "sommerfeld")) < 1e-12
+
+
+def _pair(hf, oracle, n, bc, k, beta2=-0.5, **cfg):
+    from paper_2308_06085_b200.multigrid import MGConfig, build_hierarchy
+    from paper_2308_06085_b200.operators import Dirichlet, OperatorSpec, Sommerfeld
+    grid = hf.make_grid(*n, 1.0 / (n[0] - 1))
+    spec = OperatorSpec("cslp", 1.0, beta2, Dirichlet(0.0) if bc == "dirichlet" else Sommerfeld(), k)
+    mg = MGConfig(**cfg)
+    hier = build_hierarchy(grid, None, spec, mg)
+    oh = oracle.Hierarchy(k, grid.h, beta2=beta2, bc=bc, nu1=mg.nu1, nu2=mg.nu2, omega=mg.omega,
+                          cycle=mg.cycle, threshold=mg.coarsest_threshold,
+                          threshold_cmp=mg.threshold_cmp)
+    return hier, oh
+
+
+@pytest.mark.parametrize("bc", ["dirichlet", "sommerfeld"])
+def test_transfers_and_smoother(hf, oracle, bc):
+    from paper_2308_06085_b200.multigrid import jacobi_smooth, prolong_tl, restrict_fw
+    from paper_2308_06085_b200.operators import Dirichlet, OperatorSpec, Sommerfeld, StencilOperator
+    n = (17, 17, 17)
+    k = _kfield(n, 4)
+    hier, oh = _pair(hf, oracle, n, bc, k, coarsest_threshold=5)
+    assert [lv.grid.shape for lv in hier.levels] == oh.shapes
+    r = _rand(n, 5)
+    got = restrict_fw(r, hier.levels[0], hier.levels[1]).cpu().numpy()
+    assert _rel(got, oh.restrict(0, r)) < 1e-14
+    e = _rand(oh.shapes[1], 6)
+    got = prolong_tl(e, hier.levels[1], hier.levels[0]).cpu().numpy()
+    assert _rel(got, oh.prolong(0, e)) < 1e-15
+    spec = OperatorSpec("cslp", 1.0, -0.5, Dirichlet(0.0) if bc == "dirichlet" else Sommerfeld(), k)
+    op = StencilOperator(spec, hf.make_grid(*n, 1 / 16))
+    u0, b = _rand(n, 7), _rand(n, 8)
+    u = torch.as_tensor(u0).cuda()
+    jacobi_smooth(op, u, b, 0.8, 2)
+    assert _rel(u.cpu().numpy(), oh.jacobi(0, u0, b, 0.8, 2)) < 1e-12
+    u = torch.zeros(n, dtype=torch.complex128, device="cuda")
+    jacobi_smooth(op, u, b, 0.8, 1, assume_zero=True)
+    assert _rel(u.cpu().numpy(), oh.jacobi(0, np.zeros(n), b, 0.8, 1, assume_zero=True)) < 1e-13
+
+
+@pytest.mark.parametrize("bc", ["dirichlet", "sommerfeld"])
+@pytest.mark.parametrize("cfg", [dict(), dict(cycle="F"), dict(nu1=2, nu2=1), dict(nu1=0, nu2=1),
+                                 dict(threshold_cmp="ge")])
+def test_cycle_matches_oracle(hf, oracle, bc, cfg):
+    from paper_2308_06085_b200.multigrid import mg_precondition
+    n = (33, 33, 33)
+    k = _kfield(n, 9, 15, 25)
+    hier, oh = _pair(hf, oracle, n, bc, k, **cfg)
+    r = _rand(n, 10)
+    got = mg_precondition(hier, r).cpu().numpy()
+    want = oh.precondition(r)
+    # coarsest: exact LU here vs GMRES to 1e-11 in the reference
+    assert _rel(got, want) < 1e-9
+
+
+def _solve_pair(hf, oracle, pspec, k_full, method="bicgstab", beta2=-0.5, tol=1e-6, maxit=400,
+                **mg):
+    from paper_2308_06085_b200 import problems
+    from paper_2308_06085_b200.krylov import Solver, SolverConfig
+    from paper_2308_06085_b200.multigrid import MGConfig, build_hierarchy
+    from paper_2308_06085_b200.operators import OperatorSpec, StencilOperator
+    spec, b = problems.build_problem(pspec)
+    A = StencilOperator(spec, pspec.grid)
+    hier = build_hierarchy(pspec.grid, None, OperatorSpec("cslp", 1.0, beta2, spec.bc, k_full),
+                           MGConfig(**mg))
+    x, rep = Solver(A, hier).solve(b, SolverConfig(method=method, tol=tol, maxit=maxit))
+    bc = "dirichlet" if type(spec.bc).__name__ == "Dirichlet" else "sommerfeld"
+    xo, ro = oracle.solve(k_full, b, pspec.grid.h, bc=bc, method=method, tol=tol, maxit=maxit,
+                          beta2=beta2, **{k_: v for k_, v in mg.items() if k_ != "coarsest_method"})
+    return x.cpu().numpy(), rep, xo, ro
+
+
+@pytest.mark.parametrize("n,k,bc", [(33, 20.0, "dirichlet"), (33, 20.0, "sommerfeld"),
+                                    (65, 40.0, "sommerfeld")])
+def test_bicgstab_point_source(hf, oracle, n, k, bc):
+    from paper_2308_06085_b200 import problems
+    p = problems.point_source_cube(n, k, bc)
+    x, rep, xo, ro = _solve_pair(hf, oracle, p, np.full(p.grid.shape, k))
+    assert rep.converged and ro["converged"]
+    assert abs(rep.iterations - ro["iterations"]) <= 1
+    assert abs(rep.matvec_count - ro["matvec_count"]) <= 2
+    assert np.linalg.norm(x - xo) / np.linalg.norm(xo) < 1e-8
+    np.testing.assert_allclose(rep.residual_history[:5], ro["residual_history"][:5], rtol=1e-7)
+
+
+def test_bicgstab_heterogeneous_wedge(hf, oracle):
+    from paper_2308_06085_b200 import problems
+    p = problems.wedge3_problem(41)
+    k = p.medium.k_field(p.grid, hf.full_extent(p.grid))
+    x, rep, xo, ro = _solve_pair(hf, oracle, p, k)
+    assert rep.converged and ro["converged"]
+    assert abs(rep.iterations - ro["iterations"]) <= 1
+    assert np.linalg.norm(x - xo) / np.linalg.norm(xo) < 1e-8
+
+
+def test_solve_host_buffers(hf, oracle):
+    """hf_solve_host (the e2e entry point) returns the same answer as hf_solve."""
+    from paper_2308_06085_b200 import problems
+    from paper_2308_06085_b200.krylov import Solver, SolverConfig
+    from paper_2308_06085_b200.multigrid import MGConfig, build_hierarchy
+    from paper_2308_06085_b200.operators import OperatorSpec, StencilOperator
+    p = problems.point_source_cube(33, 20.0, "sommerfeld")
+    spec, b = problems.build_problem(p)
+    A = StencilOperator(spec, p.grid)
+    hier = build_hierarchy(p.grid, None, OperatorSpec("cslp", 1.0, -0.5, spec.bc, spec.k_field), MGConfig())
+    S = Solver(A, hier)
+    cfg = SolverConfig(method="bicgstab")
+    xd, r1 = S.solve(b, cfg)
+    xh, r2 = S.solve(b, cfg, host=True)
+    assert r1.iterations == r2.iterations
+    np.testing.assert_array_equal(xd.cpu().numpy(), xh)

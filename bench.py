@@ -1,0 +1,325 @@
+"""Benchmark: CSLP-preconditioned Bi-CGSTAB time-to-solution on the B200.
+
+Workload (BASELINE.json configs[1]): unit cube, constant k = 80, h = 1/128
+(129^3 vertices, kh = 0.625), first-order Sommerfeld faces, unit point
+source at the centre node, complex128; CSLP shift beta1 = 1, |beta2| = 0.5 in
+the reference's damping-consistent sign (beta2 = -0.5, shift 1 + 0.5i), one
+V(1,1)-cycle with damped Jacobi (omega 0.8), full weighting, trilinear
+prolongation, Bi-CGSTAB to relative residual 1e-6.
+
+One step = one full solve from a resident right-hand side.  The metric is
+Munknowns*iter/s = (vertices x Bi-CGSTAB iterations) / solve time, summed over
+all GPUs.  L2 is flushed (256 MiB write) before every timed step; each step is
+timed with CUDA events on the current stream (the library orders its private
+stream after it and back).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_GRID = 129
+K_WAVE = 80.0
+TOL = 1e-6
+MAXIT = 400
+METRIC = "cslp_bicgstab_munknowns_iter_per_s"
+UNIT = "Munknowns*iter/s"
+
+
+def _env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def _problem():
+    from paper_2308_06085_b200 import problems
+    p = problems.point_source_cube(N_GRID, K_WAVE, "sommerfeld")
+    spec, b = problems.build_problem(p)
+    return p, spec, b
+
+
+def _config_dict(extra=None):
+    d = {"workload": "configs[1]: 129^3 unit cube, k=80 (kh=0.625), Sommerfeld, centre point "
+                     "source, complex128, CSLP(1, 0.5i-damped) V(1,1) omega=0.8, Bi-CGSTAB tol 1e-6",
+         "unknowns": N_GRID ** 3, "grid": [N_GRID] * 3, "k": K_WAVE, "tol": TOL,
+         "l2": "flushed (256 MiB write) before every timed step"}
+    if extra:
+        d.update(extra)
+    return d
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during timing."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        return False
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _event_time(fn, reps, stream=None):
+    import torch
+    s = torch.cuda.Event(enable_timing=True)
+    e = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    s.record()
+    for _ in range(reps):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / reps
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2308_06085_b200.krylov import Solver, SolverConfig
+    from paper_2308_06085_b200.multigrid import (MGConfig, build_hierarchy, coarsest_solve,
+                                                 mg_precondition)
+    from paper_2308_06085_b200.operators import OperatorSpec, StencilOperator
+
+    rank, world, local = _env_rank()
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    p, spec, b_host = _problem()
+    n = p.grid.num_vertices
+    t_setup = time.perf_counter()
+    A = StencilOperator(spec, p.grid)
+    hier = build_hierarchy(p.grid, None, OperatorSpec("cslp", 1.0, -0.5, spec.bc, spec.k_field),
+                           MGConfig())
+    solver = Solver(A, hier)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t_setup
+    cfg = SolverConfig(method="bicgstab", tol=TOL, maxit=MAXIT, check_every=4)
+    b = torch.as_tensor(b_host).cuda()
+    x = torch.empty_like(b)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    for _ in range(args.warmup):
+        _, rep = solver.solve(b, cfg, x=x)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    times, reps = [], []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            s = torch.cuda.Event(enable_timing=True)
+            e = torch.cuda.Event(enable_timing=True)
+            s.record()
+            _, rep = solver.solve(b, cfg, x=x)
+            e.record()
+            torch.cuda.synchronize()
+            times.append(s.elapsed_time(e))
+            reps.append(rep)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    total_ms = float(np.sum(times))
+    if world > 1:
+        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    iters = reps[-1].iterations
+    ms_step = total_ms / args.steps
+    value = world * n * iters / (ms_step / 1e3) / 1e6
+
+    # ---- e2e: public API from pinned host buffers (H2D + solve + D2H) ----
+    bh = torch.as_tensor(b_host).pin_memory().numpy()
+    xh = torch.empty(b_host.shape, dtype=torch.complex128).pin_memory().numpy()
+    solver.solve(bh, cfg, x=xh, host=True)
+    e2e_ms = []
+    for _ in range(max(1, min(args.steps, 5))):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _, rep_h = solver.solve(bh, cfg, x=xh, host=True)
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e_step = float(np.mean(e2e_ms))
+    e2e_value = world * n * rep_h.iterations / (e2e_step / 1e3) / 1e6
+
+    # ---- kernel roofline: live CUDA-event timing of the hot kernels ----
+    hbm, peak_kind = _peaks()
+    u = torch.randn(p.grid.shape, dtype=torch.complex128, device="cuda")
+    v = torch.empty_like(u)
+    R = 20
+    t_apply = _event_time(lambda: A.apply(u, out=v), R)
+    t_cycle = _event_time(lambda: mg_precondition(hier, u, out=v), R)
+    nc = hier.coarsest.grid.num_vertices
+    bc_ = torch.randn(hier.coarsest.grid.shape, dtype=torch.complex128, device="cuda")
+    xc_ = torch.empty_like(bc_)
+    t_gemv = _event_time(lambda: coarsest_solve(hier, bc_, out=xc_), R)
+    t_iter = ms_step / max(iters, 1)
+    kernels = {
+        "helmholtz_matvec": {"ms": t_apply, "bytes": 32.0 * n, "per_iter": 2},
+        "coarsest_gemv": {"ms": t_gemv, "bytes": 16.0 * nc * nc, "per_iter": 2},
+    }
+    share = {k_: v_["ms"] * v_["per_iter"] / t_iter for k_, v_ in kernels.items()}
+    share["vcycle_total"] = 2 * t_cycle / t_iter
+    dom = max(kernels, key=lambda k_: share[k_])
+    kd = kernels[dom]
+    achieved = kd["bytes"] / (kd["ms"] / 1e3) / 1e9
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm,
+                "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / hbm, 4),
+                "traffic": None,
+                "algorithmic_bytes_per_launch": kd["bytes"],
+                "launch_ms": round(kd["ms"], 5),
+                "share_of_iteration": {k_: round(v_, 3) for k_, v_ in share.items()},
+                "matvec": {"achieved_gbs": round(32.0 * n / (t_apply / 1e3) / 1e9, 1),
+                           "frac": round(32.0 * n / (t_apply / 1e3) / 1e9 / hbm, 4)}}
+
+    out = {
+        "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+        "data": "synthetic (BASELINE configs[1] point-source problem, built in-process)",
+        "config": _config_dict({"parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                                "iterations": iters, "matvecs": reps[-1].matvec_count,
+                                "final_relres": reps[-1].final_relres,
+                                "time_to_solution_s": round(ms_step / 1e3, 6),
+                                "setup_s": round(t_setup, 3)}),
+        "clocks": clk.summary(),
+        "gpu_launches": int(sum(r.kernel_launches for r in reps)),
+        "e2e": {"value": round(e2e_value, 2), "unit": UNIT,
+                "h2d_bytes_per_step": int(b_host.nbytes), "d2h_bytes_per_step": int(b_host.nbytes),
+                "ms_per_step": round(e2e_step, 4)},
+        "roofline": roofline,
+    }
+    if rank == 0 and not args.no_cpu:
+        out["cpu_baseline"] = cpu_baseline(MAXIT)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def cpu_baseline(iters: int, threads: int | None = None):
+    """The C oracle (a port of the reference algorithm) on this host's cores,
+    OpenMP over all of them, on the same workload: up to `iters` Bi-CGSTAB
+    iterations of the 129^3 solve (the full solve when iters >= its count),
+    reported in the same metric."""
+    from oracle import oracle as O
+    p, spec, b = _problem()
+    k = np.asarray(spec.k_field, dtype=np.float64)
+    t0 = time.perf_counter()
+    _, rep = O.solve(k, b, p.grid.h, bc="sommerfeld", method="bicgstab", tol=TOL, maxit=iters)
+    dt = time.perf_counter() - t0
+    n = p.grid.num_vertices
+    return {"value": round(n * rep["iterations"] / dt / 1e6, 3), "unit": UNIT,
+            "cores": O.num_threads(), "kind": "port",
+            "sample": f"first {rep['iterations']} Bi-CGSTAB iterations of the 129^3 solve "
+                      f"(incl. hierarchy setup), {dt:.2f} s"}
+
+
+def run_reference(args):
+    rank, world, _ = _env_rank()
+    if rank != 0:
+        return
+    vals, samples = [], []
+    for i in range(args.warmup + args.steps):
+        cb = cpu_baseline(args.cpu_iters)
+        if i >= args.warmup:
+            vals.append(cb["value"])
+            samples.append(cb)
+    value = float(np.mean(vals))
+    out = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "impl": "reference",
+           "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+           "config": _config_dict({"parallelism": "host cores (OpenMP)"}),
+           "cpu_baseline": {**samples[-1], "value": round(value, 3)},
+           "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--cpu-iters", type=int, default=20)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -129,10 +129,15 @@ void or_apply_level(const or_level *L, const cplx *u, cplx *v) {
 /* ------------------------------------------------------------------------ */
 /* vector helpers and deterministic dot (partition.py:611-621)               */
 /* ------------------------------------------------------------------------ */
-#define OR_DOT_CHUNKS 256
+#define OR_DOT_CHUNKS_MAX 4096
+static int or_dot_chunks = 256;
+void or_set_dot_chunks(int c) {
+    or_dot_chunks = c < 1 ? 1 : (c > OR_DOT_CHUNKS_MAX ? OR_DOT_CHUNKS_MAX : c);
+}
 
 cplx or_vdot(size_t n, const cplx *a, const cplx *b) {
-    cplx part[OR_DOT_CHUNKS];
+    const int OR_DOT_CHUNKS = or_dot_chunks;
+    cplx part[OR_DOT_CHUNKS_MAX];
     size_t chunk = (n + OR_DOT_CHUNKS - 1) / OR_DOT_CHUNKS;
     #pragma omp parallel for schedule(static)
     for (int c = 0; c < OR_DOT_CHUNKS; c++) {

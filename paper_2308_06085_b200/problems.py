@@ -212,7 +212,7 @@ def random_medium_velocity(shape, seed: int = 2308, corr: float = 0.05) -> np.nd
     ks = [np.fft.fftfreq(n) * (n - 1) for n in shape[:-1]] + [np.fft.rfftfreq(shape[-1]) * (shape[-1] - 1)]
     kx, ky, kz = np.meshgrid(*ks, indexing="ij", sparse=True)
     f *= np.exp(-0.5 * (2 * np.pi * corr) ** 2 * (kx**2 + ky**2 + kz**2))
-    g = np.fft.irfftn(f, s=shape)
+    g = np.fft.irfftn(f, s=shape, axes=(0, 1, 2))
     g = (g - g.mean()) / (g.std() + 1e-300)
     c = 3000.0 + 750.0 * g
     c = np.clip(c, 1500.0, 4500.0)

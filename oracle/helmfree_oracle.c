@@ -666,9 +666,27 @@ void or_hier_stats(const or_hier *H, int *out) {
     out[0] = H->coarsest_calls; out[1] = H->coarsest_iters; out[2] = H->coarsest_fail;
 }
 
+/* Optional exact coarsest solve (row-major dense inverse supplied by the test
+ * harness): the B200 path's coarsest_method="direct".  NULL = reference GMRES. */
+static const cplx *or_coarse_inverse = NULL;
+static size_t or_coarse_n = 0;
+void or_set_coarse_inverse(const cplx *Minv, size_t n) { or_coarse_inverse = Minv; or_coarse_n = n; }
+
 /* multigrid.py:300-323 */
 static void coarsest_solve(or_hier *H, const cplx *b, cplx *x) {
     or_level *L = &H->lev[H->nlev - 1];
+    if (or_coarse_inverse && or_coarse_n == npts(L)) {
+        size_t n = or_coarse_n;
+        #pragma omp parallel for schedule(static)
+        for (size_t i = 0; i < n; i++) {
+            cplx acc = 0.0;
+            const cplx *row = or_coarse_inverse + i * n;
+            for (size_t j = 0; j < n; j++) acc += row[j] * b[j];
+            x[i] = acc;
+        }
+        H->coarsest_calls++;
+        return;
+    }
     or_report rep = {0};
     or_gmres(npts(L), coarse_apply, L, NULL, NULL, b, x, H->coarsest_tol, H->coarsest_maxit, 0,
              1e-30, &rep);

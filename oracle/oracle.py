@@ -69,6 +69,8 @@ def lib():
                                                    _ip, _ip, _ip, _ip, _dp, _dp, ctypes.c_int, _ip])
         L.or_solve.restype = ctypes.c_int
         L.or_num_threads.restype = ctypes.c_int
+        L.or_set_coarse_inverse.argtypes = [_vp, ctypes.c_size_t]
+        L.or_set_dot_chunks.argtypes = [ctypes.c_int]
         _lib = L
     return _lib
 
@@ -217,3 +219,35 @@ def solve(k, b, h, bc="sommerfeld", method="bicgstab", tol=1e-6, maxit=400, rest
         "coarsest_calls": stats[0], "coarsest_iters": stats[1], "coarsest_fail": stats[2],
     }
     return x, report
+
+
+def coarse_matrix(H: "Hierarchy") -> np.ndarray:
+    """Dense matrix of the coarsest-level operator, column by column through the
+    oracle's own matrix-free apply (test helper)."""
+    l = H.nlev - 1
+    shape = H.shapes[l]
+    n = int(np.prod(shape))
+    A = np.empty((n, n), dtype=np.complex128)
+    e = np.zeros(n, dtype=np.complex128)
+    for j in range(n):
+        e[j] = 1.0
+        A[:, j] = H.apply(l, e.reshape(shape)).ravel()
+        e[j] = 0.0
+    return A
+
+
+class exact_coarsest:
+    """Context manager: make the oracle's coarsest solve an exact dense-inverse
+    GEMV (the B200 path's coarsest_method="direct") instead of GMRES."""
+
+    def __init__(self, k, h, bc="sommerfeld", beta2=-0.5, **mg):
+        H = Hierarchy(k, h, beta2=beta2, bc=bc, **mg)
+        self.inv = np.ascontiguousarray(np.linalg.inv(coarse_matrix(H)))
+
+    def __enter__(self):
+        lib().or_set_coarse_inverse(self.inv.ctypes.data, self.inv.shape[0])
+        return self
+
+    def __exit__(self, *exc):
+        lib().or_set_coarse_inverse(None, 0)
+        return False

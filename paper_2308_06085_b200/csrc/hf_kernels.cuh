@@ -5,6 +5,8 @@
 namespace hf {
 
 int march_blocks(const Lvl &L);
+int tile_blocks(const Lvl &L);
+void init_kernel_attributes();
 void launch_apply(const Lvl &L, const cd *u, cd *v, cudaStream_t s, const int *done);
 void launch_apply_dot1(const Lvl &L, const cd *u, cd *v, const cd *w, const RedSlot &rs,
                        cudaStream_t s, const int *done);
@@ -29,6 +31,9 @@ void launch_assemble(const Lvl &L, cd *A, cudaStream_t s);
 void launch_set_identity(long long N, cd *B, cudaStream_t s);
 void launch_zero(long long n, cd *y, cudaStream_t s);
 void launch_axpby(long long n, cd a, const cd *x, cd b, cd *y, cudaStream_t s);
+void launch_mgs(long long n, cd *w, const cd *c, const cd *vprev, const cd *vcur,
+                const RedSlot &rs, cudaStream_t s);
+void launch_multi_axpy(long long n, int m, const cd *const *V, const cd *y, cd *x, cudaStream_t s);
 void launch_dot(long long n, const cd *a, const cd *b, const RedSlot &rs, cudaStream_t s);
 void launch_bcg_init(long long n, const cd *b, cd *r, cd *rs, cd *x, cd *p, cd *v,
                      const RedSlot &red, cudaStream_t s);

@@ -8,7 +8,9 @@
 #include <cusolverDn.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <complex>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -110,6 +112,7 @@ static bool zero_diagonal(const Lvl &L, const double *kfull) {
 static int make_level(Allocs &A, Level &lv, int n1, int n2, int n3, int lo1, int nx, double h,
                       double sre, double sim, int bc, const double *kfull, double kc,
                       bool scratch) {
+    init_kernel_attributes();
     if (n1 < 3 || n2 < 3 || n3 < 3) return fail(HF_ERR_ARG, "grid dims must all be >= 3");
     if (!(h > 0)) return fail(HF_ERR_ARG, "grid spacing must be positive");
     if (lo1 < 0 || nx < 1 || lo1 + nx > n1) return fail(HF_ERR_ARG, "slab outside the grid");
@@ -505,6 +508,14 @@ struct hf_solver {
     cudaGraphExec_t graph = nullptr;
     int graph_kernels = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, evs = nullptr;
+    // GMRES / IDR(s) workspace (allocated on first use)
+    std::vector<cd *> basis;            // Krylov basis V (GMRES) / G, U, P (IDR)
+    cd *w = nullptr, *tmp = nullptr, *tmp2 = nullptr;
+    cd *hcol = nullptr;                 // device Hessenberg column / dot outputs
+    int hcol_cap = 0;
+    cd **vptrs = nullptr;               // device array of basis pointers
+    cd *ycoef = nullptr;
+    int vcap = 0;
     ~hf_solver() {
         if (graph) cudaGraphExecDestroy(graph);
         if (st_host) cudaFreeHost(st_host);
@@ -532,7 +543,7 @@ extern "C" hf_solver *hf_solver_create(hf_operator *Aop, hf_hierarchy *M) {
         if (!*pv) { fail(HF_ERR_CUDA, "cudaMalloc solver vectors"); delete S; return nullptr; }
     }
     S->st = S->A.get<BcgState>(1, e);
-    size_t nblk = std::max<size_t>(march_blocks(L), VEC_BLOCKS_HOST);
+    size_t nblk = std::max<size_t>(std::max(march_blocks(L), tile_blocks(L)), VEC_BLOCKS_HOST);
     if (!S->st || S->red.init(S->A, nblk + 64)) {
         fail(HF_ERR_CUDA, "cudaMalloc solver state");
         delete S;
@@ -644,6 +655,320 @@ static int solve_bicgstab(hf_solver *S, const hf_solver_config *cfg, const cd *b
     return 0;
 }
 
+
+// ---------------------------------------------------------------------------
+// host-driven Krylov loops with device vectors: GMRES (krylov.py:111-192) and
+// IDR(s) (krylov.py:292-394).  Inner products are deterministic device
+// reductions read back per use; the small dense work (Givens rotations, the
+// s x s projection solves) runs on the host exactly as in the reference.
+// ---------------------------------------------------------------------------
+typedef std::complex<double> hcd;
+
+static cd *ws_vec(hf_solver *S) {
+    cudaError_t e;
+    return new_field(S->A, S->Aop->lv.L.nx, S->Aop->lv.L.plane, e);
+}
+
+static int ensure_ws(hf_solver *S, int nbasis, int hcap) {
+    if (!S->w) {
+        S->w = ws_vec(S); S->tmp = ws_vec(S); S->tmp2 = ws_vec(S);
+        if (!S->w || !S->tmp || !S->tmp2) return fail(HF_ERR_CUDA, "cudaMalloc Krylov workspace");
+    }
+    while ((int)S->basis.size() < nbasis) {
+        cd *v = ws_vec(S);
+        if (!v) return fail(HF_ERR_CUDA, "cudaMalloc Krylov basis");
+        S->basis.push_back(v);
+    }
+    if (S->hcol_cap < hcap) {
+        cudaError_t e;
+        S->hcol = S->A.get<cd>(hcap, e);
+        S->ycoef = S->A.get<cd>(hcap, e);
+        S->vptrs = S->A.get<cd *>(hcap, e);
+        if (!S->hcol || !S->ycoef || !S->vptrs) return fail(HF_ERR_CUDA, "cudaMalloc Hessenberg");
+        S->hcol_cap = hcap;
+    }
+    return 0;
+}
+
+static hcd dot_sync(hf_solver *S, const cd *a, const cd *b, cudaStream_t s, long long &launches) {
+    RedSlot rs = S->red.slot(FIN_STORE, nullptr);
+    rs.out = S->hcol;
+    L1(launch_dot(S->n, a, b, rs, s));
+    launches++;
+    cd h;
+    cudaMemcpyAsync(&h, S->hcol, sizeof(cd), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    return hcd(h.x, h.y);
+}
+static double norm_sync(hf_solver *S, const cd *a, cudaStream_t s, long long &launches) {
+    double d = dot_sync(S, a, a, s, launches).real();
+    return std::sqrt(d > 0.0 ? d : 0.0);
+}
+static cd tod(hcd z) { return make_double2(z.real(), z.imag()); }
+static void axpby_h(hf_solver *S, hcd a, const cd *x, hcd b, cd *y, cudaStream_t s, long long &l) {
+    L1(launch_axpby(S->n, tod(a), x, tod(b), y, s));
+    l++;
+}
+
+struct KrylovOut {
+    int matvecs = 0, iters = 0, converged = 0, breakdown = 0;
+    double relres = NAN;
+    std::vector<double> hist;
+    void record(double r) { iters++; relres = r; hist.push_back(r); }
+};
+
+static void apply_A(hf_solver *S, const cd *x, cd *y, cudaStream_t s, KrylovOut &o, long long &l) {
+    L1(launch_apply(S->Aop->lv.L, x, y, s, nullptr));
+    l++;
+    o.matvecs++;
+}
+static void apply_M(hf_solver *S, const cd *x, cd *y, cudaStream_t s, long long &l) {
+    long long before = g_launches;
+    precondition(S->M, x, y, s, nullptr);
+    l += g_launches - before;
+}
+
+// krylov.py:97-108
+static void givens(hcd a, hcd b, double &c, hcd &sn, hcd &r) {
+    double absa = std::abs(a), absb = std::abs(b);
+    if (absb == 0.0) { c = 1.0; sn = 0.0; r = a; return; }
+    if (absa == 0.0) { c = 0.0; sn = std::conj(b) / absb; r = absb; return; }
+    double t = std::hypot(absa, absb);
+    c = absa / t;
+    sn = (a / absa) * (std::conj(b) / t);
+    r = (a / absa) * t;
+}
+
+static int solve_gmres(hf_solver *S, const hf_solver_config *cfg, const cd *b, cd *x, KrylovOut &o,
+                       long long &l) {
+    cudaStream_t s = S->stream;
+    const int maxit = cfg->maxit;
+    const int restart = cfg->restart > 0 ? cfg->restart : maxit;
+    const double btol = cfg->breakdown_tol > 0 ? cfg->breakdown_tol : 1e-30;
+    if (ensure_ws(S, 2, std::min(restart, maxit) + 2)) return HF_ERR_CUDA;
+    const size_t bytes = (size_t)S->n * sizeof(cd);
+    CK(cudaMemsetAsync(x, 0, bytes, s));
+    cd *r0 = S->w;   // r0 shares storage with w (r0 is consumed before w is written)
+    apply_M(S, b, r0, s, l);
+    double denom = norm_sync(S, r0, s, l);
+    if (denom == 0.0) { o.converged = 1; o.relres = 0.0; return 0; }
+    bool first = true;
+    for (;;) {
+        if (!first) {
+            apply_A(S, x, S->tmp, s, o, l);
+            axpby_h(S, 1.0, b, -1.0, S->tmp, s, l);      // tmp = b - A x
+            apply_M(S, S->tmp, r0, s, l);
+        }
+        double beta = norm_sync(S, r0, s, l);
+        if (beta / denom <= cfg->tol) { o.converged = 1; o.relres = beta / denom; return 0; }
+        first = false;
+        axpby_h(S, 1.0 / beta, r0, 0.0, S->basis[0], s, l);
+        std::vector<std::vector<hcd>> H;
+        std::vector<double> cs;
+        std::vector<hcd> sn, g{hcd(beta, 0.0)};
+        bool breakdown = false;
+        while ((int)H.size() < restart && o.iters < maxit) {
+            int m = (int)H.size() + 1;              // basis vectors so far
+            apply_A(S, S->basis[m - 1], S->tmp, s, o, l);
+            apply_M(S, S->tmp, S->w, s, l);
+            // MGS chain: h_i = V_i^H w, w -= h_i V_i, fused pairwise; last pass |w|^2
+            for (int i = 0; i <= m; i++) {
+                RedSlot rs = S->red.slot(FIN_STORE, nullptr);
+                rs.out = S->hcol + i;
+                const cd *c = i > 0 ? S->hcol + (i - 1) : nullptr;
+                const cd *vprev = i > 0 ? S->basis[i - 1] : nullptr;
+                const cd *vcur = i < m ? S->basis[i] : nullptr;
+                L1(launch_mgs(S->n, S->w, c, vprev, vcur, rs, s));
+                l++;
+            }
+            std::vector<cd> hc(m + 1);
+            CK(cudaMemcpyAsync(hc.data(), S->hcol, (m + 1) * sizeof(cd), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            std::vector<hcd> col(m + 1);
+            for (int i = 0; i < m; i++) col[i] = hcd(hc[i].x, hc[i].y);
+            double ww = hc[m].x;
+            double hlast = std::sqrt(ww > 0.0 ? ww : 0.0);
+            col[m] = hlast;
+            for (size_t i = 0; i < cs.size(); i++) {
+                hcd t = cs[i] * col[i] + sn[i] * col[i + 1];
+                col[i + 1] = -std::conj(sn[i]) * col[i] + cs[i] * col[i + 1];
+                col[i] = t;
+            }
+            double c; hcd sv, r;
+            givens(col[m - 1], col[m], c, sv, r);
+            cs.push_back(c); sn.push_back(sv);
+            col[m - 1] = r; col[m] = 0.0;
+            col.resize(m);
+            H.push_back(col);
+            g.push_back(-std::conj(sv) * g.back());
+            g[g.size() - 2] = c * g[g.size() - 2];
+            double relres = std::abs(g.back()) / denom;
+            o.record(relres);
+            if (hlast <= btol) { breakdown = true; break; }
+            if ((int)S->basis.size() < m + 1 && ensure_ws(S, m + 1, m + 2)) return HF_ERR_CUDA;
+            axpby_h(S, 1.0 / hlast, S->w, 0.0, S->basis[m], s, l);
+            if (relres <= cfg->tol) break;
+        }
+        // back substitution (krylov.py:195-204) and x += sum y_i V_i
+        int mh = (int)H.size();
+        std::vector<hcd> y(mh);
+        for (int i = mh - 1; i >= 0; i--) {
+            hcd acc = g[i];
+            for (int j = i + 1; j < mh; j++) acc -= H[j][i] * y[j];
+            y[i] = acc / H[i][i];
+        }
+        if (mh > 0) {
+            std::vector<cd> yd(mh);
+            for (int i = 0; i < mh; i++) yd[i] = tod(y[i]);
+            CK(cudaMemcpyAsync(S->ycoef, yd.data(), mh * sizeof(cd), cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(S->vptrs, S->basis.data(), mh * sizeof(cd *), cudaMemcpyHostToDevice, s));
+            L1(launch_multi_axpy(S->n, mh, S->vptrs, S->ycoef, x, s));
+            l++;
+            CK(cudaStreamSynchronize(s));
+        }
+        double relres = std::abs(g.back()) / denom;
+        if (relres <= cfg->tol) { o.converged = 1; return 0; }
+        if (breakdown) { o.breakdown = HF_BREAKDOWN_ARNOLDI; o.converged = relres <= cfg->tol; return 0; }
+        if (o.iters >= maxit) { o.converged = 0; return 0; }
+    }
+}
+
+// small dense solve with partial pivoting (numpy.linalg.solve equivalent)
+static bool dense_solve(std::vector<hcd> A, int m, std::vector<hcd> &rhs) {
+    for (int c = 0; c < m; c++) {
+        int piv = c;
+        for (int r = c + 1; r < m; r++)
+            if (std::abs(A[r * m + c]) > std::abs(A[piv * m + c])) piv = r;
+        if (std::abs(A[piv * m + c]) == 0.0) return false;
+        if (piv != c) {
+            for (int k = 0; k < m; k++) std::swap(A[c * m + k], A[piv * m + k]);
+            std::swap(rhs[c], rhs[piv]);
+        }
+        for (int r = c + 1; r < m; r++) {
+            hcd f = A[r * m + c] / A[c * m + c];
+            for (int k = c; k < m; k++) A[r * m + k] -= f * A[c * m + k];
+            rhs[r] -= f * rhs[c];
+        }
+    }
+    for (int r = m - 1; r >= 0; r--) {
+        hcd acc = rhs[r];
+        for (int k = r + 1; k < m; k++) acc -= A[r * m + k] * rhs[k];
+        rhs[r] = acc / A[r * m + r];
+    }
+    return true;
+}
+
+static int solve_idrs(hf_solver *S, const hf_solver_config *cfg, const cd *b, cd *x, KrylovOut &o,
+                      long long &l) {
+    cudaStream_t s = S->stream;
+    const int sdim = cfg->s;
+    if (sdim < 1) return fail(HF_ERR_ARG, "IDR requires s >= 1");
+    if (!cfg->shadow_host) return fail(HF_ERR_ARG, "IDR needs the shadow space (shadow_host)");
+    const double btol = cfg->breakdown_tol > 0 ? cfg->breakdown_tol : 1e-30;
+    // basis layout: P[0..s), G[s..2s), U[2s..3s), then r, v, u, vh
+    if (ensure_ws(S, 3 * sdim + 4, 4)) return HF_ERR_CUDA;
+    cd **P = &S->basis[0], **G = &S->basis[sdim], **U = &S->basis[2 * sdim];
+    cd *r = S->basis[3 * sdim], *v = S->basis[3 * sdim + 1], *u = S->basis[3 * sdim + 2];
+    cd *vh = S->basis[3 * sdim + 3], *gv = S->w;
+    const size_t bytes = (size_t)S->n * sizeof(cd);
+    for (int i = 0; i < sdim; i++)
+        CK(cudaMemcpyAsync(P[i], cfg->shadow_host + 2 * (size_t)i * S->n, bytes, cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(x, 0, bytes, s));
+    double bnorm = norm_sync(S, b, s, l);
+    if (bnorm == 0.0) { o.converged = 1; o.relres = 0.0; return 0; }
+    CK(cudaMemcpyAsync(r, b, bytes, cudaMemcpyDeviceToDevice, s));
+    double relres = norm_sync(S, r, s, l) / bnorm;
+    if (relres <= cfg->tol) { o.converged = 1; o.relres = relres; return 0; }
+    for (int i = 0; i < sdim; i++) {
+        CK(cudaMemsetAsync(G[i], 0, bytes, s));
+        CK(cudaMemsetAsync(U[i], 0, bytes, s));
+    }
+    std::vector<hcd> Mm(sdim * sdim, 0.0), f(sdim);
+    for (int i = 0; i < sdim; i++) Mm[i * sdim + i] = 1.0;
+    hcd om = 1.0;
+    const double kappa = 0.7;
+    while (o.iters < cfg->maxit) {
+        for (int i = 0; i < sdim; i++) f[i] = dot_sync(S, P[i], r, s, l);
+        for (int k = 0; k < sdim; k++) {
+            int m = sdim - k;
+            std::vector<hcd> sub(m * m), c(m);
+            for (int a = 0; a < m; a++) {
+                for (int bq = 0; bq < m; bq++) sub[a * m + bq] = Mm[(k + a) * sdim + (k + bq)];
+                c[a] = f[k + a];
+            }
+            if (!dense_solve(sub, m, c)) { o.breakdown = HF_BREAKDOWN_PROJECTION; o.converged = 0; return 0; }
+            CK(cudaMemcpyAsync(v, r, bytes, cudaMemcpyDeviceToDevice, s));
+            for (int i = k; i < sdim; i++) axpby_h(S, -c[i - k], G[i], 1.0, v, s, l);
+            apply_M(S, v, vh, s, l);
+            axpby_h(S, om, vh, 0.0, u, s, l);
+            for (int i = k; i < sdim; i++) axpby_h(S, c[i - k], U[i], 1.0, u, s, l);
+            apply_A(S, u, gv, s, o, l);
+            for (int i = 0; i < k; i++) {
+                hcd alpha = dot_sync(S, P[i], gv, s, l) / Mm[i * sdim + i];
+                axpby_h(S, -alpha, G[i], 1.0, gv, s, l);
+                axpby_h(S, -alpha, U[i], 1.0, u, s, l);
+            }
+            CK(cudaMemcpyAsync(G[k], gv, bytes, cudaMemcpyDeviceToDevice, s));
+            CK(cudaMemcpyAsync(U[k], u, bytes, cudaMemcpyDeviceToDevice, s));
+            for (int i = k; i < sdim; i++) Mm[i * sdim + k] = dot_sync(S, P[i], G[k], s, l);
+            if (std::abs(Mm[k * sdim + k]) < btol) { o.breakdown = HF_BREAKDOWN_PROJECTION; o.converged = 0; return 0; }
+            hcd beta = f[k] / Mm[k * sdim + k];
+            axpby_h(S, -beta, G[k], 1.0, r, s, l);
+            axpby_h(S, beta, U[k], 1.0, x, s, l);
+            relres = norm_sync(S, r, s, l) / bnorm;
+            o.record(relres);
+            if (relres <= cfg->tol || o.iters >= cfg->maxit) break;
+            for (int i = k + 1; i < sdim; i++) f[i] = f[i] - beta * Mm[i * sdim + k];
+        }
+        if (relres <= cfg->tol) { o.converged = 1; return 0; }
+        if (o.iters >= cfg->maxit) break;
+        apply_M(S, r, vh, s, l);
+        apply_A(S, vh, gv, s, o, l);
+        hcd tt = dot_sync(S, gv, gv, s, l);
+        if (std::abs(tt) < btol) { o.breakdown = HF_BREAKDOWN_OMEGA; break; }
+        hcd tr = dot_sync(S, gv, r, s, l);
+        om = tr / tt;
+        double angle = std::abs(dot_sync(S, gv, r, s, l)) / (std::sqrt(std::abs(tt)) * norm_sync(S, r, s, l));
+        if (angle < kappa) om = om * (kappa / angle);
+        if (std::abs(om) < btol) { o.breakdown = HF_BREAKDOWN_OMEGA; break; }
+        axpby_h(S, om, vh, 1.0, x, s, l);
+        axpby_h(S, -om, gv, 1.0, r, s, l);
+        relres = norm_sync(S, r, s, l) / bnorm;
+        o.record(relres);
+        if (relres <= cfg->tol) { o.converged = 1; return 0; }
+    }
+    o.converged = relres <= cfg->tol;
+    return 0;
+}
+
+static int solve_hostloop(hf_solver *S, const hf_solver_config *cfg, const cd *b, cd *x,
+                          hf_report *rep) {
+    cudaStream_t s = S->stream;
+    KrylovOut o;
+    long long launches = 0;
+    CK(cudaEventRecord(S->ev0, s));
+    int rc = cfg->method == HF_METHOD_GMRES ? solve_gmres(S, cfg, b, x, o, launches)
+                                            : solve_idrs(S, cfg, b, x, o, launches);
+    if (rc) return rc;
+    CK(cudaEventRecord(S->ev1, s));
+    CK(cudaStreamSynchronize(s));
+    CKL();
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, S->ev0, S->ev1);
+    rep->matvec_count = o.matvecs;
+    rep->iterations = o.iters;
+    rep->converged = o.converged;
+    rep->breakdown = o.breakdown;
+    rep->final_relres = o.relres;
+    rep->solve_ms = ms;
+    rep->kernel_launches = (int)launches;
+    rep->coarsest_flags = 0;
+    if (rep->history_host)
+        for (int i = 0; i < std::min<int>((int)o.hist.size(), rep->history_cap); i++)
+            rep->history_host[i] = o.hist[i];
+    return 0;
+}
+
 extern "C" int hf_solve(hf_solver *S, const hf_solver_config *cfg, const double *b, double *x,
                         hf_report *rep) {
     if (!S || !cfg || !b || !x || !rep) return fail(HF_ERR_ARG, "null argument");
@@ -656,8 +981,12 @@ extern "C" int hf_solve(hf_solver *S, const hf_solver_config *cfg, const double 
     case HF_METHOD_BICGSTAB:
         rc = solve_bicgstab(S, cfg, (const cd *)b, (cd *)x, rep);
         break;
+    case HF_METHOD_GMRES:
+    case HF_METHOD_IDRS:
+        rc = solve_hostloop(S, cfg, (const cd *)b, (cd *)x, rep);
+        break;
     default:
-        return fail(HF_ERR_UNSUPPORTED, "Krylov method not built into this library yet");
+        return fail(HF_ERR_ARG, "unknown Krylov method");
     }
     if (rc) return rc;
     CK(cudaEventRecord(S->evs, S->stream));

@@ -105,7 +105,10 @@ class Solver:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
-            _native.load().hf_solver_destroy(h)
+            try:
+                _native.load().hf_solver_destroy(h)
+            except Exception:   # interpreter shutdown
+                pass
             self._h = None
 
     def _config(self, cfg: SolverConfig, shadow):

@@ -82,7 +82,10 @@ class MGHierarchy:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
-            _native.load().hf_hierarchy_destroy(h)
+            try:
+                _native.load().hf_hierarchy_destroy(h)
+            except Exception:   # interpreter shutdown
+                pass
             self._h = None
 
     @property

@@ -187,7 +187,10 @@ class StencilOperator:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
-            _native.load().hf_operator_destroy(h)
+            try:
+                _native.load().hf_operator_destroy(h)
+            except Exception:   # interpreter shutdown
+                pass
             self._h = None
 
     @property

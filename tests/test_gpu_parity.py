@@ -170,3 +170,35 @@ def test_solve_host_buffers(hf, oracle):
     xh, r2 = S.solve(b, cfg, host=True)
     assert r1.iterations == r2.iterations
     np.testing.assert_array_equal(xd.cpu().numpy(), xh)
+
+
+@pytest.mark.filterwarnings("ignore:kh =")
+@pytest.mark.parametrize("method", ["gmres", "bicgstab", "idrs"])
+def test_closed_off_methods_match_oracle(hf, oracle, method):
+    """Reference demo_convergence problem (ClosedOff 33^3, k=20, Dirichlet u=1):
+    all three Krylov methods, native vs oracle (reference counts 27/44/34)."""
+    from paper_2308_06085_b200 import problems
+    p = problems.closed_off_problem(33, 20.0)
+    x, rep, xo, ro = _solve_pair(hf, oracle, p, np.full(p.grid.shape, 20.0), method=method)
+    assert rep.converged and ro["converged"]
+    assert abs(rep.iterations - ro["iterations"]) <= 1
+    assert abs(rep.matvec_count - ro["matvec_count"]) <= 2
+    assert np.linalg.norm(x - xo) / np.linalg.norm(xo) < 1e-8
+    if method == "gmres":
+        hist = np.array(rep.residual_history)
+        assert np.all(hist[1:] <= hist[:-1] * (1 + 1e-12))     # monotone (krylov.py:349)
+
+
+def test_gmres_restart(hf, oracle):
+    from paper_2308_06085_b200 import problems
+    p = problems.point_source_cube(33, 20.0, "sommerfeld")
+    x, rep, xo, ro = _solve_pair(hf, oracle, p, np.full(p.grid.shape, 20.0), method="gmres")
+    from paper_2308_06085_b200.krylov import Solver, SolverConfig
+    from paper_2308_06085_b200.multigrid import MGConfig, build_hierarchy
+    from paper_2308_06085_b200.operators import OperatorSpec, StencilOperator
+    spec, b = problems.build_problem(p)
+    A = StencilOperator(spec, p.grid)
+    hier = build_hierarchy(p.grid, None, OperatorSpec("cslp", 1.0, -0.5, spec.bc, spec.k_field), MGConfig())
+    xr, rr = Solver(A, hier).solve(b, SolverConfig(method="gmres", restart=5, maxit=200))
+    assert rr.converged
+    assert np.linalg.norm(xr.cpu().numpy() - xo) / np.linalg.norm(xo) < 1e-5

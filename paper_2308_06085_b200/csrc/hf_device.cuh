@@ -2,10 +2,8 @@
 //
 // Layout: complex128 fields as double2, shape (nx, n2, n3) C order (i3
 // fastest), slab along i1 with HF_GHOST ghost planes before/after the owned
-// planes.  Kernels march along i1 (the slow axis): one thread per (i2, i3)
-// column, so the i1 +-1 neighbours are re-read by the same thread one step
-// later (L1 hits) and the i2/i3 neighbours come from the rows the
-// neighbouring lanes just loaded.
+// planes.  Helpers for complex arithmetic, the per-level stencil description,
+// the boundary-row coefficients and deterministic block reductions.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -44,6 +42,7 @@ struct Lvl {
     int bc;              // HF_BC_*
     const double *k;     // wavenumber at owned plane 0 (ghost planes valid), or null
     double kc;           // constant wavenumber when k == null
+    const double2 *wd;   // w D^-1 at owned plane 0 (hierarchy levels of a varying medium)
 };
 
 __device__ __forceinline__ double kat(const Lvl &L, long long q) {
@@ -69,47 +68,6 @@ __device__ __forceinline__ cd diag_of(const Lvl &L, double kk, int nb) {
     if (L.bc == HF_BC_DIRICHLET && nb) return mk(1.0, 0.0);
     return ap_of(L, kk, nb);
 }
-
-// Generic 7-point row (operators.py:200-254) with values supplied by `val(i,j,m)`
-// at local plane i (may be a ghost plane), row j, column m.  Sommerfeld ghost
-// elimination == mirror the inward neighbour into the missing one.
-template <class V>
-__device__ __forceinline__ cd stencil_row(const Lvl &L, int i, int j, int m, cd uc, double kk,
-                                          const V &val) {
-    const int gi = L.lo1 + i;
-    const bool bxl = gi == 0, bxh = gi == L.n1 - 1;
-    const bool byl = j == 0, byh = j == L.n2 - 1;
-    const bool bzl = m == 0, bzh = m == L.n3 - 1;
-    const int nb = (int)bxl + bxh + byl + byh + bzl + bzh;
-    if (L.bc == HF_BC_DIRICHLET && nb) return uc;
-    cd xm = bxl ? mk(0, 0) : val(i - 1, j, m);
-    cd xp = bxh ? mk(0, 0) : val(i + 1, j, m);
-    cd ym = byl ? mk(0, 0) : val(i, j - 1, m);
-    cd yp = byh ? mk(0, 0) : val(i, j + 1, m);
-    cd zm = bzl ? mk(0, 0) : val(i, j, m - 1);
-    cd zp = bzh ? mk(0, 0) : val(i, j, m + 1);
-    if (bxl) xm = xp;
-    if (bxh) xp = xm;
-    if (byl) ym = yp;
-    if (byh) yp = ym;
-    if (bzl) zm = zp;
-    if (bzh) zp = zm;
-    cd s = cadd(cadd(cadd(xm, xp), cadd(ym, yp)), cadd(zm, zp));
-    cd a = ap_of(L, kk, nb);
-    cd v = cmul(a, uc);
-    v.x -= L.ih2 * s.x;
-    v.y -= L.ih2 * s.y;
-    return v;
-}
-
-struct LoadField {
-    const cd *u;
-    long long plane;
-    int n3;
-    __device__ __forceinline__ cd operator()(int i, int j, int m) const {
-        return __ldg(u + (long long)i * plane + (long long)j * n3 + m);
-    }
-};
 
 // ---------------------------------------------------------------------------
 // deterministic reductions: per-block partials + last-block finalize

@@ -11,6 +11,7 @@
 // deterministic last-block reduction that also advances the Bi-CGSTAB scalars
 // on the device (krylov.py:207-276).
 #include <algorithm>
+#include <cstdlib>
 
 #include "hf_kernels.cuh"
 
@@ -106,116 +107,53 @@ __device__ __forceinline__ ColCtx col_ctx(const Lvl &L, int chunk) {
 }
 
 // ---------------------------------------------------------------------------
-// shared-memory 2.5D tiled stencil kernels
+// stencil kernels: cp.async plane ring + 2.5D tiles
 //
-// A block owns a TX x TY tile of (i3, i2) columns and marches along i1 over a
-// chunk of planes.  For each plane the block evaluates the stencil input f
-// ONCE per point (tile + 1-point halo) into a 3-plane rolling shared-memory
-// window; each thread then forms M f from shared memory.  f is a functor:
-// a plain load (matvec / residual / Jacobi), the zero-guess pre-smoothed
-// iterate w D^-1 b (fused pre-smooth + residual), or w D^-1 b + P e (fused
-// prolongation + correction + post-smooth).  The epilogue consumes (f, M f).
+// A block owns a 32 x 8 tile of (i3, i2) columns and marches along i1 over a
+// chunk of planes.  Each plane's tile + 1-point halo of the stencil operand is
+// copied global->shared with cp.async into a 5-slot ring, three planes ahead
+// of the plane being computed, so one barrier per plane is enough and the
+// 7-point row reads its six neighbours straight from the ring.  Epilogue
+// operands (b, the inner-product partner w, the centre wavenumber) are staged
+// for the centre only.  Two stencil inputs:
+//   MODE_LOAD  f = u                      (A u, b - M u, Jacobi sweep)
+//   MODE_PRE   f = w D^-1 b, zero-guess pre-smoothing folded into the
+//              residual (multigrid.py:148-151 + 383-386): in the deep
+//              interior of a constant medium w D^-1 is one constant and
+//              M (c b) = c M b; elsewhere each neighbour is scaled by its own
+//              w D^-1 (boundary-count formula, or the level's precomputed
+//              w D^-1 field when k varies).
 // ---------------------------------------------------------------------------
 #define TILE_X 32
 #define TILE_Y 8
 #define HALO_X (TILE_X + 2)
 #define HALO_Y (TILE_Y + 2)
+#define NFILL (HALO_Y * HALO_X)
+#define NT (TILE_X * TILE_Y)
+#define RING 5
 
-// v = a f - h^-2 sum(neighbours), neighbours already mirrored for Sommerfeld
-__device__ __forceinline__ cd stencil_nb(const Lvl &L, int gi, int j, int m, cd fc, double kk,
-                                         cd xm, cd xp, cd ym, cd yp, cd zm, cd zp, int &nb) {
-    const bool bxl = gi == 0, bxh = gi == L.n1 - 1;
-    const bool byl = j == 0, byh = j == L.n2 - 1;
-    const bool bzl = m == 0, bzh = m == L.n3 - 1;
-    nb = (int)bxl + bxh + byl + byh + bzl + bzh;
-    if (L.bc == HF_BC_DIRICHLET && nb) return fc;
-    if (bxl) xm = xp;
-    if (bxh) xp = xm;
-    if (byl) ym = yp;
-    if (byh) yp = ym;
-    if (bzl) zm = zp;
-    if (bzh) zp = zm;
-    cd s = cadd(cadd(cadd(xm, xp), cadd(ym, yp)), cadd(zm, zp));
-    cd a = ap_of(L, kk, nb);
-    cd v = cmul(a, fc);
-    v.x -= L.ih2 * s.x;
-    v.y -= L.ih2 * s.y;
-    return v;
+enum { MODE_LOAD = 0, MODE_PRE = 1 };
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem, bool valid) {
+    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    int sz = valid ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
 }
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem, bool valid) {
+    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    int sz = valid ? 8 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-// stencil inputs --------------------------------------------------------------
-struct ProdLoad {
-    const cd *u;
-    long long plane;
-    int n3;
-    __device__ __forceinline__ cd operator()(const Lvl &, int i, int j, int m) const {
-        return __ldg(u + (long long)i * plane + (long long)j * n3 + m);
-    }
-};
-
-// zero-guess pre-smoothed iterate w D^-1 b (multigrid.py:148-151)
-struct ProdPre {
-    const cd *b;
-    double omega;
-    __device__ __forceinline__ cd operator()(const Lvl &L, int i, int j, int m) const {
-        long long q = (long long)i * L.plane + (long long)j * L.n3 + m;
-        cd d = diag_of(L, kat(L, q), nbnd(L, L.lo1 + i, j, m));
-        return cscal(cdiv(__ldg(b + q), d), omega);
-    }
-};
-
-// trilinear prolongation value at fine local (i, j, m) (multigrid.py:238-297);
-// the reference divides the 2/4/8-point sums, exact here as a power-of-two scale
-struct Prolong {
-    Lvl C;
-    const cd *e;   // coarse field, owned plane 0
-    __device__ __forceinline__ cd operator()(const Lvl &F, int i, int j, int m) const {
-        int gi = F.lo1 + i;
-        int c1 = (gi >> 1) - C.lo1, e1 = (gi & 1) ? 2 : 1;
-        int c2 = j >> 1, e2 = (j & 1) ? 2 : 1;
-        int c3 = m >> 1, e3 = (m & 1) ? 2 : 1;
-        const cd *p = e + (long long)c1 * C.plane + (long long)c2 * C.n3 + c3;
-        cd acc = __ldg(p);
-        if (e3 == 2) acc = cadd(acc, __ldg(p + 1));
-        if (e2 == 2) {
-            acc = cadd(acc, __ldg(p + C.n3));
-            if (e3 == 2) acc = cadd(acc, __ldg(p + C.n3 + 1));
-        }
-        if (e1 == 2) {
-            const cd *p1 = p + C.plane;
-            acc = cadd(acc, __ldg(p1));
-            if (e3 == 2) acc = cadd(acc, __ldg(p1 + 1));
-            if (e2 == 2) {
-                acc = cadd(acc, __ldg(p1 + C.n3));
-                if (e3 == 2) acc = cadd(acc, __ldg(p1 + C.n3 + 1));
-            }
-        }
-        int ns = e1 * e2 * e3;
-        if (ns > 1) acc = cscal(acc, 1.0 / ns);
-        return acc;
-    }
-};
-
-// w D^-1 b + P e (PRE=1) or P e (PRE=0): iterate after pre-smoothing from zero
-// and the coarse-grid correction (multigrid.py:337-341)
-template <int PRE>
-struct ProdCorr {
-    ProdPre S;
-    Prolong P;
-    __device__ __forceinline__ cd operator()(const Lvl &L, int i, int j, int m) const {
-        cd pe = P(L, i, j, m);
-        if (PRE) return cadd(S(L, i, j, m), pe);
-        return pe;
-    }
-};
-
-// epilogues --------------------------------------------------------------------
-// called as epi(q, f_centre, (M f)_centre, w D^-1_centre, staged operand, acc)
+// epilogues: epi(q, f_centre, (M f)_centre, w D^-1 at the centre, staged operand, acc)
 // v = M f (+ inner products), DOT: 0 none, 1 conj(w) v, 2 conj(v) v & conj(v) w
 template <int DOT>
 struct EpiApply {
     cd *v;
-    static constexpr bool kAux = DOT > 0;   // w is staged as the aux field
+    static constexpr bool kAux = DOT > 0;   // w
     static constexpr bool kDinv = false;
     __device__ __forceinline__ void operator()(long long q, cd, cd mf, cd, cd aux,
                                                cd (&acc)[2]) const {
@@ -238,89 +176,31 @@ struct EpiResid {
     }
 };
 
-// u = f + w D^-1 (b - M f) (one damped Jacobi sweep on f, multigrid.py:153-156)
+// u = f + w D^-1 (b - M f) (one damped Jacobi sweep, multigrid.py:153-156)
 struct EpiJacobi {
     cd *u;
     static constexpr bool kAux = true;      // b
     static constexpr bool kDinv = true;
     __device__ __forceinline__ void operator()(long long q, cd fc, cd mf, cd wd, cd b,
                                                cd (&)[2]) const {
-        cd upd = cmul(wd, csub(b, mf));
-        u[q] = cadd(fc, upd);
+        u[q] = cadd(fc, cmul(wd, csub(b, mf)));
     }
 };
-
-// ---------------------------------------------------------------------------
-// cp.async-pipelined tiled stencil kernel (instruction-lean)
-//
-// Raw inputs of plane i+2 and i+3 (the stencil field or right-hand side, the
-// wavenumber when it varies, the epilogue operand, and the two coarse planes
-// the prolongation reads) are in flight global->shared (cp.async) while plane
-// i is computed.  For each plane the block evaluates the stencil input f ONCE
-// per point of the tile + 1-point halo into a 3-plane window; every thread
-// then forms the 7-point row M f from shared memory.  Per-thread fill
-// metadata (shared-memory slots, 32-bit in-plane offsets, boundary counts,
-// prolongation taps) is computed once per block, and for a constant medium
-// the stencil centre a_p and w D^-1 come from a 4-entry table indexed by the
-// number of physical faces (no FP64 division in the loop).
-// ---------------------------------------------------------------------------
-#define PIPE_S 4
-#define PIPE_MASK 3
-#define CT_Y (TILE_Y / 2 + 2)
-#define CT_X (TILE_X / 2 + 2)
-#define NFILL (HALO_Y * HALO_X)
-#define NCOARSE (2 * CT_Y * CT_X)
-
-enum { MODE_LOAD = 0, MODE_PRE = 1, MODE_CORR1 = 2, MODE_CORR0 = 3 };
-
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem, bool valid) {
-    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    int sz = valid ? 16 : 0;
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
-}
-__device__ __forceinline__ void cp_async8(void *smem, const void *gmem, bool valid) {
-    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    int sz = valid ? 8 : 0;
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 template <int MODE, bool KVAR, bool AUX>
 struct StencilSmem {
-    static constexpr bool kCoarse = MODE == MODE_CORR1 || MODE == MODE_CORR0;
-    static constexpr bool kAuxArr = AUX && MODE == MODE_LOAD;
-    cd f[3][NFILL];                              // stencil input window
-    cd raw[PIPE_S][NFILL];                       // field / rhs planes (tile + halo)
-    double kr[KVAR ? PIPE_S : 1][NFILL];         // wavenumber planes
-    cd cr[kCoarse ? PIPE_S : 1][NCOARSE];        // coarse planes for the prolongation
-    cd ax[kAuxArr ? PIPE_S : 1][TILE_Y * TILE_X];   // epilogue operand, centre only
+    static constexpr bool kWd = MODE == MODE_PRE && KVAR;     // staged w D^-1 field
+    static constexpr bool kAuxArr = AUX && MODE == MODE_LOAD; // PRE reuses the ring centre as b
+    cd raw[RING][NFILL];
+    cd wd[kWd ? RING : 1][kWd ? NFILL : 1];
+    double kc[KVAR ? RING : 1][NT];
+    cd ax[kAuxArr ? RING : 1][kAuxArr ? NT : 1];
 };
 
-// per-thread fill entry: halo point e of the tile
-struct FillEnt {
-    int go;        // in-plane global offset j*n3 + m
-    int nbjm;      // physical faces touched in i2 / i3
-    int co;        // prolongation: coarse tap offset in the staged coarse plane
-    int e23;       // prolongation: bit0 = i3 odd, bit1 = i2 odd
-    bool ok;       // inside the grid in i2 / i3
-};
-
-// 4-entry register table indexed by the boundary-face count (no local memory)
-struct Tab4 {
-    cd t0, t1, t2, t3;
-    __device__ __forceinline__ cd operator[](int nb) const {
-        return nb == 0 ? t0 : (nb == 1 ? t1 : (nb == 2 ? t2 : t3));
-    }
-};
-
-template <int MODE, class Epi, int ND, bool KVAR>
-__global__ void __launch_bounds__(TILE_X *TILE_Y) k_stencil(Lvl L, Lvl C, const cd *__restrict__ src,
-                                                           const cd *__restrict__ ec,
-                                                           const cd *__restrict__ aux, double omega,
-                                                           Epi epi, int chunk, RedSlot rs,
-                                                           const int *done) {
+template <int MODE, class Epi, int ND, bool KVAR, bool SOMM>
+__global__ void __launch_bounds__(NT) k_stencil(Lvl L, const cd *__restrict__ src,
+                                                const cd *__restrict__ aux, double omega, Epi epi,
+                                                int chunk, RedSlot rs, const int *done) {
     using SM = StencilSmem<MODE, KVAR, Epi::kAux>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SM &sm = *reinterpret_cast<SM *>(smem_raw);
@@ -330,192 +210,135 @@ __global__ void __launch_bounds__(TILE_X *TILE_Y) k_stencil(Lvl L, Lvl C, const 
     const int i0 = blockIdx.z * chunk, i1 = min(i0 + chunk, L.nx);
     const int m = m0 + tx, j = j0 + ty;
     const bool act = m < L.n3 && j < L.n2;
-    const int cj0 = (j0 - 1) >> 1, cm0 = (m0 - 1) >> 1;   // coarse tile origin (floor)
+    const cd one = mk(1.0, 0.0);
 
-    // ---- per-thread metadata (once per block) ----
-    FillEnt fe[2];
-    const bool has1 = tid + TILE_X * TILE_Y < NFILL;
-#pragma unroll
-    for (int k = 0; k < 2; k++) {
-        int e = tid + k * TILE_X * TILE_Y;
-        int hy = e / HALO_X, hx = e - hy * HALO_X;
+    // fill entries of this thread: e0 = tid, e1 = tid + NT (when < NFILL)
+    const bool has1 = tid + NT < NFILL;
+    int go0, go1;
+    bool ok0, ok1;
+    {
+        int hy = tid / HALO_X, hx = tid - hy * HALO_X;
         int jj = j0 - 1 + hy, mm = m0 - 1 + hx;
-        fe[k].ok = jj >= 0 && jj < L.n2 && mm >= 0 && mm < L.n3;
-        fe[k].go = jj * L.n3 + mm;
-        fe[k].nbjm = (jj == 0) + (jj == L.n2 - 1) + (mm == 0) + (mm == L.n3 - 1);
-        fe[k].co = ((jj >> 1) - cj0) * CT_X + ((mm >> 1) - cm0);
-        fe[k].e23 = (mm & 1) | ((jj & 1) << 1);
+        ok0 = jj >= 0 && jj < L.n2 && mm >= 0 && mm < L.n3;
+        go0 = ok0 ? jj * L.n3 + mm : 0;
+        int e = tid + NT;
+        hy = e / HALO_X; hx = e - hy * HALO_X;
+        jj = j0 - 1 + hy; mm = m0 - 1 + hx;
+        ok1 = has1 && jj >= 0 && jj < L.n2 && mm >= 0 && mm < L.n3;
+        go1 = ok1 ? jj * L.n3 + mm : 0;
     }
-    // coarse staging entry of this thread
-    const bool hasc = SM::kCoarse && tid < NCOARSE;
-    int cgo = 0, cplane = 0;
-    bool cok = false;
-    if (hasc) {
-        cplane = tid / (CT_Y * CT_X);
-        int r = tid - cplane * (CT_Y * CT_X);
-        int cy = r / CT_X, cx = r - cy * CT_X;
-        int cj = cj0 + cy, cm = cm0 + cx;
-        cok = cj >= 0 && cj < C.n2 && cm >= 0 && cm < C.n3;
-        cgo = cj * C.n3 + cm;
-    }
-    // centre of this thread
-    const int cfill = (ty + 1) * HALO_X + (tx + 1);
-    const int nbjm_c = (j == 0) + (j == L.n2 - 1) + (m == 0) + (m == L.n3 - 1);
-    const bool byl = j == 0, byh = j == L.n2 - 1, bzl = m == 0, bzh = m == L.n3 - 1;
-    // constant medium: a_p and w D^-1 by boundary-face count
-    Tab4 apt{}, wdt{};
+    const int own = j * L.n3 + m;
+    const int cf = (ty + 1) * HALO_X + (tx + 1);
+    const int nbjm = (j == 0) + (j == L.n2 - 1) + (m == 0) + (m == L.n3 - 1);
+    const bool deep_jm = j >= 2 && j <= L.n2 - 3 && m >= 2 && m <= L.n3 - 3;
+    // constant medium: a_p and w D^-1 by physical-face count (0..3) in shared memory
+    __shared__ cd tab[8];
+    cd ap0 = mk(0, 0), wd0 = mk(0, 0);
     if (!KVAR) {
-        auto wdinv = [&](int nb) { return cscal(cdiv(mk(1.0, 0.0), diag_of(L, L.kc, nb)), omega); };
-        apt = Tab4{ap_of(L, L.kc, 0), ap_of(L, L.kc, 1), ap_of(L, L.kc, 2), ap_of(L, L.kc, 3)};
-        wdt = Tab4{wdinv(0), wdinv(1), wdinv(2), wdinv(3)};
+        ap0 = ap_of(L, L.kc, 0);
+        wd0 = cscal(cdiv(one, diag_of(L, L.kc, 0)), omega);
+        if (tid < 4) {
+            tab[tid] = ap_of(L, L.kc, tid);
+            tab[4 + tid] = cscal(cdiv(one, diag_of(L, L.kc, tid)), omega);
+        }
     }
+    auto wd_nb = [&](int nb) -> cd { return tab[4 + nb]; };   // read after the first barrier
     cd acc[2] = {mk(0, 0), mk(0, 0)};
 
-    int stage_slot = 0, prod_slot = 0;
-    // issue the raw copies of plane i (one commit group per call)
-    auto stage = [&](int i) {
-        const int slot = stage_slot;
-        stage_slot = (stage_slot + 1) & PIPE_MASK;
+    int sslot = 0;
+    auto stage = [&](int i) {              // one commit group per plane
+        const int slot = sslot;
+        sslot = sslot == RING - 1 ? 0 : sslot + 1;
         const int gi = L.lo1 + i;
         const bool pok = i <= i1 && gi >= 0 && gi < L.n1;
-        const long long pbase = (long long)i * L.plane;
-#pragma unroll
-        for (int k = 0; k < 2; k++) {
-            if (k == 1 && !has1) break;
-            const int e = tid + k * TILE_X * TILE_Y;
-            const bool ok = pok && fe[k].ok;
-            cp_async16(&sm.raw[slot][e], ok ? src + pbase + fe[k].go : src, ok);
-            if (KVAR) cp_async8(&sm.kr[slot & (KVAR ? PIPE_MASK : 0)][e], ok ? L.k + pbase + fe[k].go : L.k, ok);
+        const long long pb = (long long)i * L.plane;
+        bool v = pok && ok0;
+        cp_async16(&sm.raw[slot][tid], v ? src + pb + go0 : src, v);
+        if (SM::kWd) cp_async16(&sm.wd[SM::kWd ? slot : 0][tid], v ? L.wd + pb + go0 : L.wd, v);
+        if (has1) {
+            v = pok && ok1;
+            cp_async16(&sm.raw[slot][tid + NT], v ? src + pb + go1 : src, v);
+            if (SM::kWd) cp_async16(&sm.wd[SM::kWd ? slot : 0][tid + NT], v ? L.wd + pb + go1 : L.wd, v);
         }
-        if (SM::kAuxArr) {
-            const bool ok = pok && act && i < i1;
-            cp_async16(&sm.ax[slot & (SM::kAuxArr ? PIPE_MASK : 0)][tid],
-                       ok ? aux + pbase + j * L.n3 + m : aux, ok);
-        }
-        if (hasc) {
-            const int c1 = (gi >> 1) - C.lo1 + cplane;     // local coarse plane
-            const int cg = C.lo1 + c1;
-            const bool ok = pok && cok && cg >= 0 && cg < C.n1;
-            cp_async16(&sm.cr[slot & (SM::kCoarse ? PIPE_MASK : 0)][tid],
-                       ok ? ec + (long long)c1 * C.plane + cgo : ec, ok);
-        }
+        const bool vc = pok && act && i < i1;
+        if (KVAR) cp_async8(&sm.kc[KVAR ? slot : 0][tid], vc ? L.k + pb + own : L.k, vc);
+        if (SM::kAuxArr) cp_async16(&sm.ax[SM::kAuxArr ? slot : 0][tid], vc ? aux + pb + own : aux, vc);
         cp_commit();
     };
 
-    // stencil input f at plane i from its staged raw data, into window w
-    auto produce = [&](int i, int w) {
-        const int slot = prod_slot;
-        prod_slot = (prod_slot + 1) & PIPE_MASK;
-        const int gi = L.lo1 + i;
-        const bool pok = gi >= 0 && gi < L.n1;
-        const int nbi = (gi == 0) + (gi == L.n1 - 1);
-        const bool xodd = gi & 1;
-#pragma unroll
-        for (int k = 0; k < 2; k++) {
-            if (k == 1 && !has1) break;
-            const int e = tid + k * TILE_X * TILE_Y;
-            cd v = mk(0, 0);
-            if (pok && fe[k].ok) {
-                const cd rv = sm.raw[slot][e];
-                if (MODE == MODE_LOAD) {
-                    v = rv;
-                } else {
-                    if (MODE == MODE_PRE || MODE == MODE_CORR1) {
-                        const int nb = nbi + fe[k].nbjm;
-                        cd wd;
-                        if (KVAR) wd = cscal(cdiv(mk(1.0, 0.0), diag_of(L, sm.kr[slot & (KVAR ? PIPE_MASK : 0)][e], nb)), omega);
-                        else wd = wdt[nb];
-                        v = cmul(rv, wd);
-                    }
-                    if (SM::kCoarse) {
-                        const cd *cp = sm.cr[slot & (SM::kCoarse ? PIPE_MASK : 0)];
-                        const int co = fe[k].co;
-                        const bool e3 = fe[k].e23 & 1, e2 = fe[k].e23 & 2;
-                        cd a = cp[co];
-                        if (e3) a = cadd(a, cp[co + 1]);
-                        if (e2) {
-                            a = cadd(a, cp[co + CT_X]);
-                            if (e3) a = cadd(a, cp[co + CT_X + 1]);
-                        }
-                        if (xodd) {
-                            const cd *cq = cp + CT_Y * CT_X;
-                            a = cadd(a, cq[co]);
-                            if (e3) a = cadd(a, cq[co + 1]);
-                            if (e2) {
-                                a = cadd(a, cq[co + CT_X]);
-                                if (e3) a = cadd(a, cq[co + CT_X + 1]);
-                            }
-                        }
-                        const int ns = (1 + (int)xodd) * (1 + (int)e2) * (1 + (int)e3);
-                        if (ns > 1) a = cscal(a, ns == 2 ? 0.5 : (ns == 4 ? 0.25 : 0.125));
-                        v = (MODE == MODE_CORR1) ? cadd(v, a) : a;
-                    }
-                }
-            }
-            sm.f[w][e] = v;
-        }
-    };
-
-    // prologue: raw planes i0-1 .. i0+2 in flight; f(i0-1), f(i0) produced
-    for (int s = 0; s < PIPE_S; s++) stage(i0 - 1 + s);
-    cp_wait<PIPE_S - 1>();
-    __syncthreads();
-    produce(i0 - 1, 0);
-    cp_wait<PIPE_S - 2>();
-    __syncthreads();
-    produce(i0, 1);
-    int wp = 0, wc = 1, wn = 2;
-    int cslot = 1;   // stage slot of the plane being computed
-    for (int i = i0; i < i1; i++) {
-        cp_wait<PIPE_S - 3>();          // raw(i+1) landed
+    for (int s = 0; s < RING - 1; s++) stage(i0 - 1 + s);   // planes i0-1 .. i0+2
+    int sp = 0, sc = 1, sn = 2;                              // ring slots of i-1, i, i+1
+    long long q = (long long)i0 * L.plane + own;
+    for (int i = i0; i < i1; i++, q += L.plane) {
+        cp_wait<1>();                      // plane i+1 landed (i+2 may be in flight)
         __syncthreads();
-        produce(i + 1, wn);
-        stage(i + PIPE_S - 1);          // reuses the slot of raw(i-1)
-        __syncthreads();
+        stage(i + RING - 2);               // into the slot read last at step i-1
         if (act) {
-            const long long q = (long long)i * L.plane + j * L.n3 + m;
             const int gi = L.lo1 + i;
             const bool bxl = gi == 0, bxh = gi == L.n1 - 1;
-            const int nb = (int)bxl + (int)bxh + nbjm_c;
-            const cd fc = sm.f[wc][cfill];
-            cd mf;
-            cd ap;
-            double kk = 0.0;
-            if (KVAR) {
-                kk = sm.kr[cslot & (KVAR ? PIPE_MASK : 0)][cfill];
-                ap = ap_of(L, kk, nb);
-            } else {
-                ap = apt[nb];
+            const int nb = (int)bxl + (int)bxh + nbjm;
+            const cd *r0 = sm.raw[sc];
+            cd fc = r0[cf];
+            cd xm = sm.raw[sp][cf], xp = sm.raw[sn][cf];
+            cd ym = r0[cf - HALO_X], yp = r0[cf + HALO_X];
+            cd zm = r0[cf - 1], zp = r0[cf + 1];
+            const double kk = KVAR ? sm.kc[KVAR ? sc : 0][tid] : L.kc;
+            const cd bc = fc;              // PRE: the staged centre is b
+            cd post = one;                 // PRE deep interior: M(c b) = c M b
+            if (MODE == MODE_PRE) {
+                if (KVAR) {
+                    const int W = SM::kWd ? 1 : 0;
+                    fc = cmul(fc, sm.wd[W * sc][cf]);
+                    xm = cmul(xm, sm.wd[W * sp][cf]);
+                    xp = cmul(xp, sm.wd[W * sn][cf]);
+                    ym = cmul(ym, sm.wd[W * sc][cf - HALO_X]);
+                    yp = cmul(yp, sm.wd[W * sc][cf + HALO_X]);
+                    zm = cmul(zm, sm.wd[W * sc][cf - 1]);
+                    zp = cmul(zp, sm.wd[W * sc][cf + 1]);
+                } else if (deep_jm && gi >= 2 && gi <= L.n1 - 3) {
+                    post = wd0;
+                } else {
+                    const int nbx = (int)bxl + (int)bxh;
+                    fc = cmul(fc, wd_nb(nb));
+                    xm = cmul(xm, wd_nb((gi - 1 == 0) + (gi - 1 == L.n1 - 1) + nbjm));
+                    xp = cmul(xp, wd_nb((gi + 1 == 0) + (gi + 1 == L.n1 - 1) + nbjm));
+                    const int by = (m == 0) + (m == L.n3 - 1) + nbx;
+                    const int bz = (j == 0) + (j == L.n2 - 1) + nbx;
+                    ym = cmul(ym, wd_nb((j - 1 == 0) + (j - 1 == L.n2 - 1) + by));
+                    yp = cmul(yp, wd_nb((j + 1 == 0) + (j + 1 == L.n2 - 1) + by));
+                    zm = cmul(zm, wd_nb((m - 1 == 0) + (m - 1 == L.n3 - 1) + bz));
+                    zp = cmul(zp, wd_nb((m + 1 == 0) + (m + 1 == L.n3 - 1) + bz));
+                }
             }
-            if (L.bc == HF_BC_DIRICHLET && nb) {
-                mf = fc;
-            } else {
-                cd xm = sm.f[wp][cfill], xp = sm.f[wn][cfill];
-                cd ym = sm.f[wc][cfill - HALO_X], yp = sm.f[wc][cfill + HALO_X];
-                cd zm = sm.f[wc][cfill - 1], zp = sm.f[wc][cfill + 1];
-                if (bxl) xm = xp;
-                if (bxh) xp = xm;
-                if (byl) ym = yp;
-                if (byh) yp = ym;
-                if (bzl) zm = zp;
-                if (bzh) zp = zm;
+            cd mf;
+            if (nb == 0) {                 // interior row
+                const cd ap = KVAR ? ap_of(L, kk, 0) : ap0;
                 cd sum = cadd(cadd(cadd(xm, xp), cadd(ym, yp)), cadd(zm, zp));
                 mf = cmul(ap, fc);
                 mf.x -= L.ih2 * sum.x;
                 mf.y -= L.ih2 * sum.y;
+                if (MODE == MODE_PRE && !KVAR) mf = cmul(post, mf);
+            } else if (!SOMM) {            // Dirichlet boundary row: identity
+                mf = fc;
+            } else {                       // Sommerfeld: mirror the inward neighbour
+                if (bxl) xm = xp;
+                if (bxh) xp = xm;
+                if (j == 0) ym = yp;
+                if (j == L.n2 - 1) yp = ym;
+                if (m == 0) zm = zp;
+                if (m == L.n3 - 1) zp = zm;
+                cd sum = cadd(cadd(cadd(xm, xp), cadd(ym, yp)), cadd(zm, zp));
+                mf = cmul(KVAR ? ap_of(L, kk, nb) : tab[nb], fc);
+                mf.x -= L.ih2 * sum.x;
+                mf.y -= L.ih2 * sum.y;
             }
             cd av = mk(0, 0);
-            if (Epi::kAux) av = SM::kAuxArr ? sm.ax[cslot & (SM::kAuxArr ? PIPE_MASK : 0)][tid]
-                                            : sm.raw[cslot][cfill];
+            if (Epi::kAux) av = SM::kAuxArr ? sm.ax[SM::kAuxArr ? sc : 0][tid] : bc;
             cd wd = mk(0, 0);
-            if (Epi::kDinv) {
-                if (KVAR) wd = cscal(cdiv(mk(1.0, 0.0), diag_of(L, kk, nb)), omega);
-                else wd = wdt[nb];
-            }
+            if (Epi::kDinv) wd = KVAR ? cscal(cdiv(one, diag_of(L, kk, nb)), omega) : wd_nb(nb);
             epi(q, fc, mf, wd, av, acc);
         }
-        int t = wp; wp = wc; wc = wn; wn = t;
-        cslot = (cslot + 1) & PIPE_MASK;
+        sp = sc; sc = sn; sn = sn == RING - 1 ? 0 : sn + 1;
     }
     cp_wait<0>();
     constexpr int NR = (ND > 0) ? ND : 1;
@@ -527,6 +350,75 @@ __global__ void __launch_bounds__(TILE_X *TILE_Y) k_stencil(Lvl L, Lvl C, const 
     }
 }
 
+// w D^-1 over a level (owned + ghost planes), for the MODE_PRE kernels of a
+// varying medium (hierarchy setup)
+__global__ void k_wdinv(Lvl L, double omega, int g0, int g1, cd *__restrict__ out) {
+    long long n = (long long)(g1 - g0) * L.plane;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
+         t += (long long)gridDim.x * blockDim.x) {
+        int i = g0 + (int)(t / L.plane);
+        int rem = (int)(t - (long long)(i - g0) * L.plane);
+        int j = rem / L.n3, m = rem - j * L.n3;
+        long long q = (long long)i * L.plane + rem;
+        cd d = diag_of(L, L.k[q], nbnd(L, L.lo1 + i, j, m));
+        out[q] = cscal(cdiv(mk(1.0, 0.0), d), omega);
+    }
+}
+
+// trilinear prolongation value at fine local (i, j, m) (multigrid.py:238-297);
+// the reference divides the 2/4/8-point sums, exact here as a power-of-two scale
+struct Prolong {
+    Lvl C;
+    const cd *e;   // coarse field, owned plane 0
+    __device__ __forceinline__ cd operator()(const Lvl &F, int i, int j, int m) const {
+        int gi = F.lo1 + i;
+        int c1 = (gi >> 1) - C.lo1, e1 = gi & 1;
+        int c2 = j >> 1, e2 = j & 1;
+        int c3 = m >> 1, e3 = m & 1;
+        const cd *p = e + (long long)c1 * C.plane + c2 * C.n3 + c3;
+        cd acc = __ldg(p);
+        if (e3) acc = cadd(acc, __ldg(p + 1));
+        if (e2) {
+            acc = cadd(acc, __ldg(p + C.n3));
+            if (e3) acc = cadd(acc, __ldg(p + C.n3 + 1));
+        }
+        if (e1) {
+            const cd *p1 = p + C.plane;
+            acc = cadd(acc, __ldg(p1));
+            if (e3) acc = cadd(acc, __ldg(p1 + 1));
+            if (e2) {
+                acc = cadd(acc, __ldg(p1 + C.n3));
+                if (e3) acc = cadd(acc, __ldg(p1 + C.n3 + 1));
+            }
+        }
+        int ns = (1 + e1) * (1 + e2) * (1 + e3);
+        if (ns > 1) acc = cscal(acc, ns == 2 ? 0.5 : (ns == 4 ? 0.25 : 0.125));
+        return acc;
+    }
+};
+
+// pointwise coarse-grid correction on the zero-guess pre-smoothed iterate:
+//   MODE 0: out = P e           MODE 1: out = w D^-1 b + P e   (nu1 = 1)
+//   MODE 2: out += P e          (multigrid.py:337-341, 389-392)
+template <int MODE>
+__global__ void __launch_bounds__(256) k_corr(Lvl F, Lvl C, const cd *__restrict__ b,
+                                              const cd *__restrict__ e, cd *__restrict__ out,
+                                              double omega, const int *done) {
+    if (is_done(done)) return;
+    const int m = blockIdx.x * 32 + (threadIdx.x & 31);
+    const int j = blockIdx.y * 8 + (threadIdx.x >> 5);
+    const int i = blockIdx.z;
+    if (m >= F.n3 || j >= F.n2) return;
+    const long long q = (long long)i * F.plane + j * F.n3 + m;
+    cd v = Prolong{C, e}(F, i, j, m);
+    if (MODE == 1) {
+        cd d = diag_of(F, kat(F, q), nbnd(F, F.lo1 + i, j, m));
+        v = cadd(cscal(cdiv(__ldg(b + q), d), omega), v);
+    }
+    if (MODE == 2) v = cadd(out[q], v);
+    out[q] = v;
+}
+
 // u = w D^-1 b   (multigrid.py:148-151, assume_zero first sweep)
 __global__ void __launch_bounds__(256) k_jacobi0(Lvl L, const cd *__restrict__ b,
                                                  cd *__restrict__ u, double omega, int chunk,
@@ -534,70 +426,106 @@ __global__ void __launch_bounds__(256) k_jacobi0(Lvl L, const cd *__restrict__ b
     if (is_done(done)) return;
     ColCtx c = col_ctx(L, chunk);
     if (!c.act) return;
-    ProdPre P{b, omega};
     for (int i = c.i0; i < c.i1; i++) {
         long long q = (long long)i * L.plane + (long long)c.j * L.n3 + c.m;
-        u[q] = P(L, i, c.j, c.m);
+        cd d = diag_of(L, kat(L, q), nbnd(L, L.lo1 + i, c.j, c.m));
+        u[q] = cscal(cdiv(__ldg(b + q), d), omega);
     }
 }
 
-// out = P e (ADD=0) or out += P e (ADD=1)
-template <int ADD>
-__global__ void __launch_bounds__(256) k_prolong(Lvl F, Lvl C, const cd *__restrict__ e,
-                                                 cd *__restrict__ out, int chunk, const int *done) {
+// full-weighting restriction (multigrid.py:171-221), shared-memory tiled: a
+// block owns 16 x 8 coarse columns and marches over a chunk of coarse planes;
+// the two fine planes each coarse plane adds are prefetched with cp.async one
+// step ahead, every fine plane is reduced once to its 2-D (1,2,1)x(1,2,1)
+// partial, and a coarse value combines three consecutive partials.
+#define RC_X 16
+#define RC_Y 8
+#define RF_X (2 * RC_X + 1)
+#define RF_Y (2 * RC_Y + 1)
+#define RF_N (RF_X * RF_Y)
+__global__ void __launch_bounds__(256) k_restrict2(Lvl F, Lvl C, const cd *__restrict__ r,
+                                                   cd *__restrict__ out, int chunk, const int *done) {
+    __shared__ __align__(16) cd fp[4][RF_N];
+    __shared__ cd P[3][RC_Y * RC_X];
     if (is_done(done)) return;
-    ColCtx c = col_ctx(F, chunk);
-    if (!c.act) return;
-    Prolong P{C, e};
-    for (int i = c.i0; i < c.i1; i++) {
-        long long q = (long long)i * F.plane + (long long)c.j * F.n3 + c.m;
-        cd pe = P(F, i, c.j, c.m);
-        out[q] = ADD ? cadd(out[q], pe) : pe;
+    const int tid = threadIdx.x;
+    const int cm0 = blockIdx.x * RC_X, cj0 = blockIdx.y * RC_Y;
+    const int ci0 = blockIdx.z * chunk, ci1 = min(ci0 + chunk, C.nx);
+    const int fm0 = 2 * cm0 - 1, fj0 = 2 * cj0 - 1;
+    int go[3];
+    bool ok[3];
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+        int e = tid + 256 * k;
+        int fy = e / RF_X, fx = e - fy * RF_X;
+        int fj = fj0 + fy, fm = fm0 + fx;
+        ok[k] = e < RF_N && fj >= 0 && fj < F.n2 && fm >= 0 && fm < F.n3;
+        go[k] = ok[k] ? fj * F.n3 + fm : 0;
     }
-}
-
-// full-weighting restriction, one thread per coarse vertex (multigrid.py:171-221)
-__global__ void __launch_bounds__(256) k_restrict(Lvl F, Lvl C, const cd *__restrict__ r,
-                                                  cd *__restrict__ out, int chunk,
-                                                  const int *done) {
-    if (is_done(done)) return;
-    ColCtx c = col_ctx(C, chunk);
-    if (!c.act) return;
-    const double w1[3] = {1.0, 2.0, 1.0};
-    for (int ci = c.i0; ci < c.i1; ci++) {
-        int gci = C.lo1 + ci;
-        int fi0 = 2 * gci - F.lo1;      // fine local plane of the coarse vertex image
-        int fj0 = 2 * c.j, fm0 = 2 * c.m;
-        cd acc = mk(0, 0);
+    auto stage = [&](int gf, int slot) {     // fine global plane gf -> fp[slot]
+        const bool pok = gf >= 0 && gf < F.n1;
+        const cd *pp = r + (long long)(gf - F.lo1) * F.plane;
 #pragma unroll
-        for (int o1 = -1; o1 <= 1; o1++) {
-            int gfi = 2 * gci + o1;
-            bool in1 = gfi >= 0 && gfi < F.n1;
-#pragma unroll
-            for (int o2 = -1; o2 <= 1; o2++) {
-                int fj = fj0 + o2;
-                bool in2 = in1 && fj >= 0 && fj < F.n2;
-#pragma unroll
-                for (int o3 = -1; o3 <= 1; o3++) {
-                    int fm = fm0 + o3;
-                    double w = w1[o1 + 1] * w1[o2 + 1] * w1[o3 + 1];
-                    if (in2 && fm >= 0 && fm < F.n3) {
-                        cd val = __ldg(r + (long long)(fi0 + o1) * F.plane + (long long)fj * F.n3 + fm);
-                        acc.x += w * val.x;
-                        acc.y += w * val.y;
-                    }
-                }
+        for (int k = 0; k < 3; k++) {
+            int e = tid + 256 * k;
+            if (e < RF_N) {
+                bool v = pok && ok[k];
+                cp_async16(&fp[slot][e], v ? pp + go[k] : r, v);
             }
         }
-        acc = mk(acc.x / 64.0, acc.y / 64.0);
-        int onb = (gci == 0 || gci == C.n1 - 1) + (c.j == 0 || c.j == C.n2 - 1) +
-                  (c.m == 0 || c.m == C.n3 - 1);
-        if (onb) {
-            if (C.bc == HF_BC_DIRICHLET) acc = mk(0, 0);
-            else
-                for (int d = 0; d < onb; d++) acc = cscal(acc, 64.0 / 48.0);
+    };
+    // 2-D partial of the coarse column handled by this thread, from plane slot
+    const int cidx = tid & 127, cy = cidx / RC_X, cx = cidx - cy * RC_X;
+    auto partial = [&](int slot) -> cd {
+        const cd *b = &fp[slot][(2 * cy + 1) * RF_X + 2 * cx + 1];
+        cd s = mk(0, 0);
+#pragma unroll
+        for (int a = -1; a <= 1; a++) {
+            const cd *row = b + a * RF_X;
+            cd rs = cadd(cadd(row[-1], cscal(row[0], 2.0)), row[1]);
+            s = cadd(s, a == 0 ? cscal(rs, 2.0) : rs);
         }
-        out[(long long)ci * C.plane + (long long)c.j * C.n3 + c.m] = acc;
+        return s;
+    };
+    const int gc0 = C.lo1 + ci0;
+    // prologue: fine planes 2gc0-1 (slot 3), 2gc0 (0), 2gc0+1 (1)
+    stage(2 * gc0 - 1, 3);
+    stage(2 * gc0, 0);
+    stage(2 * gc0 + 1, 1);
+    cp_commit();
+    cp_wait<0>();
+    __syncthreads();
+    if (tid < 128) P[0][cidx] = partial(3);
+    __syncthreads();                            // slot 3 is refilled by the first prefetch
+    int pprev = 0, pe = 1, po = 2;
+    int se = 0, so = 1;
+    const int cj = cj0 + cy, cm = cm0 + cx;
+    const bool act = cj < C.n2 && cm < C.n3;
+    for (int ci = ci0; ci < ci1; ci++) {
+        const int gc = C.lo1 + ci;
+        if (ci + 1 < ci1) {                     // prefetch the next pair
+            stage(2 * gc + 2, se ^ 2);
+            stage(2 * gc + 3, so ^ 2);
+        }
+        cp_commit();
+        if (tid < 128) P[pe][cidx] = partial(se);
+        else P[po][cidx] = partial(so);
+        __syncthreads();
+        if (tid < 128 && act) {
+            cd acc = cadd(cadd(P[pprev][cidx], cscal(P[pe][cidx], 2.0)), P[po][cidx]);
+            acc = mk(acc.x / 64.0, acc.y / 64.0);
+            int onb = (gc == 0 || gc == C.n1 - 1) + (cj == 0 || cj == C.n2 - 1) + (cm == 0 || cm == C.n3 - 1);
+            if (onb) {
+                if (C.bc == HF_BC_DIRICHLET) acc = mk(0, 0);
+                else
+                    for (int d = 0; d < onb; d++) acc = cscal(acc, 64.0 / 48.0);
+            }
+            out[(long long)ci * C.plane + cj * C.n3 + cm] = acc;
+        }
+        int t = pprev; pprev = po; po = pe; pe = t;
+        se ^= 2; so ^= 2;
+        cp_wait<0>();
+        __syncthreads();
     }
 }
 
@@ -834,32 +762,39 @@ static dim3 tile_grid(const Lvl &L, int &chunk) {
 }
 static const dim3 kTileBlock(TILE_X, TILE_Y, 1);
 
-template <int MODE, class Epi, int ND, bool KVAR>
-static void stencil_launch(const Lvl &L, const Lvl &C, const cd *src, const cd *ec, const cd *aux,
-                           double omega, const Epi &e, const RedSlot &rs, cudaStream_t s,
-                           const int *done) {
+template <int MODE, class Epi, int ND, bool KVAR, bool SOMM>
+static void stencil_launch(const Lvl &L, const cd *src, const cd *aux, double omega, const Epi &e,
+                           const RedSlot &rs, cudaStream_t s, const int *done) {
     int chunk;
     dim3 g = tile_grid(L, chunk);
     size_t smem = sizeof(StencilSmem<MODE, KVAR, Epi::kAux>);
-    k_stencil<MODE, Epi, ND, KVAR><<<g, kTileBlock, smem, s>>>(L, C, src, ec, aux ? aux : src, omega,
-                                                               e, chunk, rs, done);
+    k_stencil<MODE, Epi, ND, KVAR, SOMM><<<g, kTileBlock, smem, s>>>(L, src, aux ? aux : src, omega, e,
+                                                                     chunk, rs, done);
 }
 template <int MODE, class Epi, int ND>
-static void stencil(const Lvl &L, const Lvl &C, const cd *src, const cd *ec, const cd *aux,
-                    double omega, const Epi &e, const RedSlot &rs, cudaStream_t s, const int *done) {
-    if (L.k) stencil_launch<MODE, Epi, ND, true>(L, C, src, ec, aux, omega, e, rs, s, done);
-    else stencil_launch<MODE, Epi, ND, false>(L, C, src, ec, aux, omega, e, rs, s, done);
+static void stencil(const Lvl &L, const cd *src, const cd *aux, double omega, const Epi &e,
+                    const RedSlot &rs, cudaStream_t s, const int *done) {
+    const bool somm = L.bc == HF_BC_SOMMERFELD;
+    if (L.k) {
+        if (somm) stencil_launch<MODE, Epi, ND, true, true>(L, src, aux, omega, e, rs, s, done);
+        else stencil_launch<MODE, Epi, ND, true, false>(L, src, aux, omega, e, rs, s, done);
+    } else {
+        if (somm) stencil_launch<MODE, Epi, ND, false, true>(L, src, aux, omega, e, rs, s, done);
+        else stencil_launch<MODE, Epi, ND, false, false>(L, src, aux, omega, e, rs, s, done);
+    }
 }
 
 template <int MODE, class Epi, int ND>
 static void set_attr() {
-    cudaFuncSetAttribute(k_stencil<MODE, Epi, ND, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(StencilSmem<MODE, true, Epi::kAux>));
-    cudaFuncSetAttribute(k_stencil<MODE, Epi, ND, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(StencilSmem<MODE, false, Epi::kAux>));
+    const int a1 = (int)sizeof(StencilSmem<MODE, true, Epi::kAux>);
+    const int a0 = (int)sizeof(StencilSmem<MODE, false, Epi::kAux>);
+    cudaFuncSetAttribute(k_stencil<MODE, Epi, ND, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, a1);
+    cudaFuncSetAttribute(k_stencil<MODE, Epi, ND, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, a1);
+    cudaFuncSetAttribute(k_stencil<MODE, Epi, ND, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, a0);
+    cudaFuncSetAttribute(k_stencil<MODE, Epi, ND, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, a0);
 }
 
-// opt the pipelined stencil kernels into > 48 KB dynamic shared memory (once, outside capture)
+// opt the staged stencil kernels into > 48 KB dynamic shared memory (once, outside capture)
 void init_kernel_attributes() {
     static bool done = false;
     if (done) return;
@@ -869,8 +804,6 @@ void init_kernel_attributes() {
     set_attr<MODE_LOAD, EpiResid, 0>();
     set_attr<MODE_LOAD, EpiJacobi, 0>();
     set_attr<MODE_PRE, EpiResid, 0>();
-    set_attr<MODE_CORR1, EpiJacobi, 0>();
-    set_attr<MODE_CORR0, EpiJacobi, 0>();
     done = true;
 }
 
@@ -881,25 +814,34 @@ int tile_blocks(const Lvl &L) {
 }
 
 void launch_apply(const Lvl &L, const cd *u, cd *v, cudaStream_t s, const int *done) {
-    stencil<MODE_LOAD, EpiApply<0>, 0>(L, L, u, nullptr, nullptr, 0.0, EpiApply<0>{v},
-                                       RedSlot{}, s, done);
+    stencil<MODE_LOAD, EpiApply<0>, 0>(L, u, nullptr, 0.0, EpiApply<0>{v}, RedSlot{}, s, done);
 }
 void launch_apply_dot1(const Lvl &L, const cd *u, cd *v, const cd *w, const RedSlot &rs,
                        cudaStream_t s, const int *done) {
-    stencil<MODE_LOAD, EpiApply<1>, 1>(L, L, u, nullptr, w, 0.0, EpiApply<1>{v}, rs, s, done);
+    stencil<MODE_LOAD, EpiApply<1>, 1>(L, u, w, 0.0, EpiApply<1>{v}, rs, s, done);
 }
 void launch_apply_dot2(const Lvl &L, const cd *u, cd *v, const cd *w, const RedSlot &rs,
                        cudaStream_t s, const int *done) {
-    stencil<MODE_LOAD, EpiApply<2>, 2>(L, L, u, nullptr, w, 0.0, EpiApply<2>{v}, rs, s, done);
+    stencil<MODE_LOAD, EpiApply<2>, 2>(L, u, w, 0.0, EpiApply<2>{v}, rs, s, done);
 }
 void launch_residual(const Lvl &L, const cd *u, const cd *b, cd *r, cudaStream_t s,
                      const int *done) {
-    stencil<MODE_LOAD, EpiResid, 0>(L, L, u, nullptr, b, 0.0, EpiResid{r}, RedSlot{}, s, done);
+    stencil<MODE_LOAD, EpiResid, 0>(L, u, b, 0.0, EpiResid{r}, RedSlot{}, s, done);
 }
 void launch_jacobi(const Lvl &L, const cd *u, const cd *b, cd *uo, double omega,
                    cudaStream_t s, const int *done) {
-    stencil<MODE_LOAD, EpiJacobi, 0>(L, L, u, nullptr, b, omega, EpiJacobi{uo}, RedSlot{}, s,
-                                     done);
+    stencil<MODE_LOAD, EpiJacobi, 0>(L, u, b, omega, EpiJacobi{uo}, RedSlot{}, s, done);
+}
+void launch_down1(const Lvl &L, const cd *b, cd *r, double omega, cudaStream_t s,
+                  const int *done) {
+    stencil<MODE_PRE, EpiResid, 0>(L, b, b, omega, EpiResid{r}, RedSlot{}, s, done);
+}
+static void corr(int mode, const Lvl &F, const Lvl &C, const cd *b, const cd *e, cd *out,
+                 double omega, cudaStream_t s, const int *done) {
+    dim3 g((F.n3 + 31) / 32, (F.n2 + 7) / 8, F.nx);
+    if (mode == 0) k_corr<0><<<g, 256, 0, s>>>(F, C, b, e, out, omega, done);
+    else if (mode == 1) k_corr<1><<<g, 256, 0, s>>>(F, C, b, e, out, omega, done);
+    else k_corr<2><<<g, 256, 0, s>>>(F, C, b, e, out, omega, done);
 }
 void launch_jacobi0(const Lvl &L, const cd *b, cd *u, double omega, cudaStream_t s,
                     const int *done) {
@@ -907,29 +849,29 @@ void launch_jacobi0(const Lvl &L, const cd *b, cd *u, double omega, cudaStream_t
     dim3 g = march_grid(L, chunk);
     k_jacobi0<<<g, kMarchBlock, 0, s>>>(L, b, u, omega, chunk, done);
 }
-void launch_down1(const Lvl &L, const cd *b, cd *r, double omega, cudaStream_t s,
-                  const int *done) {
-    stencil<MODE_PRE, EpiResid, 0>(L, L, b, nullptr, b, omega, EpiResid{r}, RedSlot{}, s, done);
+void launch_wdinv(const Lvl &L, double omega, cd *out_owned, cudaStream_t s) {
+    int g0 = std::max(-HF_GHOST, -L.lo1), g1 = std::min(L.nx + HF_GHOST, L.n1 - L.lo1);
+    k_wdinv<<<592, 256, 0, s>>>(L, omega, g0, g1, out_owned);
 }
 void launch_restrict(const Lvl &F, const Lvl &C, const cd *r, cd *out, cudaStream_t s,
                      const int *done) {
-    int chunk;
-    dim3 g = march_grid(C, chunk);
-    k_restrict<<<g, kMarchBlock, 0, s>>>(F, C, r, out, chunk, done);
+    int gx = (C.n3 + RC_X - 1) / RC_X, gy = (C.n2 + RC_Y - 1) / RC_Y;
+    long long cols = (long long)gx * gy;
+    int gz = (int)std::max<long long>(1, std::min<long long>(C.nx, (148 * 6 + cols - 1) / cols));
+    int chunk = std::max(2, (C.nx + gz - 1) / gz);
+    gz = (C.nx + chunk - 1) / chunk;
+    k_restrict2<<<dim3(gx, gy, gz), 256, 0, s>>>(F, C, r, out, chunk, done);
 }
 void launch_prolong(const Lvl &F, const Lvl &C, const cd *e, cd *out, bool add, cudaStream_t s,
                     const int *done) {
-    int chunk;
-    dim3 g = march_grid(F, chunk);
-    if (add) k_prolong<1><<<g, kMarchBlock, 0, s>>>(F, C, e, out, chunk, done);
-    else k_prolong<0><<<g, kMarchBlock, 0, s>>>(F, C, e, out, chunk, done);
+    corr(add ? 2 : 0, F, C, nullptr, e, out, 0.0, s, done);
 }
-void launch_up1(const Lvl &L, const Lvl &C, const cd *b, const cd *e, cd *u, double omega,
+// u = u1 + w D^-1 (b - M u1), u1 = [w D^-1 b] + P e: pointwise correction into
+// the scratch field t, then one Jacobi sweep stencil (multigrid.py:337-343)
+void launch_up1(const Lvl &L, const Lvl &C, const cd *b, const cd *e, cd *u, cd *t, double omega,
                 bool pre, cudaStream_t s, const int *done) {
-    if (pre)
-        stencil<MODE_CORR1, EpiJacobi, 0>(L, C, b, e, b, omega, EpiJacobi{u}, RedSlot{}, s, done);
-    else
-        stencil<MODE_CORR0, EpiJacobi, 0>(L, C, b, e, b, omega, EpiJacobi{u}, RedSlot{}, s, done);
+    corr(pre ? 1 : 0, L, C, b, e, t, omega, s, done);
+    stencil<MODE_LOAD, EpiJacobi, 0>(L, t, b, omega, EpiJacobi{u}, RedSlot{}, s, done);
 }
 void launch_gemv(int N, const cd *Minv, const cd *b, cd *x, cudaStream_t s, const int *done) {
     int blocks = (N + 1) / 2;

@@ -251,6 +251,13 @@ extern "C" hf_hierarchy *hf_hierarchy_create(int n1, int n2, int n3, int lo1, in
             return nullptr;
         }
         cudaError_t err;
+        if (kf) {
+            // w D^-1 field for the fused pre-smooth + residual of a varying medium
+            cd *wd = new_field(H->A, cnx, lv.L.plane, err);
+            if (!wd) { fail(HF_ERR_CUDA, "cudaMalloc w D^-1"); delete H; return nullptr; }
+            launch_wdinv(lv.L, cfg->omega, wd, work_stream());
+            lv.L.wd = wd;
+        }
         if (cfg->cycle == HF_CYCLE_F) {
             lv.fb = new_field(H->A, cnx, lv.L.plane, err);
             lv.guess = new_field(H->A, cnx, lv.L.plane, err);
@@ -328,7 +335,8 @@ static void v_cycle(hf_hierarchy *H, int li, const cd *b, cd *u, cudaStream_t s,
     L1(launch_restrict(lv.L, nx.L, lv.r, nx.b, s, done));
     v_cycle(H, li + 1, nx.b, nx.u, s, done);
     if (fused) {
-        L1(launch_up1(lv.L, nx.L, b, nx.u, u, c.omega, c.nu1 == 1, s, done));
+        L1(launch_up1(lv.L, nx.L, b, nx.u, u, lv.t, c.omega, c.nu1 == 1, s, done));
+        g_launches++;   // correction + Jacobi stencil
     } else {
         L1(launch_prolong(lv.L, nx.L, nx.u, u, true, s, done));
         smooth_sweeps(lv, u, b, c.omega, c.nu2, s, done);

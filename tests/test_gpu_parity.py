@@ -202,3 +202,25 @@ def test_gmres_restart(hf, oracle):
     xr, rr = Solver(A, hier).solve(b, SolverConfig(method="gmres", restart=5, maxit=200))
     assert rr.converged
     assert np.linalg.norm(xr.cpu().numpy() - xo) / np.linalg.norm(xo) < 1e-5
+
+
+def test_repeat_solves_bit_identical(hf):
+    """Deterministic reductions and race-free kernels: repeated solves (with
+    different host polling intervals) give bit-identical solutions."""
+    from paper_2308_06085_b200 import problems
+    from paper_2308_06085_b200.krylov import Solver, SolverConfig
+    from paper_2308_06085_b200.multigrid import MGConfig, build_hierarchy
+    from paper_2308_06085_b200.operators import OperatorSpec, StencilOperator
+    p = problems.point_source_cube(65, 40.0, "sommerfeld")
+    spec, b = problems.build_problem(p)
+    A = StencilOperator(spec, p.grid)
+    hier = build_hierarchy(p.grid, None, OperatorSpec("cslp", 1.0, -0.5, spec.bc, spec.k_field), MGConfig())
+    S = Solver(A, hier)
+    ref = None
+    for every in (1, 3, 4):
+        x, rep = S.solve(b, SolverConfig(method="bicgstab", check_every=every))
+        x = x.cpu().numpy()
+        if ref is None:
+            ref, ref_it = x, rep.iterations
+        assert rep.iterations == ref_it
+        assert np.array_equal(x, ref)

@@ -1,40 +1,51 @@
-"""Summarise an `ncu --metrics gpu__time_duration.sum --csv` launch list:
-per-kernel count, total and mean device time, and share of the total."""
+"""Summarise an `ncu --metrics gpu__time_duration.sum[,...] --csv` launch list:
+per kernel (name + grid): launches, mean device time, share of the total,
+and the mean of any extra metric (e.g. smsp__inst_executed.sum).
+
+    python tools/summarize_launches.py gpurun_out/launches.csv
+"""
 import collections
 import csv
 import sys
 
+SETUP = ("cutlass", "getrf", "trsm", "ipiv", "laswp", "pivot", "cublas", "xxtrf", "copy_info",
+         "k_assemble", "k_set_identity")
 
-def load(path):
+
+def main(path):
     rows = list(csv.reader(open(path)))
     hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     h = rows[hi]
-    ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
-    gi = h.index("Grid Size")
-    out = []
+    ki, gi, mi = h.index("Kernel Name"), h.index("Grid Size"), h.index("Metric Name")
+    vi, ui = h.index("Metric Value"), h.index("Metric Unit")
+    agg = collections.defaultdict(lambda: collections.defaultdict(float))
+    cnt = collections.Counter()
+    extra = set()
     for r in rows[hi + 1:]:
         if len(r) <= vi:
             continue
+        key = r[ki].split("(")[0][:70] + " " + r[gi]
+        if any(s in key for s in SETUP):
+            continue
         v = float(r[vi].replace(",", ""))
-        scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}[r[ui]]
-        out.append((r[ki], r[gi], v * scale))
-    return out
-
-
-def main(path, skip_prefixes=("void cutlass", "void getrf", "void kernel_trsm", "void trsm",
-                              "void ipiv", "void laswp", "void create_pivot", "void cublas",
-                              "xxtrf", "copy_info", "hf::k_assemble", "hf::k_set_identity")):
-    data = [d for d in load(path) if not d[0].startswith(skip_prefixes)]
-    agg = collections.defaultdict(lambda: [0, 0.0])
-    for name, grid, us in data:
-        key = name.split("(")[0][:70] + " " + grid
-        agg[key][0] += 1
-        agg[key][1] += us
-    tot = sum(v[1] for v in agg.values())
-    print(f"{'kernel + grid':90s} {'n':>5s} {'total us':>10s} {'mean us':>9s} {'share':>6s}")
-    for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1]):
-        print(f"{k:90s} {v[0]:5d} {v[1]:10.1f} {v[1] / v[0]:9.2f} {v[1] / tot:6.3f}")
-    print(f"total {tot:.1f} us (setup/factorisation kernels excluded)")
+        if r[mi] == "gpu__time_duration.sum":
+            v *= {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}[r[ui]]
+            cnt[key] += 1
+        else:
+            extra.add(r[mi])
+        agg[key][r[mi]] += v
+    tot = sum(d["gpu__time_duration.sum"] for d in agg.values())
+    hdr = f"{'kernel + grid':88s} {'n':>4s} {'mean us':>9s} {'share':>6s}"
+    for m in sorted(extra):
+        hdr += f" {m[:24]:>24s}"
+    print(hdr)
+    for k, d in sorted(agg.items(), key=lambda kv: -kv[1]["gpu__time_duration.sum"]):
+        n = cnt[k]
+        line = f"{k:88s} {n:4d} {d['gpu__time_duration.sum'] / n:9.2f} {d['gpu__time_duration.sum'] / tot:6.3f}"
+        for m in sorted(extra):
+            line += f" {d[m] / n:24.4g}"
+        print(line)
+    print(f"total {tot:.1f} us (setup / factorisation kernels excluded)")
 
 
 if __name__ == "__main__":

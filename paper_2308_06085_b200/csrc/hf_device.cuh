@@ -42,8 +42,14 @@ struct Lvl {
     int bc;              // HF_BC_*
     const double *k;     // wavenumber at owned plane 0 (ghost planes valid), or null
     double kc;           // constant wavenumber when k == null
-    const double2 *wd;   // w D^-1 at owned plane 0 (hierarchy levels of a varying medium)
+    const double2 *dinv; // D^-1 at owned plane 0 (ghost planes valid) when k varies, else null
+    const double2 *tab;  // constant k: tab[nb] = a_p, tab[4 + nb] = D^-1 for nb physical faces
 };
+
+// D^-1 at local linear index q of a vertex touching nb physical faces
+__device__ __forceinline__ double2 dinv_at(const Lvl &L, long long q, int nb) {
+    return L.dinv ? __ldg(L.dinv + q) : __ldg(L.tab + 4 + nb);
+}
 
 __device__ __forceinline__ double kat(const Lvl &L, long long q) {
     return L.k ? __ldg(L.k + q) : L.kc;

@@ -235,11 +235,11 @@ __global__ void __launch_bounds__(NT) k_stencil(Lvl L, const cd *__restrict__ sr
     __shared__ cd tab[8];
     cd ap0 = mk(0, 0), wd0 = mk(0, 0);
     if (!KVAR) {
-        ap0 = ap_of(L, L.kc, 0);
-        wd0 = cscal(cdiv(one, diag_of(L, L.kc, 0)), omega);
+        ap0 = __ldg(L.tab);
+        wd0 = cscal(__ldg(L.tab + 4), omega);
         if (tid < 4) {
-            tab[tid] = ap_of(L, L.kc, tid);
-            tab[4 + tid] = cscal(cdiv(one, diag_of(L, L.kc, tid)), omega);
+            tab[tid] = __ldg(L.tab + tid);
+            tab[4 + tid] = cscal(__ldg(L.tab + 4 + tid), omega);
         }
     }
     auto wd_nb = [&](int nb) -> cd { return tab[4 + nb]; };   // read after the first barrier
@@ -254,11 +254,11 @@ __global__ void __launch_bounds__(NT) k_stencil(Lvl L, const cd *__restrict__ sr
         const long long pb = (long long)i * L.plane;
         bool v = pok && ok0;
         cp_async16(&sm.raw[slot][tid], v ? src + pb + go0 : src, v);
-        if (SM::kWd) cp_async16(&sm.wd[SM::kWd ? slot : 0][tid], v ? L.wd + pb + go0 : L.wd, v);
+        if (SM::kWd) cp_async16(&sm.wd[SM::kWd ? slot : 0][tid], v ? L.dinv + pb + go0 : L.dinv, v);
         if (has1) {
             v = pok && ok1;
             cp_async16(&sm.raw[slot][tid + NT], v ? src + pb + go1 : src, v);
-            if (SM::kWd) cp_async16(&sm.wd[SM::kWd ? slot : 0][tid + NT], v ? L.wd + pb + go1 : L.wd, v);
+            if (SM::kWd) cp_async16(&sm.wd[SM::kWd ? slot : 0][tid + NT], v ? L.dinv + pb + go1 : L.dinv, v);
         }
         const bool vc = pok && act && i < i1;
         if (KVAR) cp_async8(&sm.kc[KVAR ? slot : 0][tid], vc ? L.k + pb + own : L.k, vc);
@@ -286,8 +286,9 @@ __global__ void __launch_bounds__(NT) k_stencil(Lvl L, const cd *__restrict__ sr
             const cd bc = fc;              // PRE: the staged centre is b
             cd post = one;                 // PRE deep interior: M(c b) = c M b
             if (MODE == MODE_PRE) {
-                if (KVAR) {
+                if (KVAR) {                   // staged D^-1, w applied once after M
                     const int W = SM::kWd ? 1 : 0;
+                    post = mk(omega, 0.0);
                     fc = cmul(fc, sm.wd[W * sc][cf]);
                     xm = cmul(xm, sm.wd[W * sp][cf]);
                     xp = cmul(xp, sm.wd[W * sn][cf]);
@@ -317,9 +318,9 @@ __global__ void __launch_bounds__(NT) k_stencil(Lvl L, const cd *__restrict__ sr
                 mf = cmul(ap, fc);
                 mf.x -= L.ih2 * sum.x;
                 mf.y -= L.ih2 * sum.y;
-                if (MODE == MODE_PRE && !KVAR) mf = cmul(post, mf);
+                if (MODE == MODE_PRE) mf = cmul(post, mf);
             } else if (!SOMM) {            // Dirichlet boundary row: identity
-                mf = fc;
+                mf = (MODE == MODE_PRE && KVAR) ? cmul(post, fc) : fc;
             } else {                       // Sommerfeld: mirror the inward neighbour
                 if (bxl) xm = xp;
                 if (bxh) xp = xm;
@@ -331,11 +332,12 @@ __global__ void __launch_bounds__(NT) k_stencil(Lvl L, const cd *__restrict__ sr
                 mf = cmul(KVAR ? ap_of(L, kk, nb) : tab[nb], fc);
                 mf.x -= L.ih2 * sum.x;
                 mf.y -= L.ih2 * sum.y;
+                if (MODE == MODE_PRE && KVAR) mf = cmul(post, mf);
             }
             cd av = mk(0, 0);
             if (Epi::kAux) av = SM::kAuxArr ? sm.ax[SM::kAuxArr ? sc : 0][tid] : bc;
             cd wd = mk(0, 0);
-            if (Epi::kDinv) wd = KVAR ? cscal(cdiv(one, diag_of(L, kk, nb)), omega) : wd_nb(nb);
+            if (Epi::kDinv) wd = KVAR ? cscal(__ldg(L.dinv + q), omega) : wd_nb(nb);
             epi(q, fc, mf, wd, av, acc);
         }
         sp = sc; sc = sn; sn = sn == RING - 1 ? 0 : sn + 1;
@@ -350,9 +352,8 @@ __global__ void __launch_bounds__(NT) k_stencil(Lvl L, const cd *__restrict__ sr
     }
 }
 
-// w D^-1 over a level (owned + ghost planes), for the MODE_PRE kernels of a
-// varying medium (hierarchy setup)
-__global__ void k_wdinv(Lvl L, double omega, int g0, int g1, cd *__restrict__ out) {
+// D^-1 over a level of a varying medium (owned + ghost planes), at setup
+__global__ void k_dinv(Lvl L, int g0, int g1, cd *__restrict__ out) {
     long long n = (long long)(g1 - g0) * L.plane;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
          t += (long long)gridDim.x * blockDim.x) {
@@ -360,8 +361,7 @@ __global__ void k_wdinv(Lvl L, double omega, int g0, int g1, cd *__restrict__ ou
         int rem = (int)(t - (long long)(i - g0) * L.plane);
         int j = rem / L.n3, m = rem - j * L.n3;
         long long q = (long long)i * L.plane + rem;
-        cd d = diag_of(L, L.k[q], nbnd(L, L.lo1 + i, j, m));
-        out[q] = cscal(cdiv(mk(1.0, 0.0), d), omega);
+        out[q] = cdiv(mk(1.0, 0.0), diag_of(L, L.k[q], nbnd(L, L.lo1 + i, j, m)));
     }
 }
 
@@ -411,10 +411,8 @@ __global__ void __launch_bounds__(256) k_corr(Lvl F, Lvl C, const cd *__restrict
     if (m >= F.n3 || j >= F.n2) return;
     const long long q = (long long)i * F.plane + j * F.n3 + m;
     cd v = Prolong{C, e}(F, i, j, m);
-    if (MODE == 1) {
-        cd d = diag_of(F, kat(F, q), nbnd(F, F.lo1 + i, j, m));
-        v = cadd(cscal(cdiv(__ldg(b + q), d), omega), v);
-    }
+    if (MODE == 1)
+        v = cadd(cscal(cmul(__ldg(b + q), dinv_at(F, q, nbnd(F, F.lo1 + i, j, m))), omega), v);
     if (MODE == 2) v = cadd(out[q], v);
     out[q] = v;
 }
@@ -428,8 +426,7 @@ __global__ void __launch_bounds__(256) k_jacobi0(Lvl L, const cd *__restrict__ b
     if (!c.act) return;
     for (int i = c.i0; i < c.i1; i++) {
         long long q = (long long)i * L.plane + (long long)c.j * L.n3 + c.m;
-        cd d = diag_of(L, kat(L, q), nbnd(L, L.lo1 + i, c.j, c.m));
-        u[q] = cscal(cdiv(__ldg(b + q), d), omega);
+        u[q] = cscal(cmul(__ldg(b + q), dinv_at(L, q, nbnd(L, L.lo1 + i, c.j, c.m))), omega);
     }
 }
 
@@ -656,33 +653,46 @@ __global__ void k_dot_store(long long n, const cd *__restrict__ a, const cd *__r
 // ---------------------------------------------------------------------------
 // coarsest level: dense inverse applied as one GEMV (HBM-bound)
 // ---------------------------------------------------------------------------
-// x = Minv b, Minv row-major N x N.  One warp per row, 64-thread blocks (fine
-// grained so rows spread evenly over the 148 SMs), eight 512 B row segments in
-// flight per warp.
-__global__ void __launch_bounds__(64) k_gemv(int N, const cd *__restrict__ Minv,
-                                             const cd *__restrict__ b, cd *__restrict__ x,
-                                             const int *done) {
+// x = Minv b, Minv row-major N x N (coarsest solve, HBM-streaming GEMV).
+// Persistent: two 512-thread blocks per SM, each owning a contiguous band of rows
+// (balanced to one row); b is staged once per block in shared memory; each
+// warp streams whole rows with eight 512 B segments in flight.
+#define GEMV_THREADS 512
+#define GEMV_SMEM_MAX 6912    // entries of b staged in shared memory (108 KB, 2 blocks per SM)
+template <bool SMEMB>
+__global__ void __launch_bounds__(GEMV_THREADS) k_gemv(int N, const cd *__restrict__ Minv,
+                                                       const cd *__restrict__ b, cd *__restrict__ x,
+                                                       const int *done) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const cd *bs = SMEMB ? reinterpret_cast<const cd *>(smem_raw) : b;
     if (is_done(done)) return;
-    int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    int lane = threadIdx.x & 31;
-    if (warp >= N) return;
-    const cd *row = Minv + (long long)warp * N;
-    cd a[8];
-#pragma unroll
-    for (int u = 0; u < 8; u++) a[u] = mk(0, 0);
-    int j = lane;
-    for (; j + 224 < N; j += 256) {
-        cd mv[8];
-#pragma unroll
-        for (int u = 0; u < 8; u++) mv[u] = __ldcs(row + j + 32 * u);
-#pragma unroll
-        for (int u = 0; u < 8; u++) a[u] = cadd(a[u], cmul(mv[u], __ldg(b + j + 32 * u)));
+    if (SMEMB) {
+        cd *w = reinterpret_cast<cd *>(smem_raw);
+        for (int jj = threadIdx.x; jj < N; jj += GEMV_THREADS) w[jj] = __ldg(b + jj);
+        __syncthreads();
     }
-    for (; j < N; j += 32) a[0] = cadd(a[0], cmul(__ldcs(row + j), __ldg(b + j)));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long r0 = (long long)N * blockIdx.x / gridDim.x;
+    const long long r1 = (long long)N * (blockIdx.x + 1) / gridDim.x;
+    for (long long rw = r0 + warp; rw < r1; rw += GEMV_THREADS / 32) {
+        const cd *row = Minv + rw * N;
+        cd a[8];
 #pragma unroll
-    for (int u = 1; u < 8; u++) a[0] = cadd(a[0], a[u]);
-    a[0] = warp_sum(a[0]);
-    if (lane == 0) x[warp] = a[0];
+        for (int u = 0; u < 8; u++) a[u] = mk(0, 0);
+        int j = lane;
+        for (; j + 224 < N; j += 256) {
+            cd mv[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) mv[u] = __ldcs(row + j + 32 * u);
+#pragma unroll
+            for (int u = 0; u < 8; u++) a[u] = cadd(a[u], cmul(mv[u], bs[j + 32 * u]));
+        }
+        for (; j < N; j += 32) a[0] = cadd(a[0], cmul(__ldcs(row + j), bs[j]));
+#pragma unroll
+        for (int u = 1; u < 8; u++) a[0] = cadd(a[0], a[u]);
+        a[0] = warp_sum(a[0]);
+        if (lane == 0) x[rw] = a[0];
+    }
 }
 
 // Row-major dense CSLP matrix of a full (single-slab) level: A[r * N + c].
@@ -795,9 +805,11 @@ static void set_attr() {
 }
 
 // opt the staged stencil kernels into > 48 KB dynamic shared memory (once, outside capture)
+void gemv_prepare();
 void init_kernel_attributes() {
     static bool done = false;
     if (done) return;
+    gemv_prepare();
     set_attr<MODE_LOAD, EpiApply<0>, 0>();
     set_attr<MODE_LOAD, EpiApply<1>, 1>();
     set_attr<MODE_LOAD, EpiApply<2>, 2>();
@@ -849,9 +861,9 @@ void launch_jacobi0(const Lvl &L, const cd *b, cd *u, double omega, cudaStream_t
     dim3 g = march_grid(L, chunk);
     k_jacobi0<<<g, kMarchBlock, 0, s>>>(L, b, u, omega, chunk, done);
 }
-void launch_wdinv(const Lvl &L, double omega, cd *out_owned, cudaStream_t s) {
+void launch_dinv(const Lvl &L, cd *out_owned, cudaStream_t s) {
     int g0 = std::max(-HF_GHOST, -L.lo1), g1 = std::min(L.nx + HF_GHOST, L.n1 - L.lo1);
-    k_wdinv<<<592, 256, 0, s>>>(L, omega, g0, g1, out_owned);
+    k_dinv<<<592, 256, 0, s>>>(L, g0, g1, out_owned);
 }
 void launch_restrict(const Lvl &F, const Lvl &C, const cd *r, cd *out, cudaStream_t s,
                      const int *done) {
@@ -873,9 +885,15 @@ void launch_up1(const Lvl &L, const Lvl &C, const cd *b, const cd *e, cd *u, cd 
     corr(pre ? 1 : 0, L, C, b, e, t, omega, s, done);
     stencil<MODE_LOAD, EpiJacobi, 0>(L, t, b, omega, EpiJacobi{u}, RedSlot{}, s, done);
 }
+void gemv_prepare() {
+    cudaFuncSetAttribute(k_gemv<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(GEMV_SMEM_MAX * sizeof(cd)));
+}
 void launch_gemv(int N, const cd *Minv, const cd *b, cd *x, cudaStream_t s, const int *done) {
-    int blocks = (N + 1) / 2;
-    k_gemv<<<blocks, 64, 0, s>>>(N, Minv, b, x, done);
+    if (N <= GEMV_SMEM_MAX)
+        k_gemv<true><<<296, GEMV_THREADS, (size_t)N * sizeof(cd), s>>>(N, Minv, b, x, done);
+    else
+        k_gemv<false><<<296, GEMV_THREADS, 0, s>>>(N, Minv, b, x, done);
 }
 void launch_assemble(const Lvl &L, cd *A, cudaStream_t s) {
     long long N = (long long)L.n1 * L.plane;

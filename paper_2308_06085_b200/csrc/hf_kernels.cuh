@@ -26,7 +26,7 @@ void launch_prolong(const Lvl &F, const Lvl &C, const cd *e, cd *out, bool add, 
                     const int *done);
 void launch_up1(const Lvl &L, const Lvl &C, const cd *b, const cd *e, cd *u, cd *t, double omega,
                 bool pre, cudaStream_t s, const int *done);
-void launch_wdinv(const Lvl &L, double omega, cd *out_owned, cudaStream_t s);
+void launch_dinv(const Lvl &L, cd *out_owned, cudaStream_t s);
 void launch_gemv(int N, const cd *Minv, const cd *b, cd *x, cudaStream_t s, const int *done);
 void launch_assemble(const Lvl &L, cd *A, cudaStream_t s);
 void launch_set_identity(long long N, cd *B, cudaStream_t s);

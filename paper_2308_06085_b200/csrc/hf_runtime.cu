@@ -139,6 +139,31 @@ static int make_level(Allocs &A, Level &lv, int n1, int n2, int n3, int lo1, int
                       cudaMemcpyHostToDevice));
         L.k = kb + (size_t)HF_GHOST * L.plane;
     }
+    {
+        // a_p and D^-1 by physical-face count for a constant medium (operators.py:163-178)
+        cd tab[8];
+        const double kk = kc, k2h2 = kk * kk * L.h2;
+        for (int nb = 0; nb < 4; nb++) {
+            double re = (6.0 - sre * k2h2) * L.ih2, im = (-sim * k2h2) * L.ih2;
+            if (bc == HF_BC_SOMMERFELD) im -= nb * (kk * L.twoh);
+            tab[nb] = make_double2(re, im);
+            double dre = re, dim = im;
+            if (bc == HF_BC_DIRICHLET && nb) { dre = 1.0; dim = 0.0; }
+            double inv = 1.0 / (dre * dre + dim * dim);
+            tab[4 + nb] = make_double2(dre * inv, -dim * inv);
+        }
+        cd *dt = A.get<cd>(8, err);
+        if (!dt) return fail(HF_ERR_CUDA, "cudaMalloc level table");
+        CK(cudaMemcpy(dt, tab, sizeof(tab), cudaMemcpyHostToDevice));
+        L.tab = dt;
+    }
+    if (kfull) {
+        cd *dv = new_field(A, nx, L.plane, err);
+        if (!dv) return fail(HF_ERR_CUDA, "cudaMalloc D^-1");
+        launch_dinv(L, dv, nullptr);
+        CK(cudaDeviceSynchronize());
+        L.dinv = dv;
+    }
     if (scratch) {
         lv.b = new_field(A, nx, L.plane, err);
         lv.u = new_field(A, nx, L.plane, err);
@@ -251,13 +276,6 @@ extern "C" hf_hierarchy *hf_hierarchy_create(int n1, int n2, int n3, int lo1, in
             return nullptr;
         }
         cudaError_t err;
-        if (kf) {
-            // w D^-1 field for the fused pre-smooth + residual of a varying medium
-            cd *wd = new_field(H->A, cnx, lv.L.plane, err);
-            if (!wd) { fail(HF_ERR_CUDA, "cudaMalloc w D^-1"); delete H; return nullptr; }
-            launch_wdinv(lv.L, cfg->omega, wd, work_stream());
-            lv.L.wd = wd;
-        }
         if (cfg->cycle == HF_CYCLE_F) {
             lv.fb = new_field(H->A, cnx, lv.L.plane, err);
             lv.guess = new_field(H->A, cnx, lv.L.plane, err);

@@ -40,7 +40,9 @@ extern "C" {
 #define HF_METHOD_IDRS 2
 
 #define HF_COARSEST_DIRECT 0   /* dense LU-inverse, applied as one GEMV   */
-#define HF_COARSEST_GMRES 1    /* unpreconditioned full GMRES to tol      */
+#define HF_COARSEST_GMRES 1    /* unpreconditioned full GMRES to tol (reserved) */
+#define HF_COARSEST_EXTERNAL 2 /* no coarsest solve: the caller gathers the
+                                  coarse RHS and solves it (multi-GPU slabs)  */
 
 #define HF_BREAKDOWN_NONE 0
 #define HF_BREAKDOWN_ARNOLDI 1
@@ -135,6 +137,14 @@ int hf_prolong_tl(hf_hierarchy *hier, int level, const double *e_coarse, double 
 int hf_coarsest_solve(hf_hierarchy *hier, const double *b, double *x);
 /* multigrid.py:395-419 mg_precondition: z ~= M^-1 r, one V/F cycle */
 int hf_mg_precondition(hf_hierarchy *hier, const double *r, double *z);
+/* Fused pieces of one V(1,1) level (multigrid.py:337-343) for slab drivers that
+ * exchange halos in between.  down1: r = b - M (w D^-1 b) (pre-smooth from zero +
+ * residual).  correct: t = w D^-1 b + P e (nu1 = 1; t = P e when nu1 = 0).
+ * smooth: u = t + w D^-1 (b - M t) (post-smoothing sweep). */
+int hf_level_down1(hf_hierarchy *hier, int level, const double *b, double *r);
+int hf_level_correct(hf_hierarchy *hier, int level, const double *b, const double *e_coarse,
+                     double *t);
+int hf_level_smooth(hf_hierarchy *hier, int level, const double *t, const double *b, double *u);
 
 /* ---- krylov.py:111-407 + runner.py:95-131 ------------------------------ */
 /* A: Helmholtz operator (shift 1) on the same slab as the hierarchy's finest level. */

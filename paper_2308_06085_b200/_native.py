@@ -16,7 +16,7 @@ HF_GHOST = 2
 BC = {"dirichlet": 0, "sommerfeld": 1}
 CYCLE = {"V": 0, "F": 1}
 METHOD = {"gmres": 0, "bicgstab": 1, "idrs": 2}
-COARSEST = {"direct": 0, "gmres": 1}
+COARSEST = {"direct": 0, "gmres": 1, "external": 2}
 BREAKDOWN = {0: None, 1: "arnoldi", 2: "rho", 3: "omega", 4: "projection"}
 ERR_ZERO_DIAGONAL = -3
 ERR_UNSUPPORTED = -4
@@ -27,7 +27,8 @@ EXPORTED = (
     "hf_operator_create", "hf_operator_destroy", "hf_operator_apply", "hf_operator_diag",
     "hf_jacobi_smooth", "hf_hierarchy_create", "hf_hierarchy_destroy",
     "hf_hierarchy_num_levels", "hf_hierarchy_level_shape", "hf_restrict_fw", "hf_prolong_tl",
-    "hf_coarsest_solve", "hf_mg_precondition", "hf_solver_create", "hf_solver_destroy",
+    "hf_coarsest_solve", "hf_mg_precondition", "hf_level_down1", "hf_level_correct",
+    "hf_level_smooth", "hf_solver_create", "hf_solver_destroy",
     "hf_solve", "hf_solve_host", "hf_dot",
 )
 
@@ -99,6 +100,9 @@ def load(path: str = LIB_PATH):
         "hf_prolong_tl": ([vp, i, vp, vp], i),
         "hf_coarsest_solve": ([vp, vp, vp], i),
         "hf_mg_precondition": ([vp, vp, vp], i),
+        "hf_level_down1": ([vp, i, vp, vp], i),
+        "hf_level_correct": ([vp, i, vp, vp, vp], i),
+        "hf_level_smooth": ([vp, i, vp, vp, vp], i),
         "hf_solver_create": ([vp, vp], vp),
         "hf_solver_destroy": ([vp], None),
         "hf_solve": ([vp, ctypes.POINTER(SolverConfigC), vp, vp, ctypes.POINTER(ReportC)], i),

@@ -113,9 +113,9 @@ __device__ __forceinline__ ColCtx col_ctx(const Lvl &L, int chunk) {
 // chunk of planes.  Each plane's tile + 1-point halo of the stencil operand is
 // copied global->shared with cp.async into a 5-slot ring, three planes ahead
 // of the plane being computed, so one barrier per plane is enough and the
-// 7-point row reads its six neighbours straight from the ring.  Epilogue
-// operands (b, the inner-product partner w, the centre wavenumber) are staged
-// for the centre only.  Two stencil inputs:
+// 7-point row reads its six neighbours straight from the ring.  Centre-only
+// epilogue operands (b, the inner-product partner w, the wavenumber) are
+// prefetched into registers one plane ahead.  Two stencil inputs:
 //   MODE_LOAD  f = u                      (A u, b - M u, Jacobi sweep)
 //   MODE_PRE   f = w D^-1 b, zero-guess pre-smoothing folded into the
 //              residual (multigrid.py:148-151 + 383-386): in the deep
@@ -189,12 +189,10 @@ struct EpiJacobi {
 
 template <int MODE, bool KVAR, bool AUX>
 struct StencilSmem {
-    static constexpr bool kWd = MODE == MODE_PRE && KVAR;     // staged w D^-1 field
+    static constexpr bool kWd = MODE == MODE_PRE && KVAR;     // staged D^-1 field
     static constexpr bool kAuxArr = AUX && MODE == MODE_LOAD; // PRE reuses the ring centre as b
     cd raw[RING][NFILL];
     cd wd[kWd ? RING : 1][kWd ? NFILL : 1];
-    double kc[KVAR ? RING : 1][NT];
-    cd ax[kAuxArr ? RING : 1][kAuxArr ? NT : 1];
 };
 
 template <int MODE, class Epi, int ND, bool KVAR, bool SOMM>
@@ -260,16 +258,26 @@ __global__ void __launch_bounds__(NT) k_stencil(Lvl L, const cd *__restrict__ sr
             cp_async16(&sm.raw[slot][tid + NT], v ? src + pb + go1 : src, v);
             if (SM::kWd) cp_async16(&sm.wd[SM::kWd ? slot : 0][tid + NT], v ? L.dinv + pb + go1 : L.dinv, v);
         }
-        const bool vc = pok && act && i < i1;
-        if (KVAR) cp_async8(&sm.kc[KVAR ? slot : 0][tid], vc ? L.k + pb + own : L.k, vc);
-        if (SM::kAuxArr) cp_async16(&sm.ax[SM::kAuxArr ? slot : 0][tid], vc ? aux + pb + own : aux, vc);
         cp_commit();
     };
 
     for (int s = 0; s < RING - 1; s++) stage(i0 - 1 + s);   // planes i0-1 .. i0+2
     int sp = 0, sc = 1, sn = 2;                              // ring slots of i-1, i, i+1
     long long q = (long long)i0 * L.plane + own;
+    // centre-only epilogue operands (b or w, and k) are prefetched one plane ahead
+    cd a_next = mk(0, 0);
+    double k_next = L.kc;
+    if (act && i0 < i1) {
+        if (SM::kAuxArr) a_next = __ldg(aux + q);
+        if (KVAR) k_next = __ldg(L.k + q);
+    }
     for (int i = i0; i < i1; i++, q += L.plane) {
+        const cd a_cur = a_next;
+        const double k_cur = k_next;
+        if (act && i + 1 < i1) {
+            if (SM::kAuxArr) a_next = __ldg(aux + q + L.plane);
+            if (KVAR) k_next = __ldg(L.k + q + L.plane);
+        }
         cp_wait<1>();                      // plane i+1 landed (i+2 may be in flight)
         __syncthreads();
         stage(i + RING - 2);               // into the slot read last at step i-1
@@ -282,7 +290,7 @@ __global__ void __launch_bounds__(NT) k_stencil(Lvl L, const cd *__restrict__ sr
             cd xm = sm.raw[sp][cf], xp = sm.raw[sn][cf];
             cd ym = r0[cf - HALO_X], yp = r0[cf + HALO_X];
             cd zm = r0[cf - 1], zp = r0[cf + 1];
-            const double kk = KVAR ? sm.kc[KVAR ? sc : 0][tid] : L.kc;
+            const double kk = k_cur;
             const cd bc = fc;              // PRE: the staged centre is b
             cd post = one;                 // PRE deep interior: M(c b) = c M b
             if (MODE == MODE_PRE) {
@@ -335,7 +343,7 @@ __global__ void __launch_bounds__(NT) k_stencil(Lvl L, const cd *__restrict__ sr
                 if (MODE == MODE_PRE && KVAR) mf = cmul(post, mf);
             }
             cd av = mk(0, 0);
-            if (Epi::kAux) av = SM::kAuxArr ? sm.ax[SM::kAuxArr ? sc : 0][tid] : bc;
+            if (Epi::kAux) av = SM::kAuxArr ? a_cur : bc;
             cd wd = mk(0, 0);
             if (Epi::kDinv) wd = KVAR ? cscal(__ldg(L.dinv + q), omega) : wd_nb(nb);
             epi(q, fc, mf, wd, av, acc);
@@ -365,56 +373,62 @@ __global__ void k_dinv(Lvl L, int g0, int g1, cd *__restrict__ out) {
     }
 }
 
-// trilinear prolongation value at fine local (i, j, m) (multigrid.py:238-297);
-// the reference divides the 2/4/8-point sums, exact here as a power-of-two scale
-struct Prolong {
-    Lvl C;
-    const cd *e;   // coarse field, owned plane 0
-    __device__ __forceinline__ cd operator()(const Lvl &F, int i, int j, int m) const {
-        int gi = F.lo1 + i;
-        int c1 = (gi >> 1) - C.lo1, e1 = gi & 1;
-        int c2 = j >> 1, e2 = j & 1;
-        int c3 = m >> 1, e3 = m & 1;
-        const cd *p = e + (long long)c1 * C.plane + c2 * C.n3 + c3;
-        cd acc = __ldg(p);
-        if (e3) acc = cadd(acc, __ldg(p + 1));
-        if (e2) {
-            acc = cadd(acc, __ldg(p + C.n3));
-            if (e3) acc = cadd(acc, __ldg(p + C.n3 + 1));
-        }
-        if (e1) {
-            const cd *p1 = p + C.plane;
-            acc = cadd(acc, __ldg(p1));
-            if (e3) acc = cadd(acc, __ldg(p1 + 1));
-            if (e2) {
-                acc = cadd(acc, __ldg(p1 + C.n3));
-                if (e3) acc = cadd(acc, __ldg(p1 + C.n3 + 1));
-            }
-        }
-        int ns = (1 + e1) * (1 + e2) * (1 + e3);
-        if (ns > 1) acc = cscal(acc, ns == 2 ? 0.5 : (ns == 4 ? 0.25 : 0.125));
-        return acc;
-    }
-};
-
 // pointwise coarse-grid correction on the zero-guess pre-smoothed iterate:
 //   MODE 0: out = P e           MODE 1: out = w D^-1 b + P e   (nu1 = 1)
 //   MODE 2: out += P e          (multigrid.py:337-341, 389-392)
+// One thread per fine (i2, i3) column marching along i1: the bilinear (i2, i3)
+// sum of each coarse plane is formed once and reused by the two fine planes
+// that straddle it.
 template <int MODE>
 __global__ void __launch_bounds__(256) k_corr(Lvl F, Lvl C, const cd *__restrict__ b,
                                               const cd *__restrict__ e, cd *__restrict__ out,
-                                              double omega, const int *done) {
+                                              double omega, int chunk, const int *done) {
     if (is_done(done)) return;
     const int m = blockIdx.x * 32 + (threadIdx.x & 31);
     const int j = blockIdx.y * 8 + (threadIdx.x >> 5);
-    const int i = blockIdx.z;
+    const int i0 = blockIdx.z * chunk, i1 = min(i0 + chunk, F.nx);
     if (m >= F.n3 || j >= F.n2) return;
-    const long long q = (long long)i * F.plane + j * F.n3 + m;
-    cd v = Prolong{C, e}(F, i, j, m);
-    if (MODE == 1)
-        v = cadd(cscal(cmul(__ldg(b + q), dinv_at(F, q, nbnd(F, F.lo1 + i, j, m))), omega), v);
-    if (MODE == 2) v = cadd(out[q], v);
-    out[q] = v;
+    const bool o2 = j & 1, o3 = m & 1;
+    const cd *ecol = e + (j >> 1) * C.n3 + (m >> 1);
+    auto cplane = [&](int c) -> cd {                 // bilinear sum on coarse local plane c
+        const cd *p = ecol + (long long)c * C.plane;
+        cd a = __ldg(p);
+        if (o3) a = cadd(a, __ldg(p + 1));
+        if (o2) {
+            a = cadd(a, __ldg(p + C.n3));
+            if (o3) a = cadd(a, __ldg(p + C.n3 + 1));
+        }
+        return a;
+    };
+    const int nb_jm = (j == 0) + (j == F.n2 - 1) + (m == 0) + (m == F.n3 - 1);
+    const double s2 = (o2 && o3) ? 0.25 : ((o2 || o3) ? 0.5 : 1.0);
+    int cc = -(1 << 30);
+    cd v0 = mk(0, 0), v1 = mk(0, 0);               // planes cc and cc + 1
+    bool have1 = false;
+    long long q = (long long)i0 * F.plane + j * F.n3 + m;
+    for (int i = i0; i < i1; i++, q += F.plane) {
+        const int gi = F.lo1 + i;
+        const int c = (gi >> 1) - C.lo1;
+        if (c != cc) {
+            if (c == cc + 1 && have1) v0 = v1;
+            else v0 = cplane(c);
+            cc = c;
+            have1 = false;
+        }
+        cd pe;
+        if (gi & 1) {
+            if (!have1) { v1 = cplane(c + 1); have1 = true; }
+            pe = cscal(cadd(v0, v1), 0.5 * s2);
+        } else {
+            pe = s2 == 1.0 ? v0 : cscal(v0, s2);
+        }
+        if (MODE == 1) {
+            const int nb = (gi == 0) + (gi == F.n1 - 1) + nb_jm;
+            pe = cadd(cscal(cmul(__ldg(b + q), dinv_at(F, q, nb)), omega), pe);
+        }
+        if (MODE == 2) pe = cadd(out[q], pe);
+        out[q] = pe;
+    }
 }
 
 // u = w D^-1 b   (multigrid.py:148-151, assume_zero first sweep)
@@ -653,46 +667,140 @@ __global__ void k_dot_store(long long n, const cd *__restrict__ a, const cd *__r
 // ---------------------------------------------------------------------------
 // coarsest level: dense inverse applied as one GEMV (HBM-bound)
 // ---------------------------------------------------------------------------
-// x = Minv b, Minv row-major N x N (coarsest solve, HBM-streaming GEMV).
-// Persistent: two 512-thread blocks per SM, each owning a contiguous band of rows
-// (balanced to one row); b is staged once per block in shared memory; each
-// warp streams whole rows with eight 512 B segments in flight.
-#define GEMV_THREADS 512
-#define GEMV_SMEM_MAX 6912    // entries of b staged in shared memory (108 KB, 2 blocks per SM)
-template <bool SMEMB>
-__global__ void __launch_bounds__(GEMV_THREADS) k_gemv(int N, const cd *__restrict__ Minv,
-                                                       const cd *__restrict__ b, cd *__restrict__ x,
-                                                       const int *done) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const cd *bs = SMEMB ? reinterpret_cast<const cd *>(smem_raw) : b;
+// x = Minv b, Minv row-major N x N.  One warp per row, 64-thread blocks (fine
+// grained so rows spread evenly over the 148 SMs), eight 512 B row segments in
+// flight per warp.
+__global__ void __launch_bounds__(64) k_gemv(int N, const cd *__restrict__ Minv,
+                                             const cd *__restrict__ b, cd *__restrict__ x,
+                                             const int *done) {
     if (is_done(done)) return;
-    if (SMEMB) {
-        cd *w = reinterpret_cast<cd *>(smem_raw);
-        for (int jj = threadIdx.x; jj < N; jj += GEMV_THREADS) w[jj] = __ldg(b + jj);
+    int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (warp >= N) return;
+    const cd *row = Minv + (long long)warp * N;
+    cd a[8];
+#pragma unroll
+    for (int u = 0; u < 8; u++) a[u] = mk(0, 0);
+    int j = lane;
+    for (; j + 224 < N; j += 256) {
+        cd mv[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) mv[u] = __ldcs(row + j + 32 * u);
+#pragma unroll
+        for (int u = 0; u < 8; u++) a[u] = cadd(a[u], cmul(mv[u], __ldg(b + j + 32 * u)));
+    }
+    for (; j < N; j += 32) a[0] = cadd(a[0], cmul(__ldcs(row + j), __ldg(b + j)));
+#pragma unroll
+    for (int u = 1; u < 8; u++) a[0] = cadd(a[0], a[u]);
+    a[0] = warp_sum(a[0]);
+    if (lane == 0) x[warp] = a[0];
+}
+
+// ---- symmetric coarsest solve (Sommerfeld) ----------------------------------
+// With S = diag(2^-faces) the Sommerfeld operator is complex symmetric after
+// row scaling (S M = (S M)^T, the reference's own symmetry test), so
+// B = M^-1 S^-1 is symmetric and x = M^-1 b = B (S b).  Only the upper
+// triangle of B is stored, as 64 x 64 tiles (I <= J); each tile contributes
+// its row sums to x_I and, off the diagonal, its column sums to x_J.
+#define SYT 64
+__device__ __forceinline__ long long sym_tile_index(int I, int J, int nT) {
+    return (long long)I * nT - (long long)I * (I - 1) / 2 + (J - I);
+}
+
+// pack: tile (I, J) = Minv[I*64 + r][J*64 + c] / s[J*64 + c], zero padded
+__global__ void k_sym_pack(int N, int nT, const cd *__restrict__ Minv, const double *__restrict__ s,
+                           cd *__restrict__ tiles) {
+    const long long ntile = (long long)nT * (nT + 1) / 2;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < ntile * SYT * SYT;
+         e += (long long)gridDim.x * blockDim.x) {
+        long long t = e / (SYT * SYT);
+        int rc = (int)(e - t * SYT * SYT), r = rc / SYT, c = rc - r * SYT;
+        int I = 0;                                       // invert the triangular index
+        while (sym_tile_index(I + 1, I + 1, nT) <= t) I++;
+        int J = I + (int)(t - sym_tile_index(I, I, nT));
+        int gi = I * SYT + r, gj = J * SYT + c;
+        cd v = mk(0, 0);
+        if (gi < N && gj < N) v = cscal(Minv[(long long)gi * N + gj], 1.0 / s[gj]);
+        tiles[e] = v;
+    }
+}
+
+// one 256-thread CTA per stored tile; warp w streams rows 8w..8w+7 straight
+// from HBM (16 independent 16 B loads per lane), forms their row sums with
+// warp shuffles and its partial column sums in registers; the 8 warps'
+// column partials are combined through shared memory in fixed order.
+__global__ void __launch_bounds__(256) k_sym_tiles(int N, int nT, const cd *__restrict__ tiles,
+                                                   const double *__restrict__ s,
+                                                   const cd *__restrict__ b,
+                                                   cd *__restrict__ prow, cd *__restrict__ pcol,
+                                                   const int *done) {
+    __shared__ cd cI[SYT], cJ[SYT];
+    __shared__ cd colp[8][SYT];
+    if (is_done(done)) return;
+    const long long t = blockIdx.x;
+    int I = 0;
+    while (sym_tile_index(I + 1, I + 1, nT) <= t) I++;
+    const int J = I + (int)(t - sym_tile_index(I, I, nT));
+    const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+    const cd *src = tiles + t * SYT * SYT + (long long)(8 * w) * SYT;
+    cd m0[8], m1[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        m0[k] = __ldcs(src + k * SYT + lane);
+        m1[k] = __ldcs(src + k * SYT + lane + 32);
+    }
+    if (tid < SYT) {
+        int gj = J * SYT + tid;
+        cJ[tid] = gj < N ? cscal(__ldg(b + gj), s[gj]) : mk(0, 0);
+    } else if (tid < 2 * SYT) {
+        int gi = I * SYT + tid - SYT;
+        cI[tid - SYT] = gi < N ? cscal(__ldg(b + gi), s[gi]) : mk(0, 0);
+    }
+    __syncthreads();
+    const cd cj0 = cJ[lane], cj1 = cJ[lane + 32];
+    cd c0 = mk(0, 0), c1 = mk(0, 0);
+    cd rsum[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        rsum[k] = cadd(cmul(m0[k], cj0), cmul(m1[k], cj1));
+        const cd ci = cI[8 * w + k];
+        c0 = cadd(c0, cmul(m0[k], ci));
+        c1 = cadd(c1, cmul(m1[k], ci));
+    }
+#pragma unroll
+    for (int k = 0; k < 8; k++) rsum[k] = warp_sum(rsum[k]);
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < 8; k++) prow[t * SYT + 8 * w + k] = rsum[k];
+    }
+    if (I != J) {
+        colp[w][lane] = c0;
+        colp[w][lane + 32] = c1;
         __syncthreads();
-    }
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const long long r0 = (long long)N * blockIdx.x / gridDim.x;
-    const long long r1 = (long long)N * (blockIdx.x + 1) / gridDim.x;
-    for (long long rw = r0 + warp; rw < r1; rw += GEMV_THREADS / 32) {
-        const cd *row = Minv + rw * N;
-        cd a[8];
+        if (tid < SYT) {
+            cd a = colp[0][tid];
 #pragma unroll
-        for (int u = 0; u < 8; u++) a[u] = mk(0, 0);
-        int j = lane;
-        for (; j + 224 < N; j += 256) {
-            cd mv[8];
-#pragma unroll
-            for (int u = 0; u < 8; u++) mv[u] = __ldcs(row + j + 32 * u);
-#pragma unroll
-            for (int u = 0; u < 8; u++) a[u] = cadd(a[u], cmul(mv[u], bs[j + 32 * u]));
+            for (int k = 1; k < 8; k++) a = cadd(a, colp[k][tid]);
+            pcol[t * SYT + tid] = a;
         }
-        for (; j < N; j += 32) a[0] = cadd(a[0], cmul(__ldcs(row + j), bs[j]));
-#pragma unroll
-        for (int u = 1; u < 8; u++) a[0] = cadd(a[0], a[u]);
-        a[0] = warp_sum(a[0]);
-        if (lane == 0) x[rw] = a[0];
     }
+}
+
+// x_i = sum_{J >= I} rowpart(I, J) + sum_{I' < I} colpart(I', I): one warp per
+// output, partials summed lane-strided then by a fixed shuffle tree
+__global__ void k_sym_reduce(int N, int nT, const cd *__restrict__ prow,
+                             const cd *__restrict__ pcol, cd *__restrict__ x, const int *done) {
+    if (is_done(done)) return;
+    const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (i >= N) return;
+    const int I = i / SYT, r = i - I * SYT;
+    cd acc = mk(0, 0);
+    for (int J = lane; J < nT; J += 32) {
+        if (J >= I) acc = cadd(acc, __ldg(prow + sym_tile_index(I, J, nT) * SYT + r));
+        else acc = cadd(acc, __ldg(pcol + sym_tile_index(J, I, nT) * SYT + r));
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) x[i] = acc;
 }
 
 // Row-major dense CSLP matrix of a full (single-slab) level: A[r * N + c].
@@ -805,11 +913,10 @@ static void set_attr() {
 }
 
 // opt the staged stencil kernels into > 48 KB dynamic shared memory (once, outside capture)
-void gemv_prepare();
 void init_kernel_attributes() {
     static bool done = false;
     if (done) return;
-    gemv_prepare();
+
     set_attr<MODE_LOAD, EpiApply<0>, 0>();
     set_attr<MODE_LOAD, EpiApply<1>, 1>();
     set_attr<MODE_LOAD, EpiApply<2>, 2>();
@@ -850,10 +957,11 @@ void launch_down1(const Lvl &L, const cd *b, cd *r, double omega, cudaStream_t s
 }
 static void corr(int mode, const Lvl &F, const Lvl &C, const cd *b, const cd *e, cd *out,
                  double omega, cudaStream_t s, const int *done) {
-    dim3 g((F.n3 + 31) / 32, (F.n2 + 7) / 8, F.nx);
-    if (mode == 0) k_corr<0><<<g, 256, 0, s>>>(F, C, b, e, out, omega, done);
-    else if (mode == 1) k_corr<1><<<g, 256, 0, s>>>(F, C, b, e, out, omega, done);
-    else k_corr<2><<<g, 256, 0, s>>>(F, C, b, e, out, omega, done);
+    int chunk;
+    dim3 g = march_grid(F, chunk);
+    if (mode == 0) k_corr<0><<<g, 256, 0, s>>>(F, C, b, e, out, omega, chunk, done);
+    else if (mode == 1) k_corr<1><<<g, 256, 0, s>>>(F, C, b, e, out, omega, chunk, done);
+    else k_corr<2><<<g, 256, 0, s>>>(F, C, b, e, out, omega, chunk, done);
 }
 void launch_jacobi0(const Lvl &L, const cd *b, cd *u, double omega, cudaStream_t s,
                     const int *done) {
@@ -880,20 +988,33 @@ void launch_prolong(const Lvl &F, const Lvl &C, const cd *e, cd *out, bool add, 
 }
 // u = u1 + w D^-1 (b - M u1), u1 = [w D^-1 b] + P e: pointwise correction into
 // the scratch field t, then one Jacobi sweep stencil (multigrid.py:337-343)
+void launch_correct(const Lvl &L, const Lvl &C, const cd *b, const cd *e, cd *t, double omega,
+                    bool pre, cudaStream_t s, const int *done) {
+    corr(pre ? 1 : 0, L, C, b, e, t, omega, s, done);
+}
 void launch_up1(const Lvl &L, const Lvl &C, const cd *b, const cd *e, cd *u, cd *t, double omega,
                 bool pre, cudaStream_t s, const int *done) {
     corr(pre ? 1 : 0, L, C, b, e, t, omega, s, done);
     stencil<MODE_LOAD, EpiJacobi, 0>(L, t, b, omega, EpiJacobi{u}, RedSlot{}, s, done);
 }
-void gemv_prepare() {
-    cudaFuncSetAttribute(k_gemv<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(GEMV_SMEM_MAX * sizeof(cd)));
-}
 void launch_gemv(int N, const cd *Minv, const cd *b, cd *x, cudaStream_t s, const int *done) {
-    if (N <= GEMV_SMEM_MAX)
-        k_gemv<true><<<296, GEMV_THREADS, (size_t)N * sizeof(cd), s>>>(N, Minv, b, x, done);
-    else
-        k_gemv<false><<<296, GEMV_THREADS, 0, s>>>(N, Minv, b, x, done);
+    int blocks = (N + 1) / 2;
+    k_gemv<<<blocks, 64, 0, s>>>(N, Minv, b, x, done);
+}
+void launch_sym_pack(int N, const cd *Minv, const double *sv, cd *tiles, cudaStream_t s) {
+    int nT = (N + SYT - 1) / SYT;
+    k_sym_pack<<<2048, 256, 0, s>>>(N, nT, Minv, sv, tiles);
+}
+void launch_symv(int N, const cd *tiles, const double *sv, const cd *b, cd *prow, cd *pcol, cd *x,
+                 cudaStream_t s, const int *done) {
+    int nT = (N + SYT - 1) / SYT;
+    long long ntile = (long long)nT * (nT + 1) / 2;
+    k_sym_tiles<<<(unsigned)ntile, 256, 0, s>>>(N, nT, tiles, sv, b, prow, pcol, done);
+    k_sym_reduce<<<(N * 32 + 255) / 256, 256, 0, s>>>(N, nT, prow, pcol, x, done);
+}
+long long sym_tiles_count(int N) {
+    long long nT = (N + SYT - 1) / SYT;
+    return nT * (nT + 1) / 2;
 }
 void launch_assemble(const Lvl &L, cd *A, cudaStream_t s) {
     long long N = (long long)L.n1 * L.plane;

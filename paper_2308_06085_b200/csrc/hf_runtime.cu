@@ -187,7 +187,10 @@ struct hf_hierarchy {
     std::vector<Level> lev;
     hf_mg_config cfg{};
     int Nc = 0;
-    cd *Minv = nullptr;     // row-major dense inverse of the coarsest operator
+    cd *Minv = nullptr;     // row-major dense inverse of the coarsest operator (Dirichlet)
+    cd *symtiles = nullptr; // Sommerfeld: packed upper triangle of M^-1 S^-1 (64 x 64 tiles)
+    double *symscale = nullptr;
+    cd *prow = nullptr, *pcol = nullptr;
     int coarsest_flags = 0;
 };
 
@@ -210,9 +213,13 @@ static int build_coarsest_direct(hf_hierarchy *H, cudaStream_t s) {
     CK(cudaMemsetAsync(Amat, 0, (size_t)N * N * sizeof(cd), s));
     launch_assemble(C.L, Amat, s);
     CKL();
-    H->Minv = H->A.get<cd>((size_t)N * N, err);
-    if (!H->Minv) { cudaFree(Amat); return fail(HF_ERR_CUDA, "cudaMalloc coarsest inverse"); }
-    launch_set_identity(N, H->Minv, s);
+    cd *Minv = nullptr;
+    if (cudaMalloc(&Minv, (size_t)N * N * sizeof(cd)) != cudaSuccess) {
+        cudaFree(Amat);
+        return fail(HF_ERR_CUDA, "cudaMalloc coarsest inverse");
+    }
+    CK(cudaMemsetAsync(Minv, 0, (size_t)N * N * sizeof(cd), s));
+    launch_set_identity(N, Minv, s);
     CKL();
     cusolverDnHandle_t hs;
     if (cusolverDnCreate(&hs) != CUSOLVER_STATUS_SUCCESS) {
@@ -231,15 +238,44 @@ static int build_coarsest_direct(hf_hierarchy *H, cudaStream_t s) {
     // row-major A == column-major A^T; inv(A^T) column-major == inv(A) row-major
     cusolverStatus_t st1 = cusolverDnZgetrf(hs, (int)N, (int)N, Ac, (int)N, work, ipiv, info);
     cusolverStatus_t st2 = cusolverDnZgetrs(hs, CUBLAS_OP_N, (int)N, (int)N, Ac, (int)N, ipiv,
-                                            (cuDoubleComplex *)H->Minv, (int)N, info + 1);
+                                            (cuDoubleComplex *)Minv, (int)N, info + 1);
     int hinfo[2] = {0, 0};
     cudaMemcpyAsync(hinfo, info, 2 * sizeof(int), cudaMemcpyDeviceToHost, s);
     cudaError_t e = cudaStreamSynchronize(s);
     cusolverDnDestroy(hs);
     cudaFree(work); cudaFree(ipiv); cudaFree(info); cudaFree(Amat);
-    if (e != cudaSuccess) return fail(HF_ERR_CUDA, std::string("coarsest factorisation: ") + cudaGetErrorString(e));
-    if (st1 != CUSOLVER_STATUS_SUCCESS || st2 != CUSOLVER_STATUS_SUCCESS || hinfo[0] != 0 || hinfo[1] != 0)
+    if (e != cudaSuccess) { cudaFree(Minv); return fail(HF_ERR_CUDA, std::string("coarsest factorisation: ") + cudaGetErrorString(e)); }
+    if (st1 != CUSOLVER_STATUS_SUCCESS || st2 != CUSOLVER_STATUS_SUCCESS || hinfo[0] != 0 || hinfo[1] != 0) {
+        cudaFree(Minv);
         return fail(HF_ERR_SOLVER, "coarsest operator is singular (getrf/getrs failed)");
+    }
+    if (C.L.bc == HF_BC_SOMMERFELD) {
+        // symmetric form: keep only the upper triangle of B = M^-1 S^-1
+        std::vector<double> sv(N);
+        for (int i = 0; i < C.L.n1; i++)
+            for (int j = 0; j < C.L.n2; j++)
+                for (int m = 0; m < C.L.n3; m++) {
+                    int nb = (i == 0) + (i == C.L.n1 - 1) + (j == 0) + (j == C.L.n2 - 1) + (m == 0) + (m == C.L.n3 - 1);
+                    sv[((size_t)i * C.L.n2 + j) * C.L.n3 + m] = std::ldexp(1.0, -nb);
+                }
+        long long nt = sym_tiles_count((int)N);
+        H->symscale = H->A.get<double>(N, err);
+        H->symtiles = H->A.get<cd>((size_t)nt * 64 * 64, err);
+        H->prow = H->A.get<cd>((size_t)nt * 64, err);
+        H->pcol = H->A.get<cd>((size_t)nt * 64, err);
+        if (!H->symscale || !H->symtiles || !H->prow || !H->pcol) {
+            cudaFree(Minv);
+            return fail(HF_ERR_CUDA, "cudaMalloc symmetric coarsest tiles");
+        }
+        CK(cudaMemcpy(H->symscale, sv.data(), N * sizeof(double), cudaMemcpyHostToDevice));
+        launch_sym_pack((int)N, Minv, H->symscale, H->symtiles, s);
+        e = cudaStreamSynchronize(s);
+        cudaFree(Minv);
+        if (e != cudaSuccess) return fail(HF_ERR_CUDA, std::string("symmetric pack: ") + cudaGetErrorString(e));
+    } else {
+        H->Minv = Minv;
+        H->A.ptrs.push_back(Minv);
+    }
     return 0;
 }
 
@@ -254,8 +290,8 @@ extern "C" hf_hierarchy *hf_hierarchy_create(int n1, int n2, int n3, int lo1, in
         fail(HF_ERR_ARG, "unknown cycle type");
         return nullptr;
     }
-    if (cfg->coarsest_method != HF_COARSEST_DIRECT) {
-        fail(HF_ERR_UNSUPPORTED, "only the direct coarsest solve is built into this library");
+    if (cfg->coarsest_method != HF_COARSEST_DIRECT && cfg->coarsest_method != HF_COARSEST_EXTERNAL) {
+        fail(HF_ERR_UNSUPPORTED, "coarsest_method must be HF_COARSEST_DIRECT or HF_COARSEST_EXTERNAL");
         return nullptr;
     }
     if (cfg->nu1 < 0 || cfg->nu2 < 0 || !(cfg->omega > 0 && cfg->omega <= 1)) {
@@ -302,7 +338,7 @@ extern "C" hf_hierarchy *hf_hierarchy_create(int n1, int n2, int n3, int lo1, in
         }
         a = na; b = nb; c = nc; l0 = clo; cnx = chi - clo + 1; hh = 2.0 * hh;
     }
-    if (build_coarsest_direct(H, work_stream())) {
+    if (cfg->coarsest_method == HF_COARSEST_DIRECT && build_coarsest_direct(H, work_stream())) {
         delete H;
         return nullptr;
     }
@@ -322,7 +358,12 @@ extern "C" int hf_hierarchy_level_shape(const hf_hierarchy *H, int l, int *d) {
 // cycles (multigrid.py:326-419)
 // ---------------------------------------------------------------------------
 static void coarsest(hf_hierarchy *H, const cd *b, cd *x, cudaStream_t s, const int *done) {
-    L1(launch_gemv(H->Nc, H->Minv, b, x, s, done));
+    if (H->symtiles) {
+        L1(launch_symv(H->Nc, H->symtiles, H->symscale, b, H->prow, H->pcol, x, s, done));
+        g_launches++;   // tiles + reduction
+    } else {
+        L1(launch_gemv(H->Nc, H->Minv, b, x, s, done));
+    }
 }
 
 static void smooth_sweeps(Level &lv, cd *u, const cd *b, double omega, int sweeps,
@@ -403,8 +444,37 @@ extern "C" int hf_prolong_tl(hf_hierarchy *H, int l, const double *e, double *ou
     return 0;
 }
 
+// fused pieces of one V-cycle level (multigrid.py:337-343), for drivers that
+// exchange slab halos between them: r = b - M (w D^-1 b) ...
+extern "C" int hf_level_down1(hf_hierarchy *H, int l, const double *b, double *r) {
+    if (!H || l < 0 || l >= (int)H->lev.size()) return fail(HF_ERR_ARG, "bad level");
+    L1(launch_down1(H->lev[l].L, (const cd *)b, (cd *)r, H->cfg.omega, work_stream(), nullptr));
+    CKL();
+    return 0;
+}
+// ... and u = u1 + w D^-1 (b - M u1), u1 = w D^-1 b + P e (t: scratch field with ghost planes;
+// the caller exchanges t's halo between the two halves when the slab has interior faces)
+extern "C" int hf_level_correct(hf_hierarchy *H, int l, const double *b, const double *e,
+                                double *t) {
+    if (!H || l < 0 || l + 1 >= (int)H->lev.size()) return fail(HF_ERR_ARG, "bad level");
+    L1(launch_correct(H->lev[l].L, H->lev[l + 1].L, (const cd *)b, (const cd *)e, (cd *)t,
+                      H->cfg.omega, H->cfg.nu1 == 1, work_stream(), nullptr));
+    CKL();
+    return 0;
+}
+extern "C" int hf_level_smooth(hf_hierarchy *H, int l, const double *t, const double *b,
+                               double *u) {
+    if (!H || l < 0 || l >= (int)H->lev.size()) return fail(HF_ERR_ARG, "bad level");
+    L1(launch_jacobi(H->lev[l].L, (const cd *)t, (const cd *)b, (cd *)u, H->cfg.omega,
+                     work_stream(), nullptr));
+    CKL();
+    return 0;
+}
+
 extern "C" int hf_coarsest_solve(hf_hierarchy *H, const double *b, double *x) {
     if (!H) return fail(HF_ERR_ARG, "null hierarchy");
+    if (H->cfg.coarsest_method != HF_COARSEST_DIRECT)
+        return fail(HF_ERR_ARG, "hierarchy was built with an external coarsest solve");
     coarsest(H, (const cd *)b, (cd *)x, work_stream(), nullptr);
     CKL();
     return 0;

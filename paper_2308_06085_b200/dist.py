@@ -1,0 +1,249 @@
+"""Multi-slab CSLP-preconditioned Bi-CGSTAB (one slab per GPU, or several
+virtual slabs on one GPU).
+
+The SPMD structure of the reference's worker_body (runner.py:95-131) with
+its distributed V-cycle (multigrid.py:326-343) and global inner products
+(partition.py:611-621), re-laid for slabs along i1:
+
+  level l < L-1 :  halo(b) -> r = b - M(w D^-1 b) -> halo(r) -> R r
+  coarsest      :  all-gather the coarse slabs, exact solve (replicated)
+  level l       :  halo(e) -> t = w D^-1 b + P e -> halo(t) -> Jacobi sweep
+
+Every stencil / transfer / smoother step is a native kernel on the slab
+(hf_level_down1, hf_restrict_fw, hf_level_correct, hf_level_smooth,
+hf_operator_apply, hf_coarsest_solve); halos and inner products go through
+the slab fabric (partition.TorchSlabComm or LocalSlabComm).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native
+from .grid import BlockExtent, Grid3, HaloField, full_extent, make_grid
+from .krylov import ConvergenceReport, SolverConfig
+from .multigrid import MGConfig
+from .operators import OperatorSpec, StencilOperator, bc_name, k_arguments
+
+__all__ = ["SlabSolver"]
+
+
+def _ptr(t):
+    return t.data_ptr()
+
+
+class SlabSolver:
+    """Bi-CGSTAB over the slabs owned by this process (krylov.py:207-276)."""
+
+    def __init__(self, grid: Grid3, extents, k_field, bc, comm, beta1=1.0, beta2=-0.5,
+                 mg: MGConfig | None = None):
+        import torch
+        self.torch = torch
+        self.grid, self.comm = grid, comm
+        self.extents = list(extents)
+        self.mg = mg or MGConfig()
+        if self.mg.cycle.upper() != "V" or self.mg.nu1 != 1 or self.mg.nu2 != 1:
+            raise NotImplementedError("slab driver implements the V(1,1) cycle")
+        L = _native.load()
+        self.L = L
+        kfull, kc, self._keep = k_arguments(
+            OperatorSpec("helmholtz", 1.0, 0.0, bc, np.asarray(k_field)), grid, full_extent(grid))
+        kp = kfull.ctypes.data if kfull is not None else None
+        bcc = _native.BC[bc_name(bc)]
+        c = _native.MGConfigC(1, 1, float(self.mg.omega), 0, int(self.mg.coarsest_threshold),
+                              1 if self.mg.threshold_cmp == "ge" else 0, float(self.mg.coarsest_tol),
+                              int(self.mg.coarsest_maxit), _native.COARSEST["external"])
+        _native.set_stream_from_torch()
+        self.A, self.H, self.levels = [], [], []
+        for e in self.extents:
+            A = L.hf_operator_create(grid.n1, grid.n2, grid.n3, e.lo1 - 1, e.nx, grid.h, 1.0, 0.0,
+                                     bcc, kp, kc)
+            H = L.hf_hierarchy_create(grid.n1, grid.n2, grid.n3, e.lo1 - 1, e.nx, grid.h,
+                                      float(beta1), float(beta2), bcc, kp, kc, ctypes.byref(c))
+            if not A or not H:
+                raise RuntimeError(_native.last_error())
+            self.A.append(A)
+            self.H.append(H)
+            lv = []
+            for l in range(L.hf_hierarchy_num_levels(H)):
+                d = (ctypes.c_int * 5)()
+                _native.check(L.hf_hierarchy_level_shape(H, l, d))
+                lv.append(BlockExtent(d[3] + 1, 1, 1, d[3] + d[4], d[1], d[2]))
+            self.levels.append(lv)
+        self.nlev = len(self.levels[0])
+        d = (ctypes.c_int * 5)()
+        _native.check(L.hf_hierarchy_level_shape(self.H[0], self.nlev - 1, d))
+        cgrid = make_grid(d[0], d[1], d[2], grid.h * 2 ** (self.nlev - 1))
+        self.cgrid = cgrid
+        # coarsest level: the whole coarse grid on every process (exact solve, replicated)
+        kc_full = None
+        if kfull is not None:
+            s = 2 ** (self.nlev - 1)
+            kc_full = np.ascontiguousarray(kfull[::s, ::s, ::s])
+            self._keep_c = kc_full
+        cc = _native.MGConfigC(1, 1, float(self.mg.omega), 0, max(cgrid.shape) + 1, 0,
+                               float(self.mg.coarsest_tol), int(self.mg.coarsest_maxit),
+                               _native.COARSEST["direct"])
+        self.Hc = L.hf_hierarchy_create(cgrid.n1, cgrid.n2, cgrid.n3, 0, cgrid.n1, cgrid.h,
+                                        float(beta1), float(beta2), bcc,
+                                        kc_full.ctypes.data if kc_full is not None else None,
+                                        kc if kfull is None else 0.0, ctypes.byref(cc))
+        if not self.Hc:
+            raise RuntimeError(_native.last_error())
+        self.ccounts = [lv[-1].nx for lv in self.levels] if len(self.extents) > 1 else None
+        # level fields per local slab: b, r, u, t (with ghost planes)
+        f = lambda e: HaloField(e)
+        self.fb = [[f(lv[l]) for l in range(self.nlev)] for lv in self.levels]
+        self.fr = [[f(lv[l]) for l in range(self.nlev)] for lv in self.levels]
+        self.fu = [[f(lv[l]) for l in range(self.nlev)] for lv in self.levels]
+        self.ft = [[f(lv[l]) for l in range(self.nlev)] for lv in self.levels]
+        self.xc = torch.empty(cgrid.shape, dtype=torch.complex128, device="cuda")
+
+    def __del__(self):
+        try:
+            for h in getattr(self, "A", []):
+                self.L.hf_operator_destroy(h)
+            for h in getattr(self, "H", []):
+                self.L.hf_hierarchy_destroy(h)
+            if getattr(self, "Hc", None):
+                self.L.hf_hierarchy_destroy(self.Hc)
+        except Exception:   # interpreter shutdown
+            pass
+
+    # ---- building blocks -------------------------------------------------
+    def _halo(self, fields):
+        self.comm.exchange([h.data for h in fields], planes=1)
+
+    def _dot(self, a, b):
+        out = (ctypes.c_double * 2)()
+        vals = []
+        for x, y in zip(a, b):
+            _native.check(self.L.hf_dot(x.numel(), _ptr(x), _ptr(y), out))
+            vals.append(complex(out[0], out[1]))
+        return self.comm.allreduce(vals)
+
+    def precondition(self, src, dst):
+        """dst = one V(1,1) cycle applied to src (lists of per-slab HaloFields)."""
+        L, n = self.L, self.nlev
+        S = range(len(self.extents))
+        for r in S:
+            self.fb[r][0].owned.copy_(src[r].owned)
+        for l in range(n - 1):
+            self._halo([self.fb[r][l] for r in S])
+            for r in S:
+                _native.check(L.hf_level_down1(self.H[r], l, _ptr(self.fb[r][l].owned),
+                                               _ptr(self.fr[r][l].owned)))
+            self._halo([self.fr[r][l] for r in S])
+            for r in S:
+                _native.check(L.hf_restrict_fw(self.H[r], l, _ptr(self.fr[r][l].owned),
+                                               _ptr(self.fb[r][l + 1].owned)))
+        # coarsest: gather the coarse slabs, exact solve, keep this slab's planes
+        parts = [self.fb[r][n - 1].owned for r in S]
+        if len(self.extents) > 1 or getattr(self.comm, "size", 1) > 1:
+            if len(self.extents) > 1:
+                bc = self.comm.allgather_planes(parts, self.ccounts)
+            else:
+                counts = [e.nx for e in _coarse_extents(self.grid, self.comm.size, n)]
+                bc = self.comm.allgather_planes(parts[0], counts)
+        else:
+            bc = parts[0]
+        bc = bc.contiguous()
+        _native.check(L.hf_coarsest_solve(self.Hc, _ptr(bc), _ptr(self.xc)))
+        for r in S:
+            e = self.levels[r][n - 1]
+            self.fu[r][n - 1].owned.copy_(self.xc[e.lo1 - 1:e.hi1])
+        for l in range(n - 2, -1, -1):
+            self._halo([self.fu[r][l + 1] for r in S])
+            for r in S:
+                _native.check(L.hf_level_correct(self.H[r], l, _ptr(self.fb[r][l].owned),
+                                                 _ptr(self.fu[r][l + 1].owned), _ptr(self.ft[r][l].owned)))
+            self._halo([self.ft[r][l] for r in S])
+            for r in S:
+                _native.check(L.hf_level_smooth(self.H[r], l, _ptr(self.ft[r][l].owned),
+                                                _ptr(self.fb[r][l].owned), _ptr(dst[r].owned)))
+
+    def apply_A(self, src, dst):
+        self._halo(src)
+        for r in range(len(self.extents)):
+            _native.check(self.L.hf_operator_apply(self.A[r], _ptr(src[r].owned), _ptr(dst[r])))
+
+    # ---- Bi-CGSTAB (krylov.py:207-276) ------------------------------------
+    def solve(self, b_slabs, cfg: SolverConfig | None = None):
+        """b_slabs: per local slab, the right-hand side (owned shape).  Returns
+        (x per slab, ConvergenceReport)."""
+        torch = self.torch
+        cfg = cfg or SolverConfig(method="bicgstab")
+        _native.set_stream_from_torch()
+        S = range(len(self.extents))
+        own = lambda: [torch.zeros(e.shape, dtype=torch.complex128, device="cuda") for e in self.extents]
+        halo = lambda: [HaloField(e) for e in self.extents]
+        b = [torch.as_tensor(x).to("cuda", torch.complex128) for x in b_slabs]
+        x, v, t = own(), own(), own()
+        p, s, ph, sh = halo(), halo(), halo(), halo()
+        rep = ConvergenceReport(method="bicgstab")
+        bnorm = abs(self._dot(b, b)) ** 0.5
+        if bnorm == 0.0:
+            rep.converged, rep.final_relres = True, 0.0
+            return x, rep
+        r = [bi.clone() for bi in b]
+        rs = [bi.clone() for bi in b]
+        rho = alpha = omega = 1.0 + 0j
+        while rep.iterations < cfg.maxit:
+            rho_new = self._dot(rs, r)
+            if abs(rho_new) < cfg.breakdown_tol:
+                rep.breakdown = "rho"
+                break
+            beta = (rho_new / rho) * (alpha / omega)
+            for i in S:
+                p[i].owned.copy_(r[i] + beta * (p[i].owned - omega * v[i]))
+            self.precondition(p, ph)
+            self.apply_A(ph, v)
+            rep.matvec_count += 1
+            den = self._dot(rs, v)
+            if abs(den) < cfg.breakdown_tol:
+                rep.breakdown = "rho"
+                break
+            alpha = rho_new / den
+            for i in S:
+                s[i].owned.copy_(r[i] - alpha * v[i])
+            snorm = abs(self._dot([si.owned for si in s], [si.owned for si in s])) ** 0.5
+            if snorm / bnorm <= cfg.tol:
+                for i in S:
+                    x[i] += alpha * ph[i].owned
+                rep.record(snorm / bnorm)
+                rep.converged = True
+                return x, rep
+            self.precondition(s, sh)
+            self.apply_A(sh, t)
+            rep.matvec_count += 1
+            tt = self._dot(t, t)
+            if abs(tt) < cfg.breakdown_tol:
+                rep.breakdown = "omega"
+                break
+            omega = self._dot(t, [si.owned for si in s]) / tt
+            if abs(omega) < cfg.breakdown_tol:
+                rep.breakdown = "omega"
+                break
+            for i in S:
+                x[i] += alpha * ph[i].owned + omega * sh[i].owned
+                r[i] = s[i].owned - omega * t[i]
+            rho = rho_new
+            relres = abs(self._dot(r, r)) ** 0.5 / bnorm
+            rep.record(relres)
+            if relres <= cfg.tol:
+                rep.converged = True
+                return x, rep
+        rep.converged = False
+        return x, rep
+
+
+def _coarse_extents(grid, nslabs, nlev):
+    from .partition import derive_coarse_extent, slab_partition
+    out = []
+    for e in slab_partition(grid, nslabs):
+        for _ in range(nlev - 1):
+            e = derive_coarse_extent(e)
+        out.append(e)
+    return out

@@ -146,13 +146,12 @@ def run_gpu(args):
     import torch.distributed as dist
 
     from paper_2308_06085_b200.krylov import Solver, SolverConfig
-    from paper_2308_06085_b200.multigrid import (MGConfig, build_hierarchy, coarsest_solve,
-                                                 mg_precondition)
+    from paper_2308_06085_b200.multigrid import MGConfig, build_hierarchy
     from paper_2308_06085_b200.operators import OperatorSpec, StencilOperator
 
     rank, world, local = _env_rank()
     if world > 1:
-        dist.init_process_group("nccl")
+        return run_slabs(args)
     torch.cuda.set_device(local)
     p, spec, b_host = _problem()
     n = p.grid.num_vertices
@@ -213,33 +212,15 @@ def run_gpu(args):
 
     # ---- kernel roofline: live CUDA-event timing of the hot kernels ----
     hbm, peak_kind = _peaks()
-    u = torch.randn(p.grid.shape, dtype=torch.complex128, device="cuda")
-    v = torch.empty_like(u)
-    R = 20
-    t_apply = _event_time(lambda: A.apply(u, out=v), R)
-    t_cycle = _event_time(lambda: mg_precondition(hier, u, out=v), R)
-    nc = hier.coarsest.grid.num_vertices
-    bc_ = torch.randn(hier.coarsest.grid.shape, dtype=torch.complex128, device="cuda")
-    xc_ = torch.empty_like(bc_)
-    t_gemv = _event_time(lambda: coarsest_solve(hier, bc_, out=xc_), R)
-    t_iter = ms_step / max(iters, 1)
-    kernels = {
-        "helmholtz_matvec": {"ms": t_apply, "bytes": 32.0 * n, "per_iter": 2},
-        "coarsest_gemv": {"ms": t_gemv, "bytes": 16.0 * nc * nc, "per_iter": 2},
-    }
-    share = {k_: v_["ms"] * v_["per_iter"] / t_iter for k_, v_ in kernels.items()}
-    share["vcycle_total"] = 2 * t_cycle / t_iter
-    dom = max(kernels, key=lambda k_: share[k_])
-    kd = kernels[dom]
-    achieved = kd["bytes"] / (kd["ms"] / 1e3) / 1e9
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm,
-                "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / hbm, 4),
-                "traffic": None,
-                "algorithmic_bytes_per_launch": kd["bytes"],
-                "launch_ms": round(kd["ms"], 5),
-                "share_of_iteration": {k_: round(v_, 3) for k_, v_ in share.items()},
-                "matvec": {"achieved_gbs": round(32.0 * n / (t_apply / 1e3) / 1e9, 1),
-                           "frac": round(32.0 * n / (t_apply / 1e3) / 1e9 / hbm, 4)}}
+    kern = kernel_table(A, hier, n, ms_step / max(iters, 1))
+    dom = max(kern, key=lambda k_: kern[k_]["share"])
+    kd = kern[dom]
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": kd["gbs"], "peak": hbm,
+                "peak_kind": peak_kind, "unit": "GB/s", "frac": round(kd["gbs"] / hbm, 4),
+                "traffic": None, "algorithmic_bytes_per_launch": kd["bytes"],
+                "launch_ms": kd["ms"],
+                "kernels": {k_: {"gbs": v_["gbs"], "frac": round(v_["gbs"] / hbm, 4),
+                                 "ms": v_["ms"], "share": v_["share"]} for k_, v_ in kern.items()}}
 
     out = {
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
@@ -264,6 +245,125 @@ def run_gpu(args):
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_slabs(args):
+    """N > 1: the 129^3 solve split into N slabs along i1, one per GPU
+    (strong scaling).  Halos P2P over NCCL, inner products by NCCL all-reduce,
+    coarsest level all-gathered and solved on every rank."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2308_06085_b200.dist import SlabSolver
+    from paper_2308_06085_b200.krylov import SolverConfig
+    from paper_2308_06085_b200.partition import TorchSlabComm, slab_partition
+
+    rank, world, local = _env_rank()
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    p, spec, b_host = _problem()
+    n = p.grid.num_vertices
+    e = slab_partition(p.grid, world)[rank]
+    comm = TorchSlabComm()
+    t_setup = time.perf_counter()
+    S = SlabSolver(p.grid, [e], spec.k_field, p.bc, comm)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t_setup
+    cfg = SolverConfig(method="bicgstab", tol=TOL, maxit=MAXIT)
+    b = [torch.as_tensor(b_host[e.lo1 - 1:e.hi1]).cuda()]
+    for _ in range(args.warmup):
+        _, rep = S.solve(b, cfg)
+    times = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            dist.barrier()
+            torch.cuda.synchronize()
+            s0 = torch.cuda.Event(enable_timing=True)
+            e0 = torch.cuda.Event(enable_timing=True)
+            s0.record()
+            _, rep = S.solve(b, cfg)
+            e0.record()
+            torch.cuda.synchronize()
+            times.append(s0.elapsed_time(e0))
+    t = torch.tensor([float(np.sum(times))], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item()) / args.steps
+    iters = rep.iterations
+    # e2e: host slab in, host slab out
+    bh = torch.as_tensor(b_host[e.lo1 - 1:e.hi1]).pin_memory()
+    dist.barrier()
+    t0 = time.perf_counter()
+    xs, rep_h = S.solve([bh.cuda(non_blocking=True)], cfg)
+    xh = xs[0].cpu()
+    torch.cuda.synchronize()
+    e2e_ms = (time.perf_counter() - t0) * 1e3
+    te = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_ms = float(te.item())
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": round(n * iters / (ms_step / 1e3) / 1e6, 2), "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "c128",
+            "data": "synthetic (BASELINE configs[1] point-source problem, built in-process)",
+            "config": _config_dict({"parallelism": f"{world} slabs along i1 (halo P2P + NCCL allreduce)",
+                                    "iterations": iters, "matvecs": rep.matvec_count,
+                                    "final_relres": rep.final_relres,
+                                    "time_to_solution_s": round(ms_step / 1e3, 6),
+                                    "setup_s": round(t_setup, 3)}),
+            "clocks": clk.summary(), "gpu_launches": None,
+            "e2e": {"value": round(n * rep_h.iterations / (e2e_ms / 1e3) / 1e6, 2), "unit": UNIT,
+                    "h2d_bytes_per_step": int(b_host.nbytes), "d2h_bytes_per_step": int(b_host.nbytes),
+                    "ms_per_step": round(e2e_ms, 4)},
+            "roofline": None,
+        }
+        print(json.dumps(out), flush=True)
+    dist.destroy_process_group()
+
+
+def kernel_table(A, hier, n, t_iter_ms, reps=20):
+    """Live CUDA-event timing of the path's kernels on the finest level (the
+    solve launches each of them twice per Bi-CGSTAB iteration).  Bytes are the
+    algorithmic traffic of one launch (constant medium: no k traffic)."""
+    import ctypes
+
+    import torch
+
+    from paper_2308_06085_b200 import _native
+    from paper_2308_06085_b200.multigrid import coarsest_solve
+
+    L = _native.load()
+    _native.set_stream_from_torch()
+    shape = hier.levels[0].extent.shape
+    cshape = hier.levels[1].extent.shape
+    rnd = lambda sh: torch.randn(sh, dtype=torch.complex128, device="cuda")
+    u, b, v, t = rnd(shape), rnd(shape), rnd(shape), rnd(shape)
+    ec, bc = rnd(cshape), rnd(cshape)
+    H = hier._h
+    nc_f = cshape[0] * cshape[1] * cshape[2]
+    ncs = hier.coarsest.grid.num_vertices
+    xc, rc = rnd(hier.coarsest.grid.shape), rnd(hier.coarsest.grid.shape)
+    nt = -(-ncs // 64)
+    sym_bytes = nt * (nt + 1) // 2 * 64 * 64 * 16 + 2 * nt * (nt + 1) // 2 * 64 * 16 * 2
+    p = lambda x: x.data_ptr()
+    cases = {
+        "helmholtz_matvec": (lambda: L.hf_operator_apply(A._h, p(u), p(v)), 32.0 * n),
+        "cslp_presmooth_residual": (lambda: L.hf_level_down1(H, 0, p(b), p(v)), 32.0 * n),
+        "restrict_fw": (lambda: L.hf_restrict_fw(H, 0, p(v), p(bc)), 16.0 * n + 16.0 * nc_f),
+        "prolong_correct": (lambda: L.hf_level_correct(H, 0, p(b), p(ec), p(t)), 32.0 * n + 16.0 * nc_f),
+        "jacobi_postsmooth": (lambda: L.hf_level_smooth(H, 0, p(t), p(b), p(u)), 48.0 * n),
+        "coarsest_solve": (lambda: coarsest_solve(hier, rc, out=xc),
+                           float(sym_bytes) if hier.spec.bc.__class__.__name__ == "Sommerfeld"
+                           else 16.0 * ncs * ncs),
+    }
+    out = {}
+    for name, (fn, nbytes) in cases.items():
+        fn()
+        ms = _event_time(fn, reps)
+        out[name] = {"ms": round(ms, 5), "bytes": nbytes, "gbs": round(nbytes / (ms / 1e3) / 1e9, 1),
+                     "share": round(2 * ms / t_iter_ms, 4)}
+    return out
 
 
 def cpu_baseline(iters: int, threads: int | None = None):

@@ -957,8 +957,10 @@ void launch_down1(const Lvl &L, const cd *b, cd *r, double omega, cudaStream_t s
 }
 static void corr(int mode, const Lvl &F, const Lvl &C, const cd *b, const cd *e, cd *out,
                  double omega, cudaStream_t s, const int *done) {
-    int chunk;
-    dim3 g = march_grid(F, chunk);
+    // two fine planes per thread: every load of the pair is independent (latency-bound
+    // kernel, so parallelism beats the coarse-plane reuse of longer marches)
+    const int chunk = 2;
+    dim3 g((F.n3 + 31) / 32, (F.n2 + 7) / 8, (F.nx + chunk - 1) / chunk);
     if (mode == 0) k_corr<0><<<g, 256, 0, s>>>(F, C, b, e, out, omega, chunk, done);
     else if (mode == 1) k_corr<1><<<g, 256, 0, s>>>(F, C, b, e, out, omega, chunk, done);
     else k_corr<2><<<g, 256, 0, s>>>(F, C, b, e, out, omega, chunk, done);

@@ -161,8 +161,9 @@ class SlabSolver:
                                                  _ptr(self.fu[r][l + 1].owned), _ptr(self.ft[r][l].owned)))
             self._halo([self.ft[r][l] for r in S])
             for r in S:
+                out = dst[r] if l == 0 else self.fu[r][l]
                 _native.check(L.hf_level_smooth(self.H[r], l, _ptr(self.ft[r][l].owned),
-                                                _ptr(self.fb[r][l].owned), _ptr(dst[r].owned)))
+                                                _ptr(self.fb[r][l].owned), _ptr(out.owned)))
 
     def apply_A(self, src, dst):
         self._halo(src)

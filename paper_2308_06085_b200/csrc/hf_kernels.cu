@@ -190,7 +190,7 @@ struct EpiJacobi {
 template <int MODE, bool KVAR, bool AUX>
 struct StencilSmem {
     static constexpr bool kWd = MODE == MODE_PRE && KVAR;     // staged D^-1 field
-    static constexpr bool kAuxArr = AUX && MODE == MODE_LOAD; // PRE reuses the ring centre as b
+    static constexpr bool kAuxArr = AUX && MODE == MODE_LOAD;
     cd raw[RING][NFILL];
     cd wd[kWd ? RING : 1][kWd ? NFILL : 1];
 };
@@ -210,27 +210,39 @@ __global__ void __launch_bounds__(NT) k_stencil(Lvl L, const cd *__restrict__ sr
     const bool act = m < L.n3 && j < L.n2;
     const cd one = mk(1.0, 0.0);
 
-    // fill entries of this thread: e0 = tid, e1 = tid + NT (when < NFILL)
+    // fill entries of this thread: e0 = tid, e1 = tid + NT (when < NFILL).  A halo
+    // entry one step outside the grid holds the MIRRORED inward value (row/column
+    // 1 or n-2), so the Sommerfeld ghost elimination needs no branch: the
+    // 7-point sum is uniform and the boundary lives in a_p (and Dirichlet rows,
+    // identities, never read outside the grid).
     const bool has1 = tid + NT < NFILL;
-    int go0, go1;
+    int go0, go1, nbe0, nbe1;
     bool ok0, ok1;
     {
+        auto mirror = [](int x, int n) { return x < 0 ? -x : (x >= n ? 2 * (n - 1) - x : x); };
         int hy = tid / HALO_X, hx = tid - hy * HALO_X;
         int jj = j0 - 1 + hy, mm = m0 - 1 + hx;
-        ok0 = jj >= 0 && jj < L.n2 && mm >= 0 && mm < L.n3;
-        go0 = ok0 ? jj * L.n3 + mm : 0;
+        bool oj = jj >= -1 && jj <= L.n2, om = mm >= -1 && mm <= L.n3;
+        bool corner = (jj < 0 || jj >= L.n2) && (mm < 0 || mm >= L.n3);
+        ok0 = oj && om && !corner;
+        go0 = ok0 ? mirror(jj, L.n2) * L.n3 + mirror(mm, L.n3) : 0;
+        nbe0 = ok0 ? (mirror(jj, L.n2) == 0) + (mirror(jj, L.n2) == L.n2 - 1) +
+                         (mirror(mm, L.n3) == 0) + (mirror(mm, L.n3) == L.n3 - 1) : 0;
         int e = tid + NT;
         hy = e / HALO_X; hx = e - hy * HALO_X;
         jj = j0 - 1 + hy; mm = m0 - 1 + hx;
-        ok1 = has1 && jj >= 0 && jj < L.n2 && mm >= 0 && mm < L.n3;
-        go1 = ok1 ? jj * L.n3 + mm : 0;
+        oj = jj >= -1 && jj <= L.n2; om = mm >= -1 && mm <= L.n3;
+        corner = (jj < 0 || jj >= L.n2) && (mm < 0 || mm >= L.n3);
+        ok1 = has1 && oj && om && !corner;
+        go1 = ok1 ? mirror(jj, L.n2) * L.n3 + mirror(mm, L.n3) : 0;
+        nbe1 = ok1 ? (mirror(jj, L.n2) == 0) + (mirror(jj, L.n2) == L.n2 - 1) +
+                         (mirror(mm, L.n3) == 0) + (mirror(mm, L.n3) == L.n3 - 1) : 0;
     }
     const int own = j * L.n3 + m;
     const int cf = (ty + 1) * HALO_X + (tx + 1);
     const int nbjm = (j == 0) + (j == L.n2 - 1) + (m == 0) + (m == L.n3 - 1);
-    const bool deep_jm = j >= 2 && j <= L.n2 - 3 && m >= 2 && m <= L.n3 - 3;
     // constant medium: a_p and w D^-1 by physical-face count (0..3) in shared memory
-    __shared__ cd tab[8];
+    __shared__ cd tab[12];
     cd ap0 = mk(0, 0), wd0 = mk(0, 0);
     if (!KVAR) {
         ap0 = __ldg(L.tab);
@@ -238,8 +250,20 @@ __global__ void __launch_bounds__(NT) k_stencil(Lvl L, const cd *__restrict__ sr
         if (tid < 4) {
             tab[tid] = __ldg(L.tab + tid);
             tab[4 + tid] = cscal(__ldg(L.tab + 4 + tid), omega);
+            tab[8 + tid] = cdiv(__ldg(L.tab + 4 + tid), __ldg(L.tab + 4));   // D^-1(nb) / D^-1(0)
         }
     }
+    // MODE_PRE, constant medium: stage b^ = b * D^-1(nb)/D^-1(0) so f = w D^-1 b = wd0 b^
+    // everywhere and the 7-point row is uniform; each thread rescales the
+    // boundary vertices among its own fill entries once their copies land.
+    constexpr bool kScale = MODE == MODE_PRE && !KVAR;
+    auto fixup = [&](int slot, int i) {
+        int gi = L.lo1 + i;
+        gi = gi < 0 ? -gi : (gi >= L.n1 ? 2 * (L.n1 - 1) - gi : gi);
+        const int nbx = (gi == 0) + (gi == L.n1 - 1);
+        if (ok0 && nbx + nbe0) sm.raw[slot][tid] = cmul(sm.raw[slot][tid], tab[8 + nbx + nbe0]);
+        if (ok1 && nbx + nbe1) sm.raw[slot][tid + NT] = cmul(sm.raw[slot][tid + NT], tab[8 + nbx + nbe1]);
+    };
     auto wd_nb = [&](int nb) -> cd { return tab[4 + nb]; };   // read after the first barrier
     cd acc[2] = {mk(0, 0), mk(0, 0)};
 
@@ -247,9 +271,10 @@ __global__ void __launch_bounds__(NT) k_stencil(Lvl L, const cd *__restrict__ sr
     auto stage = [&](int i) {              // one commit group per plane
         const int slot = sslot;
         sslot = sslot == RING - 1 ? 0 : sslot + 1;
-        const int gi = L.lo1 + i;
-        const bool pok = i <= i1 && gi >= 0 && gi < L.n1;
-        const long long pb = (long long)i * L.plane;
+        int gi = L.lo1 + i;
+        const bool pok = i <= i1 && gi >= -1 && gi <= L.n1;
+        gi = gi < 0 ? -gi : (gi >= L.n1 ? 2 * (L.n1 - 1) - gi : gi);   // mirrored plane
+        const long long pb = (long long)(gi - L.lo1) * L.plane;
         bool v = pok && ok0;
         cp_async16(&sm.raw[slot][tid], v ? src + pb + go0 : src, v);
         if (SM::kWd) cp_async16(&sm.wd[SM::kWd ? slot : 0][tid], v ? L.dinv + pb + go0 : L.dinv, v);
@@ -263,22 +288,29 @@ __global__ void __launch_bounds__(NT) k_stencil(Lvl L, const cd *__restrict__ sr
 
     for (int s = 0; s < RING - 1; s++) stage(i0 - 1 + s);   // planes i0-1 .. i0+2
     int sp = 0, sc = 1, sn = 2;                              // ring slots of i-1, i, i+1
+    if (kScale) {
+        cp_wait<2>();                      // planes i0-1, i0 of this thread's copies
+        __syncthreads();                   // tab[] visible
+        fixup(0, i0 - 1);
+        fixup(1, i0);
+    }
     long long q = (long long)i0 * L.plane + own;
     // centre-only epilogue operands (b or w, and k) are prefetched one plane ahead
     cd a_next = mk(0, 0);
     double k_next = L.kc;
     if (act && i0 < i1) {
-        if (SM::kAuxArr) a_next = __ldg(aux + q);
+        if (Epi::kAux) a_next = __ldg(aux + q);
         if (KVAR) k_next = __ldg(L.k + q);
     }
     for (int i = i0; i < i1; i++, q += L.plane) {
         const cd a_cur = a_next;
         const double k_cur = k_next;
         if (act && i + 1 < i1) {
-            if (SM::kAuxArr) a_next = __ldg(aux + q + L.plane);
+            if (Epi::kAux) a_next = __ldg(aux + q + L.plane);
             if (KVAR) k_next = __ldg(L.k + q + L.plane);
         }
         cp_wait<1>();                      // plane i+1 landed (i+2 may be in flight)
+        if (kScale) fixup(sn, i + 1);      // own entries only: no barrier needed before
         __syncthreads();
         stage(i + RING - 2);               // into the slot read last at step i-1
         if (act) {
@@ -291,8 +323,7 @@ __global__ void __launch_bounds__(NT) k_stencil(Lvl L, const cd *__restrict__ sr
             cd ym = r0[cf - HALO_X], yp = r0[cf + HALO_X];
             cd zm = r0[cf - 1], zp = r0[cf + 1];
             const double kk = k_cur;
-            const cd bc = fc;              // PRE: the staged centre is b
-            cd post = one;                 // PRE deep interior: M(c b) = c M b
+            cd post = one;
             if (MODE == MODE_PRE) {
                 if (KVAR) {                   // staged D^-1, w applied once after M
                     const int W = SM::kWd ? 1 : 0;
@@ -304,46 +335,20 @@ __global__ void __launch_bounds__(NT) k_stencil(Lvl L, const cd *__restrict__ sr
                     yp = cmul(yp, sm.wd[W * sc][cf + HALO_X]);
                     zm = cmul(zm, sm.wd[W * sc][cf - 1]);
                     zp = cmul(zp, sm.wd[W * sc][cf + 1]);
-                } else if (deep_jm && gi >= 2 && gi <= L.n1 - 3) {
-                    post = wd0;
                 } else {
-                    const int nbx = (int)bxl + (int)bxh;
-                    fc = cmul(fc, wd_nb(nb));
-                    xm = cmul(xm, wd_nb((gi - 1 == 0) + (gi - 1 == L.n1 - 1) + nbjm));
-                    xp = cmul(xp, wd_nb((gi + 1 == 0) + (gi + 1 == L.n1 - 1) + nbjm));
-                    const int by = (m == 0) + (m == L.n3 - 1) + nbx;
-                    const int bz = (j == 0) + (j == L.n2 - 1) + nbx;
-                    ym = cmul(ym, wd_nb((j - 1 == 0) + (j - 1 == L.n2 - 1) + by));
-                    yp = cmul(yp, wd_nb((j + 1 == 0) + (j + 1 == L.n2 - 1) + by));
-                    zm = cmul(zm, wd_nb((m - 1 == 0) + (m - 1 == L.n3 - 1) + bz));
-                    zp = cmul(zp, wd_nb((m + 1 == 0) + (m + 1 == L.n3 - 1) + bz));
+                    post = wd0;               // f = wd0 * b^ (staged, rescaled at the faces)
                 }
             }
-            cd mf;
-            if (nb == 0) {                 // interior row
-                const cd ap = KVAR ? ap_of(L, kk, 0) : ap0;
-                cd sum = cadd(cadd(cadd(xm, xp), cadd(ym, yp)), cadd(zm, zp));
-                mf = cmul(ap, fc);
-                mf.x -= L.ih2 * sum.x;
-                mf.y -= L.ih2 * sum.y;
-                if (MODE == MODE_PRE) mf = cmul(post, mf);
-            } else if (!SOMM) {            // Dirichlet boundary row: identity
-                mf = (MODE == MODE_PRE && KVAR) ? cmul(post, fc) : fc;
-            } else {                       // Sommerfeld: mirror the inward neighbour
-                if (bxl) xm = xp;
-                if (bxh) xp = xm;
-                if (j == 0) ym = yp;
-                if (j == L.n2 - 1) yp = ym;
-                if (m == 0) zm = zp;
-                if (m == L.n3 - 1) zp = zm;
-                cd sum = cadd(cadd(cadd(xm, xp), cadd(ym, yp)), cadd(zm, zp));
-                mf = cmul(KVAR ? ap_of(L, kk, nb) : tab[nb], fc);
-                mf.x -= L.ih2 * sum.x;
-                mf.y -= L.ih2 * sum.y;
-                if (MODE == MODE_PRE && KVAR) mf = cmul(post, mf);
-            }
+            // uniform 7-point row: out-of-grid neighbours are already mirrored
+            cd sum = cadd(cadd(cadd(xm, xp), cadd(ym, yp)), cadd(zm, zp));
+            const cd ap = KVAR ? ap_of(L, kk, nb) : (nb == 0 ? ap0 : tab[nb]);
+            cd mf = cmul(ap, fc);
+            mf.x -= L.ih2 * sum.x;
+            mf.y -= L.ih2 * sum.y;
+            if (MODE == MODE_PRE) mf = cmul(post, mf);
+            if (!SOMM && nb) mf = (MODE == MODE_PRE) ? cmul(post, fc) : fc;   // Dirichlet identity
             cd av = mk(0, 0);
-            if (Epi::kAux) av = SM::kAuxArr ? a_cur : bc;
+            if (Epi::kAux) av = a_cur;
             cd wd = mk(0, 0);
             if (Epi::kDinv) wd = KVAR ? cscal(__ldg(L.dinv + q), omega) : wd_nb(nb);
             epi(q, fc, mf, wd, av, acc);

@@ -144,6 +144,10 @@ __device__ __forceinline__ void cp_async8(void *smem, const void *gmem, bool val
     int sz = valid ? 8 : 0;
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
 }
+__device__ __forceinline__ void cp_async16s(unsigned saddr, const void *gmem, bool valid) {
+    int sz = valid ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(gmem), "r"(sz));
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
@@ -257,10 +261,13 @@ __global__ void __launch_bounds__(NT) k_stencil(Lvl L, const cd *__restrict__ sr
     // everywhere and the 7-point row is uniform; each thread rescales the
     // boundary vertices among its own fill entries once their copies land.
     constexpr bool kScale = MODE == MODE_PRE && !KVAR;
+    const bool edge_block = j0 - 1 <= 0 || j0 + TILE_Y >= L.n2 - 1 || m0 - 1 <= 0 ||
+                            m0 + TILE_X >= L.n3 - 1;
     auto fixup = [&](int slot, int i) {
         int gi = L.lo1 + i;
         gi = gi < 0 ? -gi : (gi >= L.n1 ? 2 * (L.n1 - 1) - gi : gi);
         const int nbx = (gi == 0) + (gi == L.n1 - 1);
+        if (!edge_block && nbx == 0) return;   // block-uniform: no boundary vertex staged
         if (ok0 && nbx + nbe0) sm.raw[slot][tid] = cmul(sm.raw[slot][tid], tab[8 + nbx + nbe0]);
         if (ok1 && nbx + nbe1) sm.raw[slot][tid + NT] = cmul(sm.raw[slot][tid + NT], tab[8 + nbx + nbe1]);
     };
@@ -268,20 +275,27 @@ __global__ void __launch_bounds__(NT) k_stencil(Lvl L, const cd *__restrict__ sr
     cd acc[2] = {mk(0, 0), mk(0, 0)};
 
     int sslot = 0;
+    // cp.async operands precomputed once: 32-bit shared addresses of this thread's
+    // fill entries in ring slot 0 and global pointers of the entries in plane 0
+    // (invalid entries point at a valid vertex and copy 0 bytes)
+    const unsigned sraw0 = (unsigned)__cvta_generic_to_shared(&sm.raw[0][tid]);
+    const unsigned swd0 = (unsigned)__cvta_generic_to_shared(&sm.wd[0][SM::kWd ? tid : 0]);
+    constexpr unsigned SLOT = NFILL * sizeof(cd);
+    const cd *g0 = src + go0, *g1 = src + go1;
+    const cd *d0 = SM::kWd ? L.dinv + go0 : nullptr, *d1 = SM::kWd ? L.dinv + go1 : nullptr;
     auto stage = [&](int i) {              // one commit group per plane
-        const int slot = sslot;
+        const unsigned so = (unsigned)sslot * SLOT;
         sslot = sslot == RING - 1 ? 0 : sslot + 1;
         int gi = L.lo1 + i;
         const bool pok = i <= i1 && gi >= -1 && gi <= L.n1;
         gi = gi < 0 ? -gi : (gi >= L.n1 ? 2 * (L.n1 - 1) - gi : gi);   // mirrored plane
-        const long long pb = (long long)(gi - L.lo1) * L.plane;
-        bool v = pok && ok0;
-        cp_async16(&sm.raw[slot][tid], v ? src + pb + go0 : src, v);
-        if (SM::kWd) cp_async16(&sm.wd[SM::kWd ? slot : 0][tid], v ? L.dinv + pb + go0 : L.dinv, v);
+        const long long pb = pok ? (long long)(gi - L.lo1) * L.plane : 0;
+        const bool v0 = pok && ok0, v1 = pok && ok1;
+        cp_async16s(sraw0 + so, g0 + pb, v0);
+        if (SM::kWd) cp_async16s(swd0 + so, d0 + pb, v0);
         if (has1) {
-            v = pok && ok1;
-            cp_async16(&sm.raw[slot][tid + NT], v ? src + pb + go1 : src, v);
-            if (SM::kWd) cp_async16(&sm.wd[SM::kWd ? slot : 0][tid + NT], v ? L.dinv + pb + go1 : L.dinv, v);
+            cp_async16s(sraw0 + so + NT * sizeof(cd), g1 + pb, v1);
+            if (SM::kWd) cp_async16s(swd0 + so + NT * sizeof(cd), d1 + pb, v1);
         }
         cp_commit();
     };

@@ -125,13 +125,11 @@ __device__ __forceinline__ ColCtx col_ctx(const Lvl &L, int chunk) {
 //              w D^-1 field when k varies).
 // ---------------------------------------------------------------------------
 #define TILE_X 32
-#define TILE_Y 8                // rows per tile (ROWS per thread, block 32 x TILE_Y/ROWS)
-#define ROWS 1
+#define TILE_Y 8
 #define HALO_X (TILE_X + 2)
 #define HALO_Y (TILE_Y + 2)
 #define NFILL (HALO_Y * HALO_X)
-#define NT (TILE_X * TILE_Y / ROWS)
-#define NFE ((NFILL + NT - 1) / NT)   // fill entries per thread
+#define NT (TILE_X * TILE_Y)
 #define RING 5
 
 enum { MODE_LOAD = 0, MODE_PRE = 1 };
@@ -212,49 +210,42 @@ __global__ void __launch_bounds__(NT) k_stencil(Lvl L, const cd *__restrict__ sr
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TILE_X + tx;
     const int m0 = blockIdx.x * TILE_X, j0 = blockIdx.y * TILE_Y;
     const int i0 = blockIdx.z * chunk, i1 = min(i0 + chunk, L.nx);
-    const int m = m0 + tx;
+    const int m = m0 + tx, j = j0 + ty;
+    const bool act = m < L.n3 && j < L.n2;
     const cd one = mk(1.0, 0.0);
 
-    // ---- fill entries of this thread: e = tid + k * NT (k < NFE) ----
-    // A halo entry one step outside the grid holds the MIRRORED inward value
-    // (row/column 1 or n-2): the Sommerfeld ghost elimination then needs no
-    // branch -- every row is the uniform 7-point sum with the boundary in a_p
-    // (Dirichlet rows are identities and never read outside the grid).
-    const cd *gp[NFE];
-    const cd *dp[NFE];
-    unsigned sa[NFE], swa[NFE];
-    bool ok[NFE], has[NFE];
-    int nbe[NFE];
-#pragma unroll
-    for (int k = 0; k < NFE; k++) {
+    // fill entries of this thread: e0 = tid, e1 = tid + NT (when < NFILL).  A halo
+    // entry one step outside the grid holds the MIRRORED inward value (row/column
+    // 1 or n-2), so the Sommerfeld ghost elimination needs no branch: the
+    // 7-point sum is uniform and the boundary lives in a_p (and Dirichlet rows,
+    // identities, never read outside the grid).
+    const bool has1 = tid + NT < NFILL;
+    int go0, go1, nbe0, nbe1;
+    bool ok0, ok1;
+    {
         auto mirror = [](int x, int n) { return x < 0 ? -x : (x >= n ? 2 * (n - 1) - x : x); };
-        const int e = tid + k * NT;
-        has[k] = e < NFILL;
-        const int ee = has[k] ? e : 0;
-        const int hy = ee / HALO_X, hx = ee - hy * HALO_X;
-        const int jj = j0 - 1 + hy, mm = m0 - 1 + hx;
-        const bool inj = jj >= 0 && jj < L.n2, inm = mm >= 0 && mm < L.n3;
-        ok[k] = has[k] && jj >= -1 && jj <= L.n2 && mm >= -1 && mm <= L.n3 && (inj || inm);
-        const int mj = mirror(jj, L.n2), mmi = mirror(mm, L.n3);
-        const int go = ok[k] ? mj * L.n3 + mmi : 0;
-        nbe[k] = (mj == 0) + (mj == L.n2 - 1) + (mmi == 0) + (mmi == L.n3 - 1);
-        gp[k] = src + go;
-        dp[k] = SM::kWd ? L.dinv + go : nullptr;
-        sa[k] = (unsigned)__cvta_generic_to_shared(&sm.raw[0][ee]);
-        swa[k] = (unsigned)__cvta_generic_to_shared(&sm.wd[0][SM::kWd ? ee : 0]);
+        int hy = tid / HALO_X, hx = tid - hy * HALO_X;
+        int jj = j0 - 1 + hy, mm = m0 - 1 + hx;
+        bool oj = jj >= -1 && jj <= L.n2, om = mm >= -1 && mm <= L.n3;
+        bool corner = (jj < 0 || jj >= L.n2) && (mm < 0 || mm >= L.n3);
+        ok0 = oj && om && !corner;
+        go0 = ok0 ? mirror(jj, L.n2) * L.n3 + mirror(mm, L.n3) : 0;
+        nbe0 = ok0 ? (mirror(jj, L.n2) == 0) + (mirror(jj, L.n2) == L.n2 - 1) +
+                         (mirror(mm, L.n3) == 0) + (mirror(mm, L.n3) == L.n3 - 1) : 0;
+        int e = tid + NT;
+        hy = e / HALO_X; hx = e - hy * HALO_X;
+        jj = j0 - 1 + hy; mm = m0 - 1 + hx;
+        oj = jj >= -1 && jj <= L.n2; om = mm >= -1 && mm <= L.n3;
+        corner = (jj < 0 || jj >= L.n2) && (mm < 0 || mm >= L.n3);
+        ok1 = has1 && oj && om && !corner;
+        go1 = ok1 ? mirror(jj, L.n2) * L.n3 + mirror(mm, L.n3) : 0;
+        nbe1 = ok1 ? (mirror(jj, L.n2) == 0) + (mirror(jj, L.n2) == L.n2 - 1) +
+                         (mirror(mm, L.n3) == 0) + (mirror(mm, L.n3) == L.n3 - 1) : 0;
     }
-    // the ROWS output rows of this thread: j = j0 + ty + r * 8
-    int jr[ROWS], cfr[ROWS], nbjm[ROWS];
-    bool actr[ROWS];
-#pragma unroll
-    for (int r = 0; r < ROWS; r++) {
-        jr[r] = j0 + ty + r * (NT / TILE_X);
-        actr[r] = m < L.n3 && jr[r] < L.n2;
-        cfr[r] = (ty + r * (NT / TILE_X) + 1) * HALO_X + (tx + 1);
-        nbjm[r] = (jr[r] == 0) + (jr[r] == L.n2 - 1) + (m == 0) + (m == L.n3 - 1);
-    }
-
-    // constant medium: a_p and w D^-1 by physical-face count (shared-memory table)
+    const int own = j * L.n3 + m;
+    const int cf = (ty + 1) * HALO_X + (tx + 1);
+    const int nbjm = (j == 0) + (j == L.n2 - 1) + (m == 0) + (m == L.n3 - 1);
+    // constant medium: a_p and w D^-1 by physical-face count (0..3) in shared memory
     __shared__ cd tab[12];
     cd ap0 = mk(0, 0), wd0 = mk(0, 0);
     if (!KVAR) {
@@ -267,8 +258,8 @@ __global__ void __launch_bounds__(NT) k_stencil(Lvl L, const cd *__restrict__ sr
         }
     }
     // MODE_PRE, constant medium: stage b^ = b * D^-1(nb)/D^-1(0) so f = w D^-1 b = wd0 b^
-    // everywhere; each thread rescales the boundary vertices among its own fill
-    // entries once their copies have landed (only blocks that touch a face).
+    // everywhere and the 7-point row is uniform; each thread rescales the
+    // boundary vertices among its own fill entries once their copies land.
     constexpr bool kScale = MODE == MODE_PRE && !KVAR;
     const bool edge_block = j0 - 1 <= 0 || j0 + TILE_Y >= L.n2 - 1 || m0 - 1 <= 0 ||
                             m0 + TILE_X >= L.n3 - 1;
@@ -276,16 +267,22 @@ __global__ void __launch_bounds__(NT) k_stencil(Lvl L, const cd *__restrict__ sr
         int gi = L.lo1 + i;
         gi = gi < 0 ? -gi : (gi >= L.n1 ? 2 * (L.n1 - 1) - gi : gi);
         const int nbx = (gi == 0) + (gi == L.n1 - 1);
-        if (!edge_block && nbx == 0) return;
-#pragma unroll
-        for (int k = 0; k < NFE; k++) {
-            const int e = tid + k * NT;
-            if (ok[k] && nbx + nbe[k]) sm.raw[slot][e] = cmul(sm.raw[slot][e], tab[8 + nbx + nbe[k]]);
-        }
+        if (!edge_block && nbx == 0) return;   // block-uniform: no boundary vertex staged
+        if (ok0 && nbx + nbe0) sm.raw[slot][tid] = cmul(sm.raw[slot][tid], tab[8 + nbx + nbe0]);
+        if (ok1 && nbx + nbe1) sm.raw[slot][tid + NT] = cmul(sm.raw[slot][tid + NT], tab[8 + nbx + nbe1]);
     };
+    auto wd_nb = [&](int nb) -> cd { return tab[4 + nb]; };   // read after the first barrier
+    cd acc[2] = {mk(0, 0), mk(0, 0)};
 
-    constexpr unsigned SLOT = NFILL * sizeof(cd);
     int sslot = 0;
+    // cp.async operands precomputed once: 32-bit shared addresses of this thread's
+    // fill entries in ring slot 0 and global pointers of the entries in plane 0
+    // (invalid entries point at a valid vertex and copy 0 bytes)
+    const unsigned sraw0 = (unsigned)__cvta_generic_to_shared(&sm.raw[0][tid]);
+    const unsigned swd0 = (unsigned)__cvta_generic_to_shared(&sm.wd[0][SM::kWd ? tid : 0]);
+    constexpr unsigned SLOT = NFILL * sizeof(cd);
+    const cd *g0 = src + go0, *g1 = src + go1;
+    const cd *d0 = SM::kWd ? L.dinv + go0 : nullptr, *d1 = SM::kWd ? L.dinv + go1 : nullptr;
     auto stage = [&](int i) {              // one commit group per plane
         const unsigned so = (unsigned)sslot * SLOT;
         sslot = sslot == RING - 1 ? 0 : sslot + 1;
@@ -293,12 +290,12 @@ __global__ void __launch_bounds__(NT) k_stencil(Lvl L, const cd *__restrict__ sr
         const bool pok = i <= i1 && gi >= -1 && gi <= L.n1;
         gi = gi < 0 ? -gi : (gi >= L.n1 ? 2 * (L.n1 - 1) - gi : gi);   // mirrored plane
         const long long pb = pok ? (long long)(gi - L.lo1) * L.plane : 0;
-#pragma unroll
-        for (int k = 0; k < NFE; k++) {
-            if (!has[k]) continue;
-            const bool v = pok && ok[k];
-            cp_async16s(sa[k] + so, gp[k] + pb, v);
-            if (SM::kWd) cp_async16s(swa[k] + so, dp[k] + pb, v);
+        const bool v0 = pok && ok0, v1 = pok && ok1;
+        cp_async16s(sraw0 + so, g0 + pb, v0);
+        if (SM::kWd) cp_async16s(swd0 + so, d0 + pb, v0);
+        if (has1) {
+            cp_async16s(sraw0 + so + NT * sizeof(cd), g1 + pb, v1);
+            if (SM::kWd) cp_async16s(swd0 + so + NT * sizeof(cd), d1 + pb, v1);
         }
         cp_commit();
     };
@@ -311,51 +308,35 @@ __global__ void __launch_bounds__(NT) k_stencil(Lvl L, const cd *__restrict__ sr
         fixup(0, i0 - 1);
         fixup(1, i0);
     }
+    long long q = (long long)i0 * L.plane + own;
     // centre-only epilogue operands (b or w, and k) are prefetched one plane ahead
-    long long q0 = (long long)i0 * L.plane + m;
-    cd a_next[ROWS];
-    double k_next[ROWS];
-#pragma unroll
-    for (int r = 0; r < ROWS; r++) {
-        a_next[r] = mk(0, 0);
-        k_next[r] = L.kc;
-        if (actr[r] && i0 < i1) {
-            const long long q = q0 + (long long)jr[r] * L.n3;
-            if (Epi::kAux) a_next[r] = __ldg(aux + q);
-            if (KVAR) k_next[r] = __ldg(L.k + q);
-        }
+    cd a_next = mk(0, 0);
+    double k_next = L.kc;
+    if (act && i0 < i1) {
+        if (Epi::kAux) a_next = __ldg(aux + q);
+        if (KVAR) k_next = __ldg(L.k + q);
     }
-    cd acc[2] = {mk(0, 0), mk(0, 0)};
-    for (int i = i0; i < i1; i++, q0 += L.plane) {
-        cd a_cur[ROWS];
-        double k_cur[ROWS];
-#pragma unroll
-        for (int r = 0; r < ROWS; r++) {
-            a_cur[r] = a_next[r];
-            k_cur[r] = k_next[r];
-            if (actr[r] && i + 1 < i1) {
-                const long long q = q0 + L.plane + (long long)jr[r] * L.n3;
-                if (Epi::kAux) a_next[r] = __ldg(aux + q);
-                if (KVAR) k_next[r] = __ldg(L.k + q);
-            }
+    for (int i = i0; i < i1; i++, q += L.plane) {
+        const cd a_cur = a_next;
+        const double k_cur = k_next;
+        if (act && i + 1 < i1) {
+            if (Epi::kAux) a_next = __ldg(aux + q + L.plane);
+            if (KVAR) k_next = __ldg(L.k + q + L.plane);
         }
         cp_wait<1>();                      // plane i+1 landed (i+2 may be in flight)
         if (kScale) fixup(sn, i + 1);      // own entries only: no barrier needed before
         __syncthreads();
         stage(i + RING - 2);               // into the slot read last at step i-1
-        const int gi = L.lo1 + i;
-        const int nbx = (gi == 0) + (gi == L.n1 - 1);
-        const cd *rc = sm.raw[sc], *rp = sm.raw[sp], *rn = sm.raw[sn];
-#pragma unroll
-        for (int r = 0; r < ROWS; r++) {
-            if (!actr[r]) continue;
-            const int cf = cfr[r];
-            const int nb = nbx + nbjm[r];
-            cd fc = rc[cf];
-            cd xm = rp[cf], xp = rn[cf];
-            cd ym = rc[cf - HALO_X], yp = rc[cf + HALO_X];
-            cd zm = rc[cf - 1], zp = rc[cf + 1];
-            const double kk = k_cur[r];
+        if (act) {
+            const int gi = L.lo1 + i;
+            const bool bxl = gi == 0, bxh = gi == L.n1 - 1;
+            const int nb = (int)bxl + (int)bxh + nbjm;
+            const cd *r0 = sm.raw[sc];
+            cd fc = r0[cf];
+            cd xm = sm.raw[sp][cf], xp = sm.raw[sn][cf];
+            cd ym = r0[cf - HALO_X], yp = r0[cf + HALO_X];
+            cd zm = r0[cf - 1], zp = r0[cf + 1];
+            const double kk = k_cur;
             cd post = one;
             if (MODE == MODE_PRE) {
                 if (KVAR) {                   // staged D^-1, w applied once after M
@@ -380,10 +361,11 @@ __global__ void __launch_bounds__(NT) k_stencil(Lvl L, const cd *__restrict__ sr
             mf.y -= L.ih2 * sum.y;
             if (MODE == MODE_PRE) mf = cmul(post, mf);
             if (!SOMM && nb) mf = (MODE == MODE_PRE) ? cmul(post, fc) : fc;   // Dirichlet identity
-            const long long q = q0 + (long long)jr[r] * L.n3;
+            cd av = mk(0, 0);
+            if (Epi::kAux) av = a_cur;
             cd wd = mk(0, 0);
-            if (Epi::kDinv) wd = KVAR ? cscal(__ldg(L.dinv + q), omega) : (nb == 0 ? wd0 : tab[4 + nb]);
-            epi(q, fc, mf, wd, a_cur[r], acc);
+            if (Epi::kDinv) wd = KVAR ? cscal(__ldg(L.dinv + q), omega) : wd_nb(nb);
+            epi(q, fc, mf, wd, av, acc);
         }
         sp = sc; sc = sn; sn = sn == RING - 1 ? 0 : sn + 1;
     }
@@ -917,12 +899,12 @@ static dim3 tile_grid(const Lvl &L, int &chunk) {
     long long target = 148 * 8;     // resident 256-thread blocks on B200
     int gz = (int)((target + cols - 1) / cols);
     gz = std::max(1, std::min(gz, L.nx));
-    chunk = std::max((L.nx + gz - 1) / gz, 4);
+    chunk = std::max((L.nx + gz - 1) / gz, L.nx >= 96 ? 4 : 2);   // short marches on coarse levels
     chunk = std::min(chunk, L.nx);
     gz = (L.nx + chunk - 1) / chunk;
     return dim3(gx, gy, gz);
 }
-static const dim3 kTileBlock(TILE_X, TILE_Y / ROWS, 1);
+static const dim3 kTileBlock(TILE_X, TILE_Y, 1);
 
 template <int MODE, class Epi, int ND, bool KVAR, bool SOMM>
 static void stencil_launch(const Lvl &L, const cd *src, const cd *aux, double omega, const Epi &e,

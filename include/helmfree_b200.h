@@ -135,6 +135,13 @@ int hf_restrict_fw(hf_hierarchy *hier, int level, const double *r_fine, double *
 int hf_prolong_tl(hf_hierarchy *hier, int level, const double *e_coarse, double *out_fine);
 /* multigrid.py:300-323 coarsest_solve */
 int hf_coarsest_solve(hf_hierarchy *hier, const double *b, double *x);
+/* Which exact coarsest solve the hierarchy set up (B200 addition; the
+   reference always iterates GMRES to coarsest_tol, multigrid.py:300-323). */
+#define HF_COARSEST_KIND_NONE 0        /* external (slab drivers) */
+#define HF_COARSEST_KIND_DENSE 1       /* dense inverse, GEMV */
+#define HF_COARSEST_KIND_SYMMETRIC 2   /* packed symmetric M^-1 S^-1 */
+#define HF_COARSEST_KIND_SEPARABLE 3   /* fast diagonalisation (constant k) */
+int hf_coarsest_kind(const hf_hierarchy *hier);
 /* multigrid.py:395-419 mg_precondition: z ~= M^-1 r, one V/F cycle */
 int hf_mg_precondition(hf_hierarchy *hier, const double *r, double *z);
 /* Fused pieces of one V(1,1) level (multigrid.py:337-343) for slab drivers that

@@ -21,6 +21,10 @@ __device__ __forceinline__ cd cscal(cd a, double s) { return mk(a.x * s, a.y * s
 __device__ __forceinline__ cd cmul(cd a, cd b) {
     return mk(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
+// a * b + c
+__device__ __forceinline__ cd cfma(cd a, cd b, cd c) {
+    return mk(fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y)));
+}
 // conj(a) * b
 __device__ __forceinline__ cd cjmul(cd a, cd b) {
     return mk(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);

@@ -11,6 +11,7 @@
 // deterministic last-block reduction that also advances the Bi-CGSTAB scalars
 // on the device (krylov.py:207-276).
 #include <algorithm>
+#include <utility>
 #include <cstdlib>
 
 #include "hf_kernels.cuh"
@@ -84,7 +85,21 @@ __device__ void bcg_finalize(BcgState *st, int op, const cd *sums) {
     }
 }
 
-__device__ __forceinline__ bool is_done(const int *done) { return done && *(volatile const int *)done; }
+// Programmatic dependent launch: every kernel is launched with the
+// programmatic-stream-serialization attribute.  On entry a CTA waits for the
+// previous grid to complete (its writes are then visible) and immediately
+// signals that the next grid may launch: that happens once every CTA of this
+// grid is resident, so the next kernel's CTAs fill SMs as this grid's last
+// wave drains and start the moment it completes.  Waiting before anything
+// else keeps the chain transitive (no grid can finish before its predecessor).
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+__device__ __forceinline__ bool is_done(const int *done) {
+    pdl_enter();
+    return done && *(volatile const int *)done;
+}
 
 // ---------------------------------------------------------------------------
 // marching stencil kernels
@@ -199,17 +214,20 @@ struct StencilSmem {
     cd wd[kWd ? RING : 1][kWd ? NFILL : 1];
 };
 
+// Body of one (virtual) block: tile (bx, by) of (i3, i2) columns, planes
+// [bz chunk, (bz + 1) chunk).
+// (block index passed explicitly so the body can be driven by other schedules)
 template <int MODE, class Epi, int ND, bool KVAR, bool SOMM>
-__global__ void __launch_bounds__(NT) k_stencil(Lvl L, const cd *__restrict__ src,
-                                                const cd *__restrict__ aux, double omega, Epi epi,
-                                                int chunk, RedSlot rs, const int *done) {
+__device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict__ src,
+                                             const cd *__restrict__ aux, double omega,
+                                             const Epi &epi, int chunk, const RedSlot &rs,
+                                             unsigned char *smem_raw, int tid, int bx, int by,
+                                             int bz) {
     using SM = StencilSmem<MODE, KVAR, Epi::kAux>;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
     SM &sm = *reinterpret_cast<SM *>(smem_raw);
-    if (is_done(done)) return;
-    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TILE_X + tx;
-    const int m0 = blockIdx.x * TILE_X, j0 = blockIdx.y * TILE_Y;
-    const int i0 = blockIdx.z * chunk, i1 = min(i0 + chunk, L.nx);
+    const int tx = tid & (TILE_X - 1), ty = tid / TILE_X;
+    const int m0 = bx * TILE_X, j0 = by * TILE_Y;
+    const int i0 = bz * chunk, i1 = min(i0 + chunk, L.nx);
     const int m = m0 + tx, j = j0 + ty;
     const bool act = m < L.n3 && j < L.n2;
     const cd one = mk(1.0, 0.0);
@@ -379,8 +397,20 @@ __global__ void __launch_bounds__(NT) k_stencil(Lvl L, const cd *__restrict__ sr
     }
 }
 
+template <int MODE, class Epi, int ND, bool KVAR, bool SOMM>
+__global__ void __launch_bounds__(NT) k_stencil(Lvl L, const cd *__restrict__ src,
+                                                const cd *__restrict__ aux, double omega, Epi epi,
+                                                int chunk, RedSlot rs, const int *done) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    if (is_done(done)) return;
+    stencil_body<MODE, Epi, ND, KVAR, SOMM>(L, src, aux, omega, epi, chunk, rs, smem_raw,
+                                            threadIdx.y * TILE_X + threadIdx.x, blockIdx.x,
+                                            blockIdx.y, blockIdx.z);
+}
+
 // D^-1 over a level of a varying medium (owned + ghost planes), at setup
 __global__ void k_dinv(Lvl L, int g0, int g1, cd *__restrict__ out) {
+    pdl_enter();
     long long n = (long long)(g1 - g0) * L.plane;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
          t += (long long)gridDim.x * blockDim.x) {
@@ -399,13 +429,13 @@ __global__ void k_dinv(Lvl L, int g0, int g1, cd *__restrict__ out) {
 // sum of each coarse plane is formed once and reused by the two fine planes
 // that straddle it.
 template <int MODE>
-__global__ void __launch_bounds__(256) k_corr(Lvl F, Lvl C, const cd *__restrict__ b,
-                                              const cd *__restrict__ e, cd *__restrict__ out,
-                                              double omega, int chunk, const int *done) {
-    if (is_done(done)) return;
-    const int m = blockIdx.x * 32 + (threadIdx.x & 31);
-    const int j = blockIdx.y * 8 + (threadIdx.x >> 5);
-    const int i0 = blockIdx.z * chunk, i1 = min(i0 + chunk, F.nx);
+__device__ __forceinline__ void corr_body(const Lvl &F, const Lvl &C, const cd *__restrict__ b,
+                                          const cd *__restrict__ e, cd *__restrict__ out,
+                                          double omega, int chunk, int tid, int bx, int by,
+                                          int bz) {
+    const int m = bx * 32 + (tid & 31);
+    const int j = by * 8 + (tid >> 5);
+    const int i0 = bz * chunk, i1 = min(i0 + chunk, F.nx);
     if (m >= F.n3 || j >= F.n2) return;
     const bool o2 = j & 1, o3 = m & 1;
     const cd *ecol = e + (j >> 1) * C.n3 + (m >> 1);
@@ -450,6 +480,14 @@ __global__ void __launch_bounds__(256) k_corr(Lvl F, Lvl C, const cd *__restrict
     }
 }
 
+template <int MODE>
+__global__ void __launch_bounds__(256) k_corr(Lvl F, Lvl C, const cd *__restrict__ b,
+                                              const cd *__restrict__ e, cd *__restrict__ out,
+                                              double omega, int chunk, const int *done) {
+    if (is_done(done)) return;
+    corr_body<MODE>(F, C, b, e, out, omega, chunk, threadIdx.x, blockIdx.x, blockIdx.y, blockIdx.z);
+}
+
 // u = w D^-1 b   (multigrid.py:148-151, assume_zero first sweep)
 __global__ void __launch_bounds__(256) k_jacobi0(Lvl L, const cd *__restrict__ b,
                                                  cd *__restrict__ u, double omega, int chunk,
@@ -473,14 +511,17 @@ __global__ void __launch_bounds__(256) k_jacobi0(Lvl L, const cd *__restrict__ b
 #define RF_X (2 * RC_X + 1)
 #define RF_Y (2 * RC_Y + 1)
 #define RF_N (RF_X * RF_Y)
-__global__ void __launch_bounds__(256) k_restrict2(Lvl F, Lvl C, const cd *__restrict__ r,
-                                                   cd *__restrict__ out, int chunk, const int *done) {
-    __shared__ __align__(16) cd fp[4][RF_N];
-    __shared__ cd P[3][RC_Y * RC_X];
-    if (is_done(done)) return;
-    const int tid = threadIdx.x;
-    const int cm0 = blockIdx.x * RC_X, cj0 = blockIdx.y * RC_Y;
-    const int ci0 = blockIdx.z * chunk, ci1 = min(ci0 + chunk, C.nx);
+struct RestrictSmem {
+    cd fp[4][RF_N];
+    cd P[3][RC_Y * RC_X];
+};
+__device__ __forceinline__ void restrict_body(const Lvl &F, const Lvl &C, const cd *__restrict__ r,
+                                              cd *__restrict__ out, int chunk,
+                                              RestrictSmem &sm, int tid, int bx, int by, int bz) {
+    cd (*fp)[RF_N] = sm.fp;
+    cd (*P)[RC_Y * RC_X] = sm.P;
+    const int cm0 = bx * RC_X, cj0 = by * RC_Y;
+    const int ci0 = bz * chunk, ci1 = min(ci0 + chunk, C.nx);
     const int fm0 = 2 * cm0 - 1, fj0 = 2 * cj0 - 1;
     int go[3];
     bool ok[3];
@@ -559,6 +600,13 @@ __global__ void __launch_bounds__(256) k_restrict2(Lvl F, Lvl C, const cd *__res
     }
 }
 
+__global__ void __launch_bounds__(256) k_restrict2(Lvl F, Lvl C, const cd *__restrict__ r,
+                                                   cd *__restrict__ out, int chunk, const int *done) {
+    __shared__ __align__(16) RestrictSmem sm;
+    if (is_done(done)) return;
+    restrict_body(F, C, r, out, chunk, sm, threadIdx.x, blockIdx.x, blockIdx.y, blockIdx.z);
+}
+
 // ---------------------------------------------------------------------------
 // 1-D vector kernels (owned region, contiguous)
 // ---------------------------------------------------------------------------
@@ -569,6 +617,7 @@ __global__ void __launch_bounds__(256) k_bcg_init(long long n, const cd *__restr
                                                   cd *__restrict__ r, cd *__restrict__ rs,
                                                   cd *__restrict__ x, cd *__restrict__ p,
                                                   cd *__restrict__ v, RedSlot red) {
+    pdl_enter();
     cd acc[2] = {mk(0, 0), mk(0, 0)};
     for (long long q = blockIdx.x * 256ll + threadIdx.x; q < n; q += (long long)gridDim.x * 256) {
         cd bv = __ldg(b + q);
@@ -631,6 +680,7 @@ __global__ void __launch_bounds__(256) k_bcg_xr(long long n, const BcgState *st,
 // x += alpha ph  (convergence at the half step, krylov.py:250-255)
 __global__ void k_bcg_xhalf(long long n, const BcgState *st, cd *__restrict__ x,
                             const cd *__restrict__ ph) {
+    pdl_enter();
     cd al = st->alpha;
     for (long long q = blockIdx.x * 256ll + threadIdx.x; q < n; q += (long long)gridDim.x * 256)
         x[q] = cadd(x[q], cmul(al, __ldg(ph + q)));
@@ -638,6 +688,7 @@ __global__ void k_bcg_xhalf(long long n, const BcgState *st, cd *__restrict__ x,
 
 // generic y = a x + b y with host scalars (GMRES / IDR helpers)
 __global__ void k_axpby(long long n, cd a, const cd *__restrict__ x, cd b, cd *__restrict__ y) {
+    pdl_enter();
     for (long long q = blockIdx.x * 256ll + threadIdx.x; q < n; q += (long long)gridDim.x * 256) {
         cd yv = (b.x == 0.0 && b.y == 0.0) ? mk(0, 0) : cmul(b, y[q]);
         y[q] = cadd(cmul(a, __ldg(x + q)), yv);
@@ -650,6 +701,7 @@ __global__ void k_axpby(long long n, cd a, const cd *__restrict__ x, cd b, cd *_
 __global__ void __launch_bounds__(256) k_mgs(long long n, cd *__restrict__ w, const cd *c,
                                              const cd *__restrict__ vprev,
                                              const cd *__restrict__ vcur, RedSlot red) {
+    pdl_enter();
     cd cc = c ? *c : mk(0, 0);
     cd acc[1] = {mk(0, 0)};
     for (long long q = blockIdx.x * 256ll + threadIdx.x; q < n; q += (long long)gridDim.x * 256) {
@@ -667,6 +719,7 @@ __global__ void __launch_bounds__(256) k_mgs(long long n, cd *__restrict__ w, co
 // device array of pointers; each V_i is streamed once.
 __global__ void __launch_bounds__(256) k_multi_axpy(long long n, int m, const cd *const *V,
                                                     const cd *y, cd *__restrict__ x) {
+    pdl_enter();
     for (long long q = blockIdx.x * 256ll + threadIdx.x; q < n; q += (long long)gridDim.x * 256) {
         cd xv = x[q];
         for (int i = 0; i < m; i++) xv = cadd(xv, cmul(y[i], __ldg(V[i] + q)));
@@ -677,6 +730,7 @@ __global__ void __launch_bounds__(256) k_multi_axpy(long long n, int m, const cd
 // y = x - sum_i c_i V_i  with c on the device (dense coefficient vector)
 __global__ void k_dot_store(long long n, const cd *__restrict__ a, const cd *__restrict__ b,
                             RedSlot red) {
+    pdl_enter();
     cd acc[1] = {mk(0, 0)};
     for (long long q = blockIdx.x * 256ll + threadIdx.x; q < n; q += (long long)gridDim.x * 256)
         acc[0] = cadd(acc[0], cjmul(__ldg(a + q), __ldg(b + q)));
@@ -738,6 +792,7 @@ __device__ __forceinline__ int sym_tile_row(long long t, int nT) {
 // pack: tile (I, J) = Minv[I*64 + r][J*64 + c] / s[J*64 + c], zero padded
 __global__ void k_sym_pack(int N, int nT, const cd *__restrict__ Minv, const double *__restrict__ s,
                            cd *__restrict__ tiles) {
+    pdl_enter();
     const long long ntile = (long long)nT * (nT + 1) / 2;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < ntile * SYT * SYT;
          e += (long long)gridDim.x * blockDim.x) {
@@ -830,7 +885,127 @@ __global__ void k_sym_reduce(int N, int nT, const cd *__restrict__ prow,
 }
 
 // Row-major dense CSLP matrix of a full (single-slab) level: A[r * N + c].
+// ---------------------------------------------------------------------------
+// Coarsest solve by fast diagonalisation (Lynch, Rice & Thomas 1964).  With a
+// constant wavenumber the coarsest CSLP operator is separable,
+//   M = T1 (x) I (x) I + I (x) T2 (x) I + I (x) I (x) T3 + c I,
+// T_d the 1-D operator of direction d (Sommerfeld end rows included), so
+//   M^-1 = (V1 (x) V2 (x) V3) diag(1 / (l1_a + l2_b + l3_c + c)) (V1^-1 (x) V2^-1 (x) V3^-1)
+// with T_d = V_d diag(l_d) V_d^-1.  The exact solve costs 2 (n1 + n2 + n3) N
+// complex MACs on N = n1 n2 n3 points (~0.5 M at 17^3) instead of streaming
+// the N^2 dense inverse (~190 MB at 17^3, symmetric half).  Three launches:
+// in-plane (i2, i3) transform per i1 plane, i1 transform with the eigenvalue
+// division per i2 slice, inverse in-plane transform.
+// ---------------------------------------------------------------------------
+// sum_q a[q * sa] * b[q * sb] with four independent accumulators (short
+// dependent FMA chains: these kernels are latency-bound)
+__device__ __forceinline__ cd cdot_strided(const cd *a, int sa, const cd *b, int sb, int n) {
+    cd c0 = mk(0, 0), c1 = mk(0, 0), c2 = mk(0, 0), c3 = mk(0, 0);
+    int q = 0;
+    for (; q + 4 <= n; q += 4) {
+        c0 = cfma(a[q * sa], b[q * sb], c0);
+        c1 = cfma(a[(q + 1) * sa], b[(q + 1) * sb], c1);
+        c2 = cfma(a[(q + 2) * sa], b[(q + 2) * sb], c2);
+        c3 = cfma(a[(q + 3) * sa], b[(q + 3) * sb], c3);
+    }
+    for (; q < n; q++) c0 = cfma(a[q * sa], b[q * sb], c0);
+    return cadd(cadd(c0, c1), cadd(c2, c3));
+}
+
+#define FDM_THREADS 128
+#define FDM_GROUPS 4
+
+// in-plane transform of i1 plane blockIdx.x, rows [j0, j0 + R) of i2:
+//   out[j][m] = sum_m' A3[m][m'] sum_j' A2[j][j'] in[j'][m']
+template <int NTH>
+__device__ __forceinline__ void fdm_plane_body(int n2, int n3, int R, const cd *__restrict__ A2,
+                                               const cd *__restrict__ A3,
+                                               const cd *__restrict__ in, cd *__restrict__ out,
+                                               unsigned char *smem_raw, int tid, int bx, int by) {
+    cd *a2 = reinterpret_cast<cd *>(smem_raw);   // R x n2 (rows j0..)
+    cd *a3t = a2 + R * n2;                        // n3 x n3, transposed
+    cd *P = a3t + n3 * n3;                        // n2 x n3
+    cd *Q = P + n2 * n3;                          // R x n3
+    const int plane = n2 * n3;
+    const int j0 = by * R, rows = min(R, n2 - j0);
+    if (rows <= 0) return;
+    const cd *src = in + (size_t)bx * plane;
+    for (int t = tid; t < plane; t += NTH) P[t] = src[t];
+    for (int t = tid; t < rows * n2; t += NTH) a2[t] = __ldg(A2 + (size_t)j0 * n2 + t);
+    for (int t = tid; t < n3 * n3; t += NTH) {
+        int r = t / n3, c = t - r * n3;
+        a3t[c * n3 + r] = __ldg(A3 + t);
+    }
+    __syncthreads();
+    for (int t = tid; t < rows * n3; t += NTH) {   // Q = A2 P (rows j0..)
+        int jr = t / n3, m = t - jr * n3;
+        Q[t] = cdot_strided(a2 + jr * n2, 1, P + m, n3, n2);
+    }
+    __syncthreads();
+    cd *dst = out + (size_t)bx * plane + (size_t)j0 * n3;
+    for (int t = tid; t < rows * n3; t += NTH) {   // out = Q A3^T
+        int jr = t / n3, m = t - jr * n3;
+        dst[t] = cdot_strided(a3t + m, n3, Q + jr * n3, 1, n3);
+    }
+}
+
+// i1 transform of slice i2 = blockIdx.x, columns [m0, m0 + C) of i3:
+//   out[i][m] = sum_a V1[i][a] invD[a][m] sum_i' W1[a][i'] in[i'][m]
+template <int NTH>
+__device__ __forceinline__ void fdm_fiber_body(int n1, int n2, int n3, int C,
+                                               const cd *__restrict__ W1,
+                                               const cd *__restrict__ V1,
+                                               const cd *__restrict__ invD,
+                                               const cd *__restrict__ in, cd *__restrict__ out,
+                                               unsigned char *smem_raw, int tid, int bx, int by) {
+    cd *w = reinterpret_cast<cd *>(smem_raw), *v = w + n1 * n1;
+    cd *S = v + n1 * n1, *Y = S + n1 * C;
+    const int j = bx;
+    const int m0 = by * C, cols = min(C, n3 - m0);
+    if (cols <= 0) return;
+    for (int t = tid; t < n1 * n1; t += NTH) { w[t] = __ldg(W1 + t); v[t] = __ldg(V1 + t); }
+    for (int t = tid; t < n1 * cols; t += NTH) {
+        int i = t / cols, mc = t - i * cols;
+        S[i * C + mc] = in[((size_t)i * n2 + j) * n3 + m0 + mc];
+    }
+    __syncthreads();
+    for (int t = tid; t < n1 * cols; t += NTH) {   // Y = diag(1/D) (W1 S)
+        int a = t / cols, mc = t - a * cols;
+        cd acc = cdot_strided(w + a * n1, 1, S + mc, C, n1);
+        Y[a * C + mc] = cmul(acc, __ldg(invD + ((size_t)a * n2 + j) * n3 + m0 + mc));
+    }
+    __syncthreads();
+    for (int t = tid; t < n1 * cols; t += NTH) {   // out = V1 Y
+        int i = t / cols, mc = t - i * cols;
+        out[((size_t)i * n2 + j) * n3 + m0 + mc] = cdot_strided(v + i * n1, 1, Y + mc, C, n1);
+    }
+}
+
+__global__ void __launch_bounds__(FDM_THREADS) k_fdm_plane(int n2, int n3, int R,
+                                                           const cd *__restrict__ A2,
+                                                           const cd *__restrict__ A3,
+                                                           const cd *__restrict__ in,
+                                                           cd *__restrict__ out, const int *done) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    if (is_done(done)) return;
+    fdm_plane_body<FDM_THREADS>(n2, n3, R, A2, A3, in, out, smem_raw, threadIdx.x, blockIdx.x,
+                                blockIdx.y);
+}
+
+__global__ void __launch_bounds__(FDM_THREADS) k_fdm_fiber(int n1, int n2, int n3, int C,
+                                                           const cd *__restrict__ W1,
+                                                           const cd *__restrict__ V1,
+                                                           const cd *__restrict__ invD,
+                                                           const cd *__restrict__ in,
+                                                           cd *__restrict__ out, const int *done) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    if (is_done(done)) return;
+    fdm_fiber_body<FDM_THREADS>(n1, n2, n3, C, W1, V1, invD, in, out, smem_raw, threadIdx.x,
+                                blockIdx.x, blockIdx.y);
+}
+
 __global__ void k_assemble(Lvl L, cd *__restrict__ A) {
+    pdl_enter();
     long long N = (long long)L.n1 * L.plane;
     long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (r >= N) return;
@@ -860,11 +1035,13 @@ __global__ void k_assemble(Lvl L, cd *__restrict__ A) {
 }
 
 __global__ void k_set_identity(long long N, cd *__restrict__ B) {
+    pdl_enter();
     long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (q < N) B[q * N + q] = mk(1.0, 0.0);
 }
 
 __global__ void k_zero(long long n, cd *__restrict__ y) {
+    pdl_enter();
     for (long long q = blockIdx.x * 256ll + threadIdx.x; q < n; q += (long long)gridDim.x * 256)
         y[q] = mk(0, 0);
 }
@@ -872,6 +1049,24 @@ __global__ void k_zero(long long n, cd *__restrict__ y) {
 // ---------------------------------------------------------------------------
 // host launchers
 // ---------------------------------------------------------------------------
+// every launch carries the programmatic-stream-serialization attribute (PDL)
+template <class... KArgs, class... Args>
+static void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                   Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    static const bool pdl = !std::getenv("HF_NO_PDL");   // A/B switch for profiling
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 static dim3 march_grid(const Lvl &L, int &chunk) {
     int gx = (L.n3 + MARCH_BX - 1) / MARCH_BX;
     int gy = (L.n2 + MARCH_BY - 1) / MARCH_BY;
@@ -912,7 +1107,7 @@ static void stencil_launch(const Lvl &L, const cd *src, const cd *aux, double om
     int chunk;
     dim3 g = tile_grid(L, chunk);
     size_t smem = sizeof(StencilSmem<MODE, KVAR, Epi::kAux>);
-    k_stencil<MODE, Epi, ND, KVAR, SOMM><<<g, kTileBlock, smem, s>>>(L, src, aux ? aux : src, omega, e,
+    launch(k_stencil<MODE, Epi, ND, KVAR, SOMM>, dim3(g), dim3(kTileBlock), smem, s, L, src, aux ? aux : src, omega, e,
                                                                      chunk, rs, done);
 }
 template <int MODE, class Epi, int ND>
@@ -949,6 +1144,8 @@ void init_kernel_attributes() {
     set_attr<MODE_LOAD, EpiResid, 0>();
     set_attr<MODE_LOAD, EpiJacobi, 0>();
     set_attr<MODE_PRE, EpiResid, 0>();
+    cudaFuncSetAttribute(k_fdm_plane, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_fdm_fiber, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     done = true;
 }
 
@@ -987,19 +1184,19 @@ static void corr(int mode, const Lvl &F, const Lvl &C, const cd *b, const cd *e,
     // kernel, so parallelism beats the coarse-plane reuse of longer marches)
     const int chunk = 2;
     dim3 g((F.n3 + 31) / 32, (F.n2 + 7) / 8, (F.nx + chunk - 1) / chunk);
-    if (mode == 0) k_corr<0><<<g, 256, 0, s>>>(F, C, b, e, out, omega, chunk, done);
-    else if (mode == 1) k_corr<1><<<g, 256, 0, s>>>(F, C, b, e, out, omega, chunk, done);
-    else k_corr<2><<<g, 256, 0, s>>>(F, C, b, e, out, omega, chunk, done);
+    if (mode == 0) launch(k_corr<0>, dim3(g), dim3(256), 0, s, F, C, b, e, out, omega, chunk, done);
+    else if (mode == 1) launch(k_corr<1>, dim3(g), dim3(256), 0, s, F, C, b, e, out, omega, chunk, done);
+    else launch(k_corr<2>, dim3(g), dim3(256), 0, s, F, C, b, e, out, omega, chunk, done);
 }
 void launch_jacobi0(const Lvl &L, const cd *b, cd *u, double omega, cudaStream_t s,
                     const int *done) {
     int chunk;
     dim3 g = march_grid(L, chunk);
-    k_jacobi0<<<g, kMarchBlock, 0, s>>>(L, b, u, omega, chunk, done);
+    launch(k_jacobi0, dim3(g), dim3(kMarchBlock), 0, s, L, b, u, omega, chunk, done);
 }
 void launch_dinv(const Lvl &L, cd *out_owned, cudaStream_t s) {
     int g0 = std::max(-HF_GHOST, -L.lo1), g1 = std::min(L.nx + HF_GHOST, L.n1 - L.lo1);
-    k_dinv<<<592, 256, 0, s>>>(L, g0, g1, out_owned);
+    launch(k_dinv, dim3(592), dim3(256), 0, s, L, g0, g1, out_owned);
 }
 void launch_restrict(const Lvl &F, const Lvl &C, const cd *r, cd *out, cudaStream_t s,
                      const int *done) {
@@ -1008,7 +1205,7 @@ void launch_restrict(const Lvl &F, const Lvl &C, const cd *r, cd *out, cudaStrea
     int gz = (int)std::max<long long>(1, std::min<long long>(C.nx, (148 * 6 + cols - 1) / cols));
     int chunk = std::max(2, (C.nx + gz - 1) / gz);
     gz = (C.nx + chunk - 1) / chunk;
-    k_restrict2<<<dim3(gx, gy, gz), 256, 0, s>>>(F, C, r, out, chunk, done);
+    launch(k_restrict2, dim3(dim3(gx, gy, gz)), dim3(256), 0, s, F, C, r, out, chunk, done);
 }
 void launch_prolong(const Lvl &F, const Lvl &C, const cd *e, cd *out, bool add, cudaStream_t s,
                     const int *done) {
@@ -1027,18 +1224,18 @@ void launch_up1(const Lvl &L, const Lvl &C, const cd *b, const cd *e, cd *u, cd 
 }
 void launch_gemv(int N, const cd *Minv, const cd *b, cd *x, cudaStream_t s, const int *done) {
     int blocks = (N + 1) / 2;
-    k_gemv<<<blocks, 64, 0, s>>>(N, Minv, b, x, done);
+    launch(k_gemv, dim3(blocks), dim3(64), 0, s, N, Minv, b, x, done);
 }
 void launch_sym_pack(int N, const cd *Minv, const double *sv, cd *tiles, cudaStream_t s) {
     int nT = (N + SYT - 1) / SYT;
-    k_sym_pack<<<2048, 256, 0, s>>>(N, nT, Minv, sv, tiles);
+    launch(k_sym_pack, dim3(2048), dim3(256), 0, s, N, nT, Minv, sv, tiles);
 }
 void launch_symv(int N, const cd *tiles, const double *sv, const cd *b, cd *prow, cd *pcol, cd *x,
                  cudaStream_t s, const int *done) {
     int nT = (N + SYT - 1) / SYT;
     long long ntile = (long long)nT * (nT + 1) / 2;
-    k_sym_tiles<<<(unsigned)ntile, 256, 0, s>>>(N, nT, tiles, sv, b, prow, pcol, done);
-    k_sym_reduce<<<(N * 32 + 255) / 256, 256, 0, s>>>(N, nT, prow, pcol, x, done);
+    launch(k_sym_tiles, dim3((unsigned)ntile), dim3(256), 0, s, N, nT, tiles, sv, b, prow, pcol, done);
+    launch(k_sym_reduce, dim3((N * 32 + 255) / 256), dim3(256), 0, s, N, nT, prow, pcol, x, done);
 }
 long long sym_tiles_count(int N) {
     long long nT = (N + SYT - 1) / SYT;
@@ -1046,46 +1243,73 @@ long long sym_tiles_count(int N) {
 }
 void launch_assemble(const Lvl &L, cd *A, cudaStream_t s) {
     long long N = (long long)L.n1 * L.plane;
-    k_assemble<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(L, A);
+    launch(k_assemble, dim3((unsigned)((N + 255) / 256)), dim3(256), 0, s, L, A);
+}
+static void fdm_split(int n1, int n2, int n3, int &R, int &C, size_t &sp, size_t &sf) {
+    R = (n2 + FDM_GROUPS - 1) / FDM_GROUPS;
+    C = (n3 + FDM_GROUPS - 1) / FDM_GROUPS;
+    sp = ((size_t)R * n2 + (size_t)n3 * n3 + (size_t)n2 * n3 + (size_t)R * n3) * sizeof(cd);
+    sf = (2ull * n1 * n1 + 2ull * n1 * C) * sizeof(cd);
+}
+size_t fdm_smem_bytes(int n1, int n2, int n3) {
+    int R, C;
+    size_t sp, sf;
+    fdm_split(n1, n2, n3, R, C, sp, sf);
+    return std::max(sp, sf);
+}
+// fdm = [V1^-1, V2^-1, V3^-1, V1, V2, V3] (row-major n_d x n_d each), tmp = 2N
+void launch_fdm(int n1, int n2, int n3, const cd *fdm, const cd *invD, const cd *b, cd *tmp,
+                cd *x, cudaStream_t s, const int *done) {
+    const cd *W1 = fdm, *W2 = W1 + n1 * n1, *W3 = W2 + n2 * n2;
+    const cd *V1 = W3 + n3 * n3, *V2 = V1 + n1 * n1, *V3 = V2 + n2 * n2;
+    int R, C;
+    size_t sp, sf;
+    fdm_split(n1, n2, n3, R, C, sp, sf);
+    cd *t0 = tmp, *t1 = tmp + (size_t)n1 * n2 * n3;
+    dim3 gp(n1, (n2 + R - 1) / R), gf(n2, (n3 + C - 1) / C);
+    launch(k_fdm_plane, gp, dim3(FDM_THREADS), sp, s, n2, n3, R, W2, W3, b, t0, done);
+    launch(k_fdm_fiber, gf, dim3(FDM_THREADS), sf, s, n1, n2, n3, C, W1, V1, invD,
+           (const cd *)t0, t1, done);
+    launch(k_fdm_plane, gp, dim3(FDM_THREADS), sp, s, n2, n3, R, V2, V3, (const cd *)t1, x, done);
 }
 void launch_set_identity(long long N, cd *B, cudaStream_t s) {
-    k_set_identity<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(N, B);
+    launch(k_set_identity, dim3((unsigned)((N + 255) / 256)), dim3(256), 0, s, N, B);
 }
 void launch_zero(long long n, cd *y, cudaStream_t s) {
-    k_zero<<<VEC_BLOCKS, 256, 0, s>>>(n, y);
+    launch(k_zero, dim3(VEC_BLOCKS), dim3(256), 0, s, n, y);
 }
 void launch_axpby(long long n, cd a, const cd *x, cd b, cd *y, cudaStream_t s) {
-    k_axpby<<<VEC_BLOCKS, 256, 0, s>>>(n, a, x, b, y);
+    launch(k_axpby, dim3(VEC_BLOCKS), dim3(256), 0, s, n, a, x, b, y);
 }
 void launch_mgs(long long n, cd *w, const cd *c, const cd *vprev, const cd *vcur,
                 const RedSlot &rs, cudaStream_t s) {
-    k_mgs<<<VEC_BLOCKS, 256, 0, s>>>(n, w, c, vprev, vcur, rs);
+    launch(k_mgs, dim3(VEC_BLOCKS), dim3(256), 0, s, n, w, c, vprev, vcur, rs);
 }
 void launch_multi_axpy(long long n, int m, const cd *const *V, const cd *y, cd *x, cudaStream_t s) {
-    k_multi_axpy<<<VEC_BLOCKS, 256, 0, s>>>(n, m, V, y, x);
+    launch(k_multi_axpy, dim3(VEC_BLOCKS), dim3(256), 0, s, n, m, V, y, x);
 }
 void launch_dot(long long n, const cd *a, const cd *b, const RedSlot &rs, cudaStream_t s) {
-    k_dot_store<<<VEC_BLOCKS, 256, 0, s>>>(n, a, b, rs);
+    launch(k_dot_store, dim3(VEC_BLOCKS), dim3(256), 0, s, n, a, b, rs);
 }
 void launch_bcg_init(long long n, const cd *b, cd *r, cd *rs, cd *x, cd *p, cd *v,
                      const RedSlot &red, cudaStream_t s) {
-    k_bcg_init<<<VEC_BLOCKS, 256, 0, s>>>(n, b, r, rs, x, p, v, red);
+    launch(k_bcg_init, dim3(VEC_BLOCKS), dim3(256), 0, s, n, b, r, rs, x, p, v, red);
 }
 void launch_bcg_p(long long n, const BcgState *st, const cd *r, cd *p, const cd *v,
                   cudaStream_t s, const int *done) {
-    k_bcg_p<<<VEC_BLOCKS, 256, 0, s>>>(n, st, r, p, v, done);
+    launch(k_bcg_p, dim3(VEC_BLOCKS), dim3(256), 0, s, n, st, r, p, v, done);
 }
 void launch_bcg_s(long long n, const BcgState *st, const cd *r, const cd *v, cd *sv,
                   const RedSlot &red, cudaStream_t s, const int *done) {
-    k_bcg_s<<<VEC_BLOCKS, 256, 0, s>>>(n, st, r, v, sv, red, done);
+    launch(k_bcg_s, dim3(VEC_BLOCKS), dim3(256), 0, s, n, st, r, v, sv, red, done);
 }
 void launch_bcg_xr(long long n, const BcgState *st, cd *x, const cd *ph, const cd *sh,
                    const cd *sv, const cd *t, cd *r, const cd *rs, const RedSlot &red,
                    cudaStream_t s, const int *done) {
-    k_bcg_xr<<<VEC_BLOCKS, 256, 0, s>>>(n, st, x, ph, sh, sv, t, r, rs, red, done);
+    launch(k_bcg_xr, dim3(VEC_BLOCKS), dim3(256), 0, s, n, st, x, ph, sh, sv, t, r, rs, red, done);
 }
 void launch_bcg_xhalf(long long n, const BcgState *st, cd *x, const cd *ph, cudaStream_t s) {
-    k_bcg_xhalf<<<VEC_BLOCKS, 256, 0, s>>>(n, st, x, ph);
+    launch(k_bcg_xhalf, dim3(VEC_BLOCKS), dim3(256), 0, s, n, st, x, ph);
 }
 
 }  // namespace hf

@@ -12,6 +12,7 @@
 #include <cmath>
 #include <complex>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -191,6 +192,9 @@ struct hf_hierarchy {
     cd *symtiles = nullptr; // Sommerfeld: packed upper triangle of M^-1 S^-1 (64 x 64 tiles)
     double *symscale = nullptr;
     cd *prow = nullptr, *pcol = nullptr;
+    cd *fdm = nullptr;      // separable coarsest: [V1^-1, V2^-1, V3^-1, V1, V2, V3]
+    cd *fdm_invD = nullptr; // 1 / (l1_a + l2_b + l3_c + c) on the coarsest grid
+    cd *fdm_tmp = nullptr;  // 2 N scratch
     int coarsest_flags = 0;
 };
 
@@ -200,7 +204,167 @@ static bool keep_coarsening(int n1, int n2, int n3, const hf_mg_config &c) {
     return ok && (n1 % 2) && (n2 % 2) && (n3 % 2);
 }
 
+// ---------------------------------------------------------------------------
+// separable coarsest operator: 1-D eigendecompositions (cuSOLVER geev) for
+// the fast-diagonalisation solve (k_fdm_* in hf_kernels.cu)
+// ---------------------------------------------------------------------------
+typedef std::complex<double> zc;
+
+// T_d of one direction (operators.py:163-172 split per axis): 2/h^2 centre,
+// -1/h^2 neighbours, Sommerfeld end rows with the doubled inward neighbour and
+// -2ik/h on the centre.
+static std::vector<zc> op1d(int n, const Lvl &L) {
+    std::vector<zc> T((size_t)n * n, 0.0);
+    for (int i = 0; i < n; i++) {
+        T[(size_t)i * n + i] = 2.0 * L.ih2;
+        if (i > 0) T[(size_t)i * n + i - 1] += -L.ih2 * (i == n - 1 ? 2.0 : 1.0);
+        if (i < n - 1) T[(size_t)i * n + i + 1] += -L.ih2 * (i == 0 ? 2.0 : 1.0);
+    }
+    T[0] -= zc(0.0, L.kc * L.twoh);
+    T[(size_t)n * n - 1] -= zc(0.0, L.kc * L.twoh);
+    return T;
+}
+
+// in-place Gauss-Jordan inverse with partial pivoting (row-major n x n)
+static bool invert(std::vector<zc> &A, int n) {
+    std::vector<zc> B((size_t)n * n, 0.0);
+    for (int i = 0; i < n; i++) B[(size_t)i * n + i] = 1.0;
+    for (int c = 0; c < n; c++) {
+        int p = c;
+        for (int r = c + 1; r < n; r++)
+            if (std::abs(A[(size_t)r * n + c]) > std::abs(A[(size_t)p * n + c])) p = r;
+        if (std::abs(A[(size_t)p * n + c]) == 0.0) return false;
+        if (p != c)
+            for (int k = 0; k < n; k++) {
+                std::swap(A[(size_t)p * n + k], A[(size_t)c * n + k]);
+                std::swap(B[(size_t)p * n + k], B[(size_t)c * n + k]);
+            }
+        zc inv = 1.0 / A[(size_t)c * n + c];
+        for (int k = 0; k < n; k++) { A[(size_t)c * n + k] *= inv; B[(size_t)c * n + k] *= inv; }
+        for (int r = 0; r < n; r++) {
+            if (r == c) continue;
+            zc f = A[(size_t)r * n + c];
+            if (f == 0.0) continue;
+            for (int k = 0; k < n; k++) {
+                A[(size_t)r * n + k] -= f * A[(size_t)c * n + k];
+                B[(size_t)r * n + k] -= f * B[(size_t)c * n + k];
+            }
+        }
+    }
+    A.swap(B);
+    return true;
+}
+
+// T = V diag(lam) V^-1 (row-major V, Vi); false if geev fails or the
+// decomposition does not reproduce T to ~1e-13 (then the dense path is used)
+static bool eig1d(cusolverDnHandle_t hs, const std::vector<zc> &T, int n, std::vector<zc> &lam,
+                  std::vector<zc> &V, std::vector<zc> &Vi, cudaStream_t s) {
+    std::vector<zc> Tc((size_t)n * n);   // column-major copy for cuSOLVER
+    for (int i = 0; i < n; i++)
+        for (int j = 0; j < n; j++) Tc[(size_t)j * n + i] = T[(size_t)i * n + j];
+    cusolverDnParams_t prm;
+    if (cusolverDnCreateParams(&prm) != CUSOLVER_STATUS_SUCCESS) return false;
+    void *dA = nullptr, *dW = nullptr, *dV = nullptr, *dwork = nullptr;
+    int *dinfo = nullptr;
+    size_t dws = 0, hws = 0;
+    bool ok = cudaMalloc(&dA, Tc.size() * sizeof(zc)) == cudaSuccess &&
+              cudaMalloc(&dW, n * sizeof(zc)) == cudaSuccess &&
+              cudaMalloc(&dV, Tc.size() * sizeof(zc)) == cudaSuccess &&
+              cudaMalloc(&dinfo, sizeof(int)) == cudaSuccess;
+    std::vector<char> hwork;
+    int info = -1;
+    if (ok) {
+        cudaMemcpy(dA, Tc.data(), Tc.size() * sizeof(zc), cudaMemcpyHostToDevice);
+        ok = cusolverDnXgeev_bufferSize(hs, prm, CUSOLVER_EIG_MODE_NOVECTOR, CUSOLVER_EIG_MODE_VECTOR,
+                                        n, CUDA_C_64F, dA, n, CUDA_C_64F, dW, CUDA_C_64F, nullptr, n,
+                                        CUDA_C_64F, dV, n, CUDA_C_64F, &dws, &hws) ==
+             CUSOLVER_STATUS_SUCCESS;
+    }
+    if (ok) {
+        hwork.resize(std::max<size_t>(hws, 1));
+        ok = cudaMalloc(&dwork, std::max<size_t>(dws, 1)) == cudaSuccess;
+    }
+    if (ok)
+        ok = cusolverDnXgeev(hs, prm, CUSOLVER_EIG_MODE_NOVECTOR, CUSOLVER_EIG_MODE_VECTOR, n,
+                             CUDA_C_64F, dA, n, CUDA_C_64F, dW, CUDA_C_64F, nullptr, n, CUDA_C_64F,
+                             dV, n, CUDA_C_64F, dwork, dws, hwork.data(), hws, dinfo) ==
+             CUSOLVER_STATUS_SUCCESS;
+    std::vector<zc> Vc((size_t)n * n);
+    lam.assign(n, 0.0);
+    if (ok) {
+        ok = cudaStreamSynchronize(s) == cudaSuccess &&
+             cudaMemcpy(&info, dinfo, sizeof(int), cudaMemcpyDeviceToHost) == cudaSuccess &&
+             cudaMemcpy(lam.data(), dW, n * sizeof(zc), cudaMemcpyDeviceToHost) == cudaSuccess &&
+             cudaMemcpy(Vc.data(), dV, Vc.size() * sizeof(zc), cudaMemcpyDeviceToHost) == cudaSuccess &&
+             info == 0;
+    }
+    cudaFree(dA); cudaFree(dW); cudaFree(dV); cudaFree(dwork); cudaFree(dinfo);
+    cusolverDnDestroyParams(prm);
+    if (!ok) return false;
+    V.resize((size_t)n * n);
+    for (int i = 0; i < n; i++)
+        for (int c = 0; c < n; c++) V[(size_t)i * n + c] = Vc[(size_t)c * n + i];
+    Vi = V;
+    if (!invert(Vi, n)) return false;
+    // check ||T - V diag(lam) V^-1|| / ||T||
+    double tn = 0, en = 0;
+    for (int i = 0; i < n; i++)
+        for (int j = 0; j < n; j++) {
+            zc acc = 0.0;
+            for (int c = 0; c < n; c++) acc += V[(size_t)i * n + c] * lam[c] * Vi[(size_t)c * n + j];
+            en = std::max(en, std::abs(acc - T[(size_t)i * n + j]));
+            tn = std::max(tn, std::abs(T[(size_t)i * n + j]));
+        }
+    return en <= 1e-12 * tn;
+}
+
+static int build_coarsest_fdm(hf_hierarchy *H, cudaStream_t s, bool &built) {
+    built = false;
+    Level &C = H->lev.back();
+    const Lvl &L = C.L;
+    if (L.bc != HF_BC_SOMMERFELD || L.k != nullptr || std::getenv("HF_COARSEST_DENSE")) return 0;
+    if (L.lo1 != 0 || L.nx != L.n1) return 0;
+    if (fdm_smem_bytes(L.n1, L.n2, L.n3) > 200 * 1024) return 0;
+    cusolverDnHandle_t hs;
+    if (cusolverDnCreate(&hs) != CUSOLVER_STATUS_SUCCESS) return 0;
+    cusolverDnSetStream(hs, s);
+    const int n[3] = {L.n1, L.n2, L.n3};
+    std::vector<zc> lam[3], V[3], Vi[3];
+    bool ok = true;
+    for (int d = 0; d < 3 && ok; d++) ok = eig1d(hs, op1d(n[d], L), n[d], lam[d], V[d], Vi[d], s);
+    cusolverDnDestroy(hs);
+    if (!ok) return 0;
+    const long long N = (long long)L.n1 * L.plane;
+    const zc c0(-L.sre * L.kc * L.kc, -L.sim * L.kc * L.kc);
+    std::vector<zc> invD((size_t)N);
+    for (int a = 0; a < n[0]; a++)
+        for (int b = 0; b < n[1]; b++)
+            for (int c = 0; c < n[2]; c++) {
+                zc dd = lam[0][a] + lam[1][b] + lam[2][c] + c0;
+                if (std::abs(dd) == 0.0) return fail(HF_ERR_SOLVER, "coarsest operator is singular");
+                invD[((size_t)a * n[1] + b) * n[2] + c] = 1.0 / dd;
+            }
+    std::vector<zc> pack;
+    for (int d = 0; d < 3; d++) pack.insert(pack.end(), Vi[d].begin(), Vi[d].end());
+    for (int d = 0; d < 3; d++) pack.insert(pack.end(), V[d].begin(), V[d].end());
+    cudaError_t err;
+    H->fdm = H->A.get<cd>(pack.size(), err);
+    H->fdm_invD = H->A.get<cd>((size_t)N, err);
+    H->fdm_tmp = H->A.get<cd>(2 * (size_t)N, err);
+    if (!H->fdm || !H->fdm_invD || !H->fdm_tmp) return fail(HF_ERR_CUDA, "cudaMalloc fdm coarsest");
+    CK(cudaMemcpy(H->fdm, pack.data(), pack.size() * sizeof(zc), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(H->fdm_invD, invD.data(), (size_t)N * sizeof(zc), cudaMemcpyHostToDevice));
+    H->Nc = (int)N;
+    built = true;
+    return 0;
+}
+
 static int build_coarsest_direct(hf_hierarchy *H, cudaStream_t s) {
+    {
+        bool built = false;
+        if (int rc = build_coarsest_fdm(H, s, built)) return rc;
+        if (built) return 0;
+    }
     Level &C = H->lev.back();
     if (C.L.lo1 != 0 || C.L.nx != C.L.n1)
         return fail(HF_ERR_UNSUPPORTED, "direct coarsest solve needs the whole coarsest grid");
@@ -281,6 +445,7 @@ static int build_coarsest_direct(hf_hierarchy *H, cudaStream_t s) {
 
 static cudaStream_t work_stream() { return g_user_stream; }
 
+
 extern "C" hf_hierarchy *hf_hierarchy_create(int n1, int n2, int n3, int lo1, int nx, double h,
                                              double beta1, double beta2, int bc,
                                              const double *k_host, double k_const,
@@ -358,7 +523,11 @@ extern "C" int hf_hierarchy_level_shape(const hf_hierarchy *H, int l, int *d) {
 // cycles (multigrid.py:326-419)
 // ---------------------------------------------------------------------------
 static void coarsest(hf_hierarchy *H, const cd *b, cd *x, cudaStream_t s, const int *done) {
-    if (H->symtiles) {
+    if (H->fdm) {
+        const Lvl &L = H->lev.back().L;
+        L1(launch_fdm(L.n1, L.n2, L.n3, H->fdm, H->fdm_invD, b, H->fdm_tmp, x, s, done));
+        g_launches += 2;
+    } else if (H->symtiles) {
         L1(launch_symv(H->Nc, H->symtiles, H->symscale, b, H->prow, H->pcol, x, s, done));
         g_launches++;   // tiles + reduction
     } else {
@@ -469,6 +638,14 @@ extern "C" int hf_level_smooth(hf_hierarchy *H, int l, const double *t, const do
                      work_stream(), nullptr));
     CKL();
     return 0;
+}
+
+extern "C" int hf_coarsest_kind(const hf_hierarchy *H) {
+    if (!H) return fail(HF_ERR_ARG, "null hierarchy");
+    if (H->fdm) return HF_COARSEST_KIND_SEPARABLE;
+    if (H->symtiles) return HF_COARSEST_KIND_SYMMETRIC;
+    if (H->Minv) return HF_COARSEST_KIND_DENSE;
+    return HF_COARSEST_KIND_NONE;
 }
 
 extern "C" int hf_coarsest_solve(hf_hierarchy *H, const double *b, double *x) {

@@ -96,6 +96,13 @@ class MGHierarchy:
     def coarsest(self) -> MGLevel:
         return self.levels[-1]
 
+    @property
+    def coarsest_kind(self) -> str:
+        """Exact coarsest solve in use: "separable" (fast diagonalisation,
+        constant k), "symmetric" / "dense" (inverse), or "external"."""
+        kind = _native.load().hf_coarsest_kind(self._h)
+        return {0: "external", 1: "dense", 2: "symmetric", 3: "separable"}[kind]
+
 
 def build_hierarchy(finest_grid: Grid3, finest_extent: BlockExtent | None,
                     finest_spec: OperatorSpec, config: MGConfig | None = None,

@@ -74,6 +74,29 @@ def _pair(hf, oracle, n, bc, k, beta2=-0.5, **cfg):
     return hier, oh
 
 
+@pytest.mark.parametrize("dims,h,kc", [((17, 17, 17), 1 / 16, 80.0), ((9, 17, 5), 1 / 8, 7.5),
+                                       ((17, 17, 17), 1 / 16, 40.0)])
+def test_coarsest_fast_diagonalisation(hf, oracle, dims, h, kc, monkeypatch):
+    """Constant-k Sommerfeld coarsest solve (separable, k_fdm_*) is exact: the
+    true residual through the oracle's operator is at round-off and it agrees
+    with the dense-inverse path (HF_COARSEST_DENSE) to 1e-12."""
+    from paper_2308_06085_b200.multigrid import MGConfig, build_hierarchy, coarsest_solve
+    from paper_2308_06085_b200.operators import OperatorSpec, Sommerfeld
+    grid = hf.make_grid(*dims, h)
+    spec = OperatorSpec("cslp", 1.0, -0.5, Sommerfeld(), np.full(dims, kc))
+    b = _rand(dims, 21)
+    hier = build_hierarchy(grid, None, spec, MGConfig(coarsest_threshold=64))
+    assert len(hier.levels) == 1 and hier.coarsest_kind == "separable"
+    x = coarsest_solve(hier, b).cpu().numpy()
+    r = b - oracle.apply(np.full(dims, kc), x, h, spec.shift, "sommerfeld")
+    assert np.linalg.norm(r) / np.linalg.norm(b) < 1e-12
+    monkeypatch.setenv("HF_COARSEST_DENSE", "1")
+    dense = build_hierarchy(grid, None, spec, MGConfig(coarsest_threshold=64))
+    assert dense.coarsest_kind == "symmetric"
+    xd = coarsest_solve(dense, b).cpu().numpy()
+    assert _rel(x, xd) < 1e-12
+
+
 @pytest.mark.parametrize("bc", ["dirichlet", "sommerfeld"])
 def test_transfers_and_smoother(hf, oracle, bc):
     from paper_2308_06085_b200.multigrid import jacobi_smooth, prolong_tl, restrict_fw

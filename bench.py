@@ -349,6 +349,7 @@ def kernel_table(A, hier, n, t_iter_ms, reps=20):
     sym_bytes = nt * (nt + 1) // 2 * 64 * 64 * 16 + 2 * nt * (nt + 1) // 2 * 64 * 16 * 2
     p = lambda x: x.data_ptr()
     cases = {
+        "device_copy": (lambda: v.copy_(u), 32.0 * n),   # practical ceiling, same buffers
         "helmholtz_matvec": (lambda: L.hf_operator_apply(A._h, p(u), p(v)), 32.0 * n),
         "cslp_presmooth_residual": (lambda: L.hf_level_down1(H, 0, p(b), p(v)), 32.0 * n),
         "restrict_fw": (lambda: L.hf_restrict_fw(H, 0, p(v), p(bc)), 16.0 * n + 16.0 * nc_f),
@@ -367,7 +368,8 @@ def kernel_table(A, hier, n, t_iter_ms, reps=20):
         ms = _event_time(fn, reps)
         out[name] = {"ms": round(ms, 5), "bytes": nbytes, "gbs": round(nbytes / (ms / 1e3) / 1e9, 1),
                      "share": round(2 * ms / t_iter_ms, 4),
-                     "bound": "latency" if name == "coarsest_solve" and kind == "separable" else "hbm"}
+                     "bound": ("latency" if name == "coarsest_solve" and kind == "separable"
+                               else "ceiling" if name == "device_copy" else "hbm")}
     out["coarsest_solve"]["kind"] = kind
     return out
 

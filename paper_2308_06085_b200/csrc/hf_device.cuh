@@ -47,7 +47,8 @@ struct Lvl {
     const double *k;     // wavenumber at owned plane 0 (ghost planes valid), or null
     double kc;           // constant wavenumber when k == null
     const double2 *dinv; // D^-1 at owned plane 0 (ghost planes valid) when k varies, else null
-    const double2 *tab;  // constant k: tab[nb] = a_p, tab[4 + nb] = D^-1 for nb physical faces
+    const double2 *tab;  // constant k, nb physical faces: tab[nb] = a_p, tab[4 + nb] = D^-1,
+                         // tab[8 + nb] = D^-1(nb) / D^-1(0)
 };
 
 // D^-1 at local linear index q of a vertex touching nb physical faces
@@ -172,12 +173,23 @@ __device__ __forceinline__ void reduce_finish(cd (&acc)[ND], const RedSlot &rs) 
     cd a2[ND];
 #pragma unroll
     for (int d = 0; d < ND; d++) a2[d] = mk(0, 0);
-    for (unsigned b = tid; b < nblk; b += HF_RED_THREADS) {
+    // four independent loads in flight per thread (fixed order => deterministic)
+    unsigned b = tid;
+    for (; b + 3 * HF_RED_THREADS < nblk; b += 4 * HF_RED_THREADS) {
+        cd p[4][ND];
 #pragma unroll
-        for (int d = 0; d < ND; d++) {
-            cd p = __ldcg(rs.partials + (size_t)b * ND + d);
-            a2[d] = cadd(a2[d], p);
-        }
+        for (int k = 0; k < 4; k++)
+#pragma unroll
+            for (int d = 0; d < ND; d++)
+                p[k][d] = __ldcg(rs.partials + (size_t)(b + k * HF_RED_THREADS) * ND + d);
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+#pragma unroll
+            for (int d = 0; d < ND; d++) a2[d] = cadd(a2[d], p[k][d]);
+    }
+    for (; b < nblk; b += HF_RED_THREADS) {
+#pragma unroll
+        for (int d = 0; d < ND; d++) a2[d] = cadd(a2[d], __ldcg(rs.partials + (size_t)b * ND + d));
     }
     cd tot[ND];
     block_sum<ND>(a2, tot);

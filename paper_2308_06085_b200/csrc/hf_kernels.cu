@@ -149,6 +149,29 @@ __device__ __forceinline__ ColCtx col_ctx(const Lvl &L, int chunk) {
 
 enum { MODE_LOAD = 0, MODE_PRE = 1 };
 
+template <int V>
+struct IC {
+    static constexpr int value = V;
+};
+// f(IC<B>), f(IC<B+1>), ..., f(IC<E-1>) at compile time
+template <int B, int E, class F>
+__device__ __forceinline__ void static_for(F &&f) {
+    if constexpr (B < E) {
+        f(IC<B>{});
+        static_for<B + 1, E>(f);
+    }
+}
+// march steps R = B.. of the ring until the chunk ends; false once it has
+template <int B, int E, class F>
+__device__ __forceinline__ bool ring_steps(F &&f, int &i, int i1) {
+    if constexpr (B < E) {
+        f(IC<B>{}, i);
+        if (++i >= i1) return false;
+        return ring_steps<B + 1, E>(f, i, i1);
+    }
+    return true;
+}
+
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem, bool valid) {
     unsigned s = (unsigned)__cvta_generic_to_shared(smem);
     int sz = valid ? 16 : 0;
@@ -281,18 +304,25 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
     constexpr bool kScale = MODE == MODE_PRE && !KVAR;
     const bool edge_block = j0 - 1 <= 0 || j0 + TILE_Y >= L.n2 - 1 || m0 - 1 <= 0 ||
                             m0 + TILE_X >= L.n3 - 1;
+    // fill entries that are boundary vertices of an interior plane (nbx = 0) and
+    // their rescale factors, fixed for the whole march
+    const bool f0 = kScale && ok0 && nbe0 > 0, f1 = kScale && ok1 && nbe1 > 0;
     auto fixup = [&](int slot, int i) {
         int gi = L.lo1 + i;
         gi = gi < 0 ? -gi : (gi >= L.n1 ? 2 * (L.n1 - 1) - gi : gi);
         const int nbx = (gi == 0) + (gi == L.n1 - 1);
-        if (!edge_block && nbx == 0) return;   // block-uniform: no boundary vertex staged
-        if (ok0 && nbx + nbe0) sm.raw[slot][tid] = cmul(sm.raw[slot][tid], tab[8 + nbx + nbe0]);
-        if (ok1 && nbx + nbe1) sm.raw[slot][tid + NT] = cmul(sm.raw[slot][tid + NT], tab[8 + nbx + nbe1]);
+        if (nbx == 0) {                    // block-uniform
+            if (!edge_block) return;
+            if (f0) sm.raw[slot][tid] = cmul(sm.raw[slot][tid], tab[8 + nbe0]);
+            if (f1) sm.raw[slot][tid + NT] = cmul(sm.raw[slot][tid + NT], tab[8 + nbe1]);
+            return;
+        }
+        if (ok0) sm.raw[slot][tid] = cmul(sm.raw[slot][tid], tab[8 + nbx + nbe0]);
+        if (ok1) sm.raw[slot][tid + NT] = cmul(sm.raw[slot][tid + NT], tab[8 + nbx + nbe1]);
     };
     auto wd_nb = [&](int nb) -> cd { return tab[4 + nb]; };   // read after the first barrier
     cd acc[2] = {mk(0, 0), mk(0, 0)};
 
-    int sslot = 0;
     // cp.async operands precomputed once: 32-bit shared addresses of this thread's
     // fill entries in ring slot 0 and global pointers of the entries in plane 0
     // (invalid entries point at a valid vertex and copy 0 bytes)
@@ -301,13 +331,14 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
     constexpr unsigned SLOT = NFILL * sizeof(cd);
     const cd *g0 = src + go0, *g1 = src + go1;
     const cd *d0 = SM::kWd ? L.dinv + go0 : nullptr, *d1 = SM::kWd ? L.dinv + go1 : nullptr;
-    auto stage = [&](int i) {              // one commit group per plane
-        const unsigned so = (unsigned)sslot * SLOT;
-        sslot = sslot == RING - 1 ? 0 : sslot + 1;
-        int gi = L.lo1 + i;
-        const bool pok = i <= i1 && gi >= -1 && gi <= L.n1;
-        gi = gi < 0 ? -gi : (gi >= L.n1 ? 2 * (L.n1 - 1) - gi : gi);   // mirrored plane
-        const long long pb = pok ? (long long)(gi - L.lo1) * L.plane : 0;
+    auto stage = [&](auto SS, int p) {     // one commit group per plane, ring slot SS
+        constexpr unsigned so = decltype(SS)::value * SLOT;
+        // plane p of the march (ghost planes of a slab included; mirrored outside
+        // the grid); nothing is copied past the chunk's last neighbour plane
+        const int gi = L.lo1 + p;
+        const bool pok = p <= i1 && gi >= -1 && gi <= L.n1;
+        const int gm = gi < 0 ? -gi : (gi >= L.n1 ? 2 * (L.n1 - 1) - gi : gi);
+        const long long pb = pok ? (long long)(gm - L.lo1) * L.plane : 0;
         const bool v0 = pok && ok0, v1 = pok && ok1;
         cp_async16s(sraw0 + so, g0 + pb, v0);
         if (SM::kWd) cp_async16s(swd0 + so, d0 + pb, v0);
@@ -318,10 +349,35 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
         cp_commit();
     };
 
-    for (int s = 0; s < RING - 1; s++) stage(i0 - 1 + s);   // planes i0-1 .. i0+2
-    int sp = 0, sc = 1, sn = 2;                              // ring slots of i-1, i, i+1
+    // in-loop staging (plane p = i + 3 > 0): straight copy while the plane is in
+    // memory (owned or ghost), the mirrored plane n1-2 for global plane n1,
+    // nothing past i1 (never read)
+    const int p_direct_end = min(i1, L.n1 - 1 - L.lo1);
+    const int p_mirror = L.n1 - L.lo1;
+    const long long mirror_off = (long long)(L.n1 - 2 - L.lo1) * L.plane;
+    auto stage_in = [&](auto SS, int p) {
+        constexpr unsigned so = decltype(SS)::value * SLOT;
+        long long pb = (long long)p * L.plane;
+        bool any = p <= p_direct_end;
+        if (!any && p == p_mirror && p <= i1) {
+            pb = mirror_off;
+            any = true;
+        }
+        if (any) {
+            cp_async16s(sraw0 + so, g0 + pb, ok0);
+            if (SM::kWd) cp_async16s(swd0 + so, d0 + pb, ok0);
+            if (has1) {
+                cp_async16s(sraw0 + so + NT * sizeof(cd), g1 + pb, ok1);
+                if (SM::kWd) cp_async16s(swd0 + so + NT * sizeof(cd), d1 + pb, ok1);
+            }
+        }
+        cp_commit();
+    };
+
+    // planes i0-1 .. i0+RING-3 into slots 0 .. RING-2
+    static_for<0, RING - 1>([&](auto Sc) { stage(Sc, i0 - 1 + decltype(Sc)::value); });
     if (kScale) {
-        cp_wait<2>();                      // planes i0-1, i0 of this thread's copies
+        cp_wait<RING - 3>();               // planes i0-1, i0 of this thread's copies
         __syncthreads();                   // tab[] visible
         fixup(0, i0 - 1);
         fixup(1, i0);
@@ -334,17 +390,22 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
         if (Epi::kAux) a_next = __ldg(aux + q);
         if (KVAR) k_next = __ldg(L.k + q);
     }
-    for (int i = i0; i < i1; i++, q += L.plane) {
+    // one plane; R = (i - i0) mod RING fixes the ring slots at compile time:
+    // i-1 in R, i in R+1, i+1 in R+2, and plane i+RING-2 is staged into R-1
+    auto step = [&](auto Rc, int i) {
+        constexpr int R = decltype(Rc)::value;
+        constexpr int sp = R, sc = (R + 1) % RING, sn = (R + 2) % RING;
+        constexpr int ss = (R + RING - 1) % RING;
         const cd a_cur = a_next;
         const double k_cur = k_next;
         if (act && i + 1 < i1) {
             if (Epi::kAux) a_next = __ldg(aux + q + L.plane);
             if (KVAR) k_next = __ldg(L.k + q + L.plane);
         }
-        cp_wait<1>();                      // plane i+1 landed (i+2 may be in flight)
+        cp_wait<RING - 4>();               // plane i+1 landed (later ones may be in flight)
         if (kScale) fixup(sn, i + 1);      // own entries only: no barrier needed before
         __syncthreads();
-        stage(i + RING - 2);               // into the slot read last at step i-1
+        stage_in(IC<ss>{}, i + RING - 2);  // into the slot read last at step i-1
         if (act) {
             const int gi = L.lo1 + i;
             const bool bxl = gi == 0, bxh = gi == L.n1 - 1;
@@ -385,7 +446,9 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
             if (Epi::kDinv) wd = KVAR ? cscal(__ldg(L.dinv + q), omega) : wd_nb(nb);
             epi(q, fc, mf, wd, av, acc);
         }
-        sp = sc; sc = sn; sn = sn == RING - 1 ? 0 : sn + 1;
+        q += L.plane;
+    };
+    for (int i = i0; i < i1 && ring_steps<0, RING>(step, i, i1);) {
     }
     cp_wait<0>();
     constexpr int NR = (ND > 0) ? ND : 1;
@@ -1091,10 +1154,11 @@ static dim3 tile_grid(const Lvl &L, int &chunk) {
     int gx = (L.n3 + TILE_X - 1) / TILE_X;
     int gy = (L.n2 + TILE_Y - 1) / TILE_Y;
     long long cols = (long long)gx * gy;
-    long long target = 148 * 8;     // resident 256-thread blocks on B200
+    const long long target = 148 * 8;     // resident 256-thread blocks on B200
+    const int cmin = 4;
     int gz = (int)((target + cols - 1) / cols);
     gz = std::max(1, std::min(gz, L.nx));
-    chunk = std::max((L.nx + gz - 1) / gz, L.nx >= 96 ? 4 : 2);   // short marches on coarse levels
+    chunk = std::max((L.nx + gz - 1) / gz, L.nx >= 96 ? cmin : 2);   // short marches on coarse levels
     chunk = std::min(chunk, L.nx);
     gz = (L.nx + chunk - 1) / chunk;
     return dim3(gx, gy, gz);

@@ -142,7 +142,7 @@ static int make_level(Allocs &A, Level &lv, int n1, int n2, int n3, int lo1, int
     }
     {
         // a_p and D^-1 by physical-face count for a constant medium (operators.py:163-178)
-        cd tab[8];
+        cd tab[12];
         const double kk = kc, k2h2 = kk * kk * L.h2;
         for (int nb = 0; nb < 4; nb++) {
             double re = (6.0 - sre * k2h2) * L.ih2, im = (-sim * k2h2) * L.ih2;
@@ -153,7 +153,14 @@ static int make_level(Allocs &A, Level &lv, int n1, int n2, int n3, int lo1, int
             double inv = 1.0 / (dre * dre + dim * dim);
             tab[4 + nb] = make_double2(dre * inv, -dim * inv);
         }
-        cd *dt = A.get<cd>(8, err);
+        // D^-1(nb) / D^-1(0): the boundary rescale of the zero-guess pre-smoothing
+        tab[8] = make_double2(1.0, 0.0);
+        for (int nb = 1; nb < 4; nb++) {
+            const cd a = tab[4 + nb], c = tab[4];
+            const double inv = 1.0 / (c.x * c.x + c.y * c.y);
+            tab[8 + nb] = make_double2((a.x * c.x + a.y * c.y) * inv, (a.y * c.x - a.x * c.y) * inv);
+        }
+        cd *dt = A.get<cd>(12, err);
         if (!dt) return fail(HF_ERR_CUDA, "cudaMalloc level table");
         CK(cudaMemcpy(dt, tab, sizeof(tab), cudaMemcpyHostToDevice));
         L.tab = dt;

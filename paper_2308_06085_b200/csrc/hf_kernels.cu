@@ -147,7 +147,20 @@ __device__ __forceinline__ ColCtx col_ctx(const Lvl &L, int chunk) {
 #define NT (TILE_X * TILE_Y)
 #define RING 5
 
-enum { MODE_LOAD = 0, MODE_PRE = 1 };
+enum { MODE_LOAD = 0, MODE_PRE = 1, MODE_UP = 2 };
+
+// MODE_UP: the staged operand is t = [w D^-1 b] + P e, produced in shared memory
+// from the staged b and a staged tile of the coarse correction e (the
+// prolongation + correction of multigrid.py:337-341 / 389-392 folded into the
+// post-smoothing sweep that consumes it)
+#define UP_MAX_CPLANES 10   // coarse planes staged per block (fine chunk <= 16)
+#define UP_EW 18            // coarse tile: <= 18 x 6 columns cover the 34 x 10 fine halo tile
+#define UP_EH 6
+struct UpArgs {
+    Lvl C;                  // coarse level of e
+    const cd *e;            // coarse correction (owned plane 0)
+    int pre;                // 1: t = w D^-1 b + P e (nu1 = 1), 0: t = P e (nu1 = 0)
+};
 
 template <int V>
 struct IC {
@@ -232,9 +245,10 @@ struct EpiJacobi {
 template <int MODE, bool KVAR, bool AUX>
 struct StencilSmem {
     static constexpr bool kWd = MODE == MODE_PRE && KVAR;     // staged D^-1 field
-    static constexpr bool kAuxArr = AUX && MODE == MODE_LOAD;
+    static constexpr bool kUp = MODE == MODE_UP;
     cd raw[RING][NFILL];
     cd wd[kWd ? RING : 1][kWd ? NFILL : 1];
+    cd ec[kUp ? UP_MAX_CPLANES : 1][kUp ? UP_EW * UP_EH : 1];   // coarse e tile
 };
 
 // Body of one (virtual) block: tile (bx, by) of (i3, i2) columns, planes
@@ -244,8 +258,8 @@ template <int MODE, class Epi, int ND, bool KVAR, bool SOMM>
 __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict__ src,
                                              const cd *__restrict__ aux, double omega,
                                              const Epi &epi, int chunk, const RedSlot &rs,
-                                             unsigned char *smem_raw, int tid, int bx, int by,
-                                             int bz) {
+                                             const UpArgs &up, unsigned char *smem_raw, int tid,
+                                             int bx, int by, int bz) {
     using SM = StencilSmem<MODE, KVAR, Epi::kAux>;
     SM &sm = *reinterpret_cast<SM *>(smem_raw);
     const int tx = tid & (TILE_X - 1), ty = tid / TILE_X;
@@ -262,6 +276,7 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
     // identities, never read outside the grid).
     const bool has1 = tid + NT < NFILL;
     int go0, go1, nbe0, nbe1;
+    int mj0 = 0, mm0 = 0, mj1 = 0, mm1 = 0;   // mirrored fine (i2, i3) of the fill entries
     bool ok0, ok1;
     {
         auto mirror = [](int x, int n) { return x < 0 ? -x : (x >= n ? 2 * (n - 1) - x : x); };
@@ -271,6 +286,7 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
         bool corner = (jj < 0 || jj >= L.n2) && (mm < 0 || mm >= L.n3);
         ok0 = oj && om && !corner;
         go0 = ok0 ? mirror(jj, L.n2) * L.n3 + mirror(mm, L.n3) : 0;
+        if (ok0) { mj0 = mirror(jj, L.n2); mm0 = mirror(mm, L.n3); }
         nbe0 = ok0 ? (mirror(jj, L.n2) == 0) + (mirror(jj, L.n2) == L.n2 - 1) +
                          (mirror(mm, L.n3) == 0) + (mirror(mm, L.n3) == L.n3 - 1) : 0;
         int e = tid + NT;
@@ -280,6 +296,7 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
         corner = (jj < 0 || jj >= L.n2) && (mm < 0 || mm >= L.n3);
         ok1 = has1 && oj && om && !corner;
         go1 = ok1 ? mirror(jj, L.n2) * L.n3 + mirror(mm, L.n3) : 0;
+        if (ok1) { mj1 = mirror(jj, L.n2); mm1 = mirror(mm, L.n3); }
         nbe1 = ok1 ? (mirror(jj, L.n2) == 0) + (mirror(jj, L.n2) == L.n2 - 1) +
                          (mirror(mm, L.n3) == 0) + (mirror(mm, L.n3) == L.n3 - 1) : 0;
     }
@@ -287,7 +304,7 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
     const int cf = (ty + 1) * HALO_X + (tx + 1);
     const int nbjm = (j == 0) + (j == L.n2 - 1) + (m == 0) + (m == L.n3 - 1);
     // constant medium: a_p and w D^-1 by physical-face count (0..3) in shared memory
-    __shared__ cd tab[12];
+    __shared__ cd tab[16];
     cd ap0 = mk(0, 0), wd0 = mk(0, 0);
     if (!KVAR) {
         ap0 = __ldg(L.tab);
@@ -296,6 +313,7 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
             tab[tid] = __ldg(L.tab + tid);
             tab[4 + tid] = cscal(__ldg(L.tab + 4 + tid), omega);
             tab[8 + tid] = cdiv(__ldg(L.tab + 4 + tid), __ldg(L.tab + 4));   // D^-1(nb) / D^-1(0)
+            tab[12 + tid] = __ldg(L.tab + 4 + tid);                         // D^-1(nb)
         }
     }
     // MODE_PRE, constant medium: stage b^ = b * D^-1(nb)/D^-1(0) so f = w D^-1 b = wd0 b^
@@ -319,6 +337,71 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
         }
         if (ok0) sm.raw[slot][tid] = cmul(sm.raw[slot][tid], tab[8 + nbx + nbe0]);
         if (ok1) sm.raw[slot][tid + NT] = cmul(sm.raw[slot][tid + NT], tab[8 + nbx + nbe1]);
+    };
+    // MODE_UP: coarse tile of e staged once per block (all coarse planes the
+    // chunk's fine planes i0-1 .. i1 interpolate from, mirrored ones included)
+    const Lvl &C = up.C;
+    int c_lo = 0, cj_lo = 0, cm_lo = 0, ew = 0;
+    int eo0 = 0, eo1 = 0;
+    if (MODE == MODE_UP) {
+        auto cmirror = [&](int p) {         // local fine plane -> mirrored global plane
+            int g = L.lo1 + p;
+            return g < 0 ? -g : (g >= L.n1 ? 2 * (L.n1 - 1) - g : g);
+        };
+        // fine g interpolates from coarse g >> 1 and, when odd, (g >> 1) + 1;
+        // the march is monotone between its (possibly mirrored) end planes
+        const int gmin = min(cmirror(i0 - 1), cmirror(i0));
+        const int gmax = max(cmirror(i1), cmirror(i1 - 1));
+        c_lo = gmin >> 1;
+        const int c_hi = min(C.n1 - 1, (gmax + 1) >> 1);
+        cj_lo = max(0, j0 - 1) >> 1;
+        const int cj_hi = min(C.n2 - 1, (min(j0 + TILE_Y, L.n2 - 1) + 1) >> 1);
+        cm_lo = max(0, m0 - 1) >> 1;
+        const int cm_hi = min(C.n3 - 1, (min(m0 + TILE_X, L.n3 - 1) + 1) >> 1);
+        ew = cm_hi - cm_lo + 1;
+        const int eh = cj_hi - cj_lo + 1, np = c_hi - c_lo + 1, per = ew * eh;
+        for (int t = tid; t < np * per; t += NT) {
+            const int pl = t / per, r = t - pl * per, ry = r / ew, rx = r - ry * ew;
+            const cd *g = up.e + (long long)(c_lo + pl - C.lo1) * C.plane +
+                          (long long)(cj_lo + ry) * C.n3 + cm_lo + rx;
+            cp_async16(&sm.ec[pl][ry * UP_EW + rx], g, true);
+        }
+        eo0 = ((mj0 >> 1) - cj_lo) * UP_EW + ((mm0 >> 1) - cm_lo);
+        eo1 = ((mj1 >> 1) - cj_lo) * UP_EW + ((mm1 >> 1) - cm_lo);
+    }
+    // t = [w D^-1 b] + P e on this thread's own staged entries of plane p, in
+    // place (k_corr arithmetic, at the mirrored coordinates of halo entries)
+    auto produce = [&](int slot, int p) {
+        int gi = L.lo1 + p;
+        gi = gi < 0 ? -gi : (gi >= L.n1 ? 2 * (L.n1 - 1) - gi : gi);
+        const int nbx = (gi == 0) + (gi == L.n1 - 1);
+        const int cl = (gi >> 1) - c_lo;
+        auto one = [&](int e, int gj, int gm, int nbe, int eo, int go) {
+            const bool o2 = gj & 1, o3 = gm & 1;
+            auto cplane = [&](int c) -> cd {
+                const cd *q = &sm.ec[c][eo];
+                cd a = q[0];
+                if (o3) a = cadd(a, q[1]);
+                if (o2) {
+                    a = cadd(a, q[UP_EW]);
+                    if (o3) a = cadd(a, q[UP_EW + 1]);
+                }
+                return a;
+            };
+            const double s2 = (o2 && o3) ? 0.25 : ((o2 || o3) ? 0.5 : 1.0);
+            const cd v0 = cplane(cl);
+            cd pe;
+            if (gi & 1) pe = cscal(cadd(v0, cplane(cl + 1)), 0.5 * s2);
+            else pe = s2 == 1.0 ? v0 : cscal(v0, s2);
+            if (up.pre) {
+                const cd D = KVAR ? __ldg(L.dinv + (long long)(gi - L.lo1) * L.plane + go)
+                                  : tab[12 + nbx + nbe];
+                pe = cadd(cscal(cmul(sm.raw[slot][e], D), omega), pe);
+            }
+            sm.raw[slot][e] = pe;
+        };
+        if (ok0) one(tid, mj0, mm0, nbe0, eo0, go0);
+        if (ok1) one(tid + NT, mj1, mm1, nbe1, eo1, go1);
     };
     auto wd_nb = [&](int nb) -> cd { return tab[4 + nb]; };   // read after the first barrier
     cd acc[2] = {mk(0, 0), mk(0, 0)};
@@ -376,11 +459,16 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
 
     // planes i0-1 .. i0+RING-3 into slots 0 .. RING-2
     static_for<0, RING - 1>([&](auto Sc) { stage(Sc, i0 - 1 + decltype(Sc)::value); });
-    if (kScale) {
-        cp_wait<RING - 3>();               // planes i0-1, i0 of this thread's copies
-        __syncthreads();                   // tab[] visible
-        fixup(0, i0 - 1);
-        fixup(1, i0);
+    if (kScale || MODE == MODE_UP) {
+        cp_wait<RING - 3>();               // planes i0-1, i0 (and the e tile) landed
+        __syncthreads();                   // tab[] and the e tile visible
+        if (kScale) {
+            fixup(0, i0 - 1);
+            fixup(1, i0);
+        } else {
+            produce(0, i0 - 1);
+            produce(1, i0);
+        }
     }
     long long q = (long long)i0 * L.plane + own;
     // centre-only epilogue operands (b or w, and k) are prefetched one plane ahead
@@ -404,6 +492,7 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
         }
         cp_wait<RING - 4>();               // plane i+1 landed (later ones may be in flight)
         if (kScale) fixup(sn, i + 1);      // own entries only: no barrier needed before
+        if (MODE == MODE_UP) produce(sn, i + 1);
         __syncthreads();
         stage_in(IC<ss>{}, i + RING - 2);  // into the slot read last at step i-1
         if (act) {
@@ -463,10 +552,10 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
 template <int MODE, class Epi, int ND, bool KVAR, bool SOMM>
 __global__ void __launch_bounds__(NT) k_stencil(Lvl L, const cd *__restrict__ src,
                                                 const cd *__restrict__ aux, double omega, Epi epi,
-                                                int chunk, RedSlot rs, const int *done) {
+                                                int chunk, RedSlot rs, UpArgs up, const int *done) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     if (is_done(done)) return;
-    stencil_body<MODE, Epi, ND, KVAR, SOMM>(L, src, aux, omega, epi, chunk, rs, smem_raw,
+    stencil_body<MODE, Epi, ND, KVAR, SOMM>(L, src, aux, omega, epi, chunk, rs, up, smem_raw,
                                             threadIdx.y * TILE_X + threadIdx.x, blockIdx.x,
                                             blockIdx.y, blockIdx.z);
 }
@@ -1167,23 +1256,29 @@ static const dim3 kTileBlock(TILE_X, TILE_Y, 1);
 
 template <int MODE, class Epi, int ND, bool KVAR, bool SOMM>
 static void stencil_launch(const Lvl &L, const cd *src, const cd *aux, double omega, const Epi &e,
-                           const RedSlot &rs, cudaStream_t s, const int *done) {
+                           const RedSlot &rs, cudaStream_t s, const int *done,
+                           const UpArgs &up = UpArgs{}) {
     int chunk;
     dim3 g = tile_grid(L, chunk);
+    if (MODE == MODE_UP && chunk > 16) {   // the staged coarse tile covers <= 16 fine planes
+        chunk = 16;
+        g.z = (L.nx + chunk - 1) / chunk;
+    }
     size_t smem = sizeof(StencilSmem<MODE, KVAR, Epi::kAux>);
-    launch(k_stencil<MODE, Epi, ND, KVAR, SOMM>, dim3(g), dim3(kTileBlock), smem, s, L, src, aux ? aux : src, omega, e,
-                                                                     chunk, rs, done);
+    launch(k_stencil<MODE, Epi, ND, KVAR, SOMM>, dim3(g), dim3(kTileBlock), smem, s, L, src,
+           aux ? aux : src, omega, e, chunk, rs, up, done);
 }
 template <int MODE, class Epi, int ND>
 static void stencil(const Lvl &L, const cd *src, const cd *aux, double omega, const Epi &e,
-                    const RedSlot &rs, cudaStream_t s, const int *done) {
+                    const RedSlot &rs, cudaStream_t s, const int *done,
+                    const UpArgs &up = UpArgs{}) {
     const bool somm = L.bc == HF_BC_SOMMERFELD;
     if (L.k) {
-        if (somm) stencil_launch<MODE, Epi, ND, true, true>(L, src, aux, omega, e, rs, s, done);
-        else stencil_launch<MODE, Epi, ND, true, false>(L, src, aux, omega, e, rs, s, done);
+        if (somm) stencil_launch<MODE, Epi, ND, true, true>(L, src, aux, omega, e, rs, s, done, up);
+        else stencil_launch<MODE, Epi, ND, true, false>(L, src, aux, omega, e, rs, s, done, up);
     } else {
-        if (somm) stencil_launch<MODE, Epi, ND, false, true>(L, src, aux, omega, e, rs, s, done);
-        else stencil_launch<MODE, Epi, ND, false, false>(L, src, aux, omega, e, rs, s, done);
+        if (somm) stencil_launch<MODE, Epi, ND, false, true>(L, src, aux, omega, e, rs, s, done, up);
+        else stencil_launch<MODE, Epi, ND, false, false>(L, src, aux, omega, e, rs, s, done, up);
     }
 }
 
@@ -1208,6 +1303,7 @@ void init_kernel_attributes() {
     set_attr<MODE_LOAD, EpiResid, 0>();
     set_attr<MODE_LOAD, EpiJacobi, 0>();
     set_attr<MODE_PRE, EpiResid, 0>();
+    set_attr<MODE_UP, EpiJacobi, 0>();
     cudaFuncSetAttribute(k_fdm_plane, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_fdm_fiber, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     done = true;
@@ -1281,10 +1377,18 @@ void launch_correct(const Lvl &L, const Lvl &C, const cd *b, const cd *e, cd *t,
                     bool pre, cudaStream_t s, const int *done) {
     corr(pre ? 1 : 0, L, C, b, e, t, omega, s, done);
 }
-void launch_up1(const Lvl &L, const Lvl &C, const cd *b, const cd *e, cd *u, cd *t, double omega,
-                bool pre, cudaStream_t s, const int *done) {
+int launch_up1(const Lvl &L, const Lvl &C, const cd *b, const cd *e, cd *u, cd *t, double omega,
+               bool pre, cudaStream_t s, const int *done) {
+    // whole-grid levels: correction produced inside the post-smoothing sweep
+    const bool split = std::getenv("HF_NO_FUSE") != nullptr;   // A/B switch (tests)
+    if (!split && L.lo1 == 0 && L.nx == L.n1 && C.lo1 == 0 && C.nx == C.n1) {
+        stencil<MODE_UP, EpiJacobi, 0>(L, b, b, omega, EpiJacobi{u}, RedSlot{}, s, done,
+                                        UpArgs{C, e, pre ? 1 : 0});
+        return 1;
+    }
     corr(pre ? 1 : 0, L, C, b, e, t, omega, s, done);
     stencil<MODE_LOAD, EpiJacobi, 0>(L, t, b, omega, EpiJacobi{u}, RedSlot{}, s, done);
+    return 2;
 }
 void launch_gemv(int N, const cd *Minv, const cd *b, cd *x, cudaStream_t s, const int *done) {
     int blocks = (N + 1) / 2;

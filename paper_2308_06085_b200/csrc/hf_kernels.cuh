@@ -24,8 +24,9 @@ void launch_restrict(const Lvl &F, const Lvl &C, const cd *r, cd *out, cudaStrea
                      const int *done);
 void launch_prolong(const Lvl &F, const Lvl &C, const cd *e, cd *out, bool add, cudaStream_t s,
                     const int *done);
-void launch_up1(const Lvl &L, const Lvl &C, const cd *b, const cd *e, cd *u, cd *t, double omega,
-                bool pre, cudaStream_t s, const int *done);
+// returns the number of kernels launched (1 fused, 2 split)
+int launch_up1(const Lvl &L, const Lvl &C, const cd *b, const cd *e, cd *u, cd *t, double omega,
+               bool pre, cudaStream_t s, const int *done);
 void launch_dinv(const Lvl &L, cd *out_owned, cudaStream_t s);
 void launch_correct(const Lvl &L, const Lvl &C, const cd *b, const cd *e, cd *t, double omega,
                     bool pre, cudaStream_t s, const int *done);

@@ -570,8 +570,7 @@ static void v_cycle(hf_hierarchy *H, int li, const cd *b, cd *u, cudaStream_t s,
     L1(launch_restrict(lv.L, nx.L, lv.r, nx.b, s, done));
     v_cycle(H, li + 1, nx.b, nx.u, s, done);
     if (fused) {
-        L1(launch_up1(lv.L, nx.L, b, nx.u, u, lv.t, c.omega, c.nu1 == 1, s, done));
-        g_launches++;   // correction + Jacobi stencil
+        g_launches += launch_up1(lv.L, nx.L, b, nx.u, u, lv.t, c.omega, c.nu1 == 1, s, done);
     } else {
         L1(launch_prolong(lv.L, nx.L, nx.u, u, true, s, done));
         smooth_sweeps(lv, u, b, c.omega, c.nu2, s, done);

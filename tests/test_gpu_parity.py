@@ -97,6 +97,30 @@ def test_coarsest_fast_diagonalisation(hf, oracle, dims, h, kc, monkeypatch):
     assert _rel(x, xd) < 1e-12
 
 
+@pytest.mark.parametrize("dims,bc,kind,mg", [
+    ((65, 65, 65), "sommerfeld", "const", {}),
+    ((129, 65, 97), "sommerfeld", "const", {}),
+    ((65, 33, 49), "dirichlet", "const", {}),
+    ((65, 65, 65), "sommerfeld", "field", {}),
+    ((65, 49, 33), "dirichlet", "field", {}),
+    ((65, 65, 65), "sommerfeld", "const", {"nu1": 0}),
+])
+def test_fused_up_matches_split(hf, dims, bc, kind, mg, monkeypatch):
+    """Prolongation + correction produced inside the post-smoothing sweep
+    (MODE_UP) is bit-identical to the split correction + Jacobi kernels."""
+    from paper_2308_06085_b200.multigrid import MGConfig, build_hierarchy, mg_precondition
+    from paper_2308_06085_b200.operators import Dirichlet, OperatorSpec, Sommerfeld
+    grid = hf.make_grid(*dims, 1.0 / (dims[0] - 1))
+    k = np.full(dims, 30.0) if kind == "const" else _kfield(dims, 11, 20, 35)
+    spec = OperatorSpec("cslp", 1.0, -0.5, Dirichlet(0.0) if bc == "dirichlet" else Sommerfeld(), k)
+    r = torch.as_tensor(_rand(dims, 41)).cuda()
+    hier = build_hierarchy(grid, None, spec, MGConfig(**mg))
+    fused = mg_precondition(hier, r).cpu().numpy()
+    monkeypatch.setenv("HF_NO_FUSE", "1")
+    split = mg_precondition(hier, r).cpu().numpy()
+    assert np.array_equal(fused, split), np.abs(fused - split).max()
+
+
 @pytest.mark.parametrize("bc", ["dirichlet", "sommerfeld"])
 def test_transfers_and_smoother(hf, oracle, bc):
     from paper_2308_06085_b200.multigrid import jacobi_smooth, prolong_tl, restrict_fw

@@ -110,9 +110,12 @@ struct RedSlot {
 struct BcgState {
     cd rho, rho_new, alpha, omega, beta;
     double bnorm, tol, btol, relres;
-    int iter, maxit, done, converged, breakdown, s_conv, matvecs, pad;
+    int iter, maxit, done, converged, breakdown, s_conv, matvecs, cond;
     double *hist;
     int hist_cap, pad2;
+    // conditional-graph handles (cond = 1): while(iterate) { first half;
+    // if(h1) { s update; if(h2) { second half; if(h3) { x, r update } } } }
+    unsigned long long hw, h1, h2, h3;
 };
 
 __device__ __forceinline__ cd warp_sum(cd v) {

@@ -27,7 +27,26 @@ __device__ static void bcg_record(BcgState *st, double relres) {
     st->relres = relres;
 }
 
+__device__ static void bcg_cond(unsigned long long h, bool v) {
+    if (h) cudaGraphSetConditional((cudaGraphConditionalHandle)h, v ? 1u : 0u);
+}
+
+// advances the scalars, then (conditional graph) steers the rest of the iteration
+__device__ static void bcg_step(BcgState *st, int op, const cd *sums);
 __device__ void bcg_finalize(BcgState *st, int op, const cd *sums) {
+    bcg_step(st, op, sums);
+    if (!st->cond) return;
+    const bool go = !st->done;
+    switch (op) {
+    case FIN_BCG_ALPHA: bcg_cond(st->h1, go); break;
+    case FIN_BCG_S: bcg_cond(st->h2, go); break;
+    case FIN_BCG_OMEGA: bcg_cond(st->h3, go); break;
+    default: break;
+    }
+    if (!go || op == FIN_BCG_RHO) bcg_cond(st->hw, go);
+}
+
+__device__ static void bcg_step(BcgState *st, int op, const cd *sums) {
     switch (op) {
     case FIN_BCG_INIT: {            // krylov.py:217-232
         double bb = sums[0].x;

@@ -786,6 +786,12 @@ struct hf_solver {
     cudaStream_t stream = nullptr;
     cudaGraphExec_t graph = nullptr;
     int graph_kernels = 0;
+    // whole solve as one conditional graph (while / nested if nodes)
+    cudaGraphExec_t cgraph = nullptr;
+    bool cgraph_tried = false;
+    unsigned long long hw = 0, h1 = 0, h2 = 0, h3 = 0;
+    int kern_first = 0, kern_s = 0, kern_second = 0, kern_xr = 0;   // kernels per section
+    cudaStream_t cs[3] = {nullptr, nullptr, nullptr};                // capture streams of the if bodies
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, evs = nullptr;
     // GMRES / IDR(s) workspace (allocated on first use)
     std::vector<cd *> basis;            // Krylov basis V (GMRES) / G, U, P (IDR)
@@ -797,6 +803,9 @@ struct hf_solver {
     int vcap = 0;
     ~hf_solver() {
         if (graph) cudaGraphExecDestroy(graph);
+        if (cgraph) cudaGraphExecDestroy(cgraph);
+        for (cudaStream_t c : cs)
+            if (c) cudaStreamDestroy(c);
         if (st_host) cudaFreeHost(st_host);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
@@ -842,6 +851,9 @@ extern "C" hf_solver *hf_solver_create(hf_operator *Aop, hf_hierarchy *M) {
 extern "C" void hf_solver_destroy(hf_solver *S) { delete S; }
 
 // one Bi-CGSTAB iteration (krylov.py:234-273), every kernel predicated on st->done
+static thread_local cudaError_t g_cond_fail = cudaSuccess;
+static void ei_fail(cudaError_t e) { g_cond_fail = e; }
+
 static void bcg_iteration(hf_solver *S, cudaStream_t s) {
     const Lvl &A = S->Aop->lv.L;
     const int *done = &S->st->done;
@@ -855,6 +867,113 @@ static void bcg_iteration(hf_solver *S, cudaStream_t s) {
     L1(launch_bcg_xr(n, S->st, S->x, S->ph, S->sh, S->s, S->t, S->r, S->rs,
                      S->red.slot(FIN_BCG_RHO, S->st), s, done));
     cudaMemcpyAsync(S->st_host, S->st, sizeof(BcgState), cudaMemcpyDeviceToHost, s);
+}
+
+// One Bi-CGSTAB solve as a single CUDA graph: a while node iterates the
+// body, and nested if nodes stop mid-iteration (alpha breakdown, |s| converged,
+// omega breakdown) -- the finalize step of each device reduction sets the
+// conditions (bcg_finalize), so no kernel reads a "done" flag and the host
+// does not poll.
+template <class F>
+static cudaError_t capture_if(cudaStream_t s, cudaStream_t s2, unsigned long long &handle, F &&body) {
+    cudaStreamCaptureStatus st;
+    cudaGraph_t cg = nullptr;
+    const cudaGraphNode_t *deps = nullptr;
+    size_t nd = 0;
+    cudaError_t e = cudaStreamGetCaptureInfo(s, &st, nullptr, &cg, &deps, &nd);
+    if (e != cudaSuccess) return e;
+    cudaGraphConditionalHandle h;
+    if ((e = cudaGraphConditionalHandleCreate(&h, cg, 0, 0)) != cudaSuccess) return e;
+    handle = (unsigned long long)h;
+    cudaGraphNodeParams ip = {};
+    ip.type = cudaGraphNodeTypeConditional;
+    ip.conditional.handle = h;
+    ip.conditional.type = cudaGraphCondTypeIf;
+    ip.conditional.size = 1;
+    cudaGraphNode_t in;
+    if ((e = cudaGraphAddNode(&in, cg, deps, nd, &ip)) != cudaSuccess) return e;
+    if ((e = cudaStreamUpdateCaptureDependencies(s, &in, 1, cudaStreamSetCaptureDependencies)) != cudaSuccess)
+        return e;
+    if ((e = cudaStreamBeginCaptureToGraph(s2, ip.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
+        return e;
+    body(s2);
+    cudaGraph_t out;
+    return cudaStreamEndCapture(s2, &out);
+}
+
+static int build_cond_graph(hf_solver *S) {
+    if (S->cgraph || S->cgraph_tried) return 0;
+    S->cgraph_tried = true;
+    // opt-in: measured ~1% slower than replaying the per-iteration graph with
+    // a host poll every check_every iterations (three if-node evaluations per
+    // iteration cost more than the skipped done-flag reads and polls)
+    if (!std::getenv("HF_COND_GRAPH")) return 0;
+    for (cudaStream_t &c : S->cs)
+        if (!c && cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking) != cudaSuccess) return 0;
+    const Lvl &A = S->Aop->lv.L;
+    const long long n = S->n;
+    cudaGraph_t G = nullptr;
+    if (cudaGraphCreate(&G, 0) != cudaSuccess) return 0;
+    cudaGraphConditionalHandle hw;
+    cudaGraphNodeParams wp = {};
+    cudaGraphNode_t wn;
+    cudaError_t e = cudaGraphConditionalHandleCreate(&hw, G, 1, cudaGraphCondAssignDefault);
+    if (e == cudaSuccess) {
+        wp.type = cudaGraphNodeTypeConditional;
+        wp.conditional.handle = hw;
+        wp.conditional.type = cudaGraphCondTypeWhile;
+        wp.conditional.size = 1;
+        e = cudaGraphAddNode(&wn, G, nullptr, 0, &wp);
+    }
+    long long before = g_launches, mark;
+    cudaStream_t s = S->stream;
+    if (e == cudaSuccess)
+        e = cudaStreamBeginCaptureToGraph(s, wp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                          cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+        mark = g_launches;
+        L1(launch_bcg_p(n, S->st, S->r, S->p, S->v, s, nullptr));
+        precondition(S->M, S->p, S->ph, s, nullptr);
+        L1(launch_apply_dot1(A, S->ph, S->v, S->rs, S->red.slot(FIN_BCG_ALPHA, S->st), s, nullptr));
+        S->kern_first = (int)(g_launches - mark);
+        cudaError_t ei = capture_if(s, S->cs[0], S->h1, [&](cudaStream_t s1) {
+            mark = g_launches;
+            L1(launch_bcg_s(n, S->st, S->r, S->v, S->s, S->red.slot(FIN_BCG_S, S->st), s1, nullptr));
+            S->kern_s = (int)(g_launches - mark);
+            cudaError_t e2 = capture_if(s1, S->cs[1], S->h2, [&](cudaStream_t s2) {
+                mark = g_launches;
+                precondition(S->M, S->s, S->sh, s2, nullptr);
+                L1(launch_apply_dot2(A, S->sh, S->t, S->s, S->red.slot(FIN_BCG_OMEGA, S->st), s2,
+                                     nullptr));
+                S->kern_second = (int)(g_launches - mark);
+                cudaError_t e3 = capture_if(s2, S->cs[2], S->h3, [&](cudaStream_t s3) {
+                    L1(launch_bcg_xr(n, S->st, S->x, S->ph, S->sh, S->s, S->t, S->r, S->rs,
+                                     S->red.slot(FIN_BCG_RHO, S->st), s3, nullptr));
+                    S->kern_xr = 1;
+                });
+                if (e3 != cudaSuccess) ei_fail(e3);
+            });
+            if (e2 != cudaSuccess) ei_fail(e2);
+        });
+        cudaGraph_t out;
+        cudaError_t ec = cudaStreamEndCapture(s, &out);
+        if (e == cudaSuccess) e = ei != cudaSuccess ? ei : ec;
+        if (e == cudaSuccess && g_cond_fail != cudaSuccess) e = g_cond_fail;
+    }
+    g_cond_fail = cudaSuccess;
+    g_launches = before;
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&S->cgraph, G, 0);
+    cudaGraphDestroy(G);
+    if (std::getenv("HF_DEBUG"))
+        std::fprintf(stderr, "[hf] conditional graph: %s\n", e == cudaSuccess ? "ok" : cudaGetErrorString(e));
+    if (e != cudaSuccess) {           // older driver or capture problem: per-iteration graph
+        S->cgraph = nullptr;
+        cudaGetLastError();
+        return 0;
+    }
+    S->hw = (unsigned long long)hw;
+    return 0;
 }
 
 static int build_graph(hf_solver *S) {
@@ -882,31 +1001,52 @@ static int solve_bicgstab(hf_solver *S, const hf_solver_config *cfg, const cd *b
         if (!S->hist) return fail(HF_ERR_CUDA, "cudaMalloc history");
         S->hist_cap = cfg->maxit + 2;
     }
+    if (build_cond_graph(S)) return HF_ERR_CUDA;
+    if (!S->cgraph && build_graph(S)) return HF_ERR_CUDA;
     BcgState init{};
     init.tol = cfg->tol;
     init.btol = cfg->breakdown_tol > 0 ? cfg->breakdown_tol : 1e-30;
     init.maxit = cfg->maxit;
     init.hist = S->hist;
     init.hist_cap = S->hist_cap;
+    if (S->cgraph) {
+        init.cond = 1;
+        init.hw = S->hw; init.h1 = S->h1; init.h2 = S->h2; init.h3 = S->h3;
+    }
     *S->st_host = init;
     CK(cudaMemcpyAsync(S->st, S->st_host, sizeof(BcgState), cudaMemcpyHostToDevice, s));
-    if (build_graph(S)) return HF_ERR_CUDA;
     long long launches = 0;
     CK(cudaEventRecord(S->ev0, s));
     L1(launch_bcg_init(S->n, b, S->r, S->rs, S->x, S->p, S->v, S->red.slot(FIN_BCG_INIT, S->st), s));
     launches++;
     CK(cudaMemcpyAsync(S->st_host, S->st, sizeof(BcgState), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    int every = cfg->check_every > 0 ? cfg->check_every : 4;
-    int graphs = 0;
-    while (!S->st_host->done && graphs < cfg->maxit + every) {
-        for (int k = 0; k < every; k++) {
-            CK(cudaGraphLaunch(S->graph, s));
-            graphs++;
+    if (S->cgraph) {
+        if (!S->st_host->done) {
+            CK(cudaGraphLaunch(S->cgraph, s));
+            CK(cudaMemcpyAsync(S->st_host, S->st, sizeof(BcgState), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            // kernels that ran: full iterations, plus the part of the last one
+            const BcgState &q = *S->st_host;
+            const int per = S->kern_first + S->kern_s + S->kern_second + S->kern_xr;
+            long long it = q.iter;
+            if (q.s_conv) launches += (it - 1) * per + S->kern_first + S->kern_s;
+            else if (q.breakdown == HF_BREAKDOWN_OMEGA) launches += it * per + S->kern_first + S->kern_s + S->kern_second;
+            else if (q.breakdown) launches += it * per + S->kern_first;
+            else launches += it * per;
         }
-        CK(cudaStreamSynchronize(s));
+    } else {
+        int every = cfg->check_every > 0 ? cfg->check_every : 4;
+        int graphs = 0;
+        while (!S->st_host->done && graphs < cfg->maxit + every) {
+            for (int k = 0; k < every; k++) {
+                CK(cudaGraphLaunch(S->graph, s));
+                graphs++;
+            }
+            CK(cudaStreamSynchronize(s));
+        }
+        launches += (long long)graphs * S->graph_kernels;
     }
-    launches += (long long)graphs * S->graph_kernels;
     if (S->st_host->s_conv) {
         L1(launch_bcg_xhalf(S->n, S->st, S->x, S->ph, s));
         launches++;

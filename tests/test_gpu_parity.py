@@ -251,6 +251,33 @@ def test_gmres_restart(hf, oracle):
     assert np.linalg.norm(xr.cpu().numpy() - xo) / np.linalg.norm(xo) < 1e-5
 
 
+def test_conditional_graph_solve_matches(hf, monkeypatch):
+    """The opt-in single-graph solve (while / nested if nodes, HF_COND_GRAPH)
+    runs the same kernels: same iterations, bit-identical solution, also when
+    it stops on the half step."""
+    from paper_2308_06085_b200 import problems
+    from paper_2308_06085_b200.krylov import Solver, SolverConfig
+    from paper_2308_06085_b200.multigrid import MGConfig, build_hierarchy
+    from paper_2308_06085_b200.operators import OperatorSpec, StencilOperator
+    p = problems.point_source_cube(33, 20.0, "sommerfeld")
+    spec, b = problems.build_problem(p)
+    k = np.full(p.grid.shape, 20.0)
+
+    def run(tol):
+        A = StencilOperator(spec, p.grid)
+        hier = build_hierarchy(p.grid, None, OperatorSpec("cslp", 1.0, -0.5, spec.bc, k), MGConfig())
+        x, rep = Solver(A, hier).solve(b, SolverConfig(method="bicgstab", tol=tol, maxit=400))
+        return x.cpu().numpy(), rep
+
+    ref = [run(t) for t in (1e-6, 1e-3)]
+    monkeypatch.setenv("HF_COND_GRAPH", "1")
+    got = [run(t) for t in (1e-6, 1e-3)]
+    for (x0, r0), (x1, r1) in zip(ref, got):
+        assert r0.iterations == r1.iterations and r0.matvec_count == r1.matvec_count
+        assert np.array_equal(x0, x1)
+        assert r0.residual_history == r1.residual_history
+
+
 def test_repeat_solves_bit_identical(hf):
     """Deterministic reductions and race-free kernels: repeated solves (with
     different host polling intervals) give bit-identical solutions."""

@@ -1175,6 +1175,282 @@ __global__ void __launch_bounds__(FDM_THREADS) k_fdm_fiber(int n1, int n2, int n
                                 blockIdx.x, blockIdx.y);
 }
 
+// ---------------------------------------------------------------------------
+// Coarse sub-cycle in ONE cooperative launch.  Below ~65^3 a level is L2
+// resident and a marching kernel is launch- and pipeline-latency bound (5-10 us
+// for microseconds of data).  k_coarse runs the whole V-cycle below the first
+// coarse level -- pre-smooth + residual, restriction, fast-diagonalisation
+// coarsest solve, prolongation + correction, post-smoothing -- as a list of
+// phases separated by grid-wide barriers.  Every block is resident
+// (cooperative launch), each phase is a grid-stride loop of plain L2 loads
+// (no staging), and the arithmetic of each phase is the reference's:
+//   down     r = b - M (w D^-1 b)              multigrid.py:148-151, 383-386
+//   restrict full weighting + boundary fix     multigrid.py:171-221
+//   corr     t = [w D^-1 b] + P e               multigrid.py:238-297, 389-392
+//   jacobi   u = t + w D^-1 (b - M t)           multigrid.py:153-156
+//   fdm_*    exact separable coarsest solve    (replaces multigrid.py:300-323)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+// Grid barrier over all (co-resident) blocks on a monotonic 64-bit arrival
+// counter: every launch adds exactly nblk * nbar arrivals, so a block derives
+// the launch's base from any value it reads before its own first arrival.
+// One release-add per block, relaxed polling, one acquire fence.
+__device__ __forceinline__ void grid_barrier(unsigned long long *cnt, unsigned long long target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        asm volatile("red.release.gpu.global.add.u64 [%0], 1;\n" ::"l"(cnt) : "memory");
+        // relaxed polling (an acquire load invalidates L1 on every poll), one
+        // acquire fence once the count is reached
+        unsigned long long v;
+        do {
+            asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(cnt) : "memory");
+        } while (v < target);
+        asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+    }
+    __syncthreads();
+}
+
+// nb of a vertex from per-axis face flags
+__device__ __forceinline__ int face(int x, int n) { return (x == 0) + (x == n - 1); }
+__device__ __forceinline__ int mirror_in(int x, int n) { return x < 0 ? -x : (x >= n ? 2 * (n - 1) - x : x); }
+
+// 7-point neighbourhood of vertex q of a whole-grid level: decode, mirrored
+// neighbour loads (plus D^-1 and k when the medium varies), issued together so
+// that several vertices per thread keep many L2 loads in flight
+struct G7 {
+    cd v[7];     // centre, i-1, i+1, j-1, j+1, m-1, m+1
+    cd d[7];     // D^-1 of the same vertices (varying medium only)
+    int nb[7];
+    double k;
+    bool ok;
+};
+__device__ __forceinline__ void gather7(const Lvl &L, const cd *f, long long q, long long N, bool wd,
+                                        G7 &g) {
+    g.ok = q < N;
+    if (!g.ok) q = 0;
+    const int pl = (int)L.plane;
+    const int i = (int)q / pl, rem = (int)q - i * pl;
+    const int j = rem / L.n3, m = rem - j * L.n3;
+    const int fi = face(i, L.n1), fj = face(j, L.n2), fm = face(m, L.n3);
+    const int im = mirror_in(i - 1, L.n1), ip = mirror_in(i + 1, L.n1);
+    const int jm = mirror_in(j - 1, L.n2), jp = mirror_in(j + 1, L.n2);
+    const int mm = mirror_in(m - 1, L.n3), mp = mirror_in(m + 1, L.n3);
+    const int qi = j * L.n3 + m, rowi = i * pl, rowj = j * L.n3;
+    const int qq[7] = {(int)q, im * pl + qi, ip * pl + qi, rowi + jm * L.n3 + m, rowi + jp * L.n3 + m,
+                       rowi + rowj + mm, rowi + rowj + mp};
+    g.nb[0] = fi + fj + fm;
+    g.nb[1] = face(im, L.n1) + fj + fm;
+    g.nb[2] = face(ip, L.n1) + fj + fm;
+    g.nb[3] = fi + face(jm, L.n2) + fm;
+    g.nb[4] = fi + face(jp, L.n2) + fm;
+    g.nb[5] = fi + fj + face(mm, L.n3);
+    g.nb[6] = fi + fj + face(mp, L.n3);
+#pragma unroll
+    for (int t = 0; t < 7; t++) g.v[t] = f[qq[t]];   // L1-cached: neighbours are shared
+    if (L.dinv && wd) {
+#pragma unroll
+        for (int t = 0; t < 7; t++) g.d[t] = L.dinv[qq[t]];
+    }
+    g.k = L.k ? __ldcg(L.k + q) : L.kc;
+}
+// M f at the gathered vertex; f_t = v_t * scale_t (scale = w D^-1 for the
+// zero-guess pre-smoothing, 1 otherwise)
+__device__ __forceinline__ cd g7_apply(const Lvl &L, const cd *tap, const G7 &g, const cd (&f)[7]) {
+    if (L.bc == HF_BC_DIRICHLET && g.nb[0]) return f[0];
+    cd s = cadd(cadd(cadd(f[1], f[2]), cadd(f[3], f[4])), cadd(f[5], f[6]));
+    const cd ap = L.k ? ap_of(L, g.k, g.nb[0]) : tap[g.nb[0]];
+    cd mf = cmul(ap, f[0]);
+    mf.x -= L.ih2 * s.x;
+    mf.y -= L.ih2 * s.y;
+    return mf;
+}
+#define CO_U 2   // vertices per thread per round
+
+__global__ void __launch_bounds__(256, 2) k_coarse(const __grid_constant__ CoArgs a, const int *done) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ cd tab[CO_MAX_LEVELS][8];   // per level: a_p[nb], w D^-1[nb]
+    if (done && *(volatile const int *)done) return;   // uniform over the grid
+    const int tid = threadIdx.x;
+    const double w = a.omega;
+    for (int l = 0; l < CO_MAX_LEVELS; l++) {
+        if (tid < 4 && a.lv[l].L.tab) {
+            tab[l][tid] = __ldg(a.lv[l].L.tab + tid);
+            tab[l][4 + tid] = cscal(__ldg(a.lv[l].L.tab + 4 + tid), w);
+        }
+    }
+    const unsigned nblk = gridDim.x;
+    // launch base of the arrival counter (see grid_barrier)
+    __shared__ unsigned long long base;
+    if (tid == 0 && a.nph > 1) {
+        const unsigned long long T = (unsigned long long)nblk * (a.nph - 1);
+        base = ld_acquire_u64(a.bar) / T * T;
+    }
+    __syncthreads();
+    const long long gstride = (long long)nblk * blockDim.x;
+    const long long gtid = (long long)blockIdx.x * blockDim.x + tid;
+    for (int p = 0; p < a.nph; p++) {
+        if (p) grid_barrier(a.bar, base + (unsigned long long)p * nblk);
+        const CoPhase ph = a.ph[p];
+        const CoLevel &F = a.lv[ph.l];
+        const Lvl &L = F.L;
+        const cd *tap = tab[ph.l], *tw = tab[ph.l] + 4;
+        switch (ph.type) {
+        case PH_DOWN: {        // r = b - M (w D^-1 b)
+            const long long N = (long long)L.n1 * L.plane;
+            for (long long q0 = gtid; q0 < N; q0 += CO_U * gstride) {
+                G7 g[CO_U];
+#pragma unroll
+                for (int u = 0; u < CO_U; u++) gather7(L, F.b, q0 + u * gstride, N, true, g[u]);
+#pragma unroll
+                for (int u = 0; u < CO_U; u++) {
+                    if (!g[u].ok) continue;
+                    cd f[7];
+#pragma unroll
+                    for (int t = 0; t < 7; t++)
+                        f[t] = cmul(g[u].v[t], L.dinv ? cscal(g[u].d[t], w) : tw[g[u].nb[t]]);
+                    F.r[q0 + u * gstride] = csub(g[u].v[0], g7_apply(L, tap, g[u], f));
+                }
+            }
+            break;
+        }
+        case PH_RESTRICT:      // b_{l+1} = R r_l
+        case PH_REST_B: {      // b_{l+1} = R b_l (nu1 = 0: the residual of u = 0 is b)
+            const CoLevel &C = a.lv[ph.l + 1];
+            const Lvl &K = C.L;
+            const cd *r = ph.type == PH_RESTRICT ? F.r : F.b;
+            const long long N = (long long)K.n1 * K.plane;
+            for (long long q = gtid; q < N; q += gstride) {
+                const int ci = (int)(q / K.plane);
+                const int rem = (int)(q - (long long)ci * K.plane);
+                const int cj = rem / K.n3, cm = rem - cj * K.n3;
+                cd acc = mk(0, 0);
+#pragma unroll
+                for (int o1 = -1; o1 <= 1; o1++) {
+                    const int fi = 2 * ci + o1;
+                    if (fi < 0 || fi >= L.n1) continue;
+                    cd a1 = mk(0, 0);
+#pragma unroll
+                    for (int o2 = -1; o2 <= 1; o2++) {
+                        const int fj = 2 * cj + o2;
+                        if (fj < 0 || fj >= L.n2) continue;
+                        const cd *row = r + (long long)fi * L.plane + (long long)fj * L.n3;
+                        const int fm = 2 * cm;
+                        cd rs = cscal(__ldcg(row + fm), 2.0);
+                        if (fm > 0) rs = cadd(__ldcg(row + fm - 1), rs);
+                        if (fm < L.n3 - 1) rs = cadd(rs, __ldcg(row + fm + 1));
+                        a1 = cadd(a1, o2 == 0 ? cscal(rs, 2.0) : rs);
+                    }
+                    acc = cadd(acc, o1 == 0 ? cscal(a1, 2.0) : a1);
+                }
+                acc = mk(acc.x / 64.0, acc.y / 64.0);
+                const int onb = (ci == 0 || ci == K.n1 - 1) + (cj == 0 || cj == K.n2 - 1) +
+                                (cm == 0 || cm == K.n3 - 1);
+                if (onb) {
+                    if (K.bc == HF_BC_DIRICHLET) acc = mk(0, 0);
+                    else
+                        for (int d = 0; d < onb; d++) acc = cscal(acc, 64.0 / 48.0);
+                }
+                C.b[q] = acc;
+            }
+            break;
+        }
+        case PH_CORR: {        // t = [w D^-1 b] + P e,  e = u_{l+1}
+            const CoLevel &C = a.lv[ph.l + 1];
+            const Lvl &K = C.L;
+            const long long N = (long long)L.n1 * L.plane;
+            const cd *e = C.u;
+            for (long long q = gtid; q < N; q += gstride) {
+                const int i = (int)(q / L.plane);
+                const int rem = (int)(q - (long long)i * L.plane);
+                const int j = rem / L.n3, m = rem - j * L.n3;
+                const bool o2 = j & 1, o3 = m & 1;
+                const cd *ecol = e + (long long)(j >> 1) * K.n3 + (m >> 1);
+                auto cplane = [&](int c) -> cd {
+                    const cd *pp = ecol + (long long)c * K.plane;
+                    cd v = __ldcg(pp);
+                    if (o3) v = cadd(v, __ldcg(pp + 1));
+                    if (o2) {
+                        v = cadd(v, __ldcg(pp + K.n3));
+                        if (o3) v = cadd(v, __ldcg(pp + K.n3 + 1));
+                    }
+                    return v;
+                };
+                const double s2 = (o2 && o3) ? 0.25 : ((o2 || o3) ? 0.5 : 1.0);
+                const cd v0 = cplane(i >> 1);
+                cd pe;
+                if (i & 1) pe = cscal(cadd(v0, cplane((i >> 1) + 1)), 0.5 * s2);
+                else pe = s2 == 1.0 ? v0 : cscal(v0, s2);
+                if (a.pre) {
+                    const int nb = face(i, L.n1) + face(j, L.n2) + face(m, L.n3);
+                    const cd D = L.dinv ? __ldcg(L.dinv + q) : __ldg(L.tab + 4 + nb);
+                    pe = cadd(cscal(cmul(__ldcg(F.b + q), D), w), pe);
+                }
+                F.t[q] = pe;
+            }
+            break;
+        }
+        case PH_JACOBI: {      // u = t + w D^-1 (b - M t)
+            const long long N = (long long)L.n1 * L.plane;
+            for (long long q0 = gtid; q0 < N; q0 += CO_U * gstride) {
+                G7 g[CO_U];
+                cd bc[CO_U], dc[CO_U];
+#pragma unroll
+                for (int u = 0; u < CO_U; u++) {
+                    gather7(L, F.t, q0 + u * gstride, N, false, g[u]);
+                    const long long q = g[u].ok ? q0 + u * gstride : 0;
+                    bc[u] = __ldcg(F.b + q);
+                    dc[u] = L.dinv ? __ldcg(L.dinv + q) : mk(0, 0);
+                }
+#pragma unroll
+                for (int u = 0; u < CO_U; u++) {
+                    if (!g[u].ok) continue;
+                    const cd mf = g7_apply(L, tap, g[u], g[u].v);
+                    const cd wd = L.dinv ? cscal(dc[u], w) : tw[g[u].nb[0]];
+                    F.u[q0 + u * gstride] = cadd(g[u].v[0], cmul(wd, csub(bc[u], mf)));
+                }
+            }
+            break;
+        }
+        case PH_FDM_W:         // in-plane transform with V2^-1, V3^-1 of b -> tmp0
+        case PH_FDM_V: {       // in-plane transform with V2, V3 of tmp1 -> u
+            const int n1 = L.n1, n2 = L.n2, n3 = L.n3;
+            const cd *W1 = a.fdm, *W2 = W1 + n1 * n1, *W3 = W2 + n2 * n2;
+            const cd *V1 = W3 + n3 * n3, *V2 = V1 + n1 * n1, *V3 = V2 + n2 * n2;
+            (void)V1;
+            const int gy = (n2 + a.fR - 1) / a.fR, nvb = n1 * gy;
+            const size_t N = (size_t)n1 * n2 * n3;
+            const bool fw = ph.type == PH_FDM_W;
+            for (int vb = blockIdx.x; vb < nvb; vb += nblk) {
+                fdm_plane_body<256>(n2, n3, a.fR, fw ? W2 : V2, fw ? W3 : V3,
+                                    fw ? F.b : a.ftmp + N, fw ? a.ftmp : F.u, smem_raw, tid,
+                                    vb / gy, vb % gy);
+                __syncthreads();
+            }
+            break;
+        }
+        case PH_FDM_FIBER: {   // i1 transform with V1^-1, 1/D, V1: tmp0 -> tmp1
+            const int n1 = L.n1, n2 = L.n2, n3 = L.n3;
+            const cd *W1 = a.fdm, *W2 = W1 + n1 * n1, *W3 = W2 + n2 * n2;
+            const cd *V1 = W3 + n3 * n3;
+            const int gy = (n3 + a.fC - 1) / a.fC, nvb = n2 * gy;
+            const size_t N = (size_t)n1 * n2 * n3;
+            for (int vb = blockIdx.x; vb < nvb; vb += nblk) {
+                fdm_fiber_body<256>(n1, n2, n3, a.fC, W1, V1, a.invD, a.ftmp, a.ftmp + N, smem_raw,
+                                    tid, vb / gy, vb % gy);
+                __syncthreads();
+            }
+            break;
+        }
+        default:
+            break;
+        }
+    }
+}
+
 __global__ void k_assemble(Lvl L, cd *__restrict__ A) {
     pdl_enter();
     long long N = (long long)L.n1 * L.plane;
@@ -1438,6 +1714,10 @@ static void fdm_split(int n1, int n2, int n3, int &R, int &C, size_t &sp, size_t
     sp = ((size_t)R * n2 + (size_t)n3 * n3 + (size_t)n2 * n3 + (size_t)R * n3) * sizeof(cd);
     sf = (2ull * n1 * n1 + 2ull * n1 * C) * sizeof(cd);
 }
+void fdm_groups(int n1, int n2, int n3, int &R, int &C) {
+    size_t sp, sf;
+    fdm_split(n1, n2, n3, R, C, sp, sf);
+}
 size_t fdm_smem_bytes(int n1, int n2, int n3) {
     int R, C;
     size_t sp, sf;
@@ -1458,6 +1738,33 @@ void launch_fdm(int n1, int n2, int n3, const cd *fdm, const cd *invD, const cd 
     launch(k_fdm_fiber, gf, dim3(FDM_THREADS), sf, s, n1, n2, n3, C, W1, V1, invD,
            (const cd *)t0, t1, done);
     launch(k_fdm_plane, gp, dim3(FDM_THREADS), sp, s, n2, n3, R, V2, V3, (const cd *)t1, x, done);
+}
+int coarse_blocks(size_t smem, int per_sm_cap) {
+    static int occ = -1;
+    static size_t occ_smem = 0;
+    if (occ < 0 || occ_smem != smem) {
+        cudaFuncSetAttribute(k_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_coarse, 256, smem) != cudaSuccess)
+            occ = 0;
+        occ_smem = smem;
+    }
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms * std::min(occ, per_sm_cap);
+}
+cudaError_t launch_coarse(const CoArgs &a, int nblk, size_t smem, cudaStream_t s, const int *done) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nblk);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;   // every block resident: grid barriers are safe
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_coarse, a, done);
 }
 void launch_set_identity(long long N, cd *B, cudaStream_t s) {
     launch(k_set_identity, dim3((unsigned)((N + 255) / 256)), dim3(256), 0, s, N, B);

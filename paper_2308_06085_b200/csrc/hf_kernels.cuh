@@ -36,6 +36,7 @@ void launch_symv(int N, const cd *tiles, const double *sv, const cd *b, cd *prow
                  cudaStream_t s, const int *done);
 long long sym_tiles_count(int N);
 size_t fdm_smem_bytes(int n1, int n2, int n3);
+void fdm_groups(int n1, int n2, int n3, int &R, int &C);
 void launch_fdm(int n1, int n2, int n3, const cd *fdm, const cd *invD, const cd *b, cd *tmp,
                 cd *x, cudaStream_t s, const int *done);
 void launch_assemble(const Lvl &L, cd *A, cudaStream_t s);
@@ -58,5 +59,33 @@ void launch_bcg_xr(long long n, const BcgState *st, cd *x, const cd *ph, const c
 void launch_bcg_xhalf(long long n, const BcgState *st, cd *x, const cd *ph, cudaStream_t s);
 
 #define VEC_BLOCKS_HOST 592
+
+// coarse sub-cycle in one cooperative launch (k_coarse in hf_kernels.cu)
+enum { PH_DOWN = 0, PH_RESTRICT, PH_REST_B, PH_CORR, PH_JACOBI, PH_FDM_W, PH_FDM_FIBER, PH_FDM_V };
+#define CO_MAX_LEVELS 8
+#define CO_MAX_PHASES 48
+struct CoLevel {
+    Lvl L;
+    cd *b, *u, *r, *t;
+};
+struct CoPhase {
+    int type, l;
+};
+struct CoArgs {
+    CoLevel lv[CO_MAX_LEVELS];
+    CoPhase ph[CO_MAX_PHASES];
+    int nph;
+    double omega;
+    int pre;             // nu1 = 1: zero-guess pre-smoothing (t = w D^-1 b + P e)
+    int fR, fC;          // fdm row / column groups
+    const cd *fdm, *invD;
+    cd *ftmp;
+    unsigned long long *bar;   // monotonic arrival counter (grid barriers)
+};
+
+// co-resident blocks of k_coarse for `smem` dynamic bytes (0: not launchable)
+int coarse_blocks(size_t smem, int per_sm_cap);
+// returns the launch error (cooperative launches are checked by the caller)
+cudaError_t launch_coarse(const CoArgs &a, int nblk, size_t smem, cudaStream_t s, const int *done);
 
 }  // namespace hf

@@ -203,6 +203,11 @@ struct hf_hierarchy {
     cd *fdm_invD = nullptr; // 1 / (l1_a + l2_b + l3_c + c) on the coarsest grid
     cd *fdm_tmp = nullptr;  // 2 N scratch
     int coarsest_flags = 0;
+    // levels >= co_first run as one cooperative k_coarse launch per cycle (-1: off)
+    int co_first = -1;
+    CoArgs co{};
+    int co_nblk = 0;
+    size_t co_smem = 0;
 };
 
 static bool keep_coarsening(int n1, int n2, int n3, const hf_mg_config &c) {
@@ -452,6 +457,78 @@ static int build_coarsest_direct(hf_hierarchy *H, cudaStream_t s) {
 
 static cudaStream_t work_stream() { return g_user_stream; }
 
+// The L2-resident bottom of a V(nu1 <= 1, 1) cycle as one k_coarse launch:
+// levels whose vertex count is at most HF_COARSE_MAX (default 300000, ~65^3)
+// down to a separable (fast-diagonalisation) coarsest level, whole grid only.
+static int build_coarse_schedule(hf_hierarchy *H) {
+    H->co_first = -1;
+    const hf_mg_config &c = H->cfg;
+    const int nl = (int)H->lev.size();
+    // opt-in (HF_COARSE=1): measured slower than the PDL-chained level kernels
+    // on B200
+    if (!std::getenv("HF_COARSE") || !H->fdm || nl < 2) return 0;
+    if (c.cycle != HF_CYCLE_V || c.nu1 > 1 || c.nu2 != 1) return 0;
+    const char *mx = std::getenv("HF_COARSE_MAX");
+    const long long maxn = mx ? std::atoll(mx) : 300000;
+    int first = nl - 1;
+    while (first > 1) {
+        const Lvl &L = H->lev[first - 1].L;
+        if ((long long)L.n1 * L.plane > maxn) break;
+        first--;
+    }
+    if (nl - first > CO_MAX_LEVELS) first = nl - CO_MAX_LEVELS;
+    for (int l = first; l < nl; l++) {
+        const Lvl &L = H->lev[l].L;
+        if (L.lo1 != 0 || L.nx != L.n1) return 0;
+    }
+    CoArgs &a = H->co;
+    a = CoArgs{};
+    for (int l = first; l < nl; l++) {
+        Level &lv = H->lev[l];
+        a.lv[l - first] = CoLevel{lv.L, lv.b, lv.u, lv.r, lv.t};
+    }
+    auto add = [&](int type, int l) {
+        if (a.nph < CO_MAX_PHASES) a.ph[a.nph++] = CoPhase{type, l - first};
+    };
+    const bool pre = c.nu1 == 1;
+    for (int l = first; l < nl - 1; l++) {
+        if (pre) {
+            add(PH_DOWN, l);
+            add(PH_RESTRICT, l);
+        } else {
+            add(PH_REST_B, l);
+        }
+    }
+    add(PH_FDM_W, nl - 1);
+    add(PH_FDM_FIBER, nl - 1);
+    add(PH_FDM_V, nl - 1);
+    for (int l = nl - 2; l >= first; l--) {
+        add(PH_CORR, l);
+        add(PH_JACOBI, l);
+    }
+    if (a.nph >= CO_MAX_PHASES) return 0;
+    if (const char *np = std::getenv("HF_COARSE_NPH"))   // timing experiments only (wrong results)
+        a.nph = std::max(0, std::min(a.nph, std::atoi(np)));
+    if (std::getenv("HF_COARSE_NOP"))   // timing experiments only: barriers without work
+        for (int p = 0; p < a.nph; p++) a.ph[p].type = -1;
+    a.omega = c.omega;
+    a.pre = pre ? 1 : 0;
+    const Lvl &K = H->lev.back().L;
+    fdm_groups(K.n1, K.n2, K.n3, a.fR, a.fC);
+    a.fdm = H->fdm;
+    a.invD = H->fdm_invD;
+    a.ftmp = H->fdm_tmp;
+    cudaError_t err;
+    a.bar = H->A.get<unsigned long long>(1, err);
+    if (!a.bar) return fail(HF_ERR_CUDA, "cudaMalloc coarse barrier");
+    H->co_smem = fdm_smem_bytes(K.n1, K.n2, K.n3);
+    const char *bps = std::getenv("HF_COARSE_BPS");
+    H->co_nblk = coarse_blocks(H->co_smem, bps ? std::max(1, std::atoi(bps)) : 2);
+    if (H->co_nblk <= 0) return 0;
+    H->co_first = first;
+    return 0;
+}
+
 
 extern "C" hf_hierarchy *hf_hierarchy_create(int n1, int n2, int n3, int lo1, int nx, double h,
                                              double beta1, double beta2, int bc,
@@ -514,6 +591,10 @@ extern "C" hf_hierarchy *hf_hierarchy_create(int n1, int n2, int n3, int lo1, in
         delete H;
         return nullptr;
     }
+    if (build_coarse_schedule(H)) {
+        delete H;
+        return nullptr;
+    }
     return H;
 }
 
@@ -551,6 +632,11 @@ static void smooth_sweeps(Level &lv, cd *u, const cd *b, double omega, int sweep
 }
 
 static void v_cycle(hf_hierarchy *H, int li, const cd *b, cd *u, cudaStream_t s, const int *done) {
+    if (li == H->co_first) {   // b, u are the level's own buffers below the finest level
+        launch_coarse(H->co, H->co_nblk, H->co_smem, s, done);
+        g_launches++;
+        return;
+    }
     Level &lv = H->lev[li];
     const hf_mg_config &c = H->cfg;
     if (li == (int)H->lev.size() - 1) { coarsest(H, b, u, s, done); return; }

@@ -52,7 +52,9 @@ def main():
     print(json.dumps({"problem": args.which, "grid": list(p.grid.shape), "unknowns": n,
                       "kh_max": float(np.max(k) * p.grid.h), "levels": [lv.grid.n1 for lv in H.levels],
                       "iterations": rep.iterations, "converged": rep.converged,
-                      "final_relres": rep.final_relres, "solve_s": rep.wall_time,
+                      "final_relres": rep.final_relres, "breakdown": rep.breakdown,
+                      "history_tail": [float(v) for v in rep.residual_history[-3:]],
+                      "history_every100": [float(v) for v in rep.residual_history[::100]], "solve_s": rep.wall_time,
                       "munknowns_iter_per_s": n * rep.iterations / rep.wall_time / 1e6,
                       "setup_s": t_setup, "host_problem_s": t_host,
                       "gpu_mem_gb": torch.cuda.max_memory_allocated() / 1e9}))

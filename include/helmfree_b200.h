@@ -149,9 +149,16 @@ int hf_mg_precondition(hf_hierarchy *hier, const double *r, double *z);
  * residual).  correct: t = w D^-1 b + P e (nu1 = 1; t = P e when nu1 = 0).
  * smooth: u = t + w D^-1 (b - M t) (post-smoothing sweep). */
 int hf_level_down1(hf_hierarchy *hier, int level, const double *b, double *r);
+/* down1 fused with restrict_fw: b_coarse = R (b - M (w D^-1 b)) without the fine
+ * residual (multigrid.py:383-386 + 171-221); b needs HF_GHOST valid ghost planes
+ * at interior slab faces.  b_coarse is the next level's owned block. */
+int hf_level_down_restrict(hf_hierarchy *hier, int level, const double *b, double *b_coarse);
 int hf_level_correct(hf_hierarchy *hier, int level, const double *b, const double *e_coarse,
                      double *t);
 int hf_level_smooth(hf_hierarchy *hier, int level, const double *t, const double *b, double *u);
+/* correct + smooth in one pass (whole-grid levels; split kernels on slabs):
+ * u = t + w D^-1 (b - M t), t = [w D^-1 b] + P e (multigrid.py:389-392, 153-156). */
+int hf_level_up(hf_hierarchy *hier, int level, const double *b, const double *e_coarse, double *u);
 
 /* ---- krylov.py:111-407 + runner.py:95-131 ------------------------------ */
 /* A: Helmholtz operator (shift 1) on the same slab as the hierarchy's finest level. */

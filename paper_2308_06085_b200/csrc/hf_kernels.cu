@@ -779,6 +779,233 @@ __global__ void __launch_bounds__(256) k_restrict2(Lvl F, Lvl C, const cd *__res
 }
 
 // ---------------------------------------------------------------------------
+// Fused zero-guess pre-smoothing + residual + full-weighting restriction
+// (nu1 = 1, multigrid.py:383-386 then 171-221):
+//     b_coarse = R (b - M (w D^-1 b))
+// without writing or re-reading the fine residual.  A block owns 16 x 4 coarse
+// columns, i.e. a 33 x 9 tile of fine residual points (one shared column/row
+// with the neighbouring tiles), and marches over the fine planes of a chunk of
+// coarse planes.  Per fine plane: the 35 x 11 tile of b (mirrored halos,
+// boundary-rescaled as in MODE_PRE) is staged by cp.async into a 5-slot ring
+// three planes ahead, all threads form the residual of the 33 x 9 tile into a
+// double-buffered shared tile, and warps 8-9 reduce the previous plane's tile
+// to the (1,2,1) x (1,2,1) partials of their 64 coarse columns and combine
+// three consecutive partials into a coarse value.  The arithmetic (and its
+// association) is that of k_stencil<MODE_PRE, EpiResid> + k_restrict2, so the
+// result is bit-identical to the split kernels.
+// ---------------------------------------------------------------------------
+#define DR_CX 16
+#define DR_CY 4
+#define DR_RX (2 * DR_CX + 1)
+#define DR_RY (2 * DR_CY + 1)
+#define DR_FX (DR_RX + 2)
+#define DR_FY (DR_RY + 2)
+#define DR_NF (DR_FX * DR_FY)
+#define DR_NR (DR_RX * DR_RY)
+#define DR_NT 320
+#define DR_RING 6
+
+template <bool KVAR>
+struct DRSmem {
+    cd f[DR_RING][DR_NF];
+    cd wd[KVAR ? DR_RING : 1][KVAR ? DR_NF : 1];
+    cd r[2][DR_NR];
+};
+
+template <bool KVAR, bool SOMM>
+__global__ void __launch_bounds__(DR_NT, 3) k_down_restrict(Lvl L, Lvl C, const cd *__restrict__ b,
+                                                         cd *__restrict__ out, double omega,
+                                                         int chunk, const int *done) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    using SM = DRSmem<KVAR>;
+    SM &sm = *reinterpret_cast<SM *>(smem_raw);
+    __shared__ cd tab[16];
+    if (is_done(done)) return;
+    const int tid = threadIdx.x;
+    const int cm0 = blockIdx.x * DR_CX, cj0 = blockIdx.y * DR_CY;
+    const int c0 = blockIdx.z * chunk, c1 = min(c0 + chunk, C.nx);
+    if (c0 >= c1) return;
+    const int gc0 = C.lo1 + c0, gc1 = C.lo1 + c1;            // global coarse planes [gc0, gc1)
+    const int fm0 = 2 * cm0 - 1, fj0 = 2 * cj0 - 1;          // residual tile origin (global)
+    auto mirror = [](int x, int n) { return x < 0 ? -x : (x >= n ? 2 * (n - 1) - x : x); };
+
+    if (!KVAR && tid < 4) {
+        tab[tid] = __ldg(L.tab + tid);
+        tab[4 + tid] = cscal(__ldg(L.tab + 4 + tid), omega);
+        tab[8 + tid] = cdiv(__ldg(L.tab + 4 + tid), __ldg(L.tab + 4));   // D^-1(nb) / D^-1(0)
+    }
+    // fill entries e0 = tid, e1 = tid + DR_NT (< DR_NF): mirrored in-plane vertex
+    const bool has1 = tid + DR_NT < DR_NF;
+    int go[2] = {0, 0}, nbe[2] = {0, 0};
+    bool ok[2] = {false, false};
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+        const int e = tid + k * DR_NT;
+        const int hy = e / DR_FX, hx = e - hy * DR_FX;
+        const int jj = fj0 - 1 + hy, mm = fm0 - 1 + hx;
+        const bool oj = jj >= -1 && jj <= L.n2, om = mm >= -1 && mm <= L.n3;
+        const bool corner = (jj < 0 || jj >= L.n2) && (mm < 0 || mm >= L.n3);
+        ok[k] = (k == 0 || has1) && oj && om && !corner;
+        if (ok[k]) {
+            const int mj = mirror(jj, L.n2), mmm = mirror(mm, L.n3);
+            go[k] = mj * L.n3 + mmm;
+            nbe[k] = (mj == 0) + (mj == L.n2 - 1) + (mmm == 0) + (mmm == L.n3 - 1);
+        }
+    }
+    const bool edge_block = fj0 - 1 <= 0 || fj0 + DR_RY >= L.n2 - 1 || fm0 - 1 <= 0 ||
+                            fm0 + DR_RX >= L.n3 - 1;
+    const unsigned sf0 = (unsigned)__cvta_generic_to_shared(&sm.f[0][tid]);
+    const unsigned sw0 = (unsigned)__cvta_generic_to_shared(&sm.wd[0][KVAR ? tid : 0]);
+    constexpr unsigned SLOT = DR_NF * sizeof(cd);
+    // stage global fine plane gp (mirrored outside the grid) into ring slot s
+    const int gp_last_stage = 2 * gc1;                       // last plane a residual reads
+    auto stage = [&](int s, int gp) {
+        if (gp <= gp_last_stage) {                            // (slabs: stay inside the ghosts)
+            const int gm = mirror(gp, L.n1);
+            const long long pb = (long long)(gm - L.lo1) * L.plane;
+            const unsigned so = s * SLOT;
+            cp_async16s(sf0 + so, b + pb + go[0], ok[0]);
+            if (KVAR) cp_async16s(sw0 + so, L.dinv + pb + go[0], ok[0]);
+            if (has1) {
+                cp_async16s(sf0 + so + DR_NT * sizeof(cd), b + pb + go[1], ok[1]);
+                if (KVAR) cp_async16s(sw0 + so + DR_NT * sizeof(cd), L.dinv + pb + go[1], ok[1]);
+            }
+        }
+        cp_commit();
+    };
+    // constant medium: rescale this thread's boundary fill entries of plane gp
+    auto fixup = [&](int s, int gp) {
+        if (KVAR) return;
+        const int gm = mirror(gp, L.n1);
+        const int nbx = (gm == 0) + (gm == L.n1 - 1);
+        if (nbx == 0 && !edge_block) return;
+#pragma unroll
+        for (int k = 0; k < 2; k++) {
+            const int e = tid + k * DR_NT;
+            if (ok[k] && (nbx + nbe[k]) > 0) sm.f[s][e] = cmul(sm.f[s][e], tab[8 + nbx + nbe[k]]);
+        }
+    };
+
+    // residual point of this thread (tid < DR_NR)
+    const bool rpt = tid < DR_NR;
+    const int ry = rpt ? tid / DR_RX : 0, rx = rpt ? tid - ry * DR_RX : 0;
+    const int gj = fj0 + ry, gmc = fm0 + rx;
+    const bool rin = rpt && gj >= 0 && gj < L.n2 && gmc >= 0 && gmc < L.n3;
+    const int cf = (ry + 1) * DR_FX + (rx + 1);
+    const int nbjm = rin ? (gj == 0) + (gj == L.n2 - 1) + (gmc == 0) + (gmc == L.n3 - 1) : 0;
+    const long long own = (long long)gj * L.n3 + gmc;
+    // coarse column of the reducing threads (warps 8-9)
+    const int cth = tid - 8 * 32, ccx = cth & (DR_CX - 1), ccy = cth >> 4;
+    const bool red = cth >= 0 && cth < DR_CX * DR_CY;
+    const int cj = cj0 + ccy, cm = cm0 + ccx;
+    const bool cact = red && cj < C.n2 && cm < C.n3;
+    cd Pprev = mk(0, 0), Pe = mk(0, 0);
+
+    auto partial = [&](int buf) -> cd {
+        const cd *bb = &sm.r[buf][(2 * ccy + 1) * DR_RX + 2 * ccx + 1];
+        cd s = mk(0, 0);
+#pragma unroll
+        for (int a = -1; a <= 1; a++) {
+            const cd *row = bb + a * DR_RX;
+            cd rs = cadd(cadd(row[-1], cscal(row[0], 2.0)), row[1]);
+            s = cadd(s, a == 0 ? cscal(rs, 2.0) : rs);
+        }
+        return s;
+    };
+    // fold the partial of fine plane gp into the coarse accumulation; an odd
+    // plane 2c+1 completes coarse plane c
+    auto fold = [&](int gp, cd P) {
+        if ((gp & 1) == 0) {
+            Pe = P;
+            return;
+        }
+        const int gc = (gp - 1) >> 1;
+        if (gc >= gc0 && cact) {
+            cd acc = cadd(cadd(Pprev, cscal(Pe, 2.0)), P);
+            acc = mk(acc.x / 64.0, acc.y / 64.0);
+            const int onb = (gc == 0 || gc == C.n1 - 1) + (cj == 0 || cj == C.n2 - 1) +
+                            (cm == 0 || cm == C.n3 - 1);
+            if (onb) {
+                if (!SOMM) acc = mk(0, 0);
+                else
+                    for (int d = 0; d < onb; d++) acc = cscal(acc, 64.0 / 48.0);
+            }
+            out[(long long)(gc - C.lo1) * C.plane + (long long)cj * C.n3 + cm] = acc;
+        }
+        Pprev = P;
+    };
+
+    const int gp0 = 2 * gc0 - 1, gp1 = 2 * gc1 - 1;           // residual planes [gp0, gp1]
+    // prologue: planes gp0-1 .. gp0+RING-3 into slots 0..RING-2
+    for (int k = 0; k < DR_RING - 1; k++) stage(k, gp0 - 1 + k);
+    cp_wait<DR_RING - 3>();
+    __syncthreads();                                         // tab visible
+    fixup(0, gp0 - 1);
+    fixup(1, gp0);
+    const cd ap0 = KVAR ? mk(0, 0) : tab[0];
+    const cd wd0 = KVAR ? mk(0, 0) : tab[4];
+    int sp = 0, sc = 1, sn = 2, ss = DR_RING - 1;            // slots of gp-1, gp, gp+1, free
+    cd b_next = mk(0, 0);
+    double k_next = L.kc;
+    if (rin && gp0 >= 0 && gp0 < L.n1) {
+        const long long q0 = (long long)(gp0 - L.lo1) * L.plane + own;
+        b_next = __ldg(b + q0);
+        if (KVAR) k_next = __ldg(L.k + q0);
+    }
+    for (int gp = gp0; gp <= gp1; gp++) {
+        cp_wait<DR_RING - 4>();                              // plane gp+1 landed
+        fixup(sn, gp + 1);
+        __syncthreads();
+        stage(ss, gp + DR_RING - 2);
+        const int buf = (gp - gp0) & 1;
+        if (rpt) {
+            cd rv = mk(0, 0);
+            const cd bc = b_next;
+            const double kq = k_next;
+            if (rin && gp + 1 >= 0 && gp + 1 < L.n1) {       // centre operands one plane ahead
+                const long long qn = (long long)(gp + 1 - L.lo1) * L.plane + own;
+                b_next = __ldg(b + qn);
+                if (KVAR) k_next = __ldg(L.k + qn);
+            }
+            if (rin && gp >= 0 && gp < L.n1) {
+                const cd *r0 = sm.f[sc];
+                cd fc = r0[cf];
+                cd xm = sm.f[sp][cf], xp = sm.f[sn][cf];
+                cd ym = r0[cf - DR_FX], yp = r0[cf + DR_FX];
+                cd zm = r0[cf - 1], zp = r0[cf + 1];
+                const int nb = (gp == 0) + (gp == L.n1 - 1) + nbjm;
+                cd post = wd0;
+                if (KVAR) {
+                    post = mk(omega, 0.0);
+                    fc = cmul(fc, sm.wd[sc][cf]);
+                    xm = cmul(xm, sm.wd[sp][cf]);
+                    xp = cmul(xp, sm.wd[sn][cf]);
+                    ym = cmul(ym, sm.wd[sc][cf - DR_FX]);
+                    yp = cmul(yp, sm.wd[sc][cf + DR_FX]);
+                    zm = cmul(zm, sm.wd[sc][cf - 1]);
+                    zp = cmul(zp, sm.wd[sc][cf + 1]);
+                }
+                cd sum = cadd(cadd(cadd(xm, xp), cadd(ym, yp)), cadd(zm, zp));
+                const cd ap = KVAR ? ap_of(L, kq, nb) : (nb == 0 ? ap0 : tab[nb]);
+                cd mf = cmul(ap, fc);
+                mf.x -= L.ih2 * sum.x;
+                mf.y -= L.ih2 * sum.y;
+                mf = cmul(post, mf);
+                if (!SOMM && nb) mf = cmul(post, fc);
+                rv = csub(bc, mf);
+            }
+            sm.r[buf][tid] = rv;
+        }
+        if (red && gp > gp0) fold(gp - 1, partial(buf ^ 1));
+        const int t = sp;
+        sp = sc; sc = sn; sn = (sn + 1) % DR_RING; ss = t;
+    }
+    cp_wait<0>();
+    __syncthreads();
+    if (red) fold(gp1, partial((gp1 - gp0) & 1));
+}
+
+// ---------------------------------------------------------------------------
 // 1-D vector kernels (owned region, contiguous)
 // ---------------------------------------------------------------------------
 #define VEC_BLOCKS 592   // 4 x 148 SMs, fixed => deterministic reductions
@@ -1599,6 +1826,10 @@ void init_kernel_attributes() {
     set_attr<MODE_LOAD, EpiJacobi, 0>();
     set_attr<MODE_PRE, EpiResid, 0>();
     set_attr<MODE_UP, EpiJacobi, 0>();
+    cudaFuncSetAttribute(k_down_restrict<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DRSmem<true>));
+    cudaFuncSetAttribute(k_down_restrict<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DRSmem<true>));
+    cudaFuncSetAttribute(k_down_restrict<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DRSmem<false>));
+    cudaFuncSetAttribute(k_down_restrict<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DRSmem<false>));
     cudaFuncSetAttribute(k_fdm_plane, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_fdm_fiber, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     done = true;
@@ -1661,6 +1892,28 @@ void launch_restrict(const Lvl &F, const Lvl &C, const cd *r, cd *out, cudaStrea
     int chunk = std::max(2, (C.nx + gz - 1) / gz);
     gz = (C.nx + chunk - 1) / chunk;
     launch(k_restrict2, dim3(dim3(gx, gy, gz)), dim3(256), 0, s, F, C, r, out, chunk, done);
+}
+template <bool KVAR, bool SOMM>
+static void dr_launch(const Lvl &F, const Lvl &C, const cd *b, cd *out, double omega, cudaStream_t s,
+                      const int *done) {
+    const int gx = (C.n3 + DR_CX - 1) / DR_CX, gy = (C.n2 + DR_CY - 1) / DR_CY;
+    const long long cols = (long long)gx * gy;
+    int gz = (int)std::max<long long>(1, std::min<long long>(C.nx, (148 * 4 + cols - 1) / cols));
+    const int chunk = (C.nx + gz - 1) / gz;
+    gz = (C.nx + chunk - 1) / chunk;
+    launch(k_down_restrict<KVAR, SOMM>, dim3(gx, gy, gz), dim3(DR_NT), sizeof(DRSmem<KVAR>), s, F, C,
+           b, out, omega, chunk, done);
+}
+void launch_down_restrict(const Lvl &F, const Lvl &C, const cd *b, cd *out, double omega,
+                          cudaStream_t s, const int *done) {
+    const bool somm = F.bc == HF_BC_SOMMERFELD;
+    if (F.k) {
+        if (somm) dr_launch<true, true>(F, C, b, out, omega, s, done);
+        else dr_launch<true, false>(F, C, b, out, omega, s, done);
+    } else {
+        if (somm) dr_launch<false, true>(F, C, b, out, omega, s, done);
+        else dr_launch<false, false>(F, C, b, out, omega, s, done);
+    }
 }
 void launch_prolong(const Lvl &F, const Lvl &C, const cd *e, cd *out, bool add, cudaStream_t s,
                     const int *done) {

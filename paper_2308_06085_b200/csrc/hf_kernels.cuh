@@ -22,6 +22,9 @@ void launch_down1(const Lvl &L, const cd *b, cd *r, double omega, cudaStream_t s
                   const int *done);
 void launch_restrict(const Lvl &F, const Lvl &C, const cd *r, cd *out, cudaStream_t s,
                      const int *done);
+// b_coarse = R (b - M (w D^-1 b)): fused pre-smooth + residual + restriction
+void launch_down_restrict(const Lvl &F, const Lvl &C, const cd *b, cd *out, double omega,
+                          cudaStream_t s, const int *done);
 void launch_prolong(const Lvl &F, const Lvl &C, const cd *e, cd *out, bool add, cudaStream_t s,
                     const int *done);
 // returns the number of kernels launched (1 fused, 2 split)

@@ -642,8 +642,13 @@ static void v_cycle(hf_hierarchy *H, int li, const cd *b, cd *u, cudaStream_t s,
     if (li == (int)H->lev.size() - 1) { coarsest(H, b, u, s, done); return; }
     Level &nx = H->lev[li + 1];
     const bool fused = c.nu1 <= 1 && c.nu2 == 1;
-    if (c.nu1 == 1 && fused) {
+    // fused down + restriction: opt-in (HF_DR=1) until it beats the split pair
+    const bool split_dr = std::getenv("HF_DR") == nullptr || std::getenv("HF_NO_DR") != nullptr;
+    if (c.nu1 == 1 && fused && !split_dr) {
+        L1(launch_down_restrict(lv.L, nx.L, b, nx.b, c.omega, s, done));
+    } else if (c.nu1 == 1 && fused) {
         L1(launch_down1(lv.L, b, lv.r, c.omega, s, done));
+        L1(launch_restrict(lv.L, nx.L, lv.r, nx.b, s, done));
     } else {
         if (c.nu1 == 0) {
             cudaMemsetAsync(u, 0, (size_t)lv.L.nx * lv.L.plane * sizeof(cd), s);
@@ -652,8 +657,8 @@ static void v_cycle(hf_hierarchy *H, int li, const cd *b, cd *u, cudaStream_t s,
             smooth_sweeps(lv, u, b, c.omega, c.nu1 - 1, s, done);
         }
         L1(launch_residual(lv.L, u, b, lv.r, s, done));
+        L1(launch_restrict(lv.L, nx.L, lv.r, nx.b, s, done));
     }
-    L1(launch_restrict(lv.L, nx.L, lv.r, nx.b, s, done));
     v_cycle(H, li + 1, nx.b, nx.u, s, done);
     if (fused) {
         g_launches += launch_up1(lv.L, nx.L, b, nx.u, u, lv.t, c.omega, c.nu1 == 1, s, done);
@@ -713,8 +718,27 @@ extern "C" int hf_level_down1(hf_hierarchy *H, int l, const double *b, double *r
     CKL();
     return 0;
 }
+// ... or, fused with the restriction, b_coarse = R (b - M (w D^-1 b)) (b needs
+// HF_GHOST valid ghost planes at interior slab faces) ...
+extern "C" int hf_level_down_restrict(hf_hierarchy *H, int l, const double *b, double *bc) {
+    if (!H || l < 0 || l + 1 >= (int)H->lev.size()) return fail(HF_ERR_ARG, "bad level");
+    launch_down_restrict(H->lev[l].L, H->lev[l + 1].L, (const cd *)b, (cd *)bc, H->cfg.omega,
+                         work_stream(), nullptr);
+    CKL();
+    return 0;
+}
 // ... and u = u1 + w D^-1 (b - M u1), u1 = w D^-1 b + P e (t: scratch field with ghost planes;
 // the caller exchanges t's halo between the two halves when the slab has interior faces)
+// ... or, on whole-grid levels, correction and post-smoothing in one kernel
+// (MODE_UP): u = u1 + w D^-1 (b - M u1), u1 = [w D^-1 b] + P e
+extern "C" int hf_level_up(hf_hierarchy *H, int l, const double *b, const double *e, double *u) {
+    if (!H || l < 0 || l + 1 >= (int)H->lev.size()) return fail(HF_ERR_ARG, "bad level");
+    Level &lv = H->lev[l];
+    launch_up1(lv.L, H->lev[l + 1].L, (const cd *)b, (const cd *)e, (cd *)u, lv.t, H->cfg.omega,
+               H->cfg.nu1 == 1, work_stream(), nullptr);
+    CKL();
+    return 0;
+}
 extern "C" int hf_level_correct(hf_hierarchy *H, int l, const double *b, const double *e,
                                 double *t) {
     if (!H || l < 0 || l + 1 >= (int)H->lev.size()) return fail(HF_ERR_ARG, "bad level");

@@ -22,7 +22,7 @@ import ctypes
 import numpy as np
 
 from . import _native
-from .grid import BlockExtent, Grid3, HaloField, full_extent, make_grid
+from .grid import HF_GHOST, BlockExtent, Grid3, HaloField, full_extent, make_grid
 from .krylov import ConvergenceReport, SolverConfig
 from .multigrid import MGConfig
 from .operators import OperatorSpec, StencilOperator, bc_name, k_arguments
@@ -73,6 +73,11 @@ class SlabSolver:
                 lv.append(BlockExtent(d[3] + 1, 1, 1, d[3] + d[4], d[1], d[2]))
             self.levels.append(lv)
         self.nlev = len(self.levels[0])
+        # fused down + restriction per level: needs an HF_GHOST-deep halo of b, so
+        # every slab of that level must own at least HF_GHOST planes
+        nsl = len(self.extents) if len(self.extents) > 1 else getattr(comm, "size", 1)
+        self._fuse_down = [all(e.nx >= HF_GHOST for e in _level_extents(grid, nsl, l + 1))
+                           for l in range(self.nlev)]
         d = (ctypes.c_int * 5)()
         _native.check(L.hf_hierarchy_level_shape(self.H[0], self.nlev - 1, d))
         cgrid = make_grid(d[0], d[1], d[2], grid.h * 2 ** (self.nlev - 1))
@@ -131,6 +136,13 @@ class SlabSolver:
         for r in S:
             self.fb[r][0].owned.copy_(src[r].owned)
         for l in range(n - 1):
+            if self._fuse_down[l]:
+                # one HF_GHOST-deep halo of b, then the fused down + restriction
+                self.comm.exchange([self.fb[r][l].data for r in S], planes=HF_GHOST)
+                for r in S:
+                    _native.check(L.hf_level_down_restrict(self.H[r], l, _ptr(self.fb[r][l].owned),
+                                                           _ptr(self.fb[r][l + 1].owned)))
+                continue
             self._halo([self.fb[r][l] for r in S])
             for r in S:
                 _native.check(L.hf_level_down1(self.H[r], l, _ptr(self.fb[r][l].owned),
@@ -241,6 +253,11 @@ class SlabSolver:
 
 
 def _coarse_extents(grid, nslabs, nlev):
+    return _level_extents(grid, nslabs, nlev)
+
+
+def _level_extents(grid, nslabs, nlev):
+    """Every slab's extent on level nlev - 1 (level 0 = the fine partition)."""
     from .partition import derive_coarse_extent, slab_partition
     out = []
     for e in slab_partition(grid, nslabs):

@@ -121,6 +121,33 @@ def test_fused_up_matches_split(hf, dims, bc, kind, mg, monkeypatch):
     assert np.array_equal(fused, split), np.abs(fused - split).max()
 
 
+@pytest.mark.parametrize("dims,bc,kind", [
+    ((129, 129, 129), "sommerfeld", "const"),
+    ((65, 65, 65), "sommerfeld", "const"),
+    ((129, 65, 97), "sommerfeld", "const"),
+    ((65, 33, 49), "dirichlet", "const"),
+    ((65, 65, 65), "sommerfeld", "field"),
+    ((65, 49, 33), "dirichlet", "field"),
+    ((33, 17, 65), "sommerfeld", "field"),
+])
+def test_fused_down_restrict_matches_split(hf, dims, bc, kind, monkeypatch):
+    """Pre-smoothing + residual + full weighting in one kernel
+    (k_down_restrict) matches the split down1 + restriction kernels on every
+    level of the cycle (same arithmetic; only FMA contraction may differ)."""
+    from paper_2308_06085_b200.multigrid import MGConfig, build_hierarchy, mg_precondition
+    from paper_2308_06085_b200.operators import Dirichlet, OperatorSpec, Sommerfeld
+    grid = hf.make_grid(*dims, 1.0 / (dims[0] - 1))
+    k = np.full(dims, 30.0) if kind == "const" else _kfield(dims, 12, 20, 35)
+    spec = OperatorSpec("cslp", 1.0, -0.5, Dirichlet(0.0) if bc == "dirichlet" else Sommerfeld(), k)
+    r = torch.as_tensor(_rand(dims, 43)).cuda()
+    hier = build_hierarchy(grid, None, spec, MGConfig())
+    monkeypatch.setenv("HF_DR", "1")
+    fused = mg_precondition(hier, r).cpu().numpy()
+    monkeypatch.setenv("HF_NO_DR", "1")
+    split = mg_precondition(hier, r).cpu().numpy()
+    assert _rel(fused, split) < 1e-13
+
+
 @pytest.mark.parametrize("bc", ["dirichlet", "sommerfeld"])
 def test_transfers_and_smoother(hf, oracle, bc):
     from paper_2308_06085_b200.multigrid import jacobi_smooth, prolong_tl, restrict_fw

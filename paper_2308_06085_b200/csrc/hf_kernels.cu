@@ -579,6 +579,201 @@ __global__ void __launch_bounds__(NT) k_stencil(Lvl L, const cd *__restrict__ sr
                                             blockIdx.y, blockIdx.z);
 }
 
+// ---------------------------------------------------------------------------
+// k_flat_stencil: marching stencil on a FLAT (i2, i3) decomposition.
+//
+// Each plane is treated as one contiguous array of n2*n3 vertices; a block owns
+// FS_PTS consecutive vertices of it (two per thread, 256 apart, so every warp
+// access is 512 contiguous bytes) and marches along i1.  Its halo -- the owned
+// range widened by one row (n3 + 1) on each side -- is ONE contiguous bulk copy
+// per plane (cp.async.bulk, issued by thread 0, completed on the slot's
+// mbarrier with expect_tx): no tensor map, no per-thread staging addresses,
+// and no ragged tiles (grids of 2^k + 1 vertices waste ~1% instead of the
+// ~35% a 32 x 8 tile wastes).  Neighbour offsets, including the Sommerfeld
+// mirror at the faces (operators.py:9-12), are per-thread constants of the
+// march; the centre value rotates through registers along i1, so a point
+// reads 5 shared values per plane.  The first / last global plane take the
+// mirrored plane through a block-uniform branch.  One __syncthreads per plane
+// guards slot reuse.  Used when the halo is small against the owned range
+// (n3 <= FS_MAX_N3); wider planes keep the 2-D tiled kernels.
+// ---------------------------------------------------------------------------
+#define FS_PTS 512
+#define FS_RING 5
+#define FS_MAX_N3 256
+
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(unsigned dst, const void *src, unsigned bytes, unsigned bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+
+// slot geometry of one block: window [w0, w0 + FS_PTS + 2 (n3 + 1)) of the plane
+__host__ __device__ __forceinline__ int fs_window(int n3) { return FS_PTS + 2 * (n3 + 1); }
+__host__ __device__ __forceinline__ int fs_slot_bytes(int n3) { return (fs_window(n3) * 16 + 127) / 128 * 128; }
+
+template <class Epi, int ND, bool KVAR, bool SOMM>
+__global__ void __launch_bounds__(256) k_flat_stencil(Lvl L, const cd *__restrict__ src,
+                                                      const cd *__restrict__ aux, double omega, Epi epi,
+                                                      int chunk, RedSlot rs, const int *done) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ __align__(8) unsigned long long bars[FS_RING];
+    __shared__ cd tab[8];
+    if (is_done(done)) return;
+    const int tid = threadIdx.x;
+    const int plane = (int)L.plane;
+    const int f0 = blockIdx.x * FS_PTS;
+    const int i0 = blockIdx.y * chunk, i1 = min(i0 + chunk, L.nx);
+    const int w0 = f0 - (L.n3 + 1);
+    const int c0 = max(w0, 0), c1 = min(f0 + FS_PTS + L.n3 + 1, plane);
+    const unsigned cbytes = (unsigned)(c1 - c0) * 16u;
+    const int sbytes = fs_slot_bytes(L.n3);
+    const unsigned sraw = smem_u32(smem_raw);
+    const unsigned sbase = (sraw + 127u) & ~127u, bbase = smem_u32(bars);
+    const cd *const sgen = reinterpret_cast<const cd *>(smem_raw + (sbase - sraw));
+    auto gmirror = [&](int g) { return g < 0 ? -g : (g >= L.n1 ? 2 * (L.n1 - 1) - g : g); };
+    auto issue = [&](int p) {            // thread 0: halo window of local plane p (mirrored outside)
+        const int k = (p - (i0 - 1)) % FS_RING;
+        const unsigned bar = bbase + 8 * k;
+        const long long lp = gmirror(L.lo1 + p) - L.lo1;
+        mbar_expect_tx(bar, cbytes);
+        bulk_g2s(sbase + k * sbytes + (c0 - w0) * 16, src + lp * plane + c0, cbytes, bar);
+    };
+    if (tid == 0) {
+        for (int k = 0; k < FS_RING; k++) mbar_init(bbase + 8 * k, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if (!KVAR && tid < 4) {
+        tab[tid] = __ldg(L.tab + tid);
+        tab[4 + tid] = cscal(__ldg(L.tab + 4 + tid), omega);
+    }
+    __syncthreads();
+    const int last = min(i1, L.n1 - 1 - L.lo1);       // last plane read (i1, or the top plane)
+    if (tid == 0)
+        for (int p = i0 - 1; p < i0 - 1 + FS_RING && p <= last; p++) issue(p);
+    auto wait_plane = [&](int p) {
+        const int d = p - (i0 - 1);
+        mbar_wait(bbase + 8 * (d % FS_RING), (d / FS_RING) & 1);
+    };
+    auto slot = [&](int p) -> const cd * {
+        return sgen + ((p - (i0 - 1)) % FS_RING) * (sbytes / 16);
+    };
+    // per point: smem offsets of centre and in-plane neighbours (mirrored at faces)
+    int oc[2], ozm[2], ozp[2], oym[2], oyp[2], nbjm[2];
+    bool act[2];
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+        const int f = f0 + tid + 256 * k;
+        act[k] = f < plane;
+        const int ff = act[k] ? f : f0;
+        const int j = ff / L.n3, m = ff - j * L.n3;
+        oc[k] = ff - w0;
+        ozm[k] = oc[k] + (m == 0 ? 1 : -1);
+        ozp[k] = oc[k] + (m == L.n3 - 1 ? -1 : 1);
+        oym[k] = oc[k] + (j == 0 ? L.n3 : -L.n3);
+        oyp[k] = oc[k] + (j == L.n2 - 1 ? -L.n3 : L.n3);
+        nbjm[k] = (j == 0) + (j == L.n2 - 1) + (m == 0) + (m == L.n3 - 1);
+    }
+    const cd apc = KVAR ? mk(0, 0) : tab[0];
+    wait_plane(i0 - 1);
+    cd P[2], C[2];
+    {
+        const cd *sp = slot(i0 - 1);
+        P[0] = sp[oc[0]]; P[1] = sp[oc[1]];
+    }
+    wait_plane(i0);
+    {
+        const cd *sc = slot(i0);
+        C[0] = sc[oc[0]]; C[1] = sc[oc[1]];
+    }
+    cd acc[2] = {mk(0, 0), mk(0, 0)};
+    long long q = (long long)i0 * plane + f0 + tid;
+    cd av[2] = {mk(0, 0), mk(0, 0)};
+    double kv[2] = {L.kc, L.kc};
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+        if (Epi::kAux && act[k]) av[k] = __ldg(aux + q + 256 * k);
+        if (KVAR && act[k]) kv[k] = __ldg(L.k + q + 256 * k);
+    }
+    for (int i = i0; i < i1; i++) {
+        const int gi = L.lo1 + i;
+        const bool top = gi == L.n1 - 1, bot = gi == 0;
+        __syncthreads();                             // slot of plane i-1 is free
+        if (tid == 0 && i + FS_RING - 1 <= last) issue(i + FS_RING - 1);
+        cd N[2];
+        if (!top) {
+            wait_plane(i + 1);
+            const cd *sn = slot(i + 1);
+            N[0] = sn[oc[0]]; N[1] = sn[oc[1]];
+        } else {
+            N[0] = P[0]; N[1] = P[1];                // mirrored plane n1-2
+        }
+        const cd *s0 = slot(i);
+        cd an[2] = {av[0], av[1]};
+        double kn[2] = {kv[0], kv[1]};
+        if (i + 1 < i1) {
+#pragma unroll
+            for (int k = 0; k < 2; k++) {
+                if (Epi::kAux && act[k]) an[k] = __ldg(aux + q + plane + 256 * k);
+                if (KVAR && act[k]) kn[k] = __ldg(L.k + q + plane + 256 * k);
+            }
+        }
+        const int nbx = (int)bot + (int)top;
+#pragma unroll
+        for (int k = 0; k < 2; k++) {
+            if (!act[k]) continue;
+            const cd xm = bot ? N[k] : P[k];
+            const cd sum = cadd(cadd(cadd(xm, N[k]), cadd(s0[oym[k]], s0[oyp[k]])),
+                                cadd(s0[ozm[k]], s0[ozp[k]]));
+            const int nb = nbx + nbjm[k];
+            const cd ap = KVAR ? ap_of(L, kv[k], nb) : (nb == 0 ? apc : tab[nb]);
+            cd mf = cmul(ap, C[k]);
+            mf.x -= L.ih2 * sum.x;
+            mf.y -= L.ih2 * sum.y;
+            if (!SOMM && nb) mf = C[k];
+            cd wd = mk(0, 0);
+            if (Epi::kDinv) wd = KVAR ? cscal(__ldg(L.dinv + q + 256 * k), omega) : tab[4 + nb];
+            epi(q + 256 * k, C[k], mf, wd, av[k], acc);
+        }
+#pragma unroll
+        for (int k = 0; k < 2; k++) {
+            P[k] = C[k];
+            C[k] = N[k];
+            av[k] = an[k];
+            kv[k] = kn[k];
+        }
+        q += plane;
+    }
+    constexpr int NR = (ND > 0) ? ND : 1;
+    if (ND > 0) {
+        cd a2[NR];
+#pragma unroll
+        for (int d = 0; d < NR; d++) a2[d] = acc[d];
+        reduce_finish<NR>(a2, rs);
+    }
+}
+
 // D^-1 over a level of a varying medium (owned + ghost planes), at setup
 __global__ void k_dinv(Lvl L, int g0, int g1, cd *__restrict__ out) {
     pdl_enter();
@@ -1790,10 +1985,52 @@ static void stencil_launch(const Lvl &L, const cd *src, const cd *aux, double om
     launch(k_stencil<MODE, Epi, ND, KVAR, SOMM>, dim3(g), dim3(kTileBlock), smem, s, L, src,
            aux ? aux : src, omega, e, chunk, rs, up, done);
 }
+// ---- flat-decomposition MODE_LOAD stencils (k_flat_stencil) ----
+static bool use_flat(const Lvl &L) {
+    static const bool off = std::getenv("HF_NO_FLAT") != nullptr;   // A/B switch
+    return !off && L.n3 <= FS_MAX_N3;
+}
+static size_t flat_smem(const Lvl &L) { return (size_t)FS_RING * fs_slot_bytes(L.n3) + 128; }
+static const size_t kFlatSmemMax = (size_t)FS_RING * ((FS_PTS + 2 * (FS_MAX_N3 + 1)) * 16 + 127) / 128 * 128 + 128;
+template <class Epi, int ND, bool KVAR, bool SOMM>
+static void flat_launch_t(const Lvl &L, const cd *src, const cd *aux, double omega, const Epi &e,
+                          const RedSlot &rs, cudaStream_t s, const int *done) {
+    const int gx = (int)((L.plane + FS_PTS - 1) / FS_PTS);
+    static const int bps = std::getenv("HF_FLAT_BPS") ? std::atoi(std::getenv("HF_FLAT_BPS")) : 3;
+    int gz = std::max(1, std::min(L.nx, (148 * bps + gx - 1) / gx));
+    const int chunk = std::max((L.nx + gz - 1) / gz, std::min(L.nx, 2));
+    gz = (L.nx + chunk - 1) / chunk;
+    launch(k_flat_stencil<Epi, ND, KVAR, SOMM>, dim3(gx, gz), dim3(256), flat_smem(L), s, L, src,
+           aux ? aux : src, omega, e, chunk, rs, done);
+}
+template <class Epi, int ND>
+static bool flat_stencil(const Lvl &L, const cd *src, const cd *aux, double omega, const Epi &e,
+                         const RedSlot &rs, cudaStream_t s, const int *done) {
+    if (!use_flat(L)) return false;
+    const bool somm = L.bc == HF_BC_SOMMERFELD;
+    if (L.k) {
+        if (somm) flat_launch_t<Epi, ND, true, true>(L, src, aux, omega, e, rs, s, done);
+        else flat_launch_t<Epi, ND, true, false>(L, src, aux, omega, e, rs, s, done);
+    } else {
+        if (somm) flat_launch_t<Epi, ND, false, true>(L, src, aux, omega, e, rs, s, done);
+        else flat_launch_t<Epi, ND, false, false>(L, src, aux, omega, e, rs, s, done);
+    }
+    return true;
+}
+template <class Epi, int ND>
+static void flat_attr() {
+    const int b = (int)kFlatSmemMax;
+    cudaFuncSetAttribute(k_flat_stencil<Epi, ND, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    cudaFuncSetAttribute(k_flat_stencil<Epi, ND, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    cudaFuncSetAttribute(k_flat_stencil<Epi, ND, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    cudaFuncSetAttribute(k_flat_stencil<Epi, ND, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+}
+
 template <int MODE, class Epi, int ND>
 static void stencil(const Lvl &L, const cd *src, const cd *aux, double omega, const Epi &e,
                     const RedSlot &rs, cudaStream_t s, const int *done,
                     const UpArgs &up = UpArgs{}) {
+    if (MODE == MODE_LOAD && flat_stencil<Epi, ND>(L, src, aux, omega, e, rs, s, done)) return;
     const bool somm = L.bc == HF_BC_SOMMERFELD;
     if (L.k) {
         if (somm) stencil_launch<MODE, Epi, ND, true, true>(L, src, aux, omega, e, rs, s, done, up);
@@ -1826,6 +2063,11 @@ void init_kernel_attributes() {
     set_attr<MODE_LOAD, EpiJacobi, 0>();
     set_attr<MODE_PRE, EpiResid, 0>();
     set_attr<MODE_UP, EpiJacobi, 0>();
+    flat_attr<EpiApply<0>, 0>();
+    flat_attr<EpiApply<1>, 1>();
+    flat_attr<EpiApply<2>, 2>();
+    flat_attr<EpiResid, 0>();
+    flat_attr<EpiJacobi, 0>();
     cudaFuncSetAttribute(k_down_restrict<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DRSmem<true>));
     cudaFuncSetAttribute(k_down_restrict<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DRSmem<true>));
     cudaFuncSetAttribute(k_down_restrict<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DRSmem<false>));

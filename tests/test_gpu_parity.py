@@ -107,7 +107,8 @@ def test_coarsest_fast_diagonalisation(hf, oracle, dims, h, kc, monkeypatch):
 ])
 def test_fused_up_matches_split(hf, dims, bc, kind, mg, monkeypatch):
     """Prolongation + correction produced inside the post-smoothing sweep
-    (MODE_UP) is bit-identical to the split correction + Jacobi kernels."""
+    (MODE_UP) matches the split correction + Jacobi kernels (same arithmetic;
+    FMA contraction may differ between the kernels)."""
     from paper_2308_06085_b200.multigrid import MGConfig, build_hierarchy, mg_precondition
     from paper_2308_06085_b200.operators import Dirichlet, OperatorSpec, Sommerfeld
     grid = hf.make_grid(*dims, 1.0 / (dims[0] - 1))
@@ -118,7 +119,7 @@ def test_fused_up_matches_split(hf, dims, bc, kind, mg, monkeypatch):
     fused = mg_precondition(hier, r).cpu().numpy()
     monkeypatch.setenv("HF_NO_FUSE", "1")
     split = mg_precondition(hier, r).cpu().numpy()
-    assert np.array_equal(fused, split), np.abs(fused - split).max()
+    assert _rel(fused, split) < 1e-13
 
 
 @pytest.mark.parametrize("dims,bc,kind", [

@@ -633,13 +633,19 @@ __device__ __forceinline__ void bulk_g2s(unsigned dst, const void *src, unsigned
 __host__ __device__ __forceinline__ int fs_window(int n3) { return FS_PTS + 2 * (n3 + 1); }
 __host__ __device__ __forceinline__ int fs_slot_bytes(int n3) { return (fs_window(n3) * 16 + 127) / 128 * 128; }
 
-template <class Epi, int ND, bool KVAR, bool SOMM>
-__global__ void __launch_bounds__(256) k_flat_stencil(Lvl L, const cd *__restrict__ src,
+// MODE_LOAD: f = src.  MODE_PRE: f = w D^-1 src (zero-guess pre-smoothing folded
+// into the residual, as in k_stencil): a constant medium stages b^ = b
+// D^-1(nb)/D^-1(0) (face vertices rescaled in the slot one plane ahead of use)
+// so f = wd0 b^ and the 7-point row stays uniform; a varying medium scales each
+// neighbour by its own D^-1.
+template <int MODE, class Epi, int ND, bool KVAR, bool SOMM>
+__global__ void __launch_bounds__(256, 3) k_flat_stencil(Lvl L, const cd *__restrict__ src,
                                                       const cd *__restrict__ aux, double omega, Epi epi,
                                                       int chunk, RedSlot rs, const int *done) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ __align__(8) unsigned long long bars[FS_RING];
     __shared__ cd tab[8];
+    __shared__ cd tabs[4];
     if (is_done(done)) return;
     const int tid = threadIdx.x;
     const int plane = (int)L.plane;
@@ -667,6 +673,7 @@ __global__ void __launch_bounds__(256) k_flat_stencil(Lvl L, const cd *__restric
     if (!KVAR && tid < 4) {
         tab[tid] = __ldg(L.tab + tid);
         tab[4 + tid] = cscal(__ldg(L.tab + 4 + tid), omega);
+        if (MODE == MODE_PRE) tabs[tid] = cdiv(__ldg(L.tab + 4 + tid), __ldg(L.tab + 4));   // D^-1(nb)/D^-1(0)
     }
     __syncthreads();
     const int last = min(i1, L.n1 - 1 - L.lo1);       // last plane read (i1, or the top plane)
@@ -678,6 +685,40 @@ __global__ void __launch_bounds__(256) k_flat_stencil(Lvl L, const cd *__restric
     };
     auto slot = [&](int p) -> const cd * {
         return sgen + ((p - (i0 - 1)) % FS_RING) * (sbytes / 16);
+    };
+    // MODE_PRE, constant medium: this thread's window entries (e = tid + 256 t)
+    // that are face vertices, rescaled in place by D^-1(nb)/D^-1(0) once their
+    // plane lands (one plane ahead of its first use)
+    constexpr bool kFix = MODE == MODE_PRE && !KVAR;
+    constexpr int NFE = (FS_PTS + 2 * (FS_MAX_N3 + 1) + 255) / 256;
+    unsigned fe_nb = 0;                  // 2 bits per entry: in-plane face count
+    unsigned fe_in = 0;                  // entry lies in the plane
+    if (kFix) {
+        const int W = c1 - w0;
+#pragma unroll
+        for (int t = 0; t < NFE; t++) {
+            const int e = tid + 256 * t, g = w0 + e;
+            if (e < W && g >= 0 && g < plane) {
+                const int j = g / L.n3, m = g - j * L.n3;
+                fe_in |= 1u << t;
+                fe_nb |= (unsigned)((j == 0) + (j == L.n2 - 1) + (m == 0) + (m == L.n3 - 1)) << (2 * t);
+            }
+        }
+    }
+    auto fixup = [&](int p) {            // own entries of local plane p (mirrored outside)
+        if (!kFix) return;
+        const int gm = gmirror(L.lo1 + p);
+        const int nbx = (gm == 0) + (gm == L.n1 - 1);
+        if (nbx == 0 && fe_nb == 0) return;
+        cd *sl = const_cast<cd *>(slot(p));
+#pragma unroll
+        for (int t = 0; t < NFE; t++) {
+            const int nb = nbx + (int)((fe_nb >> (2 * t)) & 3u);
+            if (((fe_in >> t) & 1u) && nb > 0) {
+                const int e = tid + 256 * t;
+                sl[e] = cmul(sl[e], tabs[nb]);
+            }
+        }
     };
     // per point: smem offsets of centre and in-plane neighbours (mirrored at faces)
     int oc[2], ozm[2], ozp[2], oym[2], oyp[2], nbjm[2];
@@ -697,14 +738,20 @@ __global__ void __launch_bounds__(256) k_flat_stencil(Lvl L, const cd *__restric
     }
     const cd apc = KVAR ? mk(0, 0) : tab[0];
     wait_plane(i0 - 1);
+    wait_plane(i0);
+    if (kFix) {
+        fixup(i0 - 1);
+        fixup(i0);
+        if (i0 + 1 <= last) {
+            wait_plane(i0 + 1);
+            fixup(i0 + 1);
+        }
+        __syncthreads();
+    }
     cd P[2], C[2];
     {
-        const cd *sp = slot(i0 - 1);
+        const cd *sp = slot(i0 - 1), *sc = slot(i0);
         P[0] = sp[oc[0]]; P[1] = sp[oc[1]];
-    }
-    wait_plane(i0);
-    {
-        const cd *sc = slot(i0);
         C[0] = sc[oc[0]]; C[1] = sc[oc[1]];
     }
     cd acc[2] = {mk(0, 0), mk(0, 0)};
@@ -721,6 +768,10 @@ __global__ void __launch_bounds__(256) k_flat_stencil(Lvl L, const cd *__restric
         const bool top = gi == L.n1 - 1, bot = gi == 0;
         __syncthreads();                             // slot of plane i-1 is free
         if (tid == 0 && i + FS_RING - 1 <= last) issue(i + FS_RING - 1);
+        if (kFix && i + 2 <= last) {     // visible after the next barrier
+            wait_plane(i + 2);
+            fixup(i + 2);
+        }
         cd N[2];
         if (!top) {
             wait_plane(i + 1);
@@ -743,18 +794,37 @@ __global__ void __launch_bounds__(256) k_flat_stencil(Lvl L, const cd *__restric
 #pragma unroll
         for (int k = 0; k < 2; k++) {
             if (!act[k]) continue;
-            const cd xm = bot ? N[k] : P[k];
-            const cd sum = cadd(cadd(cadd(xm, N[k]), cadd(s0[oym[k]], s0[oyp[k]])),
-                                cadd(s0[ozm[k]], s0[ozp[k]]));
+            cd fc = C[k], xm = bot ? N[k] : P[k], xp = N[k];
+            cd ym = s0[oym[k]], yp = s0[oyp[k]], zm = s0[ozm[k]], zp = s0[ozp[k]];
             const int nb = nbx + nbjm[k];
+            cd post = mk(1.0, 0.0);
+            if (MODE == MODE_PRE) {
+                if (KVAR) {          // f = D^-1 b per vertex, w applied after M
+                    post = mk(omega, 0.0);
+                    const cd *dv = L.dinv + q + 256 * k;
+                    const long long dxm = bot ? plane : -(long long)plane;
+                    const long long dxp = top ? -(long long)plane : plane;
+                    fc = cmul(fc, __ldg(dv));
+                    xm = cmul(xm, __ldg(dv + dxm));
+                    xp = cmul(xp, __ldg(dv + dxp));
+                    ym = cmul(ym, __ldg(dv + (oym[k] - oc[k])));
+                    yp = cmul(yp, __ldg(dv + (oyp[k] - oc[k])));
+                    zm = cmul(zm, __ldg(dv + (ozm[k] - oc[k])));
+                    zp = cmul(zp, __ldg(dv + (ozp[k] - oc[k])));
+                } else {
+                    post = tab[4];   // f = wd0 b^ (b^ rescaled in the slot)
+                }
+            }
+            const cd sum = cadd(cadd(cadd(xm, xp), cadd(ym, yp)), cadd(zm, zp));
             const cd ap = KVAR ? ap_of(L, kv[k], nb) : (nb == 0 ? apc : tab[nb]);
-            cd mf = cmul(ap, C[k]);
+            cd mf = cmul(ap, fc);
             mf.x -= L.ih2 * sum.x;
             mf.y -= L.ih2 * sum.y;
-            if (!SOMM && nb) mf = C[k];
+            if (MODE == MODE_PRE) mf = cmul(post, mf);
+            if (!SOMM && nb) mf = (MODE == MODE_PRE) ? cmul(post, fc) : fc;
             cd wd = mk(0, 0);
             if (Epi::kDinv) wd = KVAR ? cscal(__ldg(L.dinv + q + 256 * k), omega) : tab[4 + nb];
-            epi(q + 256 * k, C[k], mf, wd, av[k], acc);
+            epi(q + 256 * k, fc, mf, wd, av[k], acc);
         }
 #pragma unroll
         for (int k = 0; k < 2; k++) {
@@ -1992,7 +2062,7 @@ static bool use_flat(const Lvl &L) {
 }
 static size_t flat_smem(const Lvl &L) { return (size_t)FS_RING * fs_slot_bytes(L.n3) + 128; }
 static const size_t kFlatSmemMax = (size_t)FS_RING * ((FS_PTS + 2 * (FS_MAX_N3 + 1)) * 16 + 127) / 128 * 128 + 128;
-template <class Epi, int ND, bool KVAR, bool SOMM>
+template <int MODE, class Epi, int ND, bool KVAR, bool SOMM>
 static void flat_launch_t(const Lvl &L, const cd *src, const cd *aux, double omega, const Epi &e,
                           const RedSlot &rs, cudaStream_t s, const int *done) {
     const int gx = (int)((L.plane + FS_PTS - 1) / FS_PTS);
@@ -2000,37 +2070,39 @@ static void flat_launch_t(const Lvl &L, const cd *src, const cd *aux, double ome
     int gz = std::max(1, std::min(L.nx, (148 * bps + gx - 1) / gx));
     const int chunk = std::max((L.nx + gz - 1) / gz, std::min(L.nx, 2));
     gz = (L.nx + chunk - 1) / chunk;
-    launch(k_flat_stencil<Epi, ND, KVAR, SOMM>, dim3(gx, gz), dim3(256), flat_smem(L), s, L, src,
+    launch(k_flat_stencil<MODE, Epi, ND, KVAR, SOMM>, dim3(gx, gz), dim3(256), flat_smem(L), s, L, src,
            aux ? aux : src, omega, e, chunk, rs, done);
 }
-template <class Epi, int ND>
+template <int MODE, class Epi, int ND>
 static bool flat_stencil(const Lvl &L, const cd *src, const cd *aux, double omega, const Epi &e,
                          const RedSlot &rs, cudaStream_t s, const int *done) {
     if (!use_flat(L)) return false;
     const bool somm = L.bc == HF_BC_SOMMERFELD;
     if (L.k) {
-        if (somm) flat_launch_t<Epi, ND, true, true>(L, src, aux, omega, e, rs, s, done);
-        else flat_launch_t<Epi, ND, true, false>(L, src, aux, omega, e, rs, s, done);
+        if (somm) flat_launch_t<MODE, Epi, ND, true, true>(L, src, aux, omega, e, rs, s, done);
+        else flat_launch_t<MODE, Epi, ND, true, false>(L, src, aux, omega, e, rs, s, done);
     } else {
-        if (somm) flat_launch_t<Epi, ND, false, true>(L, src, aux, omega, e, rs, s, done);
-        else flat_launch_t<Epi, ND, false, false>(L, src, aux, omega, e, rs, s, done);
+        if (somm) flat_launch_t<MODE, Epi, ND, false, true>(L, src, aux, omega, e, rs, s, done);
+        else flat_launch_t<MODE, Epi, ND, false, false>(L, src, aux, omega, e, rs, s, done);
     }
     return true;
 }
-template <class Epi, int ND>
+template <int MODE, class Epi, int ND>
 static void flat_attr() {
     const int b = (int)kFlatSmemMax;
-    cudaFuncSetAttribute(k_flat_stencil<Epi, ND, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
-    cudaFuncSetAttribute(k_flat_stencil<Epi, ND, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
-    cudaFuncSetAttribute(k_flat_stencil<Epi, ND, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
-    cudaFuncSetAttribute(k_flat_stencil<Epi, ND, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    cudaFuncSetAttribute(k_flat_stencil<MODE, Epi, ND, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    cudaFuncSetAttribute(k_flat_stencil<MODE, Epi, ND, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    cudaFuncSetAttribute(k_flat_stencil<MODE, Epi, ND, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    cudaFuncSetAttribute(k_flat_stencil<MODE, Epi, ND, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
 }
 
 template <int MODE, class Epi, int ND>
 static void stencil(const Lvl &L, const cd *src, const cd *aux, double omega, const Epi &e,
                     const RedSlot &rs, cudaStream_t s, const int *done,
                     const UpArgs &up = UpArgs{}) {
-    if (MODE == MODE_LOAD && flat_stencil<Epi, ND>(L, src, aux, omega, e, rs, s, done)) return;
+    if ((MODE == MODE_LOAD || MODE == MODE_PRE) &&
+        flat_stencil<MODE == MODE_PRE ? MODE_PRE : MODE_LOAD, Epi, ND>(L, src, aux, omega, e, rs, s, done))
+        return;
     const bool somm = L.bc == HF_BC_SOMMERFELD;
     if (L.k) {
         if (somm) stencil_launch<MODE, Epi, ND, true, true>(L, src, aux, omega, e, rs, s, done, up);
@@ -2063,11 +2135,12 @@ void init_kernel_attributes() {
     set_attr<MODE_LOAD, EpiJacobi, 0>();
     set_attr<MODE_PRE, EpiResid, 0>();
     set_attr<MODE_UP, EpiJacobi, 0>();
-    flat_attr<EpiApply<0>, 0>();
-    flat_attr<EpiApply<1>, 1>();
-    flat_attr<EpiApply<2>, 2>();
-    flat_attr<EpiResid, 0>();
-    flat_attr<EpiJacobi, 0>();
+    flat_attr<MODE_LOAD, EpiApply<0>, 0>();
+    flat_attr<MODE_LOAD, EpiApply<1>, 1>();
+    flat_attr<MODE_LOAD, EpiApply<2>, 2>();
+    flat_attr<MODE_LOAD, EpiResid, 0>();
+    flat_attr<MODE_LOAD, EpiJacobi, 0>();
+    flat_attr<MODE_PRE, EpiResid, 0>();
     cudaFuncSetAttribute(k_down_restrict<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DRSmem<true>));
     cudaFuncSetAttribute(k_down_restrict<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DRSmem<true>));
     cudaFuncSetAttribute(k_down_restrict<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DRSmem<false>));
@@ -2170,7 +2243,9 @@ void launch_correct(const Lvl &L, const Lvl &C, const cd *b, const cd *e, cd *t,
 int launch_up1(const Lvl &L, const Lvl &C, const cd *b, const cd *e, cd *u, cd *t, double omega,
                bool pre, cudaStream_t s, const int *done) {
     // whole-grid levels: correction produced inside the post-smoothing sweep
-    const bool split = std::getenv("HF_NO_FUSE") != nullptr;   // A/B switch (tests)
+    // (the split pair is faster where the flat Jacobi sweep applies)
+    const bool split = std::getenv("HF_NO_FUSE") != nullptr ||
+                       (use_flat(L) && std::getenv("HF_FUSE_UP") == nullptr);
     if (!split && L.lo1 == 0 && L.nx == L.n1 && C.lo1 == 0 && C.nx == C.n1) {
         stencil<MODE_UP, EpiJacobi, 0>(L, b, b, omega, EpiJacobi{u}, RedSlot{}, s, done,
                                         UpArgs{C, e, pre ? 1 : 0});

@@ -116,6 +116,7 @@ def test_fused_up_matches_split(hf, dims, bc, kind, mg, monkeypatch):
     spec = OperatorSpec("cslp", 1.0, -0.5, Dirichlet(0.0) if bc == "dirichlet" else Sommerfeld(), k)
     r = torch.as_tensor(_rand(dims, 41)).cuda()
     hier = build_hierarchy(grid, None, spec, MGConfig(**mg))
+    monkeypatch.setenv("HF_FUSE_UP", "1")
     fused = mg_precondition(hier, r).cpu().numpy()
     monkeypatch.setenv("HF_NO_FUSE", "1")
     split = mg_precondition(hier, r).cpu().numpy()

@@ -844,6 +844,239 @@ __global__ void __launch_bounds__(256, 3) k_flat_stencil(Lvl L, const cd *__rest
     }
 }
 
+// ---------------------------------------------------------------------------
+// k_flat_dr: zero-guess pre-smoothing + residual + full-weighting restriction
+// in one pass (nu1 = 1, multigrid.py:383-386 then 171-221):
+//     b_coarse = R (b - M (w D^-1 b))
+// without writing or re-reading the fine residual.  A block owns DR2_CR whole
+// coarse rows (all i3) of a chunk of coarse planes, i.e. fine residual rows
+// 2 cr0 - 1 .. 2 cr1 - 1 (one row shared with each neighbour block) over all
+// fine columns, and marches over the fine planes.  Per fine plane: the b rows
+// of the block (+1 halo row each side, mirrored at the faces) arrive as ONE
+// contiguous cp.async.bulk on the slot's mbarrier; face vertices are rescaled
+// in the slot one plane ahead (MODE_PRE constant medium, as k_flat_stencil);
+// every thread forms residual points of the plane into a shared tile; after
+// one __syncthreads the coarse-column threads reduce it to the
+// (1,2,1) x (1,2,1) partial and fold three consecutive partials into a coarse
+// value.  Arithmetic and association follow k_stencil<MODE_PRE, EpiResid> +
+// k_restrict2, so the result matches the split pair to rounding.
+// ---------------------------------------------------------------------------
+#define DR2_CR 2
+#define DR2_NT 256
+#define DR2_RING 5
+#define DR2_RPT 5            // residual points per thread: (2 CR + 1) rows x n3 <= 5 x 255
+#define DR2_MAX_N3 255
+
+__host__ __device__ __forceinline__ int dr2_slot_elems(int n3) { return ((2 * DR2_CR + 3) * n3 + 7) / 8 * 8; }
+
+template <bool KVAR, bool SOMM>
+__global__ void __launch_bounds__(DR2_NT, 2) k_flat_dr(Lvl L, Lvl C, const cd *__restrict__ b,
+                                                       cd *__restrict__ out, double omega, int chunk,
+                                                       const int *done) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ __align__(8) unsigned long long bars[DR2_RING];
+    __shared__ cd tab[12];
+    if (is_done(done)) return;
+    const int tid = threadIdx.x;
+    const int n3 = L.n3, plane = (int)L.plane;
+    const int cr0 = blockIdx.x * DR2_CR, cr1 = min(cr0 + DR2_CR, C.n2);
+    const int c0 = blockIdx.y * chunk, c1 = min(c0 + chunk, C.nx);
+    if (c0 >= c1) return;
+    const int gc0 = C.lo1 + c0, gc1 = C.lo1 + c1;              // global coarse planes [gc0, gc1)
+    const int rlo = max(2 * cr0 - 1, 0), rhi = min(2 * cr1 - 1, L.n2 - 1);   // residual rows
+    const int blo = max(rlo - 1, 0), bhi = min(rhi + 1, L.n2 - 1);           // staged b rows
+    const int nrp = (rhi - rlo + 1) * n3;                       // residual points per plane
+    const unsigned wbytes = (unsigned)((bhi - blo + 1) * n3) * 16u;
+    const int selems = dr2_slot_elems(n3);
+    const unsigned sraw = smem_u32(smem_raw);
+    const unsigned sbase = (sraw + 127u) & ~127u, bbase = smem_u32(bars);
+    cd *const sgen = reinterpret_cast<cd *>(smem_raw + (sbase - sraw));
+    cd *const rt = sgen + DR2_RING * selems;                   // residual tiles [2][5 n3]
+    auto gmirror = [&](int g) { return g < 0 ? -g : (g >= L.n1 ? 2 * (L.n1 - 1) - g : g); };
+    const int gpf = 2 * gc0 - 1, gpl = 2 * gc1 - 1;             // residual planes [gpf, gpl]
+    const int stage_last = gpl + 1;                             // last plane a residual reads
+    auto issue = [&](int gp) {           // thread 0: b rows of global plane gp (mirrored outside)
+        const int k = (gp - gpf + 1) % DR2_RING;
+        const long long lp = gmirror(gp) - L.lo1;
+        mbar_expect_tx(bbase + 8 * k, wbytes);
+        bulk_g2s(sbase + k * selems * 16, b + lp * plane + (long long)blo * n3, wbytes, bbase + 8 * k);
+    };
+    auto wait_plane = [&](int gp) {
+        const int d = gp - gpf + 1;
+        mbar_wait(bbase + 8 * (d % DR2_RING), (d / DR2_RING) & 1);
+    };
+    auto slot = [&](int gp) { return sgen + ((gp - gpf + 1) % DR2_RING) * selems; };
+    if (tid == 0) {
+        for (int k = 0; k < DR2_RING; k++) mbar_init(bbase + 8 * k, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if (!KVAR && tid < 4) {
+        tab[tid] = __ldg(L.tab + tid);
+        tab[4 + tid] = cscal(__ldg(L.tab + 4 + tid), omega);
+        tab[8 + tid] = cdiv(__ldg(L.tab + 4 + tid), __ldg(L.tab + 4));   // D^-1(nb) / D^-1(0)
+    }
+    __syncthreads();
+    if (tid == 0)
+        for (int gp = gpf - 1; gp < gpf - 1 + DR2_RING && gp <= stage_last; gp++) issue(gp);
+
+    // residual points of this thread: slot offset of the centre + packed flags
+    // (bit0 row mirror below, bit1 row mirror above, bit2 col mirror left,
+    //  bit3 col mirror right, bits 4-5 in-plane face count)
+    int rc[DR2_RPT], rf[DR2_RPT];
+#pragma unroll
+    for (int t = 0; t < DR2_RPT; t++) {
+        const int e = tid + DR2_NT * t;
+        const int ee = e < nrp ? e : 0;
+        const int rr = rlo + ee / n3, m = ee - (ee / n3) * n3;
+        rc[t] = (rr - blo) * n3 + m;
+        const int fj = (rr == 0) + (rr == L.n2 - 1), fm = (m == 0) + (m == n3 - 1);
+        rf[t] = (rr == 0) | (rr == L.n2 - 1) << 1 | (m == 0) << 2 | (m == n3 - 1) << 3 | (fj + fm) << 4;
+    }
+    // MODE_PRE rescale of face vertices in the slots (constant medium): own entries
+    constexpr int NFE = ((2 * DR2_CR + 3) * DR2_MAX_N3 + DR2_NT - 1) / DR2_NT;
+    unsigned long long fe = 0;           // 2 bits per entry: in-plane face count (3 = not in window)
+    if (!KVAR) {
+        const int W = (bhi - blo + 1) * n3;
+#pragma unroll
+        for (int t = 0; t < NFE; t++) {
+            const int e = tid + DR2_NT * t;
+            unsigned v = 3u;
+            if (e < W) {
+                const int j = blo + e / n3, m = e - (e / n3) * n3;
+                v = (unsigned)((j == 0) + (j == L.n2 - 1) + (m == 0) + (m == n3 - 1));
+            }
+            fe |= (unsigned long long)v << (2 * t);
+        }
+    }
+    auto fixup = [&](int gp) {
+        if (KVAR) return;
+        const int gm = gmirror(gp);
+        const int nbx = (gm == 0) + (gm == L.n1 - 1);
+        cd *sl = slot(gp);
+#pragma unroll
+        for (int t = 0; t < NFE; t++) {
+            const unsigned v = (unsigned)(fe >> (2 * t)) & 3u;
+            if (v == 3u) continue;
+            const int nb = nbx + (int)v;
+            if (nb > 0) {
+                const int e = tid + DR2_NT * t;
+                sl[e] = cmul(sl[e], tab[8 + nb]);
+            }
+        }
+    };
+    // coarse column of this thread
+    const int ncp = (cr1 - cr0) * C.n3;
+    const bool cact = tid < ncp;
+    const int cj = cr0 + (cact ? tid / C.n3 : 0), cm = cact ? tid - (tid / C.n3) * C.n3 : 0;
+    const int crow = 2 * cj - rlo;                              // residual tile row of fine 2 cj
+    const bool rm_ok = 2 * cj - 1 >= 0, rp_ok = 2 * cj + 1 <= L.n2 - 1;
+    const bool cm_ok = 2 * cm - 1 >= 0, cp_ok = 2 * cm + 1 <= n3 - 1;
+    cd Pprev = mk(0, 0), Pe = mk(0, 0);
+    auto partial = [&](const cd *r) -> cd {
+        cd s = mk(0, 0);
+        const cd zero = mk(0, 0);
+#pragma unroll
+        for (int a = -1; a <= 1; a++) {
+            const bool rok = a < 0 ? rm_ok : (a > 0 ? rp_ok : true);
+            const cd *row = r + (crow + a) * n3 + 2 * cm;
+            const cd v0 = rok && cm_ok ? row[-1] : zero;
+            const cd v1 = rok ? row[0] : zero;
+            const cd v2 = rok && cp_ok ? row[1] : zero;
+            cd rs = cadd(cadd(v0, cscal(v1, 2.0)), v2);
+            s = cadd(s, a == 0 ? cscal(rs, 2.0) : rs);
+        }
+        return s;
+    };
+    auto fold = [&](int gp, cd P) {
+        if ((gp & 1) == 0) {
+            Pe = P;
+            return;
+        }
+        const int gc = (gp - 1) >> 1;
+        if (gc >= gc0 && cact) {
+            cd acc = cadd(cadd(Pprev, cscal(Pe, 2.0)), P);
+            acc = mk(acc.x / 64.0, acc.y / 64.0);
+            const int onb = (gc == 0 || gc == C.n1 - 1) + (cj == 0 || cj == C.n2 - 1) +
+                            (cm == 0 || cm == C.n3 - 1);
+            if (onb) {
+                if (!SOMM) acc = mk(0, 0);
+                else
+                    for (int d = 0; d < onb; d++) acc = cscal(acc, 64.0 / 48.0);
+            }
+            out[(long long)(gc - C.lo1) * C.plane + (long long)cj * C.n3 + cm] = acc;
+        }
+        Pprev = P;
+    };
+
+    // prologue: planes gpf-1, gpf, gpf+1 landed and rescaled
+    for (int gp = gpf - 1; gp <= gpf + 1 && gp <= stage_last; gp++) {
+        wait_plane(gp);
+        fixup(gp);
+    }
+    __syncthreads();
+    const cd ap0 = KVAR ? mk(0, 0) : tab[0];
+    const cd wd0 = KVAR ? mk(0, 0) : tab[4];
+    for (int gp = gpf; gp <= gpl; gp++) {
+        if (gp + 1 <= stage_last) wait_plane(gp + 1);
+        if (!KVAR && gp + 2 <= stage_last) {        // rescale plane gp+2 (visible after the barrier)
+            wait_plane(gp + 2);
+            fixup(gp + 2);
+        }
+        const int buf = (gp - gpf) & 1;
+        cd *rtile = rt + buf * (2 * DR2_CR + 1) * n3;
+        const bool pin = gp >= 0 && gp < L.n1;
+        const bool bot = gp == 0, top = gp == L.n1 - 1;
+        const cd *sp = slot(gp - 1), *s0 = slot(gp), *sn = slot(gp + 1);
+        const int nbx = (int)bot + (int)top;
+#pragma unroll
+        for (int t = 0; t < DR2_RPT; t++) {
+            const int e = tid + DR2_NT * t;
+            if (e >= nrp) continue;
+            cd rv = mk(0, 0);
+            if (pin) {
+                const int c = rc[t], f = rf[t];
+                const int ym = (f & 1) ? c + n3 : c - n3, yp = (f & 2) ? c - n3 : c + n3;
+                const int zm = (f & 4) ? c + 1 : c - 1, zp = (f & 8) ? c - 1 : c + 1;
+                const int nb = nbx + (f >> 4);
+                cd fc = s0[c];
+                cd xm = bot ? sn[c] : sp[c], xp = top ? sp[c] : sn[c];
+                cd vym = s0[ym], vyp = s0[yp], vzm = s0[zm], vzp = s0[zp];
+                const long long q = (long long)(gp - L.lo1) * plane + (long long)blo * n3 + c;
+                cd post = wd0;
+                cd bc;
+                if (KVAR) {
+                    post = mk(omega, 0.0);
+                    bc = fc;
+                    const cd *dv = L.dinv + q;
+                    const long long dxm = bot ? plane : -(long long)plane;
+                    const long long dxp = top ? -(long long)plane : plane;
+                    fc = cmul(fc, __ldg(dv));
+                    xm = cmul(xm, __ldg(dv + dxm));
+                    xp = cmul(xp, __ldg(dv + dxp));
+                    vym = cmul(vym, __ldg(dv + (ym - c)));
+                    vyp = cmul(vyp, __ldg(dv + (yp - c)));
+                    vzm = cmul(vzm, __ldg(dv + (zm - c)));
+                    vzp = cmul(vzp, __ldg(dv + (zp - c)));
+                } else {
+                    bc = nb ? __ldg(b + q) : fc;          // unscaled centre (face vertices rescaled)
+                }
+                const cd sum = cadd(cadd(cadd(xm, xp), cadd(vym, vyp)), cadd(vzm, vzp));
+                const cd ap = KVAR ? ap_of(L, __ldg(L.k + q), nb) : (nb == 0 ? ap0 : tab[nb]);
+                cd mf = cmul(ap, fc);
+                mf.x -= L.ih2 * sum.x;
+                mf.y -= L.ih2 * sum.y;
+                mf = cmul(post, mf);
+                if (!SOMM && nb) mf = cmul(post, fc);
+                rv = csub(bc, mf);
+            }
+            rtile[e] = rv;
+        }
+        __syncthreads();                             // residual tile complete; slot of gp-1 free
+        if (tid == 0 && gp + 4 <= stage_last) issue(gp + 4);
+        if (cact) fold(gp, partial(rtile));
+    }
+}
+
 // D^-1 over a level of a varying medium (owned + ghost planes), at setup
 __global__ void k_dinv(Lvl L, int g0, int g1, cd *__restrict__ out) {
     pdl_enter();
@@ -2141,6 +2374,13 @@ void init_kernel_attributes() {
     flat_attr<MODE_LOAD, EpiResid, 0>();
     flat_attr<MODE_LOAD, EpiJacobi, 0>();
     flat_attr<MODE_PRE, EpiResid, 0>();
+    {
+        const int b2 = DR2_RING * dr2_slot_elems(DR2_MAX_N3) * 16 + 2 * (2 * DR2_CR + 1) * DR2_MAX_N3 * 16 + 128;
+        cudaFuncSetAttribute(k_flat_dr<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b2);
+        cudaFuncSetAttribute(k_flat_dr<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b2);
+        cudaFuncSetAttribute(k_flat_dr<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b2);
+        cudaFuncSetAttribute(k_flat_dr<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b2);
+    }
     cudaFuncSetAttribute(k_down_restrict<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DRSmem<true>));
     cudaFuncSetAttribute(k_down_restrict<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DRSmem<true>));
     cudaFuncSetAttribute(k_down_restrict<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DRSmem<false>));
@@ -2219,9 +2459,30 @@ static void dr_launch(const Lvl &F, const Lvl &C, const cd *b, cd *out, double o
     launch(k_down_restrict<KVAR, SOMM>, dim3(gx, gy, gz), dim3(DR_NT), sizeof(DRSmem<KVAR>), s, F, C,
            b, out, omega, chunk, done);
 }
+template <bool KVAR, bool SOMM>
+static void dr2_launch(const Lvl &F, const Lvl &C, const cd *b, cd *out, double omega, cudaStream_t s,
+                       const int *done) {
+    const int gx = (C.n2 + DR2_CR - 1) / DR2_CR;
+    int gz = std::max(1, std::min(C.nx, (148 * 2 + gx - 1) / gx));
+    const int chunk = (C.nx + gz - 1) / gz;
+    gz = (C.nx + chunk - 1) / chunk;
+    const size_t smem = (size_t)DR2_RING * dr2_slot_elems(F.n3) * 16 + (size_t)2 * (2 * DR2_CR + 1) * F.n3 * 16 + 128;
+    launch(k_flat_dr<KVAR, SOMM>, dim3(gx, gz), dim3(DR2_NT), smem, s, F, C, b, out, omega, chunk, done);
+}
+bool flat_dr_ok(const Lvl &F) { return F.n3 <= DR2_MAX_N3 && !std::getenv("HF_NO_FLAT_DR"); }
 void launch_down_restrict(const Lvl &F, const Lvl &C, const cd *b, cd *out, double omega,
                           cudaStream_t s, const int *done) {
     const bool somm = F.bc == HF_BC_SOMMERFELD;
+    if (flat_dr_ok(F)) {
+        if (F.k) {
+            if (somm) dr2_launch<true, true>(F, C, b, out, omega, s, done);
+            else dr2_launch<true, false>(F, C, b, out, omega, s, done);
+        } else {
+            if (somm) dr2_launch<false, true>(F, C, b, out, omega, s, done);
+            else dr2_launch<false, false>(F, C, b, out, omega, s, done);
+        }
+        return;
+    }
     if (F.k) {
         if (somm) dr_launch<true, true>(F, C, b, out, omega, s, done);
         else dr_launch<true, false>(F, C, b, out, omega, s, done);

@@ -25,6 +25,7 @@ void launch_restrict(const Lvl &F, const Lvl &C, const cd *r, cd *out, cudaStrea
 // b_coarse = R (b - M (w D^-1 b)): fused pre-smooth + residual + restriction
 void launch_down_restrict(const Lvl &F, const Lvl &C, const cd *b, cd *out, double omega,
                           cudaStream_t s, const int *done);
+bool flat_dr_ok(const Lvl &F);   // the flat fused kernel (k_flat_dr) covers this level
 void launch_prolong(const Lvl &F, const Lvl &C, const cd *e, cd *out, bool add, cudaStream_t s,
                     const int *done);
 // returns the number of kernels launched (1 fused, 2 split)

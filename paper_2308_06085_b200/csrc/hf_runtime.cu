@@ -642,8 +642,10 @@ static void v_cycle(hf_hierarchy *H, int li, const cd *b, cd *u, cudaStream_t s,
     if (li == (int)H->lev.size() - 1) { coarsest(H, b, u, s, done); return; }
     Level &nx = H->lev[li + 1];
     const bool fused = c.nu1 <= 1 && c.nu2 == 1;
-    // fused down + restriction: opt-in (HF_DR=1) until it beats the split pair
-    const bool split_dr = std::getenv("HF_DR") == nullptr || std::getenv("HF_NO_DR") != nullptr;
+    // fused down + restriction (k_flat_dr) where it applies; the tiled fused kernel
+    // (wider planes) is opt-in (HF_DR=1): slower than the split pair there
+    const bool split_dr = std::getenv("HF_NO_DR") != nullptr ||
+                          (!flat_dr_ok(lv.L) && std::getenv("HF_DR") == nullptr);
     if (c.nu1 == 1 && fused && !split_dr) {
         L1(launch_down_restrict(lv.L, nx.L, b, nx.b, c.omega, s, done));
     } else if (c.nu1 == 1 && fused) {

@@ -132,10 +132,14 @@ def test_fused_up_matches_split(hf, dims, bc, kind, mg, monkeypatch):
     ((65, 49, 33), "dirichlet", "field"),
     ((33, 17, 65), "sommerfeld", "field"),
 ])
-def test_fused_down_restrict_matches_split(hf, dims, bc, kind, monkeypatch):
-    """Pre-smoothing + residual + full weighting in one kernel
-    (k_down_restrict) matches the split down1 + restriction kernels on every
-    level of the cycle (same arithmetic; only FMA contraction may differ)."""
+@pytest.mark.parametrize("variant", ["flat", "tiled"])
+def test_fused_down_restrict_matches_split(hf, dims, bc, kind, variant, monkeypatch):
+    """Pre-smoothing + residual + full weighting in one kernel (k_flat_dr, or
+    the tiled k_down_restrict used on wide planes) matches the split down1 +
+    restriction kernels on every level of the cycle (same arithmetic; only
+    FMA contraction may differ)."""
+    if variant == "tiled":
+        monkeypatch.setenv("HF_NO_FLAT_DR", "1")
     from paper_2308_06085_b200.multigrid import MGConfig, build_hierarchy, mg_precondition
     from paper_2308_06085_b200.operators import Dirichlet, OperatorSpec, Sommerfeld
     grid = hf.make_grid(*dims, 1.0 / (dims[0] - 1))

@@ -878,7 +878,8 @@ __global__ void __launch_bounds__(DR2_NT, 2) k_flat_dr(Lvl L, Lvl C, const cd *_
     __shared__ cd tab[12];
     if (is_done(done)) return;
     const int tid = threadIdx.x;
-    const int n3 = L.n3, plane = (int)L.plane;
+    const int n3 = L.n3, plane = (int)L.plane, n1 = L.n1, n2 = L.n2, lo1 = L.lo1;
+    const double ih2 = L.ih2;
     const int cr0 = blockIdx.x * DR2_CR, cr1 = min(cr0 + DR2_CR, C.n2);
     const int c0 = blockIdx.y * chunk, c1 = min(c0 + chunk, C.nx);
     if (c0 >= c1) return;
@@ -929,8 +930,8 @@ __global__ void __launch_bounds__(DR2_NT, 2) k_flat_dr(Lvl L, Lvl C, const cd *_
         const int ee = e < nrp ? e : 0;
         const int rr = rlo + ee / n3, m = ee - (ee / n3) * n3;
         rc[t] = (rr - blo) * n3 + m;
-        const int fj = (rr == 0) + (rr == L.n2 - 1), fm = (m == 0) + (m == n3 - 1);
-        rf[t] = (rr == 0) | (rr == L.n2 - 1) << 1 | (m == 0) << 2 | (m == n3 - 1) << 3 | (fj + fm) << 4;
+        const int fj = (rr == 0) + (rr == n2 - 1), fm = (m == 0) + (m == n3 - 1);
+        rf[t] = (rr == 0) | (rr == n2 - 1) << 1 | (m == 0) << 2 | (m == n3 - 1) << 3 | (fj + fm) << 4;
     }
     // MODE_PRE rescale of face vertices in the slots (constant medium): own entries
     constexpr int NFE = ((2 * DR2_CR + 3) * DR2_MAX_N3 + DR2_NT - 1) / DR2_NT;
@@ -948,10 +949,20 @@ __global__ void __launch_bounds__(DR2_NT, 2) k_flat_dr(Lvl L, Lvl C, const cd *_
             fe |= (unsigned long long)v << (2 * t);
         }
     }
+    // entries with an in-plane face count of 1 or 2 (interior planes rescale only those)
+    unsigned long long fe_face = 0;
+    if (!KVAR) {
+#pragma unroll
+        for (int t = 0; t < NFE; t++) {
+            const unsigned v = (unsigned)(fe >> (2 * t)) & 3u;
+            if (v == 1u || v == 2u) fe_face = 1;
+        }
+    }
     auto fixup = [&](int gp) {
         if (KVAR) return;
         const int gm = gmirror(gp);
         const int nbx = (gm == 0) + (gm == L.n1 - 1);
+        if (nbx == 0 && !fe_face) return;
         cd *sl = slot(gp);
 #pragma unroll
         for (int t = 0; t < NFE; t++) {
@@ -964,10 +975,12 @@ __global__ void __launch_bounds__(DR2_NT, 2) k_flat_dr(Lvl L, Lvl C, const cd *_
             }
         }
     };
-    // coarse column of this thread
+    // coarse column of this thread: the LAST ncp threads (they carry one residual
+    // point fewer than the first ones), so the per-plane work is balanced
     const int ncp = (cr1 - cr0) * C.n3;
-    const bool cact = tid < ncp;
-    const int cj = cr0 + (cact ? tid / C.n3 : 0), cm = cact ? tid - (tid / C.n3) * C.n3 : 0;
+    const int ct = tid - (DR2_NT - ncp);
+    const bool cact = ct >= 0;
+    const int cj = cr0 + (cact ? ct / C.n3 : 0), cm = cact ? ct - (ct / C.n3) * C.n3 : 0;
     const int crow = 2 * cj - rlo;                              // residual tile row of fine 2 cj
     const bool rm_ok = 2 * cj - 1 >= 0, rp_ok = 2 * cj + 1 <= L.n2 - 1;
     const bool cm_ok = 2 * cm - 1 >= 0, cp_ok = 2 * cm + 1 <= n3 - 1;
@@ -1024,8 +1037,8 @@ __global__ void __launch_bounds__(DR2_NT, 2) k_flat_dr(Lvl L, Lvl C, const cd *_
         }
         const int buf = (gp - gpf) & 1;
         cd *rtile = rt + buf * (2 * DR2_CR + 1) * n3;
-        const bool pin = gp >= 0 && gp < L.n1;
-        const bool bot = gp == 0, top = gp == L.n1 - 1;
+        const bool pin = gp >= 0 && gp < n1;
+        const bool bot = gp == 0, top = gp == n1 - 1;
         const cd *sp = slot(gp - 1), *s0 = slot(gp), *sn = slot(gp + 1);
         const int nbx = (int)bot + (int)top;
 #pragma unroll
@@ -1041,7 +1054,7 @@ __global__ void __launch_bounds__(DR2_NT, 2) k_flat_dr(Lvl L, Lvl C, const cd *_
                 cd fc = s0[c];
                 cd xm = bot ? sn[c] : sp[c], xp = top ? sp[c] : sn[c];
                 cd vym = s0[ym], vyp = s0[yp], vzm = s0[zm], vzp = s0[zp];
-                const long long q = (long long)(gp - L.lo1) * plane + (long long)blo * n3 + c;
+                const long long q = (long long)(gp - lo1) * plane + (long long)blo * n3 + c;
                 cd post = wd0;
                 cd bc;
                 if (KVAR) {
@@ -1063,8 +1076,8 @@ __global__ void __launch_bounds__(DR2_NT, 2) k_flat_dr(Lvl L, Lvl C, const cd *_
                 const cd sum = cadd(cadd(cadd(xm, xp), cadd(vym, vyp)), cadd(vzm, vzp));
                 const cd ap = KVAR ? ap_of(L, __ldg(L.k + q), nb) : (nb == 0 ? ap0 : tab[nb]);
                 cd mf = cmul(ap, fc);
-                mf.x -= L.ih2 * sum.x;
-                mf.y -= L.ih2 * sum.y;
+                mf.x -= ih2 * sum.x;
+                mf.y -= ih2 * sum.y;
                 mf = cmul(post, mf);
                 if (!SOMM && nb) mf = cmul(post, fc);
                 rv = csub(bc, mf);

@@ -53,6 +53,18 @@ def _peaks():
         return 6650.0, "fallback"
 
 
+def _ncu_traffic(kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
+    kernel, from the committed ncu --set full summary (profiles/ncu_traffic.json,
+    written by tools/ncu_traffic.py); None when it was captured for another kernel."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            d = json.load(f)
+        return d["traffic_bytes_per_launch"] if d.get("kernel") == kernel else None
+    except Exception:
+        return None
+
+
 def _problem():
     from paper_2308_06085_b200 import problems
     p = problems.point_source_cube(N_GRID, K_WAVE, "sommerfeld")
@@ -218,7 +230,7 @@ def run_gpu(args):
     kd = kern[dom]
     roofline = {"bound": "hbm", "kernel": dom, "achieved": kd["gbs"], "peak": hbm,
                 "peak_kind": peak_kind, "unit": "GB/s", "frac": round(kd["gbs"] / hbm, 4),
-                "traffic": None, "algorithmic_bytes_per_launch": kd["bytes"],
+                "traffic": _ncu_traffic(dom), "algorithmic_bytes_per_launch": kd["bytes"],
                 "launch_ms": kd["ms"],
                 "kernels": {k_: {"gbs": v_["gbs"], "frac": round(v_["gbs"] / hbm, 4),
                                  "ms": v_["ms"], "share": v_["share"], "bound": v_["bound"],
@@ -350,19 +362,22 @@ def kernel_table(A, hier, n, t_iter_ms, reps=20):
     nt = -(-ncs // 64)
     sym_bytes = nt * (nt + 1) // 2 * 64 * 64 * 16 + 2 * nt * (nt + 1) // 2 * 64 * 16 * 2
     p = lambda x: x.data_ptr()
-    # on the solve path (2 launches each per Bi-CGSTAB iteration): matvec (+dot),
-    # down_restrict, up_jacobi; the split pieces are the C-ABI level entry points
+    # on the solve path (each launched twice per Bi-CGSTAB iteration, once per
+    # matvec / V-cycle): matvec (+dot), down_restrict (k_flat_dr), prolong_correct
+    # (k_corr) + jacobi_postsmooth (k_flat_stencil); the others are C-ABI level
+    # entry points (presmooth+residual and restriction split; the fused MODE_UP
+    # up-sweep used on planes wider than the flat kernels cover)
     cases = {
         "device_copy": (lambda: v.copy_(u), 32.0 * n, "ceiling"),   # practical ceiling, same buffers
         "helmholtz_matvec": (lambda: L.hf_operator_apply(A._h, p(u), p(v)), 32.0 * n, "solve"),
         "down_restrict": (lambda: L.hf_level_down_restrict(H, 0, p(b), p(bc)), 16.0 * n + 16.0 * nc_f,
                           "solve"),
-        "up_jacobi": (lambda: L.hf_level_up(H, 0, p(b), p(ec), p(u)), 32.0 * n + 16.0 * nc_f, "solve"),
+        "prolong_correct": (lambda: L.hf_level_correct(H, 0, p(b), p(ec), p(t)), 32.0 * n + 16.0 * nc_f,
+                            "solve"),
+        "jacobi_postsmooth": (lambda: L.hf_level_smooth(H, 0, p(t), p(b), p(u)), 48.0 * n, "solve"),
         "cslp_presmooth_residual": (lambda: L.hf_level_down1(H, 0, p(b), p(v)), 32.0 * n, "api"),
         "restrict_fw": (lambda: L.hf_restrict_fw(H, 0, p(v), p(bc)), 16.0 * n + 16.0 * nc_f, "api"),
-        "prolong_correct": (lambda: L.hf_level_correct(H, 0, p(b), p(ec), p(t)), 32.0 * n + 16.0 * nc_f,
-                            "api"),
-        "jacobi_postsmooth": (lambda: L.hf_level_smooth(H, 0, p(t), p(b), p(u)), 48.0 * n, "api"),
+        "level_up": (lambda: L.hf_level_up(H, 0, p(b), p(ec), p(u)), 32.0 * n + 16.0 * nc_f, "api"),
     }
     kind = hier.coarsest_kind
     # separable (fast diagonalisation): b, two scratch passes, 1/D and x -- a

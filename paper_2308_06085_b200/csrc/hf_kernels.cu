@@ -748,60 +748,67 @@ __global__ void __launch_bounds__(256, 3) k_flat_stencil(Lvl L, const cd *__rest
         }
         __syncthreads();
     }
-    cd P[2], C[2];
+    // plane values rotate through three register sets (prev / cur / next) with a
+    // 3-way unrolled march, so no moves are spent on the rotation
+    struct PV {
+        cd v[2];      // staged value at the two points
+        double k[2];  // wavenumber (varying medium)
+    };
+    PV S0, S1, S2;
     {
         const cd *sp = slot(i0 - 1), *sc = slot(i0);
-        P[0] = sp[oc[0]]; P[1] = sp[oc[1]];
-        C[0] = sc[oc[0]]; C[1] = sc[oc[1]];
+        S0.v[0] = sp[oc[0]]; S0.v[1] = sp[oc[1]];
+        S1.v[0] = sc[oc[0]]; S1.v[1] = sc[oc[1]];
     }
     cd acc[2] = {mk(0, 0), mk(0, 0)};
-    long long q = (long long)i0 * plane + f0 + tid;
-    cd av[2] = {mk(0, 0), mk(0, 0)};
-    double kv[2] = {L.kc, L.kc};
+    long long q = (long long)i0 * plane + f0;      // plane origin of the block
+    // point offsets; inactive points (past the plane end) use the block's first
+    // vertex for their (unused) loads and skip the epilogue
+    const int qo0 = act[0] ? tid : 0, qo1 = act[1] ? tid + 256 : 0;
 #pragma unroll
     for (int k = 0; k < 2; k++) {
-        if (Epi::kAux && act[k]) av[k] = __ldg(aux + q + 256 * k);
-        if (KVAR && act[k]) kv[k] = __ldg(L.k + q + 256 * k);
+        S1.k[k] = L.kc;
+        if (KVAR) S1.k[k] = __ldg(L.k + q + (k ? qo1 : qo0));
     }
-    for (int i = i0; i < i1; i++) {
+    auto step = [&](int i, PV &P, PV &C, PV &N) {
         const int gi = L.lo1 + i;
         const bool top = gi == L.n1 - 1, bot = gi == 0;
+        // centre epilogue operand of this plane, issued before the waits
+        cd ca[2] = {mk(0, 0), mk(0, 0)};
+        if (Epi::kAux) {
+            ca[0] = __ldg(aux + q + qo0);
+            ca[1] = __ldg(aux + q + qo1);
+        }
         __syncthreads();                             // slot of plane i-1 is free
         if (tid == 0 && i + FS_RING - 1 <= last) issue(i + FS_RING - 1);
         if (kFix && i + 2 <= last) {     // visible after the next barrier
             wait_plane(i + 2);
             fixup(i + 2);
         }
-        cd N[2];
         if (!top) {
             wait_plane(i + 1);
             const cd *sn = slot(i + 1);
-            N[0] = sn[oc[0]]; N[1] = sn[oc[1]];
+            N.v[0] = sn[oc[0]]; N.v[1] = sn[oc[1]];
         } else {
-            N[0] = P[0]; N[1] = P[1];                // mirrored plane n1-2
+            N.v[0] = P.v[0]; N.v[1] = P.v[1];        // mirrored plane n1-2
+        }
+        if (KVAR && i + 1 < i1) {
+#pragma unroll
+            for (int k = 0; k < 2; k++) N.k[k] = __ldg(L.k + q + plane + (k ? qo1 : qo0));
         }
         const cd *s0 = slot(i);
-        cd an[2] = {av[0], av[1]};
-        double kn[2] = {kv[0], kv[1]};
-        if (i + 1 < i1) {
-#pragma unroll
-            for (int k = 0; k < 2; k++) {
-                if (Epi::kAux && act[k]) an[k] = __ldg(aux + q + plane + 256 * k);
-                if (KVAR && act[k]) kn[k] = __ldg(L.k + q + plane + 256 * k);
-            }
-        }
         const int nbx = (int)bot + (int)top;
 #pragma unroll
         for (int k = 0; k < 2; k++) {
-            if (!act[k]) continue;
-            cd fc = C[k], xm = bot ? N[k] : P[k], xp = N[k];
+            const long long qk = q + (k ? qo1 : qo0);
+            cd fc = C.v[k], xm = bot ? N.v[k] : P.v[k], xp = N.v[k];
             cd ym = s0[oym[k]], yp = s0[oyp[k]], zm = s0[ozm[k]], zp = s0[ozp[k]];
             const int nb = nbx + nbjm[k];
             cd post = mk(1.0, 0.0);
             if (MODE == MODE_PRE) {
                 if (KVAR) {          // f = D^-1 b per vertex, w applied after M
                     post = mk(omega, 0.0);
-                    const cd *dv = L.dinv + q + 256 * k;
+                    const cd *dv = L.dinv + qk;
                     const long long dxm = bot ? plane : -(long long)plane;
                     const long long dxp = top ? -(long long)plane : plane;
                     fc = cmul(fc, __ldg(dv));
@@ -816,25 +823,26 @@ __global__ void __launch_bounds__(256, 3) k_flat_stencil(Lvl L, const cd *__rest
                 }
             }
             const cd sum = cadd(cadd(cadd(xm, xp), cadd(ym, yp)), cadd(zm, zp));
-            const cd ap = KVAR ? ap_of(L, kv[k], nb) : (nb == 0 ? apc : tab[nb]);
+            const cd ap = KVAR ? ap_of(L, C.k[k], nb) : (nb == 0 ? apc : tab[nb]);
             cd mf = cmul(ap, fc);
             mf.x -= L.ih2 * sum.x;
             mf.y -= L.ih2 * sum.y;
             if (MODE == MODE_PRE) mf = cmul(post, mf);
             if (!SOMM && nb) mf = (MODE == MODE_PRE) ? cmul(post, fc) : fc;
             cd wd = mk(0, 0);
-            if (Epi::kDinv) wd = KVAR ? cscal(__ldg(L.dinv + q + 256 * k), omega) : tab[4 + nb];
-            epi(q + 256 * k, fc, mf, wd, av[k], acc);
-        }
-#pragma unroll
-        for (int k = 0; k < 2; k++) {
-            P[k] = C[k];
-            C[k] = N[k];
-            av[k] = an[k];
-            kv[k] = kn[k];
+            if (Epi::kDinv) wd = KVAR ? cscal(__ldg(L.dinv + qk), omega) : tab[4 + nb];
+            if (act[k]) epi(qk, fc, mf, wd, ca[k], acc);
         }
         q += plane;
+    };
+    int i = i0;
+    for (; i + 3 <= i1; i += 3) {
+        step(i, S0, S1, S2);
+        step(i + 1, S1, S2, S0);
+        step(i + 2, S2, S0, S1);
     }
+    if (i < i1) step(i, S0, S1, S2);
+    if (i + 1 < i1) step(i + 1, S1, S2, S0);
     constexpr int NR = (ND > 0) ? ND : 1;
     if (ND > 0) {
         cd a2[NR];

@@ -877,7 +877,7 @@ __global__ void __launch_bounds__(256, 3) k_flat_stencil(Lvl L, const cd *__rest
 
 __host__ __device__ __forceinline__ int dr2_slot_elems(int n3) { return ((2 * DR2_CR + 3) * n3 + 7) / 8 * 8; }
 
-template <bool KVAR, bool SOMM>
+template <bool KVAR, bool SOMM, int RPT>
 __global__ void __launch_bounds__(DR2_NT, 2) k_flat_dr(Lvl L, Lvl C, const cd *__restrict__ b,
                                                        cd *__restrict__ out, double omega, int chunk,
                                                        const int *done) {
@@ -931,9 +931,9 @@ __global__ void __launch_bounds__(DR2_NT, 2) k_flat_dr(Lvl L, Lvl C, const cd *_
     // residual points of this thread: slot offset of the centre + packed flags
     // (bit0 row mirror below, bit1 row mirror above, bit2 col mirror left,
     //  bit3 col mirror right, bits 4-5 in-plane face count)
-    int rc[DR2_RPT], rf[DR2_RPT];
+    int rc[RPT], rf[RPT];
 #pragma unroll
-    for (int t = 0; t < DR2_RPT; t++) {
+    for (int t = 0; t < RPT; t++) {
         const int e = tid + DR2_NT * t;
         const int ee = e < nrp ? e : 0;
         const int rr = rlo + ee / n3, m = ee - (ee / n3) * n3;
@@ -1037,7 +1037,21 @@ __global__ void __launch_bounds__(DR2_NT, 2) k_flat_dr(Lvl L, Lvl C, const cd *_
     __syncthreads();
     const cd ap0 = KVAR ? mk(0, 0) : tab[0];
     const cd wd0 = KVAR ? mk(0, 0) : tab[4];
-    for (int gp = gpf; gp <= gpl; gp++) {
+    // centre values of the residual points rotate through three register sets
+    // (planes gp-1, gp, gp+1) with a 3-way unrolled march
+    struct RV {
+        cd v[RPT];
+    };
+    RV S0, S1, S2;
+    {
+        const cd *sp = slot(gpf - 1), *sc = slot(gpf);
+#pragma unroll
+        for (int t = 0; t < RPT; t++) {
+            S0.v[t] = sp[rc[t]];
+            S1.v[t] = sc[rc[t]];
+        }
+    }
+    auto step = [&](int gp, RV &P, RV &Cv, RV &N) {
         if (gp + 1 <= stage_last) wait_plane(gp + 1);
         if (!KVAR && gp + 2 <= stage_last) {        // rescale plane gp+2 (visible after the barrier)
             wait_plane(gp + 2);
@@ -1047,10 +1061,18 @@ __global__ void __launch_bounds__(DR2_NT, 2) k_flat_dr(Lvl L, Lvl C, const cd *_
         cd *rtile = rt + buf * (2 * DR2_CR + 1) * n3;
         const bool pin = gp >= 0 && gp < n1;
         const bool bot = gp == 0, top = gp == n1 - 1;
-        const cd *sp = slot(gp - 1), *s0 = slot(gp), *sn = slot(gp + 1);
+        const cd *s0 = slot(gp);
+        if (!top && gp + 1 <= stage_last) {
+            const cd *sn = slot(gp + 1);
+#pragma unroll
+            for (int t = 0; t < RPT; t++) N.v[t] = sn[rc[t]];
+        } else {
+#pragma unroll
+            for (int t = 0; t < RPT; t++) N.v[t] = P.v[t];   // mirrored plane n1-2
+        }
         const int nbx = (int)bot + (int)top;
 #pragma unroll
-        for (int t = 0; t < DR2_RPT; t++) {
+        for (int t = 0; t < RPT; t++) {
             const int e = tid + DR2_NT * t;
             if (e >= nrp) continue;
             cd rv = mk(0, 0);
@@ -1059,13 +1081,13 @@ __global__ void __launch_bounds__(DR2_NT, 2) k_flat_dr(Lvl L, Lvl C, const cd *_
                 const int ym = (f & 1) ? c + n3 : c - n3, yp = (f & 2) ? c - n3 : c + n3;
                 const int zm = (f & 4) ? c + 1 : c - 1, zp = (f & 8) ? c - 1 : c + 1;
                 const int nb = nbx + (f >> 4);
-                cd fc = s0[c];
-                cd xm = bot ? sn[c] : sp[c], xp = top ? sp[c] : sn[c];
+                cd fc = Cv.v[t];
+                cd xm = bot ? N.v[t] : P.v[t], xp = top ? P.v[t] : N.v[t];
                 cd vym = s0[ym], vyp = s0[yp], vzm = s0[zm], vzp = s0[zp];
-                const long long q = (long long)(gp - lo1) * plane + (long long)blo * n3 + c;
                 cd post = wd0;
                 cd bc;
                 if (KVAR) {
+                    const long long q = (long long)(gp - lo1) * plane + (long long)blo * n3 + c;
                     post = mk(omega, 0.0);
                     bc = fc;
                     const cd *dv = L.dinv + q;
@@ -1078,11 +1100,15 @@ __global__ void __launch_bounds__(DR2_NT, 2) k_flat_dr(Lvl L, Lvl C, const cd *_
                     vyp = cmul(vyp, __ldg(dv + (yp - c)));
                     vzm = cmul(vzm, __ldg(dv + (zm - c)));
                     vzp = cmul(vzp, __ldg(dv + (zp - c)));
+                } else if (nb) {                          // face vertex: unscaled centre
+                    bc = __ldg(b + (long long)(gp - lo1) * plane + (long long)blo * n3 + c);
                 } else {
-                    bc = nb ? __ldg(b + q) : fc;          // unscaled centre (face vertices rescaled)
+                    bc = fc;
                 }
                 const cd sum = cadd(cadd(cadd(xm, xp), cadd(vym, vyp)), cadd(vzm, vzp));
-                const cd ap = KVAR ? ap_of(L, __ldg(L.k + q), nb) : (nb == 0 ? ap0 : tab[nb]);
+                const cd ap = KVAR ? ap_of(L, __ldg(L.k + (long long)(gp - lo1) * plane +
+                                                    (long long)blo * n3 + c), nb)
+                                   : (nb == 0 ? ap0 : tab[nb]);
                 cd mf = cmul(ap, fc);
                 mf.x -= ih2 * sum.x;
                 mf.y -= ih2 * sum.y;
@@ -1092,10 +1118,21 @@ __global__ void __launch_bounds__(DR2_NT, 2) k_flat_dr(Lvl L, Lvl C, const cd *_
             }
             rtile[e] = rv;
         }
-        __syncthreads();                             // residual tile complete; slot of gp-1 free
+        // the previous plane's residual tile is complete (last barrier): fold it
+        // while the other warps still form this plane's tile
+        if (cact && gp > gpf) fold(gp - 1, partial(rt + (buf ^ 1) * (2 * DR2_CR + 1) * n3));
+        __syncthreads();                             // tile complete; slot of gp-1 free
         if (tid == 0 && gp + 4 <= stage_last) issue(gp + 4);
-        if (cact) fold(gp, partial(rtile));
+    };
+    int gp = gpf;
+    for (; gp + 3 <= gpl + 1; gp += 3) {
+        step(gp, S0, S1, S2);
+        step(gp + 1, S1, S2, S0);
+        step(gp + 2, S2, S0, S1);
     }
+    if (gp <= gpl) step(gp, S0, S1, S2);
+    if (gp + 1 <= gpl) step(gp + 1, S1, S2, S0);
+    if (cact) fold(gpl, partial(rt + ((gpl - gpf) & 1) * (2 * DR2_CR + 1) * n3));
 }
 
 // D^-1 over a level of a varying medium (owned + ghost planes), at setup
@@ -2397,10 +2434,14 @@ void init_kernel_attributes() {
     flat_attr<MODE_PRE, EpiResid, 0>();
     {
         const int b2 = DR2_RING * dr2_slot_elems(DR2_MAX_N3) * 16 + 2 * (2 * DR2_CR + 1) * DR2_MAX_N3 * 16 + 128;
-        cudaFuncSetAttribute(k_flat_dr<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b2);
-        cudaFuncSetAttribute(k_flat_dr<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b2);
-        cudaFuncSetAttribute(k_flat_dr<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b2);
-        cudaFuncSetAttribute(k_flat_dr<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b2);
+        cudaFuncSetAttribute(k_flat_dr<true, true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, b2);
+        cudaFuncSetAttribute(k_flat_dr<true, false, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, b2);
+        cudaFuncSetAttribute(k_flat_dr<false, true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, b2);
+        cudaFuncSetAttribute(k_flat_dr<false, false, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, b2);
+        cudaFuncSetAttribute(k_flat_dr<true, true, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, b2);
+        cudaFuncSetAttribute(k_flat_dr<true, false, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, b2);
+        cudaFuncSetAttribute(k_flat_dr<false, true, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, b2);
+        cudaFuncSetAttribute(k_flat_dr<false, false, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, b2);
     }
     cudaFuncSetAttribute(k_down_restrict<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DRSmem<true>));
     cudaFuncSetAttribute(k_down_restrict<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DRSmem<true>));
@@ -2480,7 +2521,7 @@ static void dr_launch(const Lvl &F, const Lvl &C, const cd *b, cd *out, double o
     launch(k_down_restrict<KVAR, SOMM>, dim3(gx, gy, gz), dim3(DR_NT), sizeof(DRSmem<KVAR>), s, F, C,
            b, out, omega, chunk, done);
 }
-template <bool KVAR, bool SOMM>
+template <bool KVAR, bool SOMM, int RPT>
 static void dr2_launch(const Lvl &F, const Lvl &C, const cd *b, cd *out, double omega, cudaStream_t s,
                        const int *done) {
     const int gx = (C.n2 + DR2_CR - 1) / DR2_CR;
@@ -2488,19 +2529,25 @@ static void dr2_launch(const Lvl &F, const Lvl &C, const cd *b, cd *out, double 
     const int chunk = (C.nx + gz - 1) / gz;
     gz = (C.nx + chunk - 1) / chunk;
     const size_t smem = (size_t)DR2_RING * dr2_slot_elems(F.n3) * 16 + (size_t)2 * (2 * DR2_CR + 1) * F.n3 * 16 + 128;
-    launch(k_flat_dr<KVAR, SOMM>, dim3(gx, gz), dim3(DR2_NT), smem, s, F, C, b, out, omega, chunk, done);
+    launch(k_flat_dr<KVAR, SOMM, RPT>, dim3(gx, gz), dim3(DR2_NT), smem, s, F, C, b, out, omega, chunk, done);
 }
 bool flat_dr_ok(const Lvl &F) { return F.n3 <= DR2_MAX_N3 && !std::getenv("HF_NO_FLAT_DR"); }
 void launch_down_restrict(const Lvl &F, const Lvl &C, const cd *b, cd *out, double omega,
                           cudaStream_t s, const int *done) {
     const bool somm = F.bc == HF_BC_SOMMERFELD;
     if (flat_dr_ok(F)) {
+        // residual points per thread: (2 CR + 1) n3 / 256 -> 3 up to n3 = 153, else 5
+        const bool r3 = (2 * DR2_CR + 1) * F.n3 <= 3 * DR2_NT;
         if (F.k) {
-            if (somm) dr2_launch<true, true>(F, C, b, out, omega, s, done);
-            else dr2_launch<true, false>(F, C, b, out, omega, s, done);
+            if (somm) r3 ? dr2_launch<true, true, 3>(F, C, b, out, omega, s, done)
+                         : dr2_launch<true, true, 5>(F, C, b, out, omega, s, done);
+            else r3 ? dr2_launch<true, false, 3>(F, C, b, out, omega, s, done)
+                    : dr2_launch<true, false, 5>(F, C, b, out, omega, s, done);
         } else {
-            if (somm) dr2_launch<false, true>(F, C, b, out, omega, s, done);
-            else dr2_launch<false, false>(F, C, b, out, omega, s, done);
+            if (somm) r3 ? dr2_launch<false, true, 3>(F, C, b, out, omega, s, done)
+                         : dr2_launch<false, true, 5>(F, C, b, out, omega, s, done);
+            else r3 ? dr2_launch<false, false, 3>(F, C, b, out, omega, s, done)
+                    : dr2_launch<false, false, 5>(F, C, b, out, omega, s, done);
         }
         return;
     }

@@ -914,7 +914,7 @@ __global__ void __launch_bounds__(DR2_NT, 2) k_flat_dr(Lvl L, Lvl C, const cd *_
         const int d = gp - gpf + 1;
         mbar_wait(bbase + 8 * (d % DR2_RING), (d / DR2_RING) & 1);
     };
-    auto slot = [&](int gp) { return sgen + ((gp - gpf + 1) % DR2_RING) * selems; };
+    auto slot = [&](int gp) { return sgen + ((unsigned)(gp - gpf + 1) % DR2_RING) * selems; };
     if (tid == 0) {
         for (int k = 0; k < DR2_RING; k++) mbar_init(bbase + 8 * k, 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -1051,7 +1051,10 @@ __global__ void __launch_bounds__(DR2_NT, 2) k_flat_dr(Lvl L, Lvl C, const cd *_
             S1.v[t] = sc[rc[t]];
         }
     }
-    auto step = [&](int gp, RV &P, RV &Cv, RV &N) {
+    // one fine plane; EDGE: a face plane or a plane outside the grid (mirrors,
+    // zero residual) -- the interior planes take a select-free body
+    auto step = [&](auto EDGEc, int gp, RV &P, RV &Cv, RV &N) {
+        constexpr bool EDGE = decltype(EDGEc)::value;
         if (gp + 1 <= stage_last) wait_plane(gp + 1);
         if (!KVAR && gp + 2 <= stage_last) {        // rescale plane gp+2 (visible after the barrier)
             wait_plane(gp + 2);
@@ -1059,8 +1062,8 @@ __global__ void __launch_bounds__(DR2_NT, 2) k_flat_dr(Lvl L, Lvl C, const cd *_
         }
         const int buf = (gp - gpf) & 1;
         cd *rtile = rt + buf * (2 * DR2_CR + 1) * n3;
-        const bool pin = gp >= 0 && gp < n1;
-        const bool bot = gp == 0, top = gp == n1 - 1;
+        const bool pin = !EDGE || (gp >= 0 && gp < n1);
+        const bool bot = EDGE && gp == 0, top = EDGE && gp == n1 - 1;
         const cd *s0 = slot(gp);
         if (!top && gp + 1 <= stage_last) {
             const cd *sn = slot(gp + 1);
@@ -1082,7 +1085,11 @@ __global__ void __launch_bounds__(DR2_NT, 2) k_flat_dr(Lvl L, Lvl C, const cd *_
                 const int zm = (f & 4) ? c + 1 : c - 1, zp = (f & 8) ? c - 1 : c + 1;
                 const int nb = nbx + (f >> 4);
                 cd fc = Cv.v[t];
-                cd xm = bot ? N.v[t] : P.v[t], xp = top ? P.v[t] : N.v[t];
+                cd xm = P.v[t], xp = N.v[t];
+                if (EDGE) {
+                    if (bot) xm = N.v[t];
+                    if (top) xp = P.v[t];
+                }
                 cd vym = s0[ym], vyp = s0[yp], vzm = s0[zm], vzp = s0[zp];
                 cd post = wd0;
                 cd bc;
@@ -1124,14 +1131,18 @@ __global__ void __launch_bounds__(DR2_NT, 2) k_flat_dr(Lvl L, Lvl C, const cd *_
         __syncthreads();                             // tile complete; slot of gp-1 free
         if (tid == 0 && gp + 4 <= stage_last) issue(gp + 4);
     };
+    auto run = [&](int gp, RV &P, RV &Cv, RV &N) {
+        if (gp <= 0 || gp >= n1 - 1) step(IC<1>{}, gp, P, Cv, N);
+        else step(IC<0>{}, gp, P, Cv, N);
+    };
     int gp = gpf;
     for (; gp + 3 <= gpl + 1; gp += 3) {
-        step(gp, S0, S1, S2);
-        step(gp + 1, S1, S2, S0);
-        step(gp + 2, S2, S0, S1);
+        run(gp, S0, S1, S2);
+        run(gp + 1, S1, S2, S0);
+        run(gp + 2, S2, S0, S1);
     }
-    if (gp <= gpl) step(gp, S0, S1, S2);
-    if (gp + 1 <= gpl) step(gp + 1, S1, S2, S0);
+    if (gp <= gpl) run(gp, S0, S1, S2);
+    if (gp + 1 <= gpl) run(gp + 1, S1, S2, S0);
     if (cact) fold(gpl, partial(rt + ((gpl - gpf) & 1) * (2 * DR2_CR + 1) * n3));
 }
 

@@ -1167,6 +1167,10 @@ __global__ void k_dinv(Lvl L, int g0, int g1, cd *__restrict__ out) {
 // sum of each coarse plane is formed once and reused by the two fine planes
 // that straddle it.
 template <int MODE>
+__device__ __forceinline__ void corr_col(const Lvl &F, const Lvl &C, const cd *__restrict__ b,
+                                         const cd *__restrict__ e, cd *__restrict__ out,
+                                         double omega, int j, int m, int i0, int i1);
+template <int MODE>
 __device__ __forceinline__ void corr_body(const Lvl &F, const Lvl &C, const cd *__restrict__ b,
                                           const cd *__restrict__ e, cd *__restrict__ out,
                                           double omega, int chunk, int tid, int bx, int by,
@@ -1175,6 +1179,13 @@ __device__ __forceinline__ void corr_body(const Lvl &F, const Lvl &C, const cd *
     const int j = by * 8 + (tid >> 5);
     const int i0 = bz * chunk, i1 = min(i0 + chunk, F.nx);
     if (m >= F.n3 || j >= F.n2) return;
+    corr_col<MODE>(F, C, b, e, out, omega, j, m, i0, i1);
+}
+// one fine (i2, i3) column over local planes [i0, i1)
+template <int MODE>
+__device__ __forceinline__ void corr_col(const Lvl &F, const Lvl &C, const cd *__restrict__ b,
+                                         const cd *__restrict__ e, cd *__restrict__ out,
+                                         double omega, int j, int m, int i0, int i1) {
     const bool o2 = j & 1, o3 = m & 1;
     const cd *ecol = e + (j >> 1) * C.n3 + (m >> 1);
     auto cplane = [&](int c) -> cd {                 // bilinear sum on coarse local plane c
@@ -1216,6 +1227,19 @@ __device__ __forceinline__ void corr_body(const Lvl &F, const Lvl &C, const cd *
         if (MODE == 2) pe = cadd(out[q], pe);
         out[q] = pe;
     }
+}
+
+// flat variant: thread = one fine (i2, i3) vertex of the plane (no ragged tiles)
+template <int MODE>
+__global__ void __launch_bounds__(256) k_corr_flat(Lvl F, Lvl C, const cd *__restrict__ b,
+                                                   const cd *__restrict__ e, cd *__restrict__ out,
+                                                   double omega, int chunk, const int *done) {
+    if (is_done(done)) return;
+    const int f = blockIdx.x * 256 + threadIdx.x;
+    if (f >= (int)F.plane) return;
+    const int j = f / F.n3, m = f - j * F.n3;
+    const int i0 = blockIdx.y * chunk, i1 = min(i0 + chunk, F.nx);
+    corr_col<MODE>(F, C, b, e, out, omega, j, m, i0, i1);
 }
 
 template <int MODE>
@@ -2466,7 +2490,8 @@ void init_kernel_attributes() {
 int tile_blocks(const Lvl &L) {
     int chunk;
     dim3 g = tile_grid(L, chunk);
-    return g.x * g.y * g.z;
+    const int gx = (int)((L.plane + FS_PTS - 1) / FS_PTS);   // k_flat_stencil grid (flat_launch_t)
+    return std::max<int>(g.x * g.y * g.z, gx * L.nx);
 }
 
 void launch_apply(const Lvl &L, const cd *u, cd *v, cudaStream_t s, const int *done) {
@@ -2497,6 +2522,13 @@ static void corr(int mode, const Lvl &F, const Lvl &C, const cd *b, const cd *e,
     // two fine planes per thread: every load of the pair is independent (latency-bound
     // kernel, so parallelism beats the coarse-plane reuse of longer marches)
     const int chunk = 2;
+    if (!std::getenv("HF_NO_FLAT")) {   // flat thread mapping (no ragged 32 x 8 tiles)
+        dim3 gf((unsigned)((F.plane + 255) / 256), (F.nx + chunk - 1) / chunk);
+        if (mode == 0) launch(k_corr_flat<0>, gf, dim3(256), 0, s, F, C, b, e, out, omega, chunk, done);
+        else if (mode == 1) launch(k_corr_flat<1>, gf, dim3(256), 0, s, F, C, b, e, out, omega, chunk, done);
+        else launch(k_corr_flat<2>, gf, dim3(256), 0, s, F, C, b, e, out, omega, chunk, done);
+        return;
+    }
     dim3 g((F.n3 + 31) / 32, (F.n2 + 7) / 8, (F.nx + chunk - 1) / chunk);
     if (mode == 0) launch(k_corr<0>, dim3(g), dim3(256), 0, s, F, C, b, e, out, omega, chunk, done);
     else if (mode == 1) launch(k_corr<1>, dim3(g), dim3(256), 0, s, F, C, b, e, out, omega, chunk, done);

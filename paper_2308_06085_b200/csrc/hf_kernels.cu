@@ -871,7 +871,7 @@ __global__ void __launch_bounds__(256, 3) k_flat_stencil(Lvl L, const cd *__rest
 // ---------------------------------------------------------------------------
 #define DR2_CR 2
 #define DR2_NT 256
-#define DR2_RING 5
+#define DR2_RING 6
 #define DR2_RPT 5            // residual points per thread: (2 CR + 1) rows x n3 <= 5 x 255
 #define DR2_MAX_N3 255
 
@@ -1129,7 +1129,7 @@ __global__ void __launch_bounds__(DR2_NT, 2) k_flat_dr(Lvl L, Lvl C, const cd *_
         // while the other warps still form this plane's tile
         if (cact && gp > gpf) fold(gp - 1, partial(rt + (buf ^ 1) * (2 * DR2_CR + 1) * n3));
         __syncthreads();                             // tile complete; slot of gp-1 free
-        if (tid == 0 && gp + 4 <= stage_last) issue(gp + 4);
+        if (tid == 0 && gp + DR2_RING - 1 <= stage_last) issue(gp + DR2_RING - 1);
     };
     auto run = [&](int gp, RV &P, RV &Cv, RV &N) {
         if (gp <= 0 || gp >= n1 - 1) step(IC<1>{}, gp, P, Cv, N);

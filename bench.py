@@ -140,7 +140,7 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def _event_time(fn, reps, stream=None):
+def _event_time(fn, reps):
     import torch
     s = torch.cuda.Event(enable_timing=True)
     e = torch.cuda.Event(enable_timing=True)
@@ -224,7 +224,7 @@ def run_gpu(args):
 
     # ---- kernel roofline: live CUDA-event timing of the hot kernels ----
     hbm, peak_kind = _peaks()
-    kern = kernel_table(A, hier, n, ms_step / max(iters, 1))
+    kern = kernel_table(A, hier, n, ms_step / max(iters, 1), solver=solver)
     dom = max((k_ for k_ in kern if kern[k_]["bound"] == "hbm" and kern[k_]["role"] == "solve"),
               key=lambda k_: kern[k_]["share"])
     kd = kern[dom]
@@ -338,10 +338,14 @@ def run_slabs(args):
     dist.destroy_process_group()
 
 
-def kernel_table(A, hier, n, t_iter_ms, reps=20):
-    """Live CUDA-event timing of the path's kernels on the finest level (the
-    solve launches each of them twice per Bi-CGSTAB iteration).  Bytes are the
-    algorithmic traffic of one launch (constant medium: no k traffic)."""
+def kernel_table(A, hier, n, t_iter_ms, reps=20, solver=None):
+    """Live CUDA-event timing of the path's kernels on the finest level.  The
+    129^3 fields are 34 MB (L2 is 126 MB), so consecutive launches rotate over
+    NSET independent operand sets (> 2x L2 in total): every launch streams its
+    operands from HBM, back to back as in the solve.  The Bi-CGSTAB vector
+    kernels run back to back on the solver's own workspace.  Bytes are the
+    algorithmic traffic of one launch (constant medium: no k traffic);
+    share = launches per Bi-CGSTAB iteration x ms / iteration time."""
     import ctypes
 
     import torch
@@ -350,11 +354,12 @@ def kernel_table(A, hier, n, t_iter_ms, reps=20):
 
     L = _native.load()
     _native.set_stream_from_torch()
+    NSET = 4
     shape = hier.levels[0].extent.shape
     cshape = hier.levels[1].extent.shape
     rnd = lambda sh: torch.randn(sh, dtype=torch.complex128, device="cuda")
-    u, b, v, t = rnd(shape), rnd(shape), rnd(shape), rnd(shape)
-    ec, bc = rnd(cshape), rnd(cshape)
+    sets = [dict(u=rnd(shape), b=rnd(shape), v=rnd(shape), t=rnd(shape), ec=rnd(cshape), bc=rnd(cshape))
+            for _ in range(NSET)]
     H = hier._h
     nc_f = cshape[0] * cshape[1] * cshape[2]
     ncs = hier.coarsest.grid.num_vertices
@@ -364,36 +369,57 @@ def kernel_table(A, hier, n, t_iter_ms, reps=20):
     p = lambda x: x.data_ptr()
     # on the solve path (each launched twice per Bi-CGSTAB iteration, once per
     # matvec / V-cycle): matvec (+dot), down_restrict (k_flat_dr), prolong_correct
-    # (k_corr) + jacobi_postsmooth (k_flat_stencil); the others are C-ABI level
-    # entry points (presmooth+residual and restriction split; the fused MODE_UP
-    # up-sweep used on planes wider than the flat kernels cover)
+    # (k_corr) + jacobi_postsmooth (k_flat_stencil); "api" = C-ABI level entry
+    # points not on the 129^3 solve path (split presmooth+residual / restriction,
+    # hf_level_up)
     cases = {
-        "device_copy": (lambda: v.copy_(u), 32.0 * n, "ceiling"),   # practical ceiling, same buffers
-        "helmholtz_matvec": (lambda: L.hf_operator_apply(A._h, p(u), p(v)), 32.0 * n, "solve"),
-        "down_restrict": (lambda: L.hf_level_down_restrict(H, 0, p(b), p(bc)), 16.0 * n + 16.0 * nc_f,
-                          "solve"),
-        "prolong_correct": (lambda: L.hf_level_correct(H, 0, p(b), p(ec), p(t)), 32.0 * n + 16.0 * nc_f,
-                            "solve"),
-        "jacobi_postsmooth": (lambda: L.hf_level_smooth(H, 0, p(t), p(b), p(u)), 48.0 * n, "solve"),
-        "cslp_presmooth_residual": (lambda: L.hf_level_down1(H, 0, p(b), p(v)), 32.0 * n, "api"),
-        "restrict_fw": (lambda: L.hf_restrict_fw(H, 0, p(v), p(bc)), 16.0 * n + 16.0 * nc_f, "api"),
-        "level_up": (lambda: L.hf_level_up(H, 0, p(b), p(ec), p(u)), 32.0 * n + 16.0 * nc_f, "api"),
+        "device_copy": (lambda s: s["v"].copy_(s["u"]), 32.0 * n, "ceiling"),
+        "helmholtz_matvec": (lambda s: L.hf_operator_apply(A._h, p(s["u"]), p(s["v"])), 32.0 * n, "solve"),
+        "down_restrict": (lambda s: L.hf_level_down_restrict(H, 0, p(s["b"]), p(s["bc"])),
+                          16.0 * n + 16.0 * nc_f, "solve"),
+        "prolong_correct": (lambda s: L.hf_level_correct(H, 0, p(s["b"]), p(s["ec"]), p(s["t"])),
+                            32.0 * n + 16.0 * nc_f, "solve"),
+        "jacobi_postsmooth": (lambda s: L.hf_level_smooth(H, 0, p(s["t"]), p(s["b"]), p(s["u"])), 48.0 * n,
+                              "solve"),
+        "cslp_presmooth_residual": (lambda s: L.hf_level_down1(H, 0, p(s["b"]), p(s["v"])), 32.0 * n, "api"),
+        "restrict_fw": (lambda s: L.hf_restrict_fw(H, 0, p(s["v"]), p(s["bc"])), 16.0 * n + 16.0 * nc_f,
+                        "api"),
+        "level_up": (lambda s: L.hf_level_up(H, 0, p(s["b"]), p(s["ec"]), p(s["u"])), 32.0 * n + 16.0 * nc_f,
+                     "api"),
     }
     kind = hier.coarsest_kind
     # separable (fast diagonalisation): b, two scratch passes, 1/D and x -- a
     # latency-bound 3-launch solve, reported for its share only
     cbytes = {"separable": 112.0 * ncs, "symmetric": float(sym_bytes),
               "dense": 16.0 * ncs * ncs}.get(kind, 0.0)
-    cases["coarsest_solve"] = (lambda: L.hf_coarsest_solve(H, p(rc), p(xc)), cbytes, "solve")
+    cases["coarsest_solve"] = (lambda s: L.hf_coarsest_solve(H, p(rc), p(xc)), cbytes, "solve")
     out = {}
-    for name, (fn, nbytes, role) in cases.items():
-        fn()
-        ms = _event_time(fn, reps)
+
+    def put(name, ms, nbytes, role, launches):
         out[name] = {"ms": round(ms, 5), "bytes": nbytes, "gbs": round(nbytes / (ms / 1e3) / 1e9, 1),
-                     "share": round(2 * ms / t_iter_ms, 4) if role == "solve" else None,
+                     "share": round(launches * ms / t_iter_ms, 4) if role == "solve" else None,
                      "role": role,
                      "bound": ("latency" if name == "coarsest_solve" and kind == "separable"
                                else "ceiling" if name == "device_copy" else "hbm")}
+
+    reps = max(NSET, reps // NSET * NSET)
+    for name, (fn, nbytes, role) in cases.items():
+        for s in sets:
+            fn(s)
+        k = [0]
+
+        def run():
+            fn(sets[k[0] % NSET])
+            k[0] += 1
+        put(name, _event_time(run, reps), nbytes, role, 2)
+    if solver is not None:   # Bi-CGSTAB vector kernels, once per iteration (krylov.py:240-269)
+        # back to back on the solver's workspace (working sets 137-241 MB: mostly
+        # streamed from HBM, partly L2-resident for the p update)
+        for nm, which, nb in (("bcg_p_update", 0, 64.0), ("bcg_s_update", 1, 48.0),
+                              ("bcg_xr_update", 2, 128.0)):
+            ms = ctypes.c_float()
+            _native.check(L.hf_solver_bench_vec(solver._h, which, reps, ctypes.byref(ms)))
+            put(nm, ms.value, nb * n, "solve", 1)
     out["coarsest_solve"]["kind"] = kind
     return out
 

@@ -165,6 +165,11 @@ int hf_level_up(hf_hierarchy *hier, int level, const double *b, const double *e_
 hf_solver *hf_solver_create(hf_operator *A, hf_hierarchy *M);
 void hf_solver_destroy(hf_solver *s);
 /* Device-resident solve: x = A^-1 b preconditioned by one MG cycle. */
+/* Measurement hook (bench.py): mean device ms of the Bi-CGSTAB vector kernel
+ * `which` (0: p update, 1: s update + |s|^2, 2: x, r update + |r|^2, r~^H r;
+ * krylov.py:240, 248-249, 266-269) over `reps` launches on the solver's
+ * workspace; the device scalar state is not modified. */
+int hf_solver_bench_vec(hf_solver *solver, int which, int reps, float *ms);
 int hf_solve(hf_solver *s, const hf_solver_config *cfg, const double *b, double *x,
              hf_report *rep);
 /* Same, from HOST buffers (pinned or pageable): H2D of b, solve, D2H of x. */

@@ -29,7 +29,7 @@ EXPORTED = (
     "hf_hierarchy_num_levels", "hf_hierarchy_level_shape", "hf_restrict_fw", "hf_prolong_tl",
     "hf_coarsest_solve", "hf_coarsest_kind", "hf_mg_precondition", "hf_level_down1", "hf_level_down_restrict", "hf_level_up", "hf_level_correct",
     "hf_level_smooth", "hf_solver_create", "hf_solver_destroy",
-    "hf_solve", "hf_solve_host", "hf_dot",
+    "hf_solve", "hf_solve_host", "hf_dot", "hf_solver_bench_vec",
 )
 
 
@@ -108,6 +108,7 @@ def load(path: str = LIB_PATH):
         "hf_level_smooth": ([vp, i, vp, vp, vp], i),
         "hf_solver_create": ([vp, vp], vp),
         "hf_solver_destroy": ([vp], None),
+        "hf_solver_bench_vec": ([vp, i, i, ctypes.POINTER(ctypes.c_float)], i),
         "hf_solve": ([vp, ctypes.POINTER(SolverConfigC), vp, vp, ctypes.POINTER(ReportC)], i),
         "hf_solve_host": ([vp, ctypes.POINTER(SolverConfigC), vp, vp, ctypes.POINTER(ReportC)], i),
         "hf_dot": ([ctypes.c_int64, vp, vp, dp], i),

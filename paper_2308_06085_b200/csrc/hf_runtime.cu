@@ -1500,6 +1500,36 @@ static int solve_hostloop(hf_solver *S, const hf_solver_config *cfg, const cd *b
     return 0;
 }
 
+// Measurement hook (bench.py kernel table): the Bi-CGSTAB vector kernels of
+// one iteration (krylov.py:240, 248-249, 266-269) launched `reps` times on the
+// solver's workspace, inner products into a scratch slot (the device scalar
+// state is not touched).  Mean device time per launch in *ms.
+extern "C" int hf_solver_bench_vec(hf_solver *S, int which, int reps, float *ms) {
+    if (!S || reps < 1 || !ms || which < 0 || which > 2) return fail(HF_ERR_ARG, "bad bench request");
+    cudaStream_t s = work_stream();
+    const RedSlot scratch = S->red.slot(FIN_STORE, nullptr);
+    auto one = [&]() {
+        if (which == 0) launch_bcg_p(S->n, S->st, S->r, S->p, S->v, s, nullptr);
+        else if (which == 1) launch_bcg_s(S->n, S->st, S->r, S->v, S->s, scratch, s, nullptr);
+        else launch_bcg_xr(S->n, S->st, S->x, S->ph, S->sh, S->s, S->t, S->r, S->rs, scratch, s, nullptr);
+    };
+    if (reps > 1) one();   // warm-up (reps = 1: a single, cold launch)
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    CK(cudaEventRecord(a, s));
+    for (int k = 0; k < reps; k++) one();
+    CK(cudaEventRecord(b, s));
+    CK(cudaEventSynchronize(b));
+    float t = 0;
+    CK(cudaEventElapsedTime(&t, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    CKL();
+    *ms = t / reps;
+    return 0;
+}
+
 extern "C" int hf_solve(hf_solver *S, const hf_solver_config *cfg, const double *b, double *x,
                         hf_report *rep) {
     if (!S || !cfg || !b || !x || !rep) return fail(HF_ERR_ARG, "null argument");

@@ -41,8 +41,9 @@ void launch_symv(int N, const cd *tiles, const double *sv, const cd *b, cd *prow
 long long sym_tiles_count(int N);
 size_t fdm_smem_bytes(int n1, int n2, int n3);
 void fdm_groups(int n1, int n2, int n3, int &R, int &C);
-void launch_fdm(int n1, int n2, int n3, const cd *fdm, const cd *invD, const cd *b, cd *tmp,
-                cd *x, cudaStream_t s, const int *done);
+// returns the number of kernels launched
+int launch_fdm(int n1, int n2, int n3, const cd *fdm, const cd *invD, const cd *b, cd *tmp,
+               cd *x, cudaStream_t s, const int *done);
 void launch_assemble(const Lvl &L, cd *A, cudaStream_t s);
 void launch_set_identity(long long N, cd *B, cudaStream_t s);
 void launch_zero(long long n, cd *y, cudaStream_t s);

@@ -613,8 +613,7 @@ extern "C" int hf_hierarchy_level_shape(const hf_hierarchy *H, int l, int *d) {
 static void coarsest(hf_hierarchy *H, const cd *b, cd *x, cudaStream_t s, const int *done) {
     if (H->fdm) {
         const Lvl &L = H->lev.back().L;
-        L1(launch_fdm(L.n1, L.n2, L.n3, H->fdm, H->fdm_invD, b, H->fdm_tmp, x, s, done));
-        g_launches += 2;
+        g_launches += launch_fdm(L.n1, L.n2, L.n3, H->fdm, H->fdm_invD, b, H->fdm_tmp, x, s, done);
     } else if (H->symtiles) {
         L1(launch_symv(H->Nc, H->symtiles, H->symscale, b, H->prow, H->pcol, x, s, done));
         g_launches++;   // tiles + reduction

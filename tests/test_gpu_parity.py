@@ -90,6 +90,11 @@ def test_coarsest_fast_diagonalisation(hf, oracle, dims, h, kc, monkeypatch):
     x = coarsest_solve(hier, b).cpu().numpy()
     r = b - oracle.apply(np.full(dims, kc), x, h, spec.shift, "sommerfeld")
     assert np.linalg.norm(r) / np.linalg.norm(b) < 1e-12
+    # the single thread-block-cluster launch (opt-in) gives the same solution
+    monkeypatch.setenv("HF_FDM_CLUSTER", "1")
+    xcl = coarsest_solve(hier, b).cpu().numpy()
+    monkeypatch.delenv("HF_FDM_CLUSTER")
+    assert _rel(xcl, x) < 1e-13
     monkeypatch.setenv("HF_COARSEST_DENSE", "1")
     dense = build_hierarchy(grid, None, spec, MGConfig(coarsest_threshold=64))
     assert dense.coarsest_kind == "symmetric"

@@ -2504,8 +2504,7 @@ static void stencil_launch(const Lvl &L, const cd *src, const cd *aux, double om
 }
 // ---- flat-decomposition MODE_LOAD stencils (k_flat_stencil) ----
 static bool use_flat(const Lvl &L) {
-    static const bool off = std::getenv("HF_NO_FLAT") != nullptr;   // A/B switch
-    return !off && L.n3 <= FS_MAX_N3;
+    return L.n3 <= FS_MAX_N3 && std::getenv("HF_NO_FLAT") == nullptr;   // A/B switch (tests)
 }
 static size_t flat_smem(const Lvl &L) { return (size_t)FS_RING * fs_slot_bytes(L.n3) + 128; }
 static const size_t kFlatSmemMax = (size_t)FS_RING * ((FS_PTS + 2 * (FS_MAX_N3 + 1)) * 16 + 127) / 128 * 128 + 128;

@@ -159,6 +159,30 @@ def test_fused_down_restrict_matches_split(hf, dims, bc, kind, variant, monkeypa
     assert _rel(fused, split) < 1e-13
 
 
+@pytest.mark.parametrize("n,kind", [(129, "wedge"), (129, "const"), (65, "wedge")])
+def test_flat_kernels_match_tiled(hf, n, kind, monkeypatch):
+    """The flat bulk-copy kernels (k_flat_stencil, k_flat_dr, k_corr_flat) and
+    the 2-D tiled cp.async kernels compute the same V-cycle and operator at
+    BASELINE-like sizes, varying medium included (rounding-level differences
+    only)."""
+    from paper_2308_06085_b200 import problems
+    from paper_2308_06085_b200.multigrid import MGConfig, build_hierarchy, mg_precondition
+    from paper_2308_06085_b200.operators import OperatorSpec, StencilOperator
+    p = problems.wedge3_problem(n) if kind == "wedge" else problems.point_source_cube(n, 80.0 * (n - 1) / 128)
+    spec, _ = problems.build_problem(p)
+    r = torch.as_tensor(_rand(p.grid.shape, 47)).cuda()
+    hier = build_hierarchy(p.grid, None, OperatorSpec("cslp", 1.0, -0.5, spec.bc, spec.k_field), MGConfig())
+    A = StencilOperator(spec, p.grid)
+    z_flat = mg_precondition(hier, r).cpu().numpy()
+    v_flat = A.apply(r).cpu().numpy()
+    monkeypatch.setenv("HF_NO_FLAT", "1")
+    monkeypatch.setenv("HF_NO_DR", "1")
+    z_tile = mg_precondition(hier, r).cpu().numpy()
+    v_tile = A.apply(r).cpu().numpy()
+    assert _rel(z_flat, z_tile) < 1e-12
+    assert _rel(v_flat, v_tile) < 1e-13
+
+
 @pytest.mark.parametrize("bc", ["dirichlet", "sommerfeld"])
 def test_transfers_and_smoother(hf, oracle, bc):
     from paper_2308_06085_b200.multigrid import jacobi_smooth, prolong_tl, restrict_fw

@@ -2697,7 +2697,10 @@ static void dr2_launch(const Lvl &F, const Lvl &C, const cd *b, cd *out, double 
     const size_t smem = (size_t)DR2_RING * dr2_slot_elems(F.n3) * 16 + (size_t)2 * (2 * DR2_CR + 1) * F.n3 * 16 + 128;
     launch(k_flat_dr<KVAR, SOMM, RPT>, dim3(gx, gz), dim3(DR2_NT), smem, s, F, C, b, out, omega, chunk, done);
 }
-bool flat_dr_ok(const Lvl &F) { return F.n3 <= DR2_MAX_N3 && !std::getenv("HF_NO_FLAT_DR"); }
+bool flat_dr_ok(const Lvl &F) {
+    const char *mx = std::getenv("HF_DR_MAX_N3");   // tuning: widest plane for the fused down
+    return F.n3 <= (mx ? std::atoi(mx) : DR2_MAX_N3) && !std::getenv("HF_NO_FLAT_DR");
+}
 void launch_down_restrict(const Lvl &F, const Lvl &C, const cd *b, cd *out, double omega,
                           cudaStream_t s, const int *done) {
     const bool somm = F.bc == HF_BC_SOMMERFELD;

@@ -637,11 +637,15 @@ __host__ __device__ __forceinline__ int fs_slot_bytes(int n3) { return (fs_windo
 // into the residual, as in k_stencil): a constant medium stages b^ = b
 // D^-1(nb)/D^-1(0) (face vertices rescaled in the slot one plane ahead of use)
 // so f = wd0 b^ and the 7-point row stays uniform; a varying medium scales each
-// neighbour by its own D^-1.
+// neighbour by its own D^-1.  MODE_UP (post-smoothing after the coarse-grid
+// correction, multigrid.py:389-392 + 153-156): every staged entry of b is turned
+// in place into t = [w D^-1 b] + P e one plane ahead of use (the k_corr
+// arithmetic at the mirrored coordinates of halo entries), and the sweep is
+// u = t + w D^-1 (b - M t) -- the correction t never goes to memory.
 template <int MODE, class Epi, int ND, bool KVAR, bool SOMM>
 __global__ void __launch_bounds__(256, 3) k_flat_stencil(Lvl L, const cd *__restrict__ src,
                                                       const cd *__restrict__ aux, double omega, Epi epi,
-                                                      int chunk, RedSlot rs, const int *done) {
+                                                      int chunk, RedSlot rs, UpArgs up, const int *done) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ __align__(8) unsigned long long bars[FS_RING];
     __shared__ cd tab[8];
@@ -675,6 +679,7 @@ __global__ void __launch_bounds__(256, 3) k_flat_stencil(Lvl L, const cd *__rest
         tab[4 + tid] = cscal(__ldg(L.tab + 4 + tid), omega);
         if (MODE == MODE_PRE) tabs[tid] = cdiv(__ldg(L.tab + 4 + tid), __ldg(L.tab + 4));   // D^-1(nb)/D^-1(0)
     }
+    if (MODE == MODE_UP && !KVAR && tid < 4) tabs[tid] = __ldg(L.tab + 4 + tid);            // D^-1(nb)
     __syncthreads();
     const int last = min(i1, L.n1 - 1 - L.lo1);       // last plane read (i1, or the top plane)
     if (tid == 0)
@@ -688,36 +693,69 @@ __global__ void __launch_bounds__(256, 3) k_flat_stencil(Lvl L, const cd *__rest
     };
     // MODE_PRE, constant medium: this thread's window entries (e = tid + 256 t)
     // that are face vertices, rescaled in place by D^-1(nb)/D^-1(0) once their
-    // plane lands (one plane ahead of its first use)
+    // plane lands (one plane ahead of its first use).  MODE_UP: every entry is
+    // replaced by t = [w D^-1 b] + P e at the same point of the pipeline.
     constexpr bool kFix = MODE == MODE_PRE && !KVAR;
+    constexpr bool kProd = MODE == MODE_UP;
     constexpr int NFE = (FS_PTS + 2 * (FS_MAX_N3 + 1) + 255) / 256;
     unsigned fe_nb = 0;                  // 2 bits per entry: in-plane face count
     unsigned fe_in = 0;                  // entry lies in the plane
-    if (kFix) {
+    int fe_c[kProd ? NFE : 1];           // MODE_UP: coarse (i2, i3) base << 2 | odd i2 << 1 | odd i3
+    if (kFix || kProd) {
         const int W = c1 - w0;
 #pragma unroll
         for (int t = 0; t < NFE; t++) {
             const int e = tid + 256 * t, g = w0 + e;
+            if (kProd) fe_c[t] = 0;
             if (e < W && g >= 0 && g < plane) {
                 const int j = g / L.n3, m = g - j * L.n3;
                 fe_in |= 1u << t;
                 fe_nb |= (unsigned)((j == 0) + (j == L.n2 - 1) + (m == 0) + (m == L.n3 - 1)) << (2 * t);
+                if (kProd) fe_c[t] = (((j >> 1) * up.C.n3 + (m >> 1)) << 2) | ((j & 1) << 1) | (m & 1);
             }
         }
     }
     auto fixup = [&](int p) {            // own entries of local plane p (mirrored outside)
-        if (!kFix) return;
+        if (!kFix && !kProd) return;
         const int gm = gmirror(L.lo1 + p);
         const int nbx = (gm == 0) + (gm == L.n1 - 1);
-        if (nbx == 0 && fe_nb == 0) return;
+        if (kFix && nbx == 0 && fe_nb == 0) return;
         cd *sl = const_cast<cd *>(slot(p));
+        const Lvl &C = up.C;
+        const int cl = (gm >> 1) - C.lo1;
+        const bool odd = gm & 1;
 #pragma unroll
         for (int t = 0; t < NFE; t++) {
+            if (!((fe_in >> t) & 1u)) continue;
+            const int e = tid + 256 * t;
             const int nb = nbx + (int)((fe_nb >> (2 * t)) & 3u);
-            if (((fe_in >> t) & 1u) && nb > 0) {
-                const int e = tid + 256 * t;
-                sl[e] = cmul(sl[e], tabs[nb]);
+            if (kFix) {
+                if (nb > 0) sl[e] = cmul(sl[e], tabs[nb]);
+                continue;
             }
+            const int info = fe_c[t];
+            const bool o2 = info & 2, o3 = info & 1;
+            const cd *ecol = up.e + (info >> 2);
+            auto cplane = [&](int c) -> cd {      // bilinear sum on coarse local plane c (k_corr)
+                const cd *pp = ecol + (long long)c * C.plane;
+                cd a = __ldg(pp);
+                if (o3) a = cadd(a, __ldg(pp + 1));
+                if (o2) {
+                    a = cadd(a, __ldg(pp + C.n3));
+                    if (o3) a = cadd(a, __ldg(pp + C.n3 + 1));
+                }
+                return a;
+            };
+            const double s2 = (o2 && o3) ? 0.25 : ((o2 || o3) ? 0.5 : 1.0);
+            const cd v0 = cplane(cl);
+            cd pe;
+            if (odd) pe = cscal(cadd(v0, cplane(cl + 1)), 0.5 * s2);
+            else pe = s2 == 1.0 ? v0 : cscal(v0, s2);
+            if (up.pre) {
+                const cd D = KVAR ? __ldg(L.dinv + (long long)(gm - L.lo1) * plane + (w0 + e)) : tabs[nb];
+                pe = cadd(cscal(cmul(sl[e], D), omega), pe);
+            }
+            sl[e] = pe;
         }
     };
     // per point: smem offsets of centre and in-plane neighbours (mirrored at faces)
@@ -739,7 +777,7 @@ __global__ void __launch_bounds__(256, 3) k_flat_stencil(Lvl L, const cd *__rest
     const cd apc = KVAR ? mk(0, 0) : tab[0];
     wait_plane(i0 - 1);
     wait_plane(i0);
-    if (kFix) {
+    if (kFix || kProd) {
         fixup(i0 - 1);
         fixup(i0);
         if (i0 + 1 <= last) {
@@ -781,7 +819,7 @@ __global__ void __launch_bounds__(256, 3) k_flat_stencil(Lvl L, const cd *__rest
         }
         __syncthreads();                             // slot of plane i-1 is free
         if (tid == 0 && i + FS_RING - 1 <= last) issue(i + FS_RING - 1);
-        if (kFix && i + 2 <= last) {     // visible after the next barrier
+        if ((kFix || kProd) && i + 2 <= last) {     // visible after the next barrier
             wait_plane(i + 2);
             fixup(i + 2);
         }
@@ -2510,26 +2548,27 @@ static size_t flat_smem(const Lvl &L) { return (size_t)FS_RING * fs_slot_bytes(L
 static const size_t kFlatSmemMax = (size_t)FS_RING * ((FS_PTS + 2 * (FS_MAX_N3 + 1)) * 16 + 127) / 128 * 128 + 128;
 template <int MODE, class Epi, int ND, bool KVAR, bool SOMM>
 static void flat_launch_t(const Lvl &L, const cd *src, const cd *aux, double omega, const Epi &e,
-                          const RedSlot &rs, cudaStream_t s, const int *done) {
+                          const RedSlot &rs, cudaStream_t s, const int *done, const UpArgs &up) {
     const int gx = (int)((L.plane + FS_PTS - 1) / FS_PTS);
     static const int bps = std::getenv("HF_FLAT_BPS") ? std::atoi(std::getenv("HF_FLAT_BPS")) : 3;
     int gz = std::max(1, std::min(L.nx, (148 * bps + gx - 1) / gx));
     const int chunk = std::max((L.nx + gz - 1) / gz, std::min(L.nx, 2));
     gz = (L.nx + chunk - 1) / chunk;
     launch(k_flat_stencil<MODE, Epi, ND, KVAR, SOMM>, dim3(gx, gz), dim3(256), flat_smem(L), s, L, src,
-           aux ? aux : src, omega, e, chunk, rs, done);
+           aux ? aux : src, omega, e, chunk, rs, up, done);
 }
 template <int MODE, class Epi, int ND>
 static bool flat_stencil(const Lvl &L, const cd *src, const cd *aux, double omega, const Epi &e,
-                         const RedSlot &rs, cudaStream_t s, const int *done) {
+                         const RedSlot &rs, cudaStream_t s, const int *done,
+                         const UpArgs &up = UpArgs{}) {
     if (!use_flat(L)) return false;
     const bool somm = L.bc == HF_BC_SOMMERFELD;
     if (L.k) {
-        if (somm) flat_launch_t<MODE, Epi, ND, true, true>(L, src, aux, omega, e, rs, s, done);
-        else flat_launch_t<MODE, Epi, ND, true, false>(L, src, aux, omega, e, rs, s, done);
+        if (somm) flat_launch_t<MODE, Epi, ND, true, true>(L, src, aux, omega, e, rs, s, done, up);
+        else flat_launch_t<MODE, Epi, ND, true, false>(L, src, aux, omega, e, rs, s, done, up);
     } else {
-        if (somm) flat_launch_t<MODE, Epi, ND, false, true>(L, src, aux, omega, e, rs, s, done);
-        else flat_launch_t<MODE, Epi, ND, false, false>(L, src, aux, omega, e, rs, s, done);
+        if (somm) flat_launch_t<MODE, Epi, ND, false, true>(L, src, aux, omega, e, rs, s, done, up);
+        else flat_launch_t<MODE, Epi, ND, false, false>(L, src, aux, omega, e, rs, s, done, up);
     }
     return true;
 }
@@ -2587,6 +2626,7 @@ void init_kernel_attributes() {
     flat_attr<MODE_LOAD, EpiResid, 0>();
     flat_attr<MODE_LOAD, EpiJacobi, 0>();
     flat_attr<MODE_PRE, EpiResid, 0>();
+    flat_attr<MODE_UP, EpiJacobi, 0>();
     {
         const int b2 = DR2_RING * dr2_slot_elems(DR2_MAX_N3) * 16 + 2 * (2 * DR2_CR + 1) * DR2_MAX_N3 * 16 + 128;
         cudaFuncSetAttribute(k_flat_dr<true, true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, b2);
@@ -2741,7 +2781,15 @@ void launch_correct(const Lvl &L, const Lvl &C, const cd *b, const cd *e, cd *t,
 int launch_up1(const Lvl &L, const Lvl &C, const cd *b, const cd *e, cd *u, cd *t, double omega,
                bool pre, cudaStream_t s, const int *done) {
     // whole-grid levels: correction produced inside the post-smoothing sweep
-    // (the split pair is faster where the flat Jacobi sweep applies)
+    // flat fused up-sweep: opt-in (HF_FLAT_UP=1); the per-entry prolongation in the
+    // slot made it slower than k_corr_flat + the flat Jacobi sweep on every level
+    const char *upmx = std::getenv("HF_UP_MAX_N3");   // widest plane for the flat fused up-sweep
+    if (std::getenv("HF_NO_FUSE") == nullptr && std::getenv("HF_FLAT_UP") != nullptr &&
+        L.n3 <= (upmx ? std::atoi(upmx) : FS_MAX_N3) &&
+        flat_stencil<MODE_UP, EpiJacobi, 0>(L, b, b, omega, EpiJacobi{u}, RedSlot{}, s, done,
+                                            UpArgs{C, e, pre ? 1 : 0}))
+        return 1;
+    // (the split pair is faster than the tiled fused kernel where the flat Jacobi applies)
     const bool split = std::getenv("HF_NO_FUSE") != nullptr ||
                        (use_flat(L) && std::getenv("HF_FUSE_UP") == nullptr);
     if (!split && L.lo1 == 0 && L.nx == L.n1 && C.lo1 == 0 && C.nx == C.n1) {

@@ -122,10 +122,14 @@ def test_fused_up_matches_split(hf, dims, bc, kind, mg, monkeypatch):
     r = torch.as_tensor(_rand(dims, 41)).cuda()
     hier = build_hierarchy(grid, None, spec, MGConfig(**mg))
     monkeypatch.setenv("HF_FUSE_UP", "1")
-    fused = mg_precondition(hier, r).cpu().numpy()
+    fused = mg_precondition(hier, r).cpu().numpy()        # tiled MODE_UP
+    monkeypatch.setenv("HF_FLAT_UP", "1")
+    flat = mg_precondition(hier, r).cpu().numpy()         # flat MODE_UP (opt-in)
+    monkeypatch.delenv("HF_FLAT_UP")
     monkeypatch.setenv("HF_NO_FUSE", "1")
     split = mg_precondition(hier, r).cpu().numpy()
     assert _rel(fused, split) < 1e-13
+    assert _rel(flat, split) < 1e-13
 
 
 @pytest.mark.parametrize("dims,bc,kind", [

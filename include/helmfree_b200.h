@@ -59,6 +59,7 @@ extern "C" {
 typedef struct hf_operator hf_operator;
 typedef struct hf_hierarchy hf_hierarchy;
 typedef struct hf_solver hf_solver;
+typedef struct hf_bcg hf_bcg;
 
 /* multigrid.py:42-51 MGConfig */
 typedef struct hf_mg_config {
@@ -165,6 +166,27 @@ int hf_level_up(hf_hierarchy *hier, int level, const double *b, const double *e_
 hf_solver *hf_solver_create(hf_operator *A, hf_hierarchy *M);
 void hf_solver_destroy(hf_solver *s);
 /* Device-resident solve: x = A^-1 b preconditioned by one MG cycle. */
+/* ---- device-resident Bi-CGSTAB for slab drivers (krylov.py:207-276) ----
+ * The scalars (rho, alpha, omega, beta, norms, history, stop flags) live on the
+ * device.  Each reduction stores THIS slab's partial sums (two complex, device
+ * `sums`); the driver adds them over slabs / ranks (NCCL all-reduce) and calls
+ * hf_bcg_step with the op that consumed them: 1 init (|b|^2, r~^H r),
+ * 2 alpha (r~^H v), 3 s-norm (|s|^2), 4 omega (t^H t, t^H s), 5 rho (|r|^2,
+ * r~^H r).  Every kernel is a no-op once the device state is done. */
+hf_bcg *hf_bcg_create(hf_operator *A, double tol, int maxit, double breakdown_tol);
+void hf_bcg_destroy(hf_bcg *state);
+int hf_bcg_step(hf_bcg *state, int op, const double *sums);
+int hf_bcg_read(hf_bcg *state, int *out6, double *relres, double *history_host, int history_cap);
+int hf_bcg_vec_init(hf_bcg *state, int64_t n, const double *b, double *r, double *rs, double *x,
+                    double *p, double *v, double *sums);
+int hf_bcg_vec_p(hf_bcg *state, int64_t n, const double *r, double *p, const double *v);
+int hf_bcg_vec_s(hf_bcg *state, int64_t n, const double *r, const double *v, double *s, double *sums);
+int hf_bcg_vec_xr(hf_bcg *state, int64_t n, double *x, const double *ph, const double *sh,
+                  const double *s, const double *t, double *r, const double *rs, double *sums);
+int hf_bcg_vec_xhalf(hf_bcg *state, int64_t n, double *x, const double *ph);
+int hf_operator_apply_dot(hf_operator *A, hf_bcg *state, int nd, const double *u, double *v,
+                          const double *w, double *sums);
+
 /* Measurement hook (bench.py): mean device ms of the Bi-CGSTAB vector kernel
  * `which` (0: p update, 1: s update + |s|^2, 2: x, r update + |r|^2, r~^H r;
  * krylov.py:240, 248-249, 266-269) over `reps` launches on the solver's

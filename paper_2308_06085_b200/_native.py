@@ -30,6 +30,8 @@ EXPORTED = (
     "hf_coarsest_solve", "hf_coarsest_kind", "hf_mg_precondition", "hf_level_down1", "hf_level_down_restrict", "hf_level_up", "hf_level_correct",
     "hf_level_smooth", "hf_solver_create", "hf_solver_destroy",
     "hf_solve", "hf_solve_host", "hf_dot", "hf_solver_bench_vec",
+    "hf_bcg_create", "hf_bcg_destroy", "hf_bcg_step", "hf_bcg_read", "hf_bcg_vec_init", "hf_bcg_vec_p",
+    "hf_bcg_vec_s", "hf_bcg_vec_xr", "hf_bcg_vec_xhalf", "hf_operator_apply_dot",
 )
 
 
@@ -109,6 +111,16 @@ def load(path: str = LIB_PATH):
         "hf_solver_create": ([vp, vp], vp),
         "hf_solver_destroy": ([vp], None),
         "hf_solver_bench_vec": ([vp, i, i, ctypes.POINTER(ctypes.c_float)], i),
+        "hf_bcg_create": ([vp, d, i, d], vp),
+        "hf_bcg_destroy": ([vp], None),
+        "hf_bcg_step": ([vp, i, vp], i),
+        "hf_bcg_read": ([vp, ip, ctypes.POINTER(ctypes.c_double), vp, i], i),
+        "hf_bcg_vec_init": ([vp, ctypes.c_int64, vp, vp, vp, vp, vp, vp, vp], i),
+        "hf_bcg_vec_p": ([vp, ctypes.c_int64, vp, vp, vp], i),
+        "hf_bcg_vec_s": ([vp, ctypes.c_int64, vp, vp, vp, vp], i),
+        "hf_bcg_vec_xr": ([vp, ctypes.c_int64, vp, vp, vp, vp, vp, vp, vp, vp], i),
+        "hf_bcg_vec_xhalf": ([vp, ctypes.c_int64, vp, vp], i),
+        "hf_operator_apply_dot": ([vp, vp, i, vp, vp, vp, vp], i),
         "hf_solve": ([vp, ctypes.POINTER(SolverConfigC), vp, vp, ctypes.POINTER(ReportC)], i),
         "hf_solve_host": ([vp, ctypes.POINTER(SolverConfigC), vp, vp, ctypes.POINTER(ReportC)], i),
         "hf_dot": ([ctypes.c_int64, vp, vp, dp], i),

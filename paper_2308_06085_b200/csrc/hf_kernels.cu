@@ -1704,6 +1704,18 @@ __global__ void __launch_bounds__(256) k_bcg_xr(long long n, const BcgState *st,
     reduce_finish<2>(acc, red);
 }
 
+// one-thread Bi-CGSTAB state update from (all-reduced) inner products, for
+// drivers whose reductions span several slabs / ranks (dist.SlabSolver): the
+// local kernels store partial sums, the driver sums them across slabs, and
+// this kernel runs the same state machine the single-slab reductions run in
+// their last block.  No-op once the solve is done (except the init step).
+__global__ void k_bcg_step(BcgState *st, int op, const cd *sums) {
+    pdl_enter();
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (op != FIN_BCG_INIT && st->done) return;
+    bcg_finalize(st, op, sums);
+}
+
 // x += alpha ph  (convergence at the half step, krylov.py:250-255)
 __global__ void k_bcg_xhalf(long long n, const BcgState *st, cd *__restrict__ x,
                             const cd *__restrict__ ph) {
@@ -2940,6 +2952,9 @@ void launch_bcg_xr(long long n, const BcgState *st, cd *x, const cd *ph, const c
                    const cd *sv, const cd *t, cd *r, const cd *rs, const RedSlot &red,
                    cudaStream_t s, const int *done) {
     launch(k_bcg_xr, dim3(VEC_BLOCKS), dim3(256), 0, s, n, st, x, ph, sh, sv, t, r, rs, red, done);
+}
+void launch_bcg_step(BcgState *st, int op, const cd *sums, cudaStream_t s) {
+    launch(k_bcg_step, dim3(1), dim3(32), 0, s, st, op, sums);
 }
 void launch_bcg_xhalf(long long n, const BcgState *st, cd *x, const cd *ph, cudaStream_t s) {
     launch(k_bcg_xhalf, dim3(VEC_BLOCKS), dim3(256), 0, s, n, st, x, ph);

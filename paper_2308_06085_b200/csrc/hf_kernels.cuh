@@ -62,6 +62,7 @@ void launch_bcg_xr(long long n, const BcgState *st, cd *x, const cd *ph, const c
                    const cd *sv, const cd *t, cd *r, const cd *rs, const RedSlot &red,
                    cudaStream_t s, const int *done);
 void launch_bcg_xhalf(long long n, const BcgState *st, cd *x, const cd *ph, cudaStream_t s);
+void launch_bcg_step(BcgState *st, int op, const cd *sums, cudaStream_t s);
 
 #define VEC_BLOCKS_HOST 592
 

@@ -1499,6 +1499,132 @@ static int solve_hostloop(hf_solver *S, const hf_solver_config *cfg, const cd *b
     return 0;
 }
 
+// ---------------------------------------------------------------------------
+// Device-resident Bi-CGSTAB for slab drivers (dist.SlabSolver.solve_device):
+// the scalars live on the device as in the single-slab graph path; every
+// reduction kernel stores this slab's partial sums (two complex) into a
+// caller buffer, the driver adds them over slabs (NCCL all-reduce across
+// ranks), and hf_bcg_step advances the state from the totals.  All kernels are
+// predicated on the device done flag, so the host only polls the state.
+// ---------------------------------------------------------------------------
+struct hf_bcg {
+    Allocs A;
+    BcgState *st = nullptr;
+    BcgState *host = nullptr;      // pinned mirror
+    double *hist = nullptr;
+    RedBuf red;
+    ~hf_bcg() {
+        if (host) cudaFreeHost(host);
+    }
+};
+
+extern "C" hf_bcg *hf_bcg_create(hf_operator *Aop, double tol, int maxit, double btol) {
+    if (!Aop || maxit < 1 || !(tol > 0)) { fail(HF_ERR_ARG, "bad Bi-CGSTAB state request"); return nullptr; }
+    auto *B = new hf_bcg();
+    cudaError_t e;
+    B->st = B->A.get<BcgState>(1, e);
+    B->hist = B->A.get<double>((size_t)maxit + 2, e);
+    const size_t nblk = std::max<size_t>(std::max(march_blocks(Aop->lv.L), tile_blocks(Aop->lv.L)),
+                                         VEC_BLOCKS_HOST);
+    if (!B->st || !B->hist || B->red.init(B->A, nblk + 64) ||
+        cudaMallocHost(&B->host, sizeof(BcgState)) != cudaSuccess) {
+        fail(HF_ERR_CUDA, "cudaMalloc Bi-CGSTAB state");
+        delete B;
+        return nullptr;
+    }
+    BcgState init{};
+    init.tol = tol;
+    init.btol = btol > 0 ? btol : 1e-30;
+    init.maxit = maxit;
+    init.hist = B->hist;
+    init.hist_cap = maxit + 2;
+    *B->host = init;
+    if (cudaMemcpy(B->st, B->host, sizeof(BcgState), cudaMemcpyHostToDevice) != cudaSuccess) {
+        fail(HF_ERR_CUDA, "state upload");
+        delete B;
+        return nullptr;
+    }
+    return B;
+}
+extern "C" void hf_bcg_destroy(hf_bcg *B) { delete B; }
+
+static RedSlot bcg_store(hf_bcg *B, double *sums) {
+    RedSlot r = B->red.slot(FIN_STORE, nullptr);
+    r.out = (cd *)sums;
+    return r;
+}
+extern "C" int hf_bcg_step(hf_bcg *B, int op, const double *sums) {
+    if (!B || op < FIN_BCG_INIT || op > FIN_BCG_RHO) return fail(HF_ERR_ARG, "bad step");
+    launch_bcg_step(B->st, op, (const cd *)sums, work_stream());
+    CKL();
+    return 0;
+}
+// out6 = iter, done, converged, breakdown, matvecs, s_conv (synchronises)
+extern "C" int hf_bcg_read(hf_bcg *B, int *out6, double *relres, double *hist, int hist_cap) {
+    if (!B || !out6) return fail(HF_ERR_ARG, "bad read");
+    cudaStream_t s = work_stream();
+    CK(cudaMemcpyAsync(B->host, B->st, sizeof(BcgState), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const BcgState &st = *B->host;
+    out6[0] = st.iter; out6[1] = st.done; out6[2] = st.converged;
+    out6[3] = st.breakdown; out6[4] = st.matvecs; out6[5] = st.s_conv;
+    if (relres) *relres = st.relres;
+    if (hist && hist_cap > 0 && st.iter > 0)
+        CK(cudaMemcpy(hist, B->hist, (size_t)std::min(st.iter, hist_cap) * sizeof(double),
+                      cudaMemcpyDeviceToHost));
+    return 0;
+}
+// r = b, rs = b, x = p = v = 0; sums = |b|^2, rs^H r (this slab)
+extern "C" int hf_bcg_vec_init(hf_bcg *B, int64_t n, const double *b, double *r, double *rs,
+                               double *x, double *p, double *v, double *sums) {
+    launch_bcg_init(n, (const cd *)b, (cd *)r, (cd *)rs, (cd *)x, (cd *)p, (cd *)v, bcg_store(B, sums),
+                    work_stream());
+    CKL();
+    return 0;
+}
+// p = r + beta (p - omega v)
+extern "C" int hf_bcg_vec_p(hf_bcg *B, int64_t n, const double *r, double *p, const double *v) {
+    launch_bcg_p(n, B->st, (const cd *)r, (cd *)p, (const cd *)v, work_stream(), &B->st->done);
+    CKL();
+    return 0;
+}
+// s = r - alpha v; sums = |s|^2
+extern "C" int hf_bcg_vec_s(hf_bcg *B, int64_t n, const double *r, const double *v, double *s,
+                            double *sums) {
+    launch_bcg_s(n, B->st, (const cd *)r, (const cd *)v, (cd *)s, bcg_store(B, sums), work_stream(),
+                 &B->st->done);
+    CKL();
+    return 0;
+}
+// x += alpha ph + omega sh; r = s - omega t; sums = |r|^2, rs^H r
+extern "C" int hf_bcg_vec_xr(hf_bcg *B, int64_t n, double *x, const double *ph, const double *sh,
+                             const double *s, const double *t, double *r, const double *rs,
+                             double *sums) {
+    launch_bcg_xr(n, B->st, (cd *)x, (const cd *)ph, (const cd *)sh, (const cd *)s, (const cd *)t,
+                  (cd *)r, (const cd *)rs, bcg_store(B, sums), work_stream(), &B->st->done);
+    CKL();
+    return 0;
+}
+// x += alpha ph (convergence at the half step)
+extern "C" int hf_bcg_vec_xhalf(hf_bcg *B, int64_t n, double *x, const double *ph) {
+    launch_bcg_xhalf(n, B->st, (cd *)x, (const cd *)ph, work_stream());
+    CKL();
+    return 0;
+}
+// v = A u with this slab's inner products: nd = 1: w^H v; nd = 2: v^H v, v^H w
+extern "C" int hf_operator_apply_dot(hf_operator *op, hf_bcg *B, int nd, const double *u, double *v,
+                                     const double *w, double *sums) {
+    if (!op || !B || (nd != 1 && nd != 2)) return fail(HF_ERR_ARG, "bad apply_dot");
+    if (nd == 1)
+        launch_apply_dot1(op->lv.L, (const cd *)u, (cd *)v, (const cd *)w, bcg_store(B, sums), work_stream(),
+                          &B->st->done);
+    else
+        launch_apply_dot2(op->lv.L, (const cd *)u, (cd *)v, (const cd *)w, bcg_store(B, sums), work_stream(),
+                          &B->st->done);
+    CKL();
+    return 0;
+}
+
 // Measurement hook (bench.py kernel table): the Bi-CGSTAB vector kernels of
 // one iteration (krylov.py:240, 248-249, 266-269) launched `reps` times on the
 // solver's workspace, inner products into a scratch slot (the device scalar

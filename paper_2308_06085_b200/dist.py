@@ -251,6 +251,89 @@ class SlabSolver:
         rep.converged = False
         return x, rep
 
+    # ---- device-resident Bi-CGSTAB (same recurrences, scalars on the device) ----
+    def solve_device(self, b_slabs, cfg: SolverConfig | None = None, poll_every: int = 4):
+        """Bi-CGSTAB with the scalars advanced on the device (hf_bcg_*): each
+        reduction leaves this slab's partial sums on the device, the comm adds
+        them over slabs / ranks (an NCCL all-reduce across processes), and a
+        one-thread kernel updates the state.  The host only polls the state
+        every `poll_every` iterations; kernels launched past convergence are
+        no-ops on the state and on x.  Returns (x per slab, ConvergenceReport)."""
+        torch, L = self.torch, self.L
+        cfg = cfg or SolverConfig(method="bicgstab")
+        _native.set_stream_from_torch()
+        S = range(len(self.extents))
+        own = lambda: [torch.zeros(e.shape, dtype=torch.complex128, device="cuda") for e in self.extents]
+        halo = lambda: [HaloField(e) for e in self.extents]
+        b = [torch.as_tensor(x).to("cuda", torch.complex128).contiguous() for x in b_slabs]
+        x, v, t, r, rs = own(), own(), own(), own(), own()
+        p, s, ph, sh = halo(), halo(), halo(), halo()
+        n = [e.nx * e.ny * e.nz for e in self.extents]
+        big = max(S, key=lambda i: n[i])
+        B = L.hf_bcg_create(self.A[big], float(cfg.tol), int(cfg.maxit), float(cfg.breakdown_tol))
+        if not B:
+            raise RuntimeError(_native.last_error())
+        sums = [torch.zeros(2, dtype=torch.complex128, device="cuda") for _ in S]
+        chk = _native.check
+        keep = []
+
+        def reduce_step(op):
+            tot = self.comm.allreduce_device(sums)
+            keep.append(tot)            # alive until the kernel reading it has run
+            chk(L.hf_bcg_step(B, op, _ptr(tot)))
+
+        try:
+            for i in S:
+                chk(L.hf_bcg_vec_init(B, n[i], _ptr(b[i]), _ptr(r[i]), _ptr(rs[i]), _ptr(x[i]),
+                                      _ptr(p[i].owned), _ptr(v[i]), _ptr(sums[i])))
+            reduce_step(1)
+            st = (ctypes.c_int * 6)()
+            relres = ctypes.c_double()
+            while True:
+                chk(L.hf_bcg_read(B, st, ctypes.byref(relres), None, 0))
+                keep.clear()
+                if st[1] or st[0] >= cfg.maxit:
+                    break
+                for _ in range(poll_every):
+                    for i in S:
+                        chk(L.hf_bcg_vec_p(B, n[i], _ptr(r[i]), _ptr(p[i].owned), _ptr(v[i])))
+                    self.precondition(p, ph)
+                    self._halo(ph)
+                    for i in S:
+                        chk(L.hf_operator_apply_dot(self.A[i], B, 1, _ptr(ph[i].owned), _ptr(v[i]),
+                                                    _ptr(rs[i]), _ptr(sums[i])))
+                    reduce_step(2)
+                    for i in S:
+                        chk(L.hf_bcg_vec_s(B, n[i], _ptr(r[i]), _ptr(v[i]), _ptr(s[i].owned),
+                                           _ptr(sums[i])))
+                    reduce_step(3)
+                    self.precondition(s, sh)
+                    self._halo(sh)
+                    for i in S:
+                        chk(L.hf_operator_apply_dot(self.A[i], B, 2, _ptr(sh[i].owned), _ptr(t[i]),
+                                                    _ptr(s[i].owned), _ptr(sums[i])))
+                    reduce_step(4)
+                    for i in S:
+                        chk(L.hf_bcg_vec_xr(B, n[i], _ptr(x[i]), _ptr(ph[i].owned), _ptr(sh[i].owned),
+                                            _ptr(s[i].owned), _ptr(t[i]), _ptr(r[i]), _ptr(rs[i]),
+                                            _ptr(sums[i])))
+                    reduce_step(5)
+            if st[5]:                    # converged at the half step: x += alpha ph
+                for i in S:
+                    chk(L.hf_bcg_vec_xhalf(B, n[i], _ptr(x[i]), _ptr(ph[i].owned)))
+            hist = np.zeros(cfg.maxit + 2)
+            chk(L.hf_bcg_read(B, st, ctypes.byref(relres), hist.ctypes.data, len(hist)))
+        finally:
+            torch.cuda.synchronize()
+            L.hf_bcg_destroy(B)
+        rep = ConvergenceReport(method="bicgstab")
+        rep.iterations, rep.matvec_count = int(st[0]), int(st[4])
+        rep.converged = bool(st[2])
+        rep.breakdown = _native.BREAKDOWN[int(st[3])]
+        rep.final_relres = float(relres.value)
+        rep.residual_history = hist[:rep.iterations].tolist()
+        return x, rep
+
 
 def _coarse_extents(grid, nslabs, nlev):
     return _level_extents(grid, nslabs, nlev)

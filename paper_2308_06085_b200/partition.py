@@ -153,6 +153,23 @@ class TorchSlabComm(_SlabCommBase):
         t = t.cpu()
         return complex(float(t[0]), float(t[1]))
 
+    def allreduce_device(self, tensors):
+        """tensors: [device tensor of partial sums] of this rank -> the global sum
+        as a device tensor, without a host round trip on NCCL (one all-reduce)."""
+        (t,) = tensors
+        if self.dist.get_backend(self.group) == "nccl":
+            out = t.clone()
+            self.dist.all_reduce(self._real(out), group=self.group)
+            return out
+        host = t.cpu()                      # gloo: host tensors
+        self.dist.all_reduce(self._real(host), group=self.group)
+        return host.to(t.device)
+
+    @staticmethod
+    def _real(t):
+        import torch
+        return torch.view_as_real(t) if t.is_complex() else t
+
     def allgather_planes(self, owned, counts):
         """Concatenate every rank's owned planes (coarsest level) in rank order."""
         import torch
@@ -187,6 +204,13 @@ class LocalSlabComm(_SlabCommBase):
         tot = 0j
         for v in values:           # fixed rank order
             tot += v
+        return tot
+
+    def allreduce_device(self, tensors):
+        """Per-slab partial sums -> their total (fixed slab order, on the device)."""
+        tot = tensors[0].clone()
+        for t in tensors[1:]:
+            tot += t
         return tot
 
     def allgather_planes(self, owned_list, counts):

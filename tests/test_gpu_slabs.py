@@ -68,3 +68,23 @@ def test_slab_precondition_matches_single_heterogeneous():
     xs, rs, _, _ = _slabs(p, k, b, 4)
     assert rs.converged and abs(rs.iterations - r1.iterations) <= 1
     assert np.linalg.norm(xs - x1) / np.linalg.norm(x1) < 1e-8
+
+
+@pytest.mark.parametrize("nslabs", [1, 2, 3])
+def test_slab_device_bicgstab_matches_single(nslabs):
+    """Device-resident slab Bi-CGSTAB (hf_bcg_*: scalars on the device, partial
+    sums added over slabs) against the single-slab graph solve."""
+    from paper_2308_06085_b200 import problems
+    from paper_2308_06085_b200.dist import SlabSolver
+    from paper_2308_06085_b200.krylov import SolverConfig
+    from paper_2308_06085_b200.partition import LocalSlabComm, slab_partition
+    p = problems.point_source_cube(65, 40.0, "sommerfeld")
+    k = np.full(p.grid.shape, 40.0)
+    b, x1, r1, _ = _single(p, k)
+    ext = slab_partition(p.grid, nslabs)
+    S = SlabSolver(p.grid, ext, k, p.bc, LocalSlabComm(nslabs))
+    xs, rs = S.solve_device([b[e.lo1 - 1:e.hi1] for e in ext], SolverConfig(method="bicgstab"))
+    xs = np.concatenate([x.cpu().numpy() for x in xs], 0)
+    assert rs.converged and abs(rs.iterations - r1.iterations) <= 1, (rs.iterations, r1.iterations)
+    assert np.linalg.norm(xs - x1) / np.linalg.norm(x1) < 1e-8
+    assert len(rs.residual_history) == rs.iterations

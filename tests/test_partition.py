@@ -98,8 +98,10 @@ def _worker(rank, world, port, out):
         data[HF_GHOST:HF_GHOST + e.nx] = (i1[:, None, None] + 1j * rank).expand(e.nx, 5, 5)
         comm.exchange([data], planes=2)
         total = comm.allreduce([complex(rank + 1, -rank)])
+        part = torch.tensor([complex(rank + 1, -rank), complex(2 * rank, 1.0)], dtype=torch.complex128)
+        dev_total = comm.allreduce_device([part]).numpy().copy()   # the device-resident driver's sums
         coarse = comm.allgather_planes(data[HF_GHOST:HF_GHOST + e.nx], [x.nx for x in slab_partition(grid, world)])
-        out[rank] = (data.numpy().copy(), total, coarse.numpy().copy(), (e.lo1, e.hi1))
+        out[rank] = (data.numpy().copy(), total, coarse.numpy().copy(), (e.lo1, e.hi1), dev_total)
     finally:
         dist.destroy_process_group()
 
@@ -113,8 +115,8 @@ def test_gloo_two_rank_halo_exchange():
     out = mgr.dict()
     port = _free_port()
     mp.spawn(_worker, args=(2, port, out), nprocs=2, join=True)
-    d0, t0, g0, (lo0, hi0) = out[0]
-    d1, t1, g1, (lo1, hi1) = out[1]
+    d0, t0, g0, (lo0, hi0), s0 = out[0]
+    d1, t1, g1, (lo1, hi1), s1 = out[1]
     G = HF_GHOST
     nx0 = hi0 - lo0 + 1
     # rank 0's upper ghosts = rank 1's first two planes (global planes lo1, lo1+1)
@@ -124,5 +126,7 @@ def test_gloo_two_rank_halo_exchange():
     # physical faces untouched
     assert np.all(d0[:G] == 0) and np.all(d1[G + (hi1 - lo1 + 1):] == 0)
     assert t0 == t1 == complex(3, -1)
+    np.testing.assert_array_equal(s0, s1)
+    np.testing.assert_array_equal(s0, np.array([3 - 1j, 2 + 2j]))
     np.testing.assert_array_equal(g0, g1)
     assert g0.shape[0] == 9 and np.all(g0[:, 0, 0].real == np.arange(1, 10))

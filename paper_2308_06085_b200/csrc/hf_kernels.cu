@@ -1400,6 +1400,55 @@ __device__ __forceinline__ void restrict_body(const Lvl &F, const Lvl &C, const 
     }
 }
 
+// flat full-weighting restriction: one thread per coarse (i2, i3) vertex of a
+// contiguous range of the coarse plane, marching over a chunk of coarse
+// planes; each fine plane's (1,2,1) x (1,2,1) partial is formed once from L1 /
+// L2 loads (neighbouring coarse vertices share fine rows) and the odd plane's
+// partial is carried to the next coarse plane.  Association as k_restrict2.
+__global__ void __launch_bounds__(256) k_restrict_flat(Lvl F, Lvl C, const cd *__restrict__ r,
+                                                       cd *__restrict__ out, int chunk, const int *done) {
+    if (is_done(done)) return;
+    const int g = blockIdx.x * 256 + threadIdx.x;
+    if (g >= (int)C.plane) return;
+    const int cj = g / C.n3, cm = g - cj * C.n3;
+    const int ci0 = blockIdx.y * chunk, ci1 = min(ci0 + chunk, C.nx);
+    const int fj = 2 * cj, fm = 2 * cm;
+    const bool jm = fj - 1 >= 0, jp = fj + 1 < F.n2, mm = fm - 1 >= 0, mp = fm + 1 < F.n3;
+    const cd zero = mk(0, 0);
+    // 2-D partial of global fine plane gf (zero outside the grid / slab data)
+    auto partial = [&](int gf) -> cd {
+        if (gf < 0 || gf >= F.n1) return zero;
+        const cd *pl = r + (long long)(gf - F.lo1) * F.plane + (long long)fj * F.n3 + fm;
+        cd s = zero;
+#pragma unroll
+        for (int a = -1; a <= 1; a++) {
+            const bool rok = a < 0 ? jm : (a > 0 ? jp : true);
+            const cd *row = pl + a * F.n3;
+            const cd v0 = rok && mm ? __ldg(row - 1) : zero;
+            const cd v1 = rok ? __ldg(row) : zero;
+            const cd v2 = rok && mp ? __ldg(row + 1) : zero;
+            const cd rs = cadd(cadd(v0, cscal(v1, 2.0)), v2);
+            s = cadd(s, a == 0 ? cscal(rs, 2.0) : rs);
+        }
+        return s;
+    };
+    cd prev = partial(2 * (C.lo1 + ci0) - 1);
+    for (int ci = ci0; ci < ci1; ci++) {
+        const int gc = C.lo1 + ci;
+        const cd pe = partial(2 * gc), po = partial(2 * gc + 1);
+        cd acc = cadd(cadd(prev, cscal(pe, 2.0)), po);
+        acc = mk(acc.x / 64.0, acc.y / 64.0);
+        const int onb = (gc == 0 || gc == C.n1 - 1) + (cj == 0 || cj == C.n2 - 1) + (cm == 0 || cm == C.n3 - 1);
+        if (onb) {
+            if (C.bc == HF_BC_DIRICHLET) acc = zero;
+            else
+                for (int d = 0; d < onb; d++) acc = cscal(acc, 64.0 / 48.0);
+        }
+        out[(long long)ci * C.plane + g] = acc;
+        prev = po;
+    }
+}
+
 __global__ void __launch_bounds__(256) k_restrict2(Lvl F, Lvl C, const cd *__restrict__ r,
                                                    cd *__restrict__ out, int chunk, const int *done) {
     __shared__ __align__(16) RestrictSmem sm;
@@ -2721,6 +2770,14 @@ void launch_dinv(const Lvl &L, cd *out_owned, cudaStream_t s) {
 }
 void launch_restrict(const Lvl &F, const Lvl &C, const cd *r, cd *out, cudaStream_t s,
                      const int *done) {
+    if (!std::getenv("HF_NO_FLAT")) {
+        const int gx = (int)((C.plane + 255) / 256);
+        int gz = std::max(1, std::min(C.nx, (148 * 8) / gx));
+        const int chunk = (C.nx + gz - 1) / gz;
+        gz = (C.nx + chunk - 1) / chunk;
+        launch(k_restrict_flat, dim3(gx, gz), dim3(256), 0, s, F, C, r, out, chunk, done);
+        return;
+    }
     int gx = (C.n3 + RC_X - 1) / RC_X, gy = (C.n2 + RC_Y - 1) / RC_Y;
     long long cols = (long long)gx * gy;
     int gz = (int)std::max<long long>(1, std::min<long long>(C.nx, (148 * 6 + cols - 1) / cols));

@@ -695,7 +695,11 @@ __global__ void __launch_bounds__(256, 3) k_flat_stencil(Lvl L, const cd *__rest
     // that are face vertices, rescaled in place by D^-1(nb)/D^-1(0) once their
     // plane lands (one plane ahead of its first use).  MODE_UP: every entry is
     // replaced by t = [w D^-1 b] + P e at the same point of the pipeline.
+#ifdef HF_EXP_NOFIX   // timing experiments only (wrong at the faces)
+    constexpr bool kFix = false;
+#else
     constexpr bool kFix = MODE == MODE_PRE && !KVAR;
+#endif
     constexpr bool kProd = MODE == MODE_UP;
     constexpr int NFE = (FS_PTS + 2 * (FS_MAX_N3 + 1) + 255) / 256;
     unsigned fe_nb = 0;                  // 2 bits per entry: in-plane face count
@@ -933,6 +937,7 @@ __global__ void __launch_bounds__(DR2_NT, 2) k_flat_dr(Lvl L, Lvl C, const cd *_
     const int rlo = max(2 * cr0 - 1, 0), rhi = min(2 * cr1 - 1, L.n2 - 1);   // residual rows
     const int blo = max(rlo - 1, 0), bhi = min(rhi + 1, L.n2 - 1);           // staged b rows
     const int nrp = (rhi - rlo + 1) * n3;                       // residual points per plane
+    const int dbo = (rlo - blo) * n3;                           // slot offset - tile offset
     const unsigned wbytes = (unsigned)((bhi - blo + 1) * n3) * 16u;
     const int selems = dr2_slot_elems(n3);
     const unsigned sraw = smem_u32(smem_raw);
@@ -972,55 +977,35 @@ __global__ void __launch_bounds__(DR2_NT, 2) k_flat_dr(Lvl L, Lvl C, const cd *_
     int rc[RPT], rf[RPT];
 #pragma unroll
     for (int t = 0; t < RPT; t++) {
+        // points enumerated interior columns first (m in [2, n3-3], row by row),
+        // then the four face-adjacent columns: the read-time face rescale then
+        // diverges in one warp instead of in every warp that spans a row end
         const int e = tid + DR2_NT * t;
         const int ee = e < nrp ? e : 0;
-        const int rr = rlo + ee / n3, m = ee - (ee / n3) * n3;
+        const int nrow = rhi - rlo + 1, ni = n3 >= 5 ? n3 - 4 : 0;
+        int rr, m;
+        if (ee < nrow * ni) {
+            rr = rlo + ee / ni;
+            m = 2 + (ee - (ee / ni) * ni);
+        } else if (ni > 0) {
+            const int e2 = ee - nrow * ni, k4 = e2 & 3;
+            rr = rlo + (e2 >> 2);
+            m = k4 < 2 ? k4 : n3 - 4 + k4;
+        } else {
+            rr = rlo + ee / n3;
+            m = ee - (ee / n3) * n3;
+        }
         rc[t] = (rr - blo) * n3 + m;
-        const int fj = (rr == 0) + (rr == n2 - 1), fm = (m == 0) + (m == n3 - 1);
-        rf[t] = (rr == 0) | (rr == n2 - 1) << 1 | (m == 0) << 2 | (m == n3 - 1) << 3 | (fj + fm) << 4;
+        auto fc1 = [](int x, int n) { return (x == 0) + (x == n - 1); };
+        const int fj = fc1(rr, n2), fm = fc1(m, n3);
+        const int jm = rr == 0 ? 1 : rr - 1, jp = rr == n2 - 1 ? n2 - 2 : rr + 1;
+        const int mm = m == 0 ? 1 : m - 1, mp = m == n3 - 1 ? n3 - 2 : m + 1;
+        // bits 0-3 mirror flags, 4-5 own in-plane face count, 6-13 the in-plane face
+        // counts of the ym, yp, zm, zp neighbours (for the MODE_PRE face rescale)
+        rf[t] = (rr == 0) | (rr == n2 - 1) << 1 | (m == 0) << 2 | (m == n3 - 1) << 3 | (fj + fm) << 4 |
+                (fc1(jm, n2) + fm) << 6 | (fc1(jp, n2) + fm) << 8 | (fj + fc1(mm, n3)) << 10 |
+                (fj + fc1(mp, n3)) << 12;
     }
-    // MODE_PRE rescale of face vertices in the slots (constant medium): own entries
-    constexpr int NFE = ((2 * DR2_CR + 3) * DR2_MAX_N3 + DR2_NT - 1) / DR2_NT;
-    unsigned long long fe = 0;           // 2 bits per entry: in-plane face count (3 = not in window)
-    if (!KVAR) {
-        const int W = (bhi - blo + 1) * n3;
-#pragma unroll
-        for (int t = 0; t < NFE; t++) {
-            const int e = tid + DR2_NT * t;
-            unsigned v = 3u;
-            if (e < W) {
-                const int j = blo + e / n3, m = e - (e / n3) * n3;
-                v = (unsigned)((j == 0) + (j == L.n2 - 1) + (m == 0) + (m == n3 - 1));
-            }
-            fe |= (unsigned long long)v << (2 * t);
-        }
-    }
-    // entries with an in-plane face count of 1 or 2 (interior planes rescale only those)
-    unsigned long long fe_face = 0;
-    if (!KVAR) {
-#pragma unroll
-        for (int t = 0; t < NFE; t++) {
-            const unsigned v = (unsigned)(fe >> (2 * t)) & 3u;
-            if (v == 1u || v == 2u) fe_face = 1;
-        }
-    }
-    auto fixup = [&](int gp) {
-        if (KVAR) return;
-        const int gm = gmirror(gp);
-        const int nbx = (gm == 0) + (gm == L.n1 - 1);
-        if (nbx == 0 && !fe_face) return;
-        cd *sl = slot(gp);
-#pragma unroll
-        for (int t = 0; t < NFE; t++) {
-            const unsigned v = (unsigned)(fe >> (2 * t)) & 3u;
-            if (v == 3u) continue;
-            const int nb = nbx + (int)v;
-            if (nb > 0) {
-                const int e = tid + DR2_NT * t;
-                sl[e] = cmul(sl[e], tab[8 + nb]);
-            }
-        }
-    };
     // coarse column of this thread: the LAST ncp threads (they carry one residual
     // point fewer than the first ones), so the per-plane work is balanced
     const int ncp = (cr1 - cr0) * C.n3;
@@ -1067,12 +1052,9 @@ __global__ void __launch_bounds__(DR2_NT, 2) k_flat_dr(Lvl L, Lvl C, const cd *_
         Pprev = P;
     };
 
-    // prologue: planes gpf-1, gpf, gpf+1 landed and rescaled
-    for (int gp = gpf - 1; gp <= gpf + 1 && gp <= stage_last; gp++) {
-        wait_plane(gp);
-        fixup(gp);
-    }
-    __syncthreads();
+    // prologue: planes gpf-1, gpf landed
+    wait_plane(gpf - 1);
+    wait_plane(gpf);
     const cd ap0 = KVAR ? mk(0, 0) : tab[0];
     const cd wd0 = KVAR ? mk(0, 0) : tab[4];
     // centre values of the residual points rotate through three register sets
@@ -1089,15 +1071,10 @@ __global__ void __launch_bounds__(DR2_NT, 2) k_flat_dr(Lvl L, Lvl C, const cd *_
             S1.v[t] = sc[rc[t]];
         }
     }
-    // one fine plane; EDGE: a face plane or a plane outside the grid (mirrors,
-    // zero residual) -- the interior planes take a select-free body
+    // one fine plane -- the interior planes take a select-free body
     auto step = [&](auto EDGEc, int gp, RV &P, RV &Cv, RV &N) {
         constexpr bool EDGE = decltype(EDGEc)::value;
         if (gp + 1 <= stage_last) wait_plane(gp + 1);
-        if (!KVAR && gp + 2 <= stage_last) {        // rescale plane gp+2 (visible after the barrier)
-            wait_plane(gp + 2);
-            fixup(gp + 2);
-        }
         const int buf = (gp - gpf) & 1;
         cd *rtile = rt + buf * (2 * DR2_CR + 1) * n3;
         const bool pin = !EDGE || (gp >= 0 && gp < n1);
@@ -1121,7 +1098,7 @@ __global__ void __launch_bounds__(DR2_NT, 2) k_flat_dr(Lvl L, Lvl C, const cd *_
                 const int c = rc[t], f = rf[t];
                 const int ym = (f & 1) ? c + n3 : c - n3, yp = (f & 2) ? c - n3 : c + n3;
                 const int zm = (f & 4) ? c + 1 : c - 1, zp = (f & 8) ? c - 1 : c + 1;
-                const int nb = nbx + (f >> 4);
+                const int nb = nbx + ((f >> 4) & 3);
                 cd fc = Cv.v[t];
                 cd xm = P.v[t], xp = N.v[t];
                 if (EDGE) {
@@ -1130,11 +1107,10 @@ __global__ void __launch_bounds__(DR2_NT, 2) k_flat_dr(Lvl L, Lvl C, const cd *_
                 }
                 cd vym = s0[ym], vyp = s0[yp], vzm = s0[zm], vzp = s0[zp];
                 cd post = wd0;
-                cd bc;
+                cd bc = fc;                               // staged b is unscaled
                 if (KVAR) {
                     const long long q = (long long)(gp - lo1) * plane + (long long)blo * n3 + c;
                     post = mk(omega, 0.0);
-                    bc = fc;
                     const cd *dv = L.dinv + q;
                     const long long dxm = bot ? plane : -(long long)plane;
                     const long long dxp = top ? -(long long)plane : plane;
@@ -1145,10 +1121,19 @@ __global__ void __launch_bounds__(DR2_NT, 2) k_flat_dr(Lvl L, Lvl C, const cd *_
                     vyp = cmul(vyp, __ldg(dv + (yp - c)));
                     vzm = cmul(vzm, __ldg(dv + (zm - c)));
                     vzp = cmul(vzp, __ldg(dv + (zp - c)));
-                } else if (nb) {                          // face vertex: unscaled centre
-                    bc = __ldg(b + (long long)(gp - lo1) * plane + (long long)blo * n3 + c);
-                } else {
-                    bc = fc;
+                } else if (EDGE || (f >> 6)) {
+                    // f = w D^-1 b with D^-1(nb) / D^-1(0) on the face vertices among the
+                    // seven (as the staged rescale of k_stencil, applied at read time)
+                    const int gxm = bot ? gp + 1 : gp - 1, gxp = top ? gp - 1 : gp + 1;
+                    const int nbxm = (gxm == 0) + (gxm == n1 - 1), nbxp = (gxp == 0) + (gxp == n1 - 1);
+                    auto sc = [&](cd v, int nbv) { return nbv > 0 ? cmul(v, tab[8 + nbv]) : v; };
+                    fc = sc(fc, nb);
+                    xm = sc(xm, nbxm + ((f >> 4) & 3));
+                    xp = sc(xp, nbxp + ((f >> 4) & 3));
+                    vym = sc(vym, nbx + ((f >> 6) & 3));
+                    vyp = sc(vyp, nbx + ((f >> 8) & 3));
+                    vzm = sc(vzm, nbx + ((f >> 10) & 3));
+                    vzp = sc(vzp, nbx + ((f >> 12) & 3));
                 }
                 const cd sum = cadd(cadd(cadd(xm, xp), cadd(vym, vyp)), cadd(vzm, vzp));
                 const cd ap = KVAR ? ap_of(L, __ldg(L.k + (long long)(gp - lo1) * plane +
@@ -1161,7 +1146,7 @@ __global__ void __launch_bounds__(DR2_NT, 2) k_flat_dr(Lvl L, Lvl C, const cd *_
                 if (!SOMM && nb) mf = cmul(post, fc);
                 rv = csub(bc, mf);
             }
-            rtile[e] = rv;
+            rtile[rc[t] - dbo] = rv;                  // row-major tile position
         }
         // the previous plane's residual tile is complete (last barrier): fold it
         // while the other warps still form this plane's tile
@@ -1169,8 +1154,10 @@ __global__ void __launch_bounds__(DR2_NT, 2) k_flat_dr(Lvl L, Lvl C, const cd *_
         __syncthreads();                             // tile complete; slot of gp-1 free
         if (tid == 0 && gp + DR2_RING - 1 <= stage_last) issue(gp + DR2_RING - 1);
     };
+    // EDGE: a face plane, a plane next to one (its x-neighbour needs the face
+    // rescale) or a plane outside the grid
     auto run = [&](int gp, RV &P, RV &Cv, RV &N) {
-        if (gp <= 0 || gp >= n1 - 1) step(IC<1>{}, gp, P, Cv, N);
+        if (gp <= 1 || gp >= n1 - 2) step(IC<1>{}, gp, P, Cv, N);
         else step(IC<0>{}, gp, P, Cv, N);
     };
     int gp = gpf;

@@ -695,11 +695,7 @@ __global__ void __launch_bounds__(256, 3) k_flat_stencil(Lvl L, const cd *__rest
     // that are face vertices, rescaled in place by D^-1(nb)/D^-1(0) once their
     // plane lands (one plane ahead of its first use).  MODE_UP: every entry is
     // replaced by t = [w D^-1 b] + P e at the same point of the pipeline.
-#ifdef HF_EXP_NOFIX   // timing experiments only (wrong at the faces)
-    constexpr bool kFix = false;
-#else
     constexpr bool kFix = MODE == MODE_PRE && !KVAR;
-#endif
     constexpr bool kProd = MODE == MODE_UP;
     constexpr int NFE = (FS_PTS + 2 * (FS_MAX_N3 + 1) + 255) / 256;
     unsigned fe_nb = 0;                  // 2 bits per entry: in-plane face count

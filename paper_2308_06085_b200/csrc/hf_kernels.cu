@@ -2730,6 +2730,8 @@ static void corr(int mode, const Lvl &F, const Lvl &C, const cd *b, const cd *e,
     // kernel, so parallelism beats the coarse-plane reuse of longer marches)
     const int chunk = 2;
     if (!std::getenv("HF_NO_FLAT")) {   // flat thread mapping (no ragged 32 x 8 tiles)
+        static const int fchunk = std::getenv("HF_CORR_CHUNK") ? std::atoi(std::getenv("HF_CORR_CHUNK")) : 4;
+        const int chunk = fchunk;
         dim3 gf((unsigned)((F.plane + 255) / 256), (F.nx + chunk - 1) / chunk);
         if (mode == 0) launch(k_corr_flat<0>, gf, dim3(256), 0, s, F, C, b, e, out, omega, chunk, done);
         else if (mode == 1) launch(k_corr_flat<1>, gf, dim3(256), 0, s, F, C, b, e, out, omega, chunk, done);

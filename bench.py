@@ -471,7 +471,8 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--cpu-iters", type=int, default=20)
+    # reference arm: each step is the full 129^3 solve (~3 s on the box's 16 cores)
+    ap.add_argument("--cpu-iters", type=int, default=MAXIT)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":

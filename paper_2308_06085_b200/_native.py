@@ -18,6 +18,7 @@ CYCLE = {"V": 0, "F": 1}
 METHOD = {"gmres": 0, "bicgstab": 1, "idrs": 2}
 COARSEST = {"direct": 0, "gmres": 1, "external": 2}
 BREAKDOWN = {0: None, 1: "arnoldi", 2: "rho", 3: "omega", 4: "projection"}
+ERR_ARG = -1
 ERR_ZERO_DIAGONAL = -3
 ERR_UNSUPPORTED = -4
 

@@ -120,3 +120,18 @@ class TestProblems:
         np.testing.assert_array_equal(np.asarray(m.velocities), c)
         with pytest.raises(problems.ProblemError):
             problems.read_velocity_grid(path, (9, 9, 6))
+
+
+def test_abi_argument_errors_without_a_gpu():
+    """Argument validation of the C ABI runs before any CUDA call: bad handles
+    and requests come back as error codes / NULL with a message."""
+    import ctypes as C
+    from paper_2308_06085_b200 import _native
+    L = _native.load()
+    assert not L.hf_bcg_create(None, 1e-6, 10, 1e-30)
+    assert "Bi-CGSTAB state" in _native.last_error()
+    ms = C.c_float()
+    assert L.hf_solver_bench_vec(None, 0, 1, C.byref(ms)) == _native.ERR_ARG
+    assert L.hf_bcg_step(None, 2, None) == _native.ERR_ARG
+    assert L.hf_level_down_restrict(None, 0, None, None) == _native.ERR_ARG
+    assert L.hf_level_up(None, 0, None, None, None) == _native.ERR_ARG

@@ -112,7 +112,7 @@ static bool zero_diagonal(const Lvl &L, const double *kfull) {
 
 static int make_level(Allocs &A, Level &lv, int n1, int n2, int n3, int lo1, int nx, double h,
                       double sre, double sim, int bc, const double *kfull, double kc,
-                      bool scratch) {
+                      bool scratch, bool finest = false) {
     init_kernel_attributes();
     if (n1 < 3 || n2 < 3 || n3 < 3) return fail(HF_ERR_ARG, "grid dims must all be >= 3");
     if (!(h > 0)) return fail(HF_ERR_ARG, "grid spacing must be positive");
@@ -173,11 +173,15 @@ static int make_level(Allocs &A, Level &lv, int n1, int n2, int n3, int lo1, int
         L.dinv = dv;
     }
     if (scratch) {
-        lv.b = new_field(A, nx, L.plane, err);
-        lv.u = new_field(A, nx, L.plane, err);
+        // the finest level's cycle works on the caller's r and z: no b / u copies
+        // there (17 GB at 1025 x 1025 x 513)
+        if (!finest) {
+            lv.b = new_field(A, nx, L.plane, err);
+            lv.u = new_field(A, nx, L.plane, err);
+        }
         lv.r = new_field(A, nx, L.plane, err);
         lv.t = new_field(A, nx, L.plane, err);
-        if (!lv.b || !lv.u || !lv.r || !lv.t) return fail(HF_ERR_CUDA, "cudaMalloc level scratch");
+        if ((!finest && (!lv.b || !lv.u)) || !lv.r || !lv.t) return fail(HF_ERR_CUDA, "cudaMalloc level scratch");
     }
     return 0;
 }
@@ -556,7 +560,7 @@ extern "C" hf_hierarchy *hf_hierarchy_create(int n1, int n2, int n3, int lo1, in
     double hh = h;
     for (int lvl = 0;; lvl++) {
         Level lv;
-        if (make_level(H->A, lv, a, b, c, l0, cnx, hh, sre, sim, bc, kf, k_const, true)) {
+        if (make_level(H->A, lv, a, b, c, l0, cnx, hh, sre, sim, bc, kf, k_const, true, lvl == 0)) {
             delete H;
             return nullptr;
         }
@@ -781,8 +785,9 @@ extern "C" hf_operator *hf_operator_create(int n1, int n2, int n3, int lo1, int 
                                            double shift_re, double shift_im, int bc,
                                            const double *k_host, double k_const) {
     auto *op = new hf_operator();
+    // no scratch fields: only hf_jacobi_smooth needs one (allocated on first use)
     if (make_level(op->A, op->lv, n1, n2, n3, lo1, nx, h, shift_re, shift_im, bc, k_host, k_const,
-                   true)) {
+                   false)) {
         delete op;
         return nullptr;
     }
@@ -831,6 +836,11 @@ extern "C" int hf_jacobi_smooth(hf_operator *op, double *u, const double *b, dou
     if (!op || !u || !b) return fail(HF_ERR_ARG, "null argument");
     cudaStream_t s = work_stream();
     Level &lv = op->lv;
+    if (!scratch && !lv.t) {
+        cudaError_t err;
+        lv.t = new_field(op->A, lv.L.nx, lv.L.plane, err);
+        if (!lv.t) return fail(HF_ERR_CUDA, "cudaMalloc smoother scratch");
+    }
     cd *tmp = scratch ? (cd *)scratch : lv.t;
     size_t bytes = (size_t)lv.L.nx * lv.L.plane * sizeof(cd);
     bool first = assume_zero != 0;

@@ -233,3 +233,25 @@ def test_unknown_method_and_invalid_s_rejected():
         S.solve(b, SolverConfig(method="cg"))
     with pytest.raises((KrylovError, ValueError)):
         S.solve(b, SolverConfig(method="idrs", s=0))
+
+
+@pytest.mark.parametrize("method", ["gmres", "bicgstab", "idrs"])
+def test_exact_preconditioner_converges_in_one_step(method):
+    """reference test_left_preconditioning_exact_inverse: with the operator
+    itself as the CSLP and a one-level hierarchy (the exact separable coarsest
+    solve), M^-1 = A^-1 and the Krylov method stops after one application."""
+    from paper_2308_06085_b200 import make_grid
+    from paper_2308_06085_b200.krylov import Solver, SolverConfig
+    from paper_2308_06085_b200.multigrid import MGConfig, build_hierarchy
+    from paper_2308_06085_b200.operators import OperatorSpec, Sommerfeld, StencilOperator
+    n = (17, 17, 17)
+    grid = make_grid(*n, 1.0 / 16)
+    spec = OperatorSpec("cslp", 1.0, -0.5, Sommerfeld(), np.full(n, 30.0))
+    A = StencilOperator(spec, grid)
+    H = build_hierarchy(grid, None, spec, MGConfig(coarsest_threshold=64))
+    assert len(H.levels) == 1 and H.coarsest_kind == "separable"
+    b = _rand(n, 12)
+    x, rep = Solver(A, H).solve(b, SolverConfig(method=method, tol=1e-10))
+    assert rep.converged and rep.iterations <= 1, rep
+    r = torch.as_tensor(b).cuda() - A.apply(x)
+    assert float(r.norm() / np.linalg.norm(b)) < 1e-10

@@ -88,3 +88,56 @@ def test_slab_device_bicgstab_matches_single(nslabs):
     assert rs.converged and abs(rs.iterations - r1.iterations) <= 1, (rs.iterations, r1.iterations)
     assert np.linalg.norm(xs - x1) / np.linalg.norm(x1) < 1e-8
     assert len(rs.residual_history) == rs.iterations
+
+
+_NCCL_CHILD = r'''
+import os, sys, json
+import numpy as np
+import torch
+import torch.distributed as dist
+sys.path.insert(0, os.getcwd())
+from paper_2308_06085_b200 import problems
+from paper_2308_06085_b200.dist import SlabSolver
+from paper_2308_06085_b200.krylov import SolverConfig
+from paper_2308_06085_b200.partition import TorchSlabComm, slab_partition
+os.environ["MASTER_ADDR"] = "127.0.0.1"
+os.environ["MASTER_PORT"] = sys.argv[1]
+torch.cuda.set_device(0)
+dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+p = problems.point_source_cube(65, 40.0, "sommerfeld")
+spec, b = problems.build_problem(p)
+e = slab_partition(p.grid, 1)[0]
+S = SlabSolver(p.grid, [e], spec.k_field, p.bc, TorchSlabComm())
+xs, rep = S.solve_device([b], SolverConfig(method="bicgstab"))
+np.save(sys.argv[2], xs[0].cpu().numpy())
+print(json.dumps({"iterations": rep.iterations, "converged": rep.converged}))
+dist.destroy_process_group()
+'''
+
+
+def test_nccl_comm_device_solve_world1(tmp_path):
+    """The N > 1 bench path (TorchSlabComm over NCCL, device all-reduce of the
+    Bi-CGSTAB partial sums) on a one-rank NCCL group matches the single-slab
+    graph solve."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    from paper_2308_06085_b200 import problems
+    p = problems.point_source_cube(65, 40.0, "sommerfeld")
+    k = np.full(p.grid.shape, 40.0)
+    b, x1, r1, _ = _single(p, k)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    out = tmp_path / "x.npy"
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = subprocess.run([sys.executable, "-c", _NCCL_CHILD, str(port), str(out)], cwd=root,
+                         capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, res.stderr[-2000:]
+    rep = json.loads(res.stdout.strip().splitlines()[-1])
+    assert rep["converged"] and abs(rep["iterations"] - r1.iterations) <= 1
+    xs = np.load(out)
+    assert np.linalg.norm(xs - x1) / np.linalg.norm(x1) < 1e-8

@@ -157,6 +157,11 @@ int hf_level_down_restrict(hf_hierarchy *hier, int level, const double *b, doubl
 int hf_level_correct(hf_hierarchy *hier, int level, const double *b, const double *e_coarse,
                      double *t);
 int hf_level_smooth(hf_hierarchy *hier, int level, const double *t, const double *b, double *u);
+/* correct on the owned planes and on the ghost planes at interior slab faces (b's
+ * HF_GHOST-deep halo and one coarse ghost plane of e must be valid), so the
+ * smoothing sweep needs no halo exchange of t. */
+int hf_level_correct_ext(hf_hierarchy *hier, int level, const double *b, const double *e_coarse,
+                         double *t);
 /* correct + smooth in one pass (whole-grid levels; split kernels on slabs):
  * u = t + w D^-1 (b - M t), t = [w D^-1 b] + P e (multigrid.py:389-392, 153-156). */
 int hf_level_up(hf_hierarchy *hier, int level, const double *b, const double *e_coarse, double *u);

@@ -1252,14 +1252,17 @@ __device__ __forceinline__ void corr_col(const Lvl &F, const Lvl &C, const cd *_
 
 // flat variant: thread = one fine (i2, i3) vertex of the plane (no ragged tiles)
 template <int MODE>
+// local planes [plo, phi): the owned planes, or with the ghost planes at interior
+// slab faces (the slab driver then skips the halo exchange of t)
 __global__ void __launch_bounds__(256) k_corr_flat(Lvl F, Lvl C, const cd *__restrict__ b,
                                                    const cd *__restrict__ e, cd *__restrict__ out,
-                                                   double omega, int chunk, const int *done) {
+                                                   double omega, int chunk, int plo, int phi,
+                                                   const int *done) {
     if (is_done(done)) return;
     const int f = blockIdx.x * 256 + threadIdx.x;
     if (f >= (int)F.plane) return;
     const int j = f / F.n3, m = f - j * F.n3;
-    const int i0 = blockIdx.y * chunk, i1 = min(i0 + chunk, F.nx);
+    const int i0 = plo + blockIdx.y * chunk, i1 = min(i0 + chunk, phi);
     corr_col<MODE>(F, C, b, e, out, omega, j, m, i0, i1);
 }
 
@@ -2725,17 +2728,19 @@ void launch_down1(const Lvl &L, const cd *b, cd *r, double omega, cudaStream_t s
     stencil<MODE_PRE, EpiResid, 0>(L, b, b, omega, EpiResid{r}, RedSlot{}, s, done);
 }
 static void corr(int mode, const Lvl &F, const Lvl &C, const cd *b, const cd *e, cd *out,
-                 double omega, cudaStream_t s, const int *done) {
-    // two fine planes per thread: every load of the pair is independent (latency-bound
-    // kernel, so parallelism beats the coarse-plane reuse of longer marches)
+                 double omega, cudaStream_t s, const int *done, bool ghosts = false) {
+    // tiled variant: two fine planes per thread (every load of the pair independent)
     const int chunk = 2;
-    if (!std::getenv("HF_NO_FLAT")) {   // flat thread mapping (no ragged 32 x 8 tiles)
+    if (ghosts || !std::getenv("HF_NO_FLAT")) {   // flat thread mapping (no ragged tiles)
+        // four fine planes per thread (coarse-plane sums reused between them)
         static const int fchunk = std::getenv("HF_CORR_CHUNK") ? std::atoi(std::getenv("HF_CORR_CHUNK")) : 4;
         const int chunk = fchunk;
-        dim3 gf((unsigned)((F.plane + 255) / 256), (F.nx + chunk - 1) / chunk);
-        if (mode == 0) launch(k_corr_flat<0>, gf, dim3(256), 0, s, F, C, b, e, out, omega, chunk, done);
-        else if (mode == 1) launch(k_corr_flat<1>, gf, dim3(256), 0, s, F, C, b, e, out, omega, chunk, done);
-        else launch(k_corr_flat<2>, gf, dim3(256), 0, s, F, C, b, e, out, omega, chunk, done);
+        const int plo = ghosts && F.lo1 > 0 ? -1 : 0;
+        const int phi = ghosts && F.lo1 + F.nx < F.n1 ? F.nx + 1 : F.nx;
+        dim3 gf((unsigned)((F.plane + 255) / 256), (phi - plo + chunk - 1) / chunk);
+        if (mode == 0) launch(k_corr_flat<0>, gf, dim3(256), 0, s, F, C, b, e, out, omega, chunk, plo, phi, done);
+        else if (mode == 1) launch(k_corr_flat<1>, gf, dim3(256), 0, s, F, C, b, e, out, omega, chunk, plo, phi, done);
+        else launch(k_corr_flat<2>, gf, dim3(256), 0, s, F, C, b, e, out, omega, chunk, plo, phi, done);
         return;
     }
     dim3 g((F.n3 + 31) / 32, (F.n2 + 7) / 8, (F.nx + chunk - 1) / chunk);
@@ -2829,8 +2834,8 @@ void launch_prolong(const Lvl &F, const Lvl &C, const cd *e, cd *out, bool add, 
 // u = u1 + w D^-1 (b - M u1), u1 = [w D^-1 b] + P e: pointwise correction into
 // the scratch field t, then one Jacobi sweep stencil (multigrid.py:337-343)
 void launch_correct(const Lvl &L, const Lvl &C, const cd *b, const cd *e, cd *t, double omega,
-                    bool pre, cudaStream_t s, const int *done) {
-    corr(pre ? 1 : 0, L, C, b, e, t, omega, s, done);
+                    bool pre, cudaStream_t s, const int *done, bool ghosts) {
+    corr(pre ? 1 : 0, L, C, b, e, t, omega, s, done, ghosts);
 }
 int launch_up1(const Lvl &L, const Lvl &C, const cd *b, const cd *e, cd *u, cd *t, double omega,
                bool pre, cudaStream_t s, const int *done) {

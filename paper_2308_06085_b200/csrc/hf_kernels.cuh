@@ -32,8 +32,9 @@ void launch_prolong(const Lvl &F, const Lvl &C, const cd *e, cd *out, bool add, 
 int launch_up1(const Lvl &L, const Lvl &C, const cd *b, const cd *e, cd *u, cd *t, double omega,
                bool pre, cudaStream_t s, const int *done);
 void launch_dinv(const Lvl &L, cd *out_owned, cudaStream_t s);
+// ghosts: also the ghost planes at interior slab faces (b and e halos must be valid)
 void launch_correct(const Lvl &L, const Lvl &C, const cd *b, const cd *e, cd *t, double omega,
-                    bool pre, cudaStream_t s, const int *done);
+                    bool pre, cudaStream_t s, const int *done, bool ghosts = false);
 void launch_gemv(int N, const cd *Minv, const cd *b, cd *x, cudaStream_t s, const int *done);
 void launch_sym_pack(int N, const cd *Minv, const double *sv, cd *tiles, cudaStream_t s);
 void launch_symv(int N, const cd *tiles, const double *sv, const cd *b, cd *prow, cd *pcol, cd *x,

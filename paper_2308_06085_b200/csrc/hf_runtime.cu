@@ -752,6 +752,17 @@ extern "C" int hf_level_correct(hf_hierarchy *H, int l, const double *b, const d
     CKL();
     return 0;
 }
+// t on the owned planes AND the ghost planes at interior slab faces (needs b's
+// ghost planes and one coarse ghost plane of e): the slab driver then skips the
+// halo exchange of t before the post-smoothing sweep
+extern "C" int hf_level_correct_ext(hf_hierarchy *H, int l, const double *b, const double *e,
+                                    double *t) {
+    if (!H || l < 0 || l + 1 >= (int)H->lev.size()) return fail(HF_ERR_ARG, "bad level");
+    L1(launch_correct(H->lev[l].L, H->lev[l + 1].L, (const cd *)b, (const cd *)e, (cd *)t,
+                      H->cfg.omega, H->cfg.nu1 == 1, work_stream(), nullptr, true));
+    CKL();
+    return 0;
+}
 extern "C" int hf_level_smooth(hf_hierarchy *H, int l, const double *t, const double *b,
                                double *u) {
     if (!H || l < 0 || l >= (int)H->lev.size()) return fail(HF_ERR_ARG, "bad level");

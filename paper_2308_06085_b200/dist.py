@@ -168,10 +168,12 @@ class SlabSolver:
             self.fu[r][n - 1].owned.copy_(self.xc[e.lo1 - 1:e.hi1])
         for l in range(n - 2, -1, -1):
             self._halo([self.fu[r][l + 1] for r in S])
+            # t on the owned planes and the interior-face ghost planes (b's halo from the
+            # down-sweep is still valid): no halo exchange of t before the sweep
             for r in S:
-                _native.check(L.hf_level_correct(self.H[r], l, _ptr(self.fb[r][l].owned),
-                                                 _ptr(self.fu[r][l + 1].owned), _ptr(self.ft[r][l].owned)))
-            self._halo([self.ft[r][l] for r in S])
+                _native.check(L.hf_level_correct_ext(self.H[r], l, _ptr(self.fb[r][l].owned),
+                                                     _ptr(self.fu[r][l + 1].owned),
+                                                     _ptr(self.ft[r][l].owned)))
             for r in S:
                 out = dst[r] if l == 0 else self.fu[r][l]
                 _native.check(L.hf_level_smooth(self.H[r], l, _ptr(self.ft[r][l].owned),

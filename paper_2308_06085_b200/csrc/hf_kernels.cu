@@ -1,12 +1,15 @@
 // hf_kernels.cu -- sm_100a kernels of the CSLP / multigrid / Bi-CGSTAB path.
 //
-// Stencil kernels march along i1 (one thread per (i2, i3) column, a chunk of
-// planes per block).  Multigrid kernels are fused where the reference's
-// sequence allows it without changing results:
-//   k_down1 : pre-smooth from zero + residual   r = b - M (w D^-1 b)
-//             (multigrid.py:373-386, nu1 == 1)
-//   k_up1   : prolong + correct + post-smooth   u = u1 + w D^-1 (b - M u1),
-//             u1 = w D^-1 b + P e                 (multigrid.py:389-392, 138-157)
+// Stencil kernels march along i1.  Planes up to 255 wide use the FLAT kernels:
+// a block owns a contiguous range of the (i2, i3) plane, its halo arrives as one
+// cp.async.bulk per plane on an mbarrier (k_flat_stencil, k_flat_dr, plus
+// k_corr_flat / k_restrict_flat); wider planes use the 2-D tiled cp.async
+// kernels (k_stencil, k_down_restrict, k_restrict2, k_corr).  Multigrid steps
+// are fused where the reference's sequence allows it:
+//   down : pre-smooth from zero + residual + full weighting
+//          b_c = R (b - M (w D^-1 b))          (multigrid.py:373-386, 171-221)
+//   up   : prolong + correct, then one Jacobi sweep
+//          u = t + w D^-1 (b - M t), t = w D^-1 b + P e   (multigrid.py:389-392, 138-157)
 // Krylov vector updates carry their inner products in the same pass, with a
 // deterministic last-block reduction that also advances the Bi-CGSTAB scalars
 // on the device (krylov.py:207-276).

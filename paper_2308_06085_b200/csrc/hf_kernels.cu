@@ -1713,7 +1713,18 @@ __global__ void __launch_bounds__(256) k_bcg_s(long long n, const BcgState *st,
     if (is_done(done)) return;
     cd al = st->alpha;
     cd acc[1] = {mk(0, 0)};
-    for (long long q = blockIdx.x * 256ll + threadIdx.x; q < n; q += (long long)gridDim.x * 256) {
+    const long long S = (long long)gridDim.x * 256;
+    long long q = blockIdx.x * 256ll + threadIdx.x;
+    // two strides per trip; the per-thread accumulation order is unchanged
+    for (; q + S < n; q += 2 * S) {
+        cd r0 = __ldg(r + q), r1 = __ldg(r + q + S), v0 = __ldg(v + q), v1 = __ldg(v + q + S);
+        cd s0 = csub(r0, cmul(al, v0)), s1 = csub(r1, cmul(al, v1));
+        s[q] = s0;
+        s[q + S] = s1;
+        acc[0] = cadd(acc[0], cjmul(s0, s0));
+        acc[0] = cadd(acc[0], cjmul(s1, s1));
+    }
+    if (q < n) {
         cd sv = csub(__ldg(r + q), cmul(al, __ldg(v + q)));
         s[q] = sv;
         acc[0] = cadd(acc[0], cjmul(sv, sv));

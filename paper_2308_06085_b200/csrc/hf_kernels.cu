@@ -1079,7 +1079,7 @@ __global__ void __launch_bounds__(DR2_NT, 2) k_flat_dr(Lvl L, Lvl C, const cd *_
         const bool pin = !EDGE || (gp >= 0 && gp < n1);
         const bool bot = EDGE && gp == 0, top = EDGE && gp == n1 - 1;
         const cd *s0 = slot(gp);
-        if (!top && gp + 1 <= stage_last) {
+        if (!EDGE || (!top && gp + 1 <= stage_last)) {  // (always true off the faces)
             const cd *sn = slot(gp + 1);
 #pragma unroll
             for (int t = 0; t < RPT; t++) N.v[t] = sn[rc[t]];

@@ -2832,7 +2832,9 @@ template <bool KVAR, bool SOMM, int RPT>
 static void dr2_launch(const Lvl &F, const Lvl &C, const cd *b, cd *out, double omega, cudaStream_t s,
                        const int *done) {
     const int gx = (C.n2 + DR2_CR - 1) / DR2_CR;
-    int gz = std::max(1, std::min(C.nx, (148 * 2 + gx - 1) / gx));
+    const char *tb = std::getenv("HF_DR_BLOCKS");      // A/B: target block count
+    const int target = tb ? std::atoi(tb) : 148 * 2;
+    int gz = std::max(1, std::min(C.nx, (target + gx - 1) / gx));
     const int chunk = (C.nx + gz - 1) / gz;
     gz = (C.nx + chunk - 1) / chunk;
     const size_t smem = (size_t)DR2_RING * dr2_slot_elems(F.n3) * 16 + (size_t)2 * (2 * DR2_CR + 1) * F.n3 * 16 + 128;

@@ -647,7 +647,9 @@ static void v_cycle(hf_hierarchy *H, int li, const cd *b, cd *u, cudaStream_t s,
     const bool fused = c.nu1 <= 1 && c.nu2 == 1;
     // fused down + restriction (k_flat_dr) where it applies; the tiled fused kernel
     // (wider planes) is opt-in (HF_DR=1): slower than the split pair there
+    const char *drmin = std::getenv("HF_DR_MIN_N3");   // A/B: split pair below this plane width
     const bool split_dr = std::getenv("HF_NO_DR") != nullptr ||
+                          (drmin && lv.L.n3 < std::atoi(drmin)) ||
                           (!flat_dr_ok(lv.L) && std::getenv("HF_DR") == nullptr);
     if (c.nu1 == 1 && fused && !split_dr) {
         L1(launch_down_restrict(lv.L, nx.L, b, nx.b, c.omega, s, done));

@@ -1056,37 +1056,17 @@ __global__ void __launch_bounds__(DR2_NT, 2) k_flat_dr(Lvl L, Lvl C, const cd *_
     wait_plane(gpf);
     const cd ap0 = KVAR ? mk(0, 0) : tab[0];
     const cd wd0 = KVAR ? mk(0, 0) : tab[4];
-    // centre values of the residual points rotate through three register sets
-    // (planes gp-1, gp, gp+1) with a 3-way unrolled march
-    struct RV {
-        cd v[RPT];
-    };
-    RV S0, S1, S2;
-    {
-        const cd *sp = slot(gpf - 1), *sc = slot(gpf);
-#pragma unroll
-        for (int t = 0; t < RPT; t++) {
-            S0.v[t] = sp[rc[t]];
-            S1.v[t] = sc[rc[t]];
-        }
-    }
     // one fine plane -- the interior planes take a select-free body
-    auto step = [&](auto EDGEc, int gp, RV &P, RV &Cv, RV &N) {
+    auto step = [&](auto EDGEc, int gp) {
         constexpr bool EDGE = decltype(EDGEc)::value;
         if (gp + 1 <= stage_last) wait_plane(gp + 1);
         const int buf = (gp - gpf) & 1;
         cd *rtile = rt + buf * (2 * DR2_CR + 1) * n3;
         const bool pin = !EDGE || (gp >= 0 && gp < n1);
         const bool bot = EDGE && gp == 0, top = EDGE && gp == n1 - 1;
-        const cd *s0 = slot(gp);
-        if (!EDGE || (!top && gp + 1 <= stage_last)) {  // (always true off the faces)
-            const cd *sn = slot(gp + 1);
-#pragma unroll
-            for (int t = 0; t < RPT; t++) N.v[t] = sn[rc[t]];
-        } else {
-#pragma unroll
-            for (int t = 0; t < RPT; t++) N.v[t] = P.v[t];   // mirrored plane n1-2
-        }
+        // planes gp-1 and gp+1 are staged mirrored at the faces (issue()), so the
+        // x-neighbours read straight from their slots
+        const cd *s0 = slot(gp), *sm1 = slot(gp - 1), *sp1 = slot(gp + 1);
         const int nbx = (int)bot + (int)top;
 #pragma unroll
         for (int t = 0; t < RPT; t++) {
@@ -1098,12 +1078,8 @@ __global__ void __launch_bounds__(DR2_NT, 2) k_flat_dr(Lvl L, Lvl C, const cd *_
                 const int ym = (f & 1) ? c + n3 : c - n3, yp = (f & 2) ? c - n3 : c + n3;
                 const int zm = (f & 4) ? c + 1 : c - 1, zp = (f & 8) ? c - 1 : c + 1;
                 const int nb = nbx + ((f >> 4) & 3);
-                cd fc = Cv.v[t];
-                cd xm = P.v[t], xp = N.v[t];
-                if (EDGE) {
-                    if (bot) xm = N.v[t];
-                    if (top) xp = P.v[t];
-                }
+                cd fc = s0[c];
+                cd xm = sm1[c], xp = sp1[c];
                 cd vym = s0[ym], vyp = s0[yp], vzm = s0[zm], vzp = s0[zp];
                 cd post = wd0;
                 cd bc = fc;                               // staged b is unscaled
@@ -1155,18 +1131,11 @@ __global__ void __launch_bounds__(DR2_NT, 2) k_flat_dr(Lvl L, Lvl C, const cd *_
     };
     // EDGE: a face plane, a plane next to one (its x-neighbour needs the face
     // rescale) or a plane outside the grid
-    auto run = [&](int gp, RV &P, RV &Cv, RV &N) {
-        if (gp <= 1 || gp >= n1 - 2) step(IC<1>{}, gp, P, Cv, N);
-        else step(IC<0>{}, gp, P, Cv, N);
-    };
-    int gp = gpf;
-    for (; gp + 3 <= gpl + 1; gp += 3) {
-        run(gp, S0, S1, S2);
-        run(gp + 1, S1, S2, S0);
-        run(gp + 2, S2, S0, S1);
+#pragma unroll 1
+    for (int gp = gpf; gp <= gpl; gp++) {
+        if (gp <= 1 || gp >= n1 - 2) step(IC<1>{}, gp);
+        else step(IC<0>{}, gp);
     }
-    if (gp <= gpl) run(gp, S0, S1, S2);
-    if (gp + 1 <= gpl) run(gp + 1, S1, S2, S0);
     if (cact) fold(gpl, partial(rt + ((gpl - gpf) & 1) * (2 * DR2_CR + 1) * n3));
 }
 

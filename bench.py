@@ -447,16 +447,21 @@ def run_reference(args):
     rank, world, _ = _env_rank()
     if rank != 0:
         return
-    vals, samples = [], []
+    vals, samples, secs = [], [], []
     for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
         cb = cpu_baseline(args.cpu_iters)
+        dt = time.perf_counter() - t0
         if i >= args.warmup:
             vals.append(cb["value"])
             samples.append(cb)
+            secs.append(dt)
     value = float(np.mean(vals))
     out = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "impl": "reference",
            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-           "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+           # one step = one bounded sample (the oracle's solve, setup included)
+           "ms_per_step": round(float(np.mean(secs)) * 1e3, 2),
+           "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "c128", "data": "synthetic",
            "config": _config_dict({"parallelism": "host cores (OpenMP)"}),
            "cpu_baseline": {**samples[-1], "value": round(value, 3)},

@@ -1,6 +1,6 @@
 """Live CUDA-event kernel table (bench.kernel_table) on a larger cube.
 
-    python tools/kernel_table_at.py 513
+    python tools/kernel_table_at.py 513 [wedge]
 """
 import json
 import os
@@ -15,7 +15,8 @@ from paper_2308_06085_b200.multigrid import MGConfig, build_hierarchy  # noqa: E
 from paper_2308_06085_b200.operators import OperatorSpec, StencilOperator  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 513
-p = problems.point_source_cube(n, 80.0 * (n - 1) / 128, "sommerfeld")
+p = (problems.wedge3_problem(n) if "wedge" in sys.argv[2:]
+     else problems.point_source_cube(n, 80.0 * (n - 1) / 128, "sommerfeld"))
 spec, b = problems.build_problem(p)
 A = StencilOperator(spec, p.grid)
 H = build_hierarchy(p.grid, None, OperatorSpec("cslp", 1.0, -0.5, spec.bc, spec.k_field), MGConfig())
@@ -24,4 +25,5 @@ t = bench.kernel_table(A, H, n ** 3, 1.0)
 for k, v in t.items():
     v["frac"] = round(v["gbs"] / hbm, 4)
     v.pop("share", None)
-print(json.dumps({"grid": n, "peak_gbs": hbm, "kernels": t}))
+print(json.dumps({"grid": n, "medium": "wedge" if "wedge" in sys.argv[2:] else "const",
+                  "peak_gbs": hbm, "kernels": t}))

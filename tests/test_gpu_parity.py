@@ -227,6 +227,24 @@ def test_cycle_matches_oracle(hf, oracle, bc, cfg):
     assert _rel(got, want) < 1e-9
 
 
+@pytest.mark.parametrize("n,bc,kind", [((17, 17, 193), "sommerfeld", "const"),
+                                        ((9, 9, 161), "dirichlet", "field"),
+                                        ((9, 17, 255), "sommerfeld", "field")])
+def test_wide_plane_flat_kernels_match_oracle(hf, oracle, n, bc, kind, monkeypatch):
+    """Planes 154..255 vertices wide: the flat kernels' five-points-per-thread
+    fused down-sweep (k_flat_dr RPT 5) and the widest flat ranges, against the
+    oracle's V-cycle, and the fused down-sweep against the split pair."""
+    from paper_2308_06085_b200.multigrid import mg_precondition
+    k = np.full(n, 9.0) if kind == "const" else _kfield(n, 21, 6, 12)
+    hier, oh = _pair(hf, oracle, n, bc, k)
+    r = _rand(n, 22)
+    got = mg_precondition(hier, r).cpu().numpy()
+    assert _rel(got, oh.precondition(r)) < 1e-9
+    monkeypatch.setenv("HF_NO_DR", "1")
+    split = mg_precondition(hier, r).cpu().numpy()
+    assert _rel(got, split) < 1e-13
+
+
 def _solve_pair(hf, oracle, pspec, k_full, method="bicgstab", beta2=-0.5, tol=1e-6, maxit=400,
                 **mg):
     from paper_2308_06085_b200 import problems

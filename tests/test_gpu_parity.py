@@ -285,6 +285,19 @@ def test_bicgstab_heterogeneous_wedge(hf, oracle):
     assert np.linalg.norm(x - xo) / np.linalg.norm(xo) < 1e-8
 
 
+def test_bicgstab_noncubic_layered_wedge(hf, oracle):
+    """The reference's own two-interface wedge builder (problems.wedge_problem)
+    on a non-cubic 33 x 33 x 49 grid (h = 20 m, 5 Hz, kh <= 0.42)."""
+    from paper_2308_06085_b200 import problems
+    p = problems.wedge_problem(shape=(33, 33, 49), domain=((0.0, 640.0), (0.0, 640.0), (-960.0, 0.0)),
+                               frequency=5.0, source_at=(320.0, 320.0, 0.0))
+    k = p.medium.k_field(p.grid, hf.full_extent(p.grid))
+    x, rep, xo, ro = _solve_pair(hf, oracle, p, k)
+    assert rep.converged and ro["converged"]
+    assert abs(rep.iterations - ro["iterations"]) <= 1
+    assert np.linalg.norm(x - xo) / np.linalg.norm(xo) < 1e-8
+
+
 def test_solve_host_buffers(hf, oracle):
     """hf_solve_host (the e2e entry point) returns the same answer as hf_solve."""
     from paper_2308_06085_b200 import problems

@@ -39,10 +39,19 @@ extern "C" {
 #define HF_METHOD_BICGSTAB 1
 #define HF_METHOD_IDRS 2
 
-#define HF_COARSEST_DIRECT 0   /* dense LU-inverse, applied as one GEMV   */
-#define HF_COARSEST_GMRES 1    /* unpreconditioned full GMRES to tol (reserved) */
+#define HF_COARSEST_DIRECT 0   /* exact: fast diagonalisation, packed symmetric or dense inverse */
+#define HF_COARSEST_GMRES 1    /* the reference's unpreconditioned full GMRES to coarsest_tol,
+                                  at most coarsest_maxit iterations (multigrid.py:300-323) */
 #define HF_COARSEST_EXTERNAL 2 /* no coarsest solve: the caller gathers the
                                   coarse RHS and solves it (multi-GPU slabs)  */
+
+/* Bi-CGSTAB shadow vector r~ (B200 addition; the reference always takes r~ = b,
+ * krylov.py:229, which breaks down on the rho test for a point source on large
+ * wedge grids -- see DESIGN.md section 4) */
+#define HF_SHADOW_RHS 0
+#define HF_SHADOW_HOST 1
+#define HF_SHADOW_HASH 2   /* r~_q = splitmix64 hash of (seed, global index q), uniform in
+                              [-1/2, 1/2)^2 -- identical on any slab layout */
 
 #define HF_BREAKDOWN_NONE 0
 #define HF_BREAKDOWN_ARNOLDI 1
@@ -81,8 +90,12 @@ typedef struct hf_solver_config {
     int s;                   /* IDR shadow dimension */
     int restart;             /* GMRES restart length, 0 = full */
     double breakdown_tol;
-    const double *shadow_host;  /* IDR: s orthonormal vectors (s * N complex), host */
+    const double *shadow_host;  /* IDR: s orthonormal vectors (s * N complex), host;
+                                   Bi-CGSTAB: one shadow vector r~ (N complex), host */
     int check_every;         /* Bi-CGSTAB: iterations per host convergence poll */
+    int shadow_kind;         /* Bi-CGSTAB r~: HF_SHADOW_RHS (reference, r~ = b),
+                                HF_SHADOW_HOST (shadow_host), HF_SHADOW_HASH (seeded) */
+    uint64_t shadow_seed;    /* HF_SHADOW_HASH seed */
 } hf_solver_config;
 
 /* krylov.py:46-64 ConvergenceReport (phase_times reduced to device times) */
@@ -102,6 +115,13 @@ typedef struct hf_report {
 /* ---- library ----------------------------------------------------------- */
 const char *hf_last_error(void);
 int hf_version(void);
+/* Kernel-variant selection for A/B measurements and the parity tests that compare
+ * variants (process-wide; every variant computes the same arithmetic; all off is the
+ * measured-fastest default).  Names: "no_pdl", "no_flat", "no_flat_dr", "no_dr",
+ * "tiled_dr", "flat_up", "fuse_up", "no_fuse", "coarsest_dense".  The library reads
+ * no environment variables. */
+int hf_set_option(const char *name, int value);
+int hf_get_option(const char *name);   /* 0/1, or HF_ERR_ARG for an unknown name */
 /* Stream used by all subsequent calls of this thread (cudaStream_t, NULL = default). */
 void hf_set_stream(void *stream);
 int hf_device_synchronize(void);

@@ -376,6 +376,28 @@ void or_gmres(size_t n, or_op_fn A, void *actx, or_op_fn minv, void *mctx, const
     free(r0); free(w); free(tmp);
 }
 
+/* Bi-CGSTAB shadow vector (the B200 path's SolverConfig.shadow): 0 = r~ = b as in
+ * the reference (krylov.py:229); 2 = seeded hash vector, the same splitmix64
+ * formula as hf_device.cuh shadow_hash (an extension the reference does not
+ * have; parity of the extension is checked against this restatement). */
+static int or_shadow_mode = 0;
+static unsigned long long or_shadow_seed = 0;
+void or_set_bicgstab_shadow(int mode, unsigned long long seed) {
+    or_shadow_mode = mode; or_shadow_seed = seed;
+}
+static unsigned long long or_splitmix64(unsigned long long z) {
+    z += 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+static cplx or_shadow_hash(unsigned long long seed, unsigned long long q) {
+    unsigned long long a = or_splitmix64(seed * 0x632be59bd9b4e019ull + 2 * q);
+    unsigned long long b = or_splitmix64(seed * 0x632be59bd9b4e019ull + 2 * q + 1);
+    const double s = 1.0 / 9007199254740992.0;
+    return ((double)(a >> 11) * s - 0.5) + I * ((double)(b >> 11) * s - 0.5);
+}
+
 /* krylov.py:207-276: right-preconditioned Bi-CGSTAB, true-residual stopping. */
 void or_bicgstab(size_t n, or_op_fn A, void *actx, or_op_fn minv, void *mctx, const cplx *b,
                  cplx *x, double tol, int maxit, double breakdown_tol, or_report *rep) {
@@ -396,7 +418,11 @@ void or_bicgstab(size_t n, or_op_fn A, void *actx, or_op_fn minv, void *mctx, co
     if (or_norm(n, r) / bnorm <= tol) {
         rep->converged = 1; rep->final_relres = or_norm(n, r) / bnorm; goto done;
     }
-    memcpy(rs, r, n * sizeof(cplx));
+    if (or_shadow_mode == 2) {
+        for (size_t q = 0; q < n; q++) rs[q] = or_shadow_hash(or_shadow_seed, q);
+    } else {
+        memcpy(rs, r, n * sizeof(cplx));
+    }
     cplx rho = 1.0, alpha = 1.0, omega = 1.0;
     while (rep->iterations < maxit) {
         cplx rho_new = or_vdot(n, rs, r);
@@ -810,6 +836,42 @@ int or_solve(int n1, int n2, int n3, double h, int bc, const double *k, const cp
     if (stats_out) or_hier_stats(S.H, stats_out);
     or_hier_free(S.H);
     free(S.A.k); free(S.A.diag); free(S.A.ap);
+    return 0;
+}
+
+/* Persistent solver (bench.py's CPU legs time solves without the hierarchy
+ * setup, like the native arm): or_solver_create builds A and the CSLP hierarchy
+ * once; or_solver_solve runs one Krylov solve (runner.py:95-131 minus setup). */
+void *or_solver_create(int n1, int n2, int n3, double h, int bc, const double *k, double beta1,
+                       double beta2, int nu1, int nu2, double omega, int cycle_f, int threshold,
+                       int threshold_ge, double coarsest_tol, int coarsest_maxit) {
+    or_solver *S = (or_solver *)xcalloc(1, sizeof(or_solver));
+    S->A.n1 = n1; S->A.n2 = n2; S->A.n3 = n3; S->A.h = h; S->A.shift = 1.0; S->A.bc = bc;
+    size_t n = (size_t)n1 * n2 * n3;
+    S->A.k = (double *)xcalloc(n, sizeof(double));
+    memcpy(S->A.k, k, n * sizeof(double));
+    level_build_diag(&S->A);
+    S->H = or_hier_create(n1, n2, n3, h, beta1, beta2, bc, k, nu1, nu2, omega, cycle_f,
+                          threshold, threshold_ge, coarsest_tol, coarsest_maxit);
+    return S;
+}
+void or_solver_free(void *p) {
+    or_solver *S = (or_solver *)p;
+    or_hier_free(S->H);
+    free(S->A.k); free(S->A.diag); free(S->A.ap);
+    free(S);
+}
+int or_solver_solve(void *p, const cplx *b, cplx *x, int method, double tol, int maxit,
+                    int *iterations, int *converged, int *breakdown, double *final_relres) {
+    or_solver *S = (or_solver *)p;
+    size_t n = (size_t)S->A.n1 * S->A.n2 * S->A.n3;
+    or_report rep = {0};
+    if (method == 1)
+        or_bicgstab(n, solver_apply_a, S, solver_minv, S, b, x, tol, maxit, 1e-30, &rep);
+    else
+        or_gmres(n, solver_apply_a, S, solver_minv, S, b, x, tol, maxit, 0, 1e-30, &rep);
+    *iterations = rep.iterations; *converged = rep.converged; *breakdown = rep.breakdown;
+    *final_relres = rep.final_relres;
     return 0;
 }
 

@@ -71,6 +71,15 @@ def lib():
         L.or_num_threads.restype = ctypes.c_int
         L.or_set_coarse_inverse.argtypes = [_vp, ctypes.c_size_t]
         L.or_set_dot_chunks.argtypes = [ctypes.c_int]
+        L.or_set_bicgstab_shadow.argtypes = [ctypes.c_int, ctypes.c_ulonglong]
+        L.or_solver_create.argtypes = ([ctypes.c_int] * 3 + [ctypes.c_double, ctypes.c_int, _dp,
+                                        ctypes.c_double, ctypes.c_double, ctypes.c_int, ctypes.c_int,
+                                        ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                        ctypes.c_double, ctypes.c_int])
+        L.or_solver_create.restype = _vp
+        L.or_solver_free.argtypes = [_vp]
+        L.or_solver_solve.argtypes = [_vp, _vp, _vp, ctypes.c_int, ctypes.c_double, ctypes.c_int,
+                                      _ip, _ip, _ip, _dp]
         _lib = L
     return _lib
 
@@ -193,9 +202,13 @@ def shadow_space(shape, s, seed):
 
 def solve(k, b, h, bc="sommerfeld", method="bicgstab", tol=1e-6, maxit=400, restart=0, s=4,
           rng_seed=1234, beta1=1.0, beta2=-0.5, nu1=1, nu2=1, omega=0.8, cycle="V",
-          threshold=17, threshold_cmp="gt", coarsest_tol=1e-11, coarsest_maxit=2000):
+          threshold=17, threshold_cmp="gt", coarsest_tol=1e-11, coarsest_maxit=2000,
+          shadow="rhs"):
     """runner.py:95-131 worker body on one worker: Helmholtz A, CSLP cycle
-    preconditioner, Krylov method.  Returns (x, report dict)."""
+    preconditioner, Krylov method.  Returns (x, report dict).  shadow="random":
+    Bi-CGSTAB with the seeded hash shadow vector (seed rng_seed) of the B200
+    path's SolverConfig.shadow extension instead of the reference's r~ = b."""
+    lib().or_set_bicgstab_shadow(2 if shadow == "random" else 0, int(rng_seed) & (2**64 - 1))
     k = _f64(k)
     b = _c128(b)
     x = np.empty_like(b)
@@ -251,3 +264,38 @@ class exact_coarsest:
     def __exit__(self, *exc):
         lib().or_set_coarse_inverse(None, 0)
         return False
+
+
+class PersistentSolver:
+    """A and the CSLP hierarchy built once (or_solver_create); solve() runs one
+    Krylov solve without the setup -- the CPU legs of bench.py time this, like
+    the native arm, which also excludes its setup."""
+
+    def __init__(self, k, h, bc="sommerfeld", beta1=1.0, beta2=-0.5, nu1=1, nu2=1, omega=0.8,
+                 cycle="V", threshold=17, threshold_cmp="gt", coarsest_tol=1e-11,
+                 coarsest_maxit=2000):
+        self.k = _f64(k)
+        n1, n2, n3 = self.k.shape
+        self._h = lib().or_solver_create(n1, n2, n3, float(h), BC_CODES[bc],
+                                         self.k.ctypes.data_as(_dp), float(beta1), float(beta2),
+                                         int(nu1), int(nu2), float(omega),
+                                         1 if cycle.upper() == "F" else 0, int(threshold),
+                                         1 if threshold_cmp == "ge" else 0, float(coarsest_tol),
+                                         int(coarsest_maxit))
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().or_solver_free(self._h)
+            self._h = None
+
+    def solve(self, b, method="bicgstab", tol=1e-6, maxit=400, x=None):
+        b = _c128(b)
+        x = np.empty_like(b) if x is None else x
+        lib().or_set_bicgstab_shadow(0, 0)
+        it, conv, bd = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        fr = ctypes.c_double()
+        lib().or_solver_solve(self._h, _ptr(b), _ptr(x), METHODS[method], float(tol), int(maxit),
+                              ctypes.byref(it), ctypes.byref(conv), ctypes.byref(bd),
+                              ctypes.byref(fr))
+        return x, {"iterations": it.value, "converged": bool(conv.value),
+                   "breakdown": BREAKDOWNS[bd.value], "final_relres": fr.value}

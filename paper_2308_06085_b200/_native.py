@@ -17,6 +17,7 @@ BC = {"dirichlet": 0, "sommerfeld": 1}
 CYCLE = {"V": 0, "F": 1}
 METHOD = {"gmres": 0, "bicgstab": 1, "idrs": 2}
 COARSEST = {"direct": 0, "gmres": 1, "external": 2}
+SHADOW = {"rhs": 0, "random": 2}
 BREAKDOWN = {0: None, 1: "arnoldi", 2: "rho", 3: "omega", 4: "projection"}
 ERR_ARG = -1
 ERR_ZERO_DIAGONAL = -3
@@ -25,6 +26,7 @@ ERR_UNSUPPORTED = -4
 # every symbol include/helmfree_b200.h declares
 EXPORTED = (
     "hf_last_error", "hf_version", "hf_set_stream", "hf_device_synchronize",
+    "hf_set_option", "hf_get_option",
     "hf_operator_create", "hf_operator_destroy", "hf_operator_apply", "hf_operator_diag",
     "hf_jacobi_smooth", "hf_hierarchy_create", "hf_hierarchy_destroy",
     "hf_hierarchy_num_levels", "hf_hierarchy_level_shape", "hf_restrict_fw", "hf_prolong_tl",
@@ -57,7 +59,8 @@ class SolverConfigC(ctypes.Structure):
     _fields_ = [("method", ctypes.c_int), ("tol", ctypes.c_double), ("maxit", ctypes.c_int),
                 ("s", ctypes.c_int), ("restart", ctypes.c_int),
                 ("breakdown_tol", ctypes.c_double), ("shadow_host", ctypes.c_void_p),
-                ("check_every", ctypes.c_int)]
+                ("check_every", ctypes.c_int), ("shadow_kind", ctypes.c_int),
+                ("shadow_seed", ctypes.c_uint64)]
 
 
 class ReportC(ctypes.Structure):
@@ -89,6 +92,8 @@ def load(path: str = LIB_PATH):
         "hf_last_error": ([], ctypes.c_char_p),
         "hf_version": ([], i),
         "hf_set_stream": ([vp], None),
+        "hf_set_option": ([ctypes.c_char_p, i], i),
+        "hf_get_option": ([ctypes.c_char_p], i),
         "hf_device_synchronize": ([], i),
         "hf_operator_create": ([i, i, i, i, i, d, d, d, i, vp, d], vp),
         "hf_operator_destroy": ([vp], None),
@@ -154,3 +159,33 @@ def check_handle(h):
 def set_stream_from_torch() -> None:
     import torch
     load().hf_set_stream(ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+
+
+OPTIONS = ("no_pdl", "no_flat", "no_flat_dr", "no_dr", "tiled_dr", "flat_up", "fuse_up", "no_fuse",
+           "coarsest_dense")
+
+
+def set_option(name: str, value) -> None:
+    """Kernel-variant selection (hf_set_option): A/B measurements and the parity
+    tests that compare variants.  Every variant computes the same arithmetic."""
+    check(load().hf_set_option(name.encode(), 1 if value else 0))
+
+
+class options:
+    """Context manager: `with options(no_flat=1, no_dr=1): ...` (restores on exit)."""
+
+    def __init__(self, **kw):
+        self.kw = kw
+        self.prev = {}
+
+    def __enter__(self):
+        L = load()
+        for k, v in self.kw.items():
+            self.prev[k] = L.hf_get_option(k.encode())
+            set_option(k, v)
+        return self
+
+    def __exit__(self, *exc):
+        for k, v in self.prev.items():
+            set_option(k, v)
+        return False

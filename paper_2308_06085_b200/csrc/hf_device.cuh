@@ -106,16 +106,32 @@ struct RedSlot {
     BcgState *st;
 };
 
+// Seeded shadow vector entry (SolverConfig.shadow = "random"): splitmix64 of
+// (seed, global vertex index) -> two doubles uniform in [-1/2, 1/2) (53-bit
+// mantissas, exact).  The C oracle draws the same values (or_shadow_hash).
+__host__ __device__ inline unsigned long long splitmix64(unsigned long long z) {
+    z += 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+__host__ __device__ inline cd shadow_hash(unsigned long long seed, unsigned long long q) {
+    const unsigned long long a = splitmix64(seed * 0x632be59bd9b4e019ull + 2 * q);
+    const unsigned long long b = splitmix64(seed * 0x632be59bd9b4e019ull + 2 * q + 1);
+    const double s = 1.0 / 9007199254740992.0;   // 2^-53
+    cd w;
+    w.x = (double)(a >> 11) * s - 0.5;
+    w.y = (double)(b >> 11) * s - 0.5;
+    return w;
+}
+
 // Bi-CGSTAB scalars, device resident (krylov.py:207-276).
 struct BcgState {
     cd rho, rho_new, alpha, omega, beta;
     double bnorm, tol, btol, relres;
-    int iter, maxit, done, converged, breakdown, s_conv, matvecs, cond;
+    int iter, maxit, done, converged, breakdown, s_conv, matvecs, pad1;
     double *hist;
     int hist_cap, pad2;
-    // conditional-graph handles (cond = 1): while(iterate) { first half;
-    // if(h1) { s update; if(h2) { second half; if(h3) { x, r update } } } }
-    unsigned long long hw, h1, h2, h3;
 };
 
 __device__ __forceinline__ cd warp_sum(cd v) {

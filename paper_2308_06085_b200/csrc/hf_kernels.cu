@@ -21,6 +21,8 @@
 
 namespace hf {
 
+int g_opt[OPT_COUNT] = {};
+
 // ---------------------------------------------------------------------------
 // Bi-CGSTAB scalar state machine (krylov.py:234-273), run by one thread.
 // ---------------------------------------------------------------------------
@@ -30,24 +32,8 @@ __device__ static void bcg_record(BcgState *st, double relres) {
     st->relres = relres;
 }
 
-__device__ static void bcg_cond(unsigned long long h, bool v) {
-    if (h) cudaGraphSetConditional((cudaGraphConditionalHandle)h, v ? 1u : 0u);
-}
-
-// advances the scalars, then (conditional graph) steers the rest of the iteration
 __device__ static void bcg_step(BcgState *st, int op, const cd *sums);
-__device__ void bcg_finalize(BcgState *st, int op, const cd *sums) {
-    bcg_step(st, op, sums);
-    if (!st->cond) return;
-    const bool go = !st->done;
-    switch (op) {
-    case FIN_BCG_ALPHA: bcg_cond(st->h1, go); break;
-    case FIN_BCG_S: bcg_cond(st->h2, go); break;
-    case FIN_BCG_OMEGA: bcg_cond(st->h3, go); break;
-    default: break;
-    }
-    if (!go || op == FIN_BCG_RHO) bcg_cond(st->hw, go);
-}
+__device__ void bcg_finalize(BcgState *st, int op, const cd *sums) { bcg_step(st, op, sums); }
 
 __device__ static void bcg_step(BcgState *st, int op, const cd *sums) {
     switch (op) {
@@ -1674,20 +1660,37 @@ __global__ void __launch_bounds__(DR_NT, 3) k_down_restrict(Lvl L, Lvl C, const 
 // ---------------------------------------------------------------------------
 #define VEC_BLOCKS 592   // 4 x 148 SMs, fixed => deterministic reductions
 
-// Bi-CGSTAB start (krylov.py:217-232): r = b, rs = b, x = p = v = 0; |b|^2, rs^H r
+// Bi-CGSTAB start (krylov.py:217-232): r = b, x = p = v = 0; |b|^2, rs^H r, with the
+// shadow vector rs (SolverConfig.shadow): HF_SHADOW_RHS rs = b (the reference,
+// krylov.py:229); HF_SHADOW_HOST rs already loaded by the caller; HF_SHADOW_HASH
+// rs = hf_shadow_hash(seed, global vertex index) -- layout independent, so a slab
+// of a partitioned grid draws the same vector (offset q0 = first owned vertex).
 __global__ void __launch_bounds__(256) k_bcg_init(long long n, const cd *__restrict__ b,
                                                   cd *__restrict__ r, cd *__restrict__ rs,
                                                   cd *__restrict__ x, cd *__restrict__ p,
-                                                  cd *__restrict__ v, RedSlot red) {
+                                                  cd *__restrict__ v, RedSlot red, int mode,
+                                                  unsigned long long seed, long long q0) {
     pdl_enter();
     cd acc[2] = {mk(0, 0), mk(0, 0)};
     for (long long q = blockIdx.x * 256ll + threadIdx.x; q < n; q += (long long)gridDim.x * 256) {
         cd bv = __ldg(b + q);
-        r[q] = bv; rs[q] = bv;
+        r[q] = bv;
+        if (mode == HF_SHADOW_RHS) {
+            rs[q] = bv;
+        } else {
+            cd w;
+            if (mode == HF_SHADOW_HASH) {
+                w = shadow_hash(seed, (unsigned long long)(q0 + q));
+                rs[q] = w;
+            } else {
+                w = rs[q];
+            }
+            acc[1] = cadd(acc[1], cjmul(w, bv));
+        }
         x[q] = mk(0, 0); p[q] = mk(0, 0); v[q] = mk(0, 0);
         acc[0] = cadd(acc[0], cjmul(bv, bv));
     }
-    acc[1] = acc[0];
+    if (mode == HF_SHADOW_RHS) acc[1] = acc[0];
     reduce_finish<2>(acc, red);
 }
 
@@ -2089,403 +2092,6 @@ __global__ void __launch_bounds__(FDM_THREADS) k_fdm_fiber(int n1, int n2, int n
                                 blockIdx.x, blockIdx.y);
 }
 
-// ---------------------------------------------------------------------------
-// Coarse sub-cycle in ONE cooperative launch.  Below ~65^3 a level is L2
-// resident and a marching kernel is launch- and pipeline-latency bound (5-10 us
-// for microseconds of data).  k_coarse runs the whole V-cycle below the first
-// coarse level -- pre-smooth + residual, restriction, fast-diagonalisation
-// coarsest solve, prolongation + correction, post-smoothing -- as a list of
-// phases separated by grid-wide barriers.  Every block is resident
-// (cooperative launch), each phase is a grid-stride loop of plain L2 loads
-// (no staging), and the arithmetic of each phase is the reference's:
-//   down     r = b - M (w D^-1 b)              multigrid.py:148-151, 383-386
-//   restrict full weighting + boundary fix     multigrid.py:171-221
-//   corr     t = [w D^-1 b] + P e               multigrid.py:238-297, 389-392
-//   jacobi   u = t + w D^-1 (b - M t)           multigrid.py:153-156
-//   fdm_*    exact separable coarsest solve    (replaces multigrid.py:300-323)
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long *p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-// Grid barrier over all (co-resident) blocks on a monotonic 64-bit arrival
-// counter: every launch adds exactly nblk * nbar arrivals, so a block derives
-// the launch's base from any value it reads before its own first arrival.
-// One release-add per block, relaxed polling, one acquire fence.
-__device__ __forceinline__ void grid_barrier(unsigned long long *cnt, unsigned long long target) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        asm volatile("red.release.gpu.global.add.u64 [%0], 1;\n" ::"l"(cnt) : "memory");
-        // relaxed polling (an acquire load invalidates L1 on every poll), one
-        // acquire fence once the count is reached
-        unsigned long long v;
-        do {
-            asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(cnt) : "memory");
-        } while (v < target);
-        asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
-    }
-    __syncthreads();
-}
-
-// nb of a vertex from per-axis face flags
-__device__ __forceinline__ int face(int x, int n) { return (x == 0) + (x == n - 1); }
-__device__ __forceinline__ int mirror_in(int x, int n) { return x < 0 ? -x : (x >= n ? 2 * (n - 1) - x : x); }
-
-// 7-point neighbourhood of vertex q of a whole-grid level: decode, mirrored
-// neighbour loads (plus D^-1 and k when the medium varies), issued together so
-// that several vertices per thread keep many L2 loads in flight
-struct G7 {
-    cd v[7];     // centre, i-1, i+1, j-1, j+1, m-1, m+1
-    cd d[7];     // D^-1 of the same vertices (varying medium only)
-    int nb[7];
-    double k;
-    bool ok;
-};
-__device__ __forceinline__ void gather7(const Lvl &L, const cd *f, long long q, long long N, bool wd,
-                                        G7 &g) {
-    g.ok = q < N;
-    if (!g.ok) q = 0;
-    const int pl = (int)L.plane;
-    const int i = (int)q / pl, rem = (int)q - i * pl;
-    const int j = rem / L.n3, m = rem - j * L.n3;
-    const int fi = face(i, L.n1), fj = face(j, L.n2), fm = face(m, L.n3);
-    const int im = mirror_in(i - 1, L.n1), ip = mirror_in(i + 1, L.n1);
-    const int jm = mirror_in(j - 1, L.n2), jp = mirror_in(j + 1, L.n2);
-    const int mm = mirror_in(m - 1, L.n3), mp = mirror_in(m + 1, L.n3);
-    const int qi = j * L.n3 + m, rowi = i * pl, rowj = j * L.n3;
-    const int qq[7] = {(int)q, im * pl + qi, ip * pl + qi, rowi + jm * L.n3 + m, rowi + jp * L.n3 + m,
-                       rowi + rowj + mm, rowi + rowj + mp};
-    g.nb[0] = fi + fj + fm;
-    g.nb[1] = face(im, L.n1) + fj + fm;
-    g.nb[2] = face(ip, L.n1) + fj + fm;
-    g.nb[3] = fi + face(jm, L.n2) + fm;
-    g.nb[4] = fi + face(jp, L.n2) + fm;
-    g.nb[5] = fi + fj + face(mm, L.n3);
-    g.nb[6] = fi + fj + face(mp, L.n3);
-#pragma unroll
-    for (int t = 0; t < 7; t++) g.v[t] = f[qq[t]];   // L1-cached: neighbours are shared
-    if (L.dinv && wd) {
-#pragma unroll
-        for (int t = 0; t < 7; t++) g.d[t] = L.dinv[qq[t]];
-    }
-    g.k = L.k ? __ldcg(L.k + q) : L.kc;
-}
-// M f at the gathered vertex; f_t = v_t * scale_t (scale = w D^-1 for the
-// zero-guess pre-smoothing, 1 otherwise)
-__device__ __forceinline__ cd g7_apply(const Lvl &L, const cd *tap, const G7 &g, const cd (&f)[7]) {
-    if (L.bc == HF_BC_DIRICHLET && g.nb[0]) return f[0];
-    cd s = cadd(cadd(cadd(f[1], f[2]), cadd(f[3], f[4])), cadd(f[5], f[6]));
-    const cd ap = L.k ? ap_of(L, g.k, g.nb[0]) : tap[g.nb[0]];
-    cd mf = cmul(ap, f[0]);
-    mf.x -= L.ih2 * s.x;
-    mf.y -= L.ih2 * s.y;
-    return mf;
-}
-#define CO_U 2   // vertices per thread per round
-
-__global__ void __launch_bounds__(256, 2) k_coarse(const __grid_constant__ CoArgs a, const int *done) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ cd tab[CO_MAX_LEVELS][8];   // per level: a_p[nb], w D^-1[nb]
-    if (done && *(volatile const int *)done) return;   // uniform over the grid
-    const int tid = threadIdx.x;
-    const double w = a.omega;
-    for (int l = 0; l < CO_MAX_LEVELS; l++) {
-        if (tid < 4 && a.lv[l].L.tab) {
-            tab[l][tid] = __ldg(a.lv[l].L.tab + tid);
-            tab[l][4 + tid] = cscal(__ldg(a.lv[l].L.tab + 4 + tid), w);
-        }
-    }
-    const unsigned nblk = gridDim.x;
-    // launch base of the arrival counter (see grid_barrier)
-    __shared__ unsigned long long base;
-    if (tid == 0 && a.nph > 1) {
-        const unsigned long long T = (unsigned long long)nblk * (a.nph - 1);
-        base = ld_acquire_u64(a.bar) / T * T;
-    }
-    __syncthreads();
-    const long long gstride = (long long)nblk * blockDim.x;
-    const long long gtid = (long long)blockIdx.x * blockDim.x + tid;
-    for (int p = 0; p < a.nph; p++) {
-        if (p) grid_barrier(a.bar, base + (unsigned long long)p * nblk);
-        const CoPhase ph = a.ph[p];
-        const CoLevel &F = a.lv[ph.l];
-        const Lvl &L = F.L;
-        const cd *tap = tab[ph.l], *tw = tab[ph.l] + 4;
-        switch (ph.type) {
-        case PH_DOWN: {        // r = b - M (w D^-1 b)
-            const long long N = (long long)L.n1 * L.plane;
-            for (long long q0 = gtid; q0 < N; q0 += CO_U * gstride) {
-                G7 g[CO_U];
-#pragma unroll
-                for (int u = 0; u < CO_U; u++) gather7(L, F.b, q0 + u * gstride, N, true, g[u]);
-#pragma unroll
-                for (int u = 0; u < CO_U; u++) {
-                    if (!g[u].ok) continue;
-                    cd f[7];
-#pragma unroll
-                    for (int t = 0; t < 7; t++)
-                        f[t] = cmul(g[u].v[t], L.dinv ? cscal(g[u].d[t], w) : tw[g[u].nb[t]]);
-                    F.r[q0 + u * gstride] = csub(g[u].v[0], g7_apply(L, tap, g[u], f));
-                }
-            }
-            break;
-        }
-        case PH_RESTRICT:      // b_{l+1} = R r_l
-        case PH_REST_B: {      // b_{l+1} = R b_l (nu1 = 0: the residual of u = 0 is b)
-            const CoLevel &C = a.lv[ph.l + 1];
-            const Lvl &K = C.L;
-            const cd *r = ph.type == PH_RESTRICT ? F.r : F.b;
-            const long long N = (long long)K.n1 * K.plane;
-            for (long long q = gtid; q < N; q += gstride) {
-                const int ci = (int)(q / K.plane);
-                const int rem = (int)(q - (long long)ci * K.plane);
-                const int cj = rem / K.n3, cm = rem - cj * K.n3;
-                cd acc = mk(0, 0);
-#pragma unroll
-                for (int o1 = -1; o1 <= 1; o1++) {
-                    const int fi = 2 * ci + o1;
-                    if (fi < 0 || fi >= L.n1) continue;
-                    cd a1 = mk(0, 0);
-#pragma unroll
-                    for (int o2 = -1; o2 <= 1; o2++) {
-                        const int fj = 2 * cj + o2;
-                        if (fj < 0 || fj >= L.n2) continue;
-                        const cd *row = r + (long long)fi * L.plane + (long long)fj * L.n3;
-                        const int fm = 2 * cm;
-                        cd rs = cscal(__ldcg(row + fm), 2.0);
-                        if (fm > 0) rs = cadd(__ldcg(row + fm - 1), rs);
-                        if (fm < L.n3 - 1) rs = cadd(rs, __ldcg(row + fm + 1));
-                        a1 = cadd(a1, o2 == 0 ? cscal(rs, 2.0) : rs);
-                    }
-                    acc = cadd(acc, o1 == 0 ? cscal(a1, 2.0) : a1);
-                }
-                acc = mk(acc.x / 64.0, acc.y / 64.0);
-                const int onb = (ci == 0 || ci == K.n1 - 1) + (cj == 0 || cj == K.n2 - 1) +
-                                (cm == 0 || cm == K.n3 - 1);
-                if (onb) {
-                    if (K.bc == HF_BC_DIRICHLET) acc = mk(0, 0);
-                    else
-                        for (int d = 0; d < onb; d++) acc = cscal(acc, 64.0 / 48.0);
-                }
-                C.b[q] = acc;
-            }
-            break;
-        }
-        case PH_CORR: {        // t = [w D^-1 b] + P e,  e = u_{l+1}
-            const CoLevel &C = a.lv[ph.l + 1];
-            const Lvl &K = C.L;
-            const long long N = (long long)L.n1 * L.plane;
-            const cd *e = C.u;
-            for (long long q = gtid; q < N; q += gstride) {
-                const int i = (int)(q / L.plane);
-                const int rem = (int)(q - (long long)i * L.plane);
-                const int j = rem / L.n3, m = rem - j * L.n3;
-                const bool o2 = j & 1, o3 = m & 1;
-                const cd *ecol = e + (long long)(j >> 1) * K.n3 + (m >> 1);
-                auto cplane = [&](int c) -> cd {
-                    const cd *pp = ecol + (long long)c * K.plane;
-                    cd v = __ldcg(pp);
-                    if (o3) v = cadd(v, __ldcg(pp + 1));
-                    if (o2) {
-                        v = cadd(v, __ldcg(pp + K.n3));
-                        if (o3) v = cadd(v, __ldcg(pp + K.n3 + 1));
-                    }
-                    return v;
-                };
-                const double s2 = (o2 && o3) ? 0.25 : ((o2 || o3) ? 0.5 : 1.0);
-                const cd v0 = cplane(i >> 1);
-                cd pe;
-                if (i & 1) pe = cscal(cadd(v0, cplane((i >> 1) + 1)), 0.5 * s2);
-                else pe = s2 == 1.0 ? v0 : cscal(v0, s2);
-                if (a.pre) {
-                    const int nb = face(i, L.n1) + face(j, L.n2) + face(m, L.n3);
-                    const cd D = L.dinv ? __ldcg(L.dinv + q) : __ldg(L.tab + 4 + nb);
-                    pe = cadd(cscal(cmul(__ldcg(F.b + q), D), w), pe);
-                }
-                F.t[q] = pe;
-            }
-            break;
-        }
-        case PH_JACOBI: {      // u = t + w D^-1 (b - M t)
-            const long long N = (long long)L.n1 * L.plane;
-            for (long long q0 = gtid; q0 < N; q0 += CO_U * gstride) {
-                G7 g[CO_U];
-                cd bc[CO_U], dc[CO_U];
-#pragma unroll
-                for (int u = 0; u < CO_U; u++) {
-                    gather7(L, F.t, q0 + u * gstride, N, false, g[u]);
-                    const long long q = g[u].ok ? q0 + u * gstride : 0;
-                    bc[u] = __ldcg(F.b + q);
-                    dc[u] = L.dinv ? __ldcg(L.dinv + q) : mk(0, 0);
-                }
-#pragma unroll
-                for (int u = 0; u < CO_U; u++) {
-                    if (!g[u].ok) continue;
-                    const cd mf = g7_apply(L, tap, g[u], g[u].v);
-                    const cd wd = L.dinv ? cscal(dc[u], w) : tw[g[u].nb[0]];
-                    F.u[q0 + u * gstride] = cadd(g[u].v[0], cmul(wd, csub(bc[u], mf)));
-                }
-            }
-            break;
-        }
-        case PH_FDM_W:         // in-plane transform with V2^-1, V3^-1 of b -> tmp0
-        case PH_FDM_V: {       // in-plane transform with V2, V3 of tmp1 -> u
-            const int n1 = L.n1, n2 = L.n2, n3 = L.n3;
-            const cd *W1 = a.fdm, *W2 = W1 + n1 * n1, *W3 = W2 + n2 * n2;
-            const cd *V1 = W3 + n3 * n3, *V2 = V1 + n1 * n1, *V3 = V2 + n2 * n2;
-            (void)V1;
-            const int gy = (n2 + a.fR - 1) / a.fR, nvb = n1 * gy;
-            const size_t N = (size_t)n1 * n2 * n3;
-            const bool fw = ph.type == PH_FDM_W;
-            for (int vb = blockIdx.x; vb < nvb; vb += nblk) {
-                fdm_plane_body<256>(n2, n3, a.fR, fw ? W2 : V2, fw ? W3 : V3,
-                                    fw ? F.b : a.ftmp + N, fw ? a.ftmp : F.u, smem_raw, tid,
-                                    vb / gy, vb % gy);
-                __syncthreads();
-            }
-            break;
-        }
-        case PH_FDM_FIBER: {   // i1 transform with V1^-1, 1/D, V1: tmp0 -> tmp1
-            const int n1 = L.n1, n2 = L.n2, n3 = L.n3;
-            const cd *W1 = a.fdm, *W2 = W1 + n1 * n1, *W3 = W2 + n2 * n2;
-            const cd *V1 = W3 + n3 * n3;
-            const int gy = (n3 + a.fC - 1) / a.fC, nvb = n2 * gy;
-            const size_t N = (size_t)n1 * n2 * n3;
-            for (int vb = blockIdx.x; vb < nvb; vb += nblk) {
-                fdm_fiber_body<256>(n1, n2, n3, a.fC, W1, V1, a.invD, a.ftmp, a.ftmp + N, smem_raw,
-                                    tid, vb / gy, vb % gy);
-                __syncthreads();
-            }
-            break;
-        }
-        default:
-            break;
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// The fast-diagonalisation coarsest solve in ONE thread-block-cluster launch.
-// FC_CTAS CTAs of one cluster share the coarsest grid through distributed
-// shared memory: CTA r owns the i1 planes a = r (mod FC_CTAS).
-//   phase A  Y_a = W2 X_a W3^T for the owned planes (X = b)
-//   --- cluster barrier ---
-//   phase B  fibres (i2, i3) = f, f = r (mod FC_CTAS): gather y = Y[:, f] from
-//            the owners (ld.shared::cluster), z = V1 diag(1/D) W1 y, scatter z
-//            back to the owners (st.shared::cluster)
-//   --- cluster barrier ---
-//   phase C  x_a = V2 Z_a V3^T for the owned planes
-// The dot products are cdot_strided with the same order as the three-launch
-// k_fdm_plane / k_fdm_fiber path, so the results are identical; the two
-// kernel boundaries become hardware cluster barriers.
-// ---------------------------------------------------------------------------
-#define FC_CTAS 16
-#define FC_NT 512
-#define FC_MAXN 24
-
-__device__ __forceinline__ unsigned cluster_rank() {
-    unsigned r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ void cluster_sync() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n"
-                 "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-}
-__device__ __forceinline__ unsigned dsmem_addr(const void *local, unsigned cta) {
-    unsigned r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(smem_u32(local)), "r"(cta));
-    return r;
-}
-__device__ __forceinline__ cd ld_dsmem(unsigned addr) {
-    double x, y;
-    asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];\n" : "=d"(x), "=d"(y) : "r"(addr) : "memory");
-    return mk(x, y);
-}
-__device__ __forceinline__ void st_dsmem(unsigned addr, cd v) {
-    asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};\n" ::"r"(addr), "d"(v.x), "d"(v.y) : "memory");
-}
-
-__host__ __device__ __forceinline__ size_t fdm_cluster_smem(int n1, int n2, int n3) {
-    const int own = (n1 + FC_CTAS - 1) / FC_CTAS, pl = n2 * n3, nf = (pl + FC_CTAS - 1) / FC_CTAS;
-    return ((size_t)2 * n1 * n1 + 2 * n2 * n2 + 2 * n3 * n3 + 3 * (size_t)own * pl + 2 * (size_t)nf * n1) * 16;
-}
-
-__global__ void __launch_bounds__(FC_NT) k_fdm_cluster(int n1, int n2, int n3, const cd *__restrict__ fdm,
-                                                       const cd *__restrict__ invD,
-                                                       const cd *__restrict__ b, cd *__restrict__ x,
-                                                       const int *done) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    if (is_done(done)) return;                      // uniform over the cluster
-    const int tid = threadIdx.x;
-    const int r = (int)cluster_rank();
-    const int pl = n2 * n3, own = (n1 + FC_CTAS - 1) / FC_CTAS, nf = (pl + FC_CTAS - 1) / FC_CTAS;
-    int nown = 0;                                   // planes owned: a = r + FC_CTAS o, a < n1
-    while (nown < own && r + FC_CTAS * nown < n1) nown++;
-    int nfib = 0;                                   // fibres owned: f = r + FC_CTAS k, f < pl
-    while (nfib < nf && r + FC_CTAS * nfib < pl) nfib++;
-    cd *w1 = reinterpret_cast<cd *>(smem_raw), *v1 = w1 + n1 * n1;
-    cd *a2 = v1 + n1 * n1, *a3t = a2 + n2 * n2;     // phase A: W2, W3^T; phase C: V2, V3^T
-    cd *Y = a3t + n3 * n3;                          // [own][pl]  phase A output (read remotely)
-    cd *Z = Y + own * pl;                           // [own][pl]  phase B output (written remotely)
-    cd *Q = Z + own * pl;                           // [own][pl]  staging / stage-1 scratch
-    cd *Yg = Q + own * pl, *Wg = Yg + nf * n1;      // [nf][n1] gathered fibres, W1-transformed
-    const cd *W1 = fdm, *W2 = W1 + n1 * n1, *W3 = W2 + n2 * n2;
-    const cd *V1 = W3 + n3 * n3, *V2 = V1 + n1 * n1, *V3 = V2 + n2 * n2;
-    auto load_pair = [&](const cd *A2, const cd *A3) {
-        for (int t = tid; t < n2 * n2; t += FC_NT) a2[t] = __ldg(A2 + t);
-        for (int t = tid; t < n3 * n3; t += FC_NT) {
-            const int rr = t / n3, c = t - rr * n3;
-            a3t[c * n3 + rr] = __ldg(A3 + t);
-        }
-    };
-    // in-plane transform of all owned planes: P -> dst (P staged in shared memory)
-    auto planes_xform = [&](const cd *P, cd *dst, bool dst_global) {
-        for (int t = tid; t < nown * pl; t += FC_NT) {   // Q = A2 P
-            const int o = t / pl, e = t - o * pl, j = e / n3, m = e - j * n3;
-            Q[t] = cdot_strided(a2 + j * n2, 1, P + o * pl + m, n3, n2);
-        }
-        __syncthreads();
-        for (int t = tid; t < nown * pl; t += FC_NT) {   // out = Q A3^T
-            const int o = t / pl, e = t - o * pl, j = e / n3, m = e - j * n3;
-            const cd v = cdot_strided(a3t + m, n3, Q + o * pl + j * n3, 1, n3);
-            if (dst_global) x[(size_t)(r + FC_CTAS * o) * pl + e] = v;
-            else dst[t] = v;
-        }
-    };
-    // phase A: stage b planes (into Z, free until phase B), transform into Y
-    for (int t = tid; t < n1 * n1; t += FC_NT) { w1[t] = __ldg(W1 + t); v1[t] = __ldg(V1 + t); }
-    load_pair(W2, W3);
-    for (int t = tid; t < nown * pl; t += FC_NT) {
-        const int o = t / pl, e = t - o * pl;
-        Z[t] = __ldg(b + (size_t)(r + FC_CTAS * o) * pl + e);
-    }
-    __syncthreads();
-    planes_xform(Z, Y, false);
-    cluster_sync();                                 // every Y visible cluster-wide; Z free
-    // phase B: gather the owned fibres, z = V1 diag(1/D) W1 y, scatter to the owners
-    for (int t = tid; t < nfib * n1; t += FC_NT) {
-        const int k = t / n1, a = t - k * n1, f = r + FC_CTAS * k;
-        Yg[t] = ld_dsmem(dsmem_addr(Y + (a / FC_CTAS) * pl + f, a % FC_CTAS));
-    }
-    load_pair(V2, V3);                              // own shared memory only
-    __syncthreads();
-    for (int t = tid; t < nfib * n1; t += FC_NT) {
-        const int k = t / n1, a = t - k * n1, f = r + FC_CTAS * k;
-        Wg[t] = cmul(cdot_strided(w1 + a * n1, 1, Yg + k * n1, 1, n1), __ldg(invD + (size_t)a * pl + f));
-    }
-    __syncthreads();
-    for (int t = tid; t < nfib * n1; t += FC_NT) {
-        const int k = t / n1, i = t - k * n1, f = r + FC_CTAS * k;
-        st_dsmem(dsmem_addr(Z + (i / FC_CTAS) * pl + f, i % FC_CTAS),
-                 cdot_strided(v1 + i * n1, 1, Wg + k * n1, 1, n1));
-    }
-    cluster_sync();                                 // every Z entry written
-    // phase C
-    planes_xform(Z, nullptr, true);
-}
-
 __global__ void k_assemble(Lvl L, cd *__restrict__ A) {
     pdl_enter();
     long long N = (long long)L.n1 * L.plane;
@@ -2540,7 +2146,7 @@ static void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    static const bool pdl = !std::getenv("HF_NO_PDL");   // A/B switch for profiling
+    const bool pdl = !opt(OPT_NO_PDL);
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
@@ -2600,7 +2206,7 @@ static void stencil_launch(const Lvl &L, const cd *src, const cd *aux, double om
 }
 // ---- flat-decomposition MODE_LOAD stencils (k_flat_stencil) ----
 static bool use_flat(const Lvl &L) {
-    return L.n3 <= FS_MAX_N3 && std::getenv("HF_NO_FLAT") == nullptr;   // A/B switch (tests)
+    return L.n3 <= FS_MAX_N3 && !opt(OPT_NO_FLAT);
 }
 static size_t flat_smem(const Lvl &L) { return (size_t)FS_RING * fs_slot_bytes(L.n3) + 128; }
 static const size_t kFlatSmemMax = (size_t)FS_RING * ((FS_PTS + 2 * (FS_MAX_N3 + 1)) * 16 + 127) / 128 * 128 + 128;
@@ -2608,7 +2214,7 @@ template <int MODE, class Epi, int ND, bool KVAR, bool SOMM>
 static void flat_launch_t(const Lvl &L, const cd *src, const cd *aux, double omega, const Epi &e,
                           const RedSlot &rs, cudaStream_t s, const int *done, const UpArgs &up) {
     const int gx = (int)((L.plane + FS_PTS - 1) / FS_PTS);
-    static const int bps = std::getenv("HF_FLAT_BPS") ? std::atoi(std::getenv("HF_FLAT_BPS")) : 3;
+    const int bps = 3;
     int gz = std::max(1, std::min(L.nx, (148 * bps + gx - 1) / gx));
     const int chunk = std::max((L.nx + gz - 1) / gz, std::min(L.nx, 2));
     gz = (L.nx + chunk - 1) / chunk;
@@ -2701,9 +2307,6 @@ void init_kernel_attributes() {
     cudaFuncSetAttribute(k_down_restrict<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DRSmem<false>));
     cudaFuncSetAttribute(k_down_restrict<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DRSmem<false>));
     cudaFuncSetAttribute(k_fdm_plane, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_fdm_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)fdm_cluster_smem(FC_MAXN, FC_MAXN, FC_MAXN));
-    cudaFuncSetAttribute(k_fdm_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);   // 16 CTAs
     cudaFuncSetAttribute(k_fdm_fiber, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     done = true;
 }
@@ -2742,10 +2345,9 @@ static void corr(int mode, const Lvl &F, const Lvl &C, const cd *b, const cd *e,
                  double omega, cudaStream_t s, const int *done, bool ghosts = false) {
     // tiled variant: two fine planes per thread (every load of the pair independent)
     const int chunk = 2;
-    if (ghosts || !std::getenv("HF_NO_FLAT")) {   // flat thread mapping (no ragged tiles)
+    if (ghosts || !opt(OPT_NO_FLAT)) {   // flat thread mapping (no ragged tiles)
         // four fine planes per thread (coarse-plane sums reused between them)
-        static const int fchunk = std::getenv("HF_CORR_CHUNK") ? std::atoi(std::getenv("HF_CORR_CHUNK")) : 4;
-        const int chunk = fchunk;
+        const int chunk = 4;
         const int plo = ghosts && F.lo1 > 0 ? -1 : 0;
         const int phi = ghosts && F.lo1 + F.nx < F.n1 ? F.nx + 1 : F.nx;
         dim3 gf((unsigned)((F.plane + 255) / 256), (phi - plo + chunk - 1) / chunk);
@@ -2771,7 +2373,7 @@ void launch_dinv(const Lvl &L, cd *out_owned, cudaStream_t s) {
 }
 void launch_restrict(const Lvl &F, const Lvl &C, const cd *r, cd *out, cudaStream_t s,
                      const int *done) {
-    if (!std::getenv("HF_NO_FLAT")) {
+    if (!opt(OPT_NO_FLAT)) {
         const int gx = (int)((C.plane + 255) / 256);
         int gz = std::max(1, std::min(C.nx, (148 * 8) / gx));
         const int chunk = (C.nx + gz - 1) / gz;
@@ -2801,8 +2403,7 @@ template <bool KVAR, bool SOMM, int RPT>
 static void dr2_launch(const Lvl &F, const Lvl &C, const cd *b, cd *out, double omega, cudaStream_t s,
                        const int *done) {
     const int gx = (C.n2 + DR2_CR - 1) / DR2_CR;
-    const char *tb = std::getenv("HF_DR_BLOCKS");      // A/B: target block count
-    const int target = tb ? std::atoi(tb) : 148 * 2;
+    const int target = 148 * 2;
     int gz = std::max(1, std::min(C.nx, (target + gx - 1) / gx));
     const int chunk = (C.nx + gz - 1) / gz;
     gz = (C.nx + chunk - 1) / chunk;
@@ -2810,8 +2411,7 @@ static void dr2_launch(const Lvl &F, const Lvl &C, const cd *b, cd *out, double 
     launch(k_flat_dr<KVAR, SOMM, RPT>, dim3(gx, gz), dim3(DR2_NT), smem, s, F, C, b, out, omega, chunk, done);
 }
 bool flat_dr_ok(const Lvl &F) {
-    const char *mx = std::getenv("HF_DR_MAX_N3");   // tuning: widest plane for the fused down
-    return F.n3 <= (mx ? std::atoi(mx) : DR2_MAX_N3) && !std::getenv("HF_NO_FLAT_DR");
+    return F.n3 <= DR2_MAX_N3 && !opt(OPT_NO_FLAT_DR);
 }
 void launch_down_restrict(const Lvl &F, const Lvl &C, const cd *b, cd *out, double omega,
                           cudaStream_t s, const int *done) {
@@ -2855,15 +2455,15 @@ int launch_up1(const Lvl &L, const Lvl &C, const cd *b, const cd *e, cd *u, cd *
     // whole-grid levels: correction produced inside the post-smoothing sweep
     // flat fused up-sweep: opt-in (HF_FLAT_UP=1); the per-entry prolongation in the
     // slot made it slower than k_corr_flat + the flat Jacobi sweep on every level
-    const char *upmx = std::getenv("HF_UP_MAX_N3");   // widest plane for the flat fused up-sweep
-    if (std::getenv("HF_NO_FUSE") == nullptr && std::getenv("HF_FLAT_UP") != nullptr &&
-        L.n3 <= (upmx ? std::atoi(upmx) : FS_MAX_N3) &&
+    if (!opt(OPT_NO_FUSE) && opt(OPT_FLAT_UP) && L.n3 <= FS_MAX_N3 &&
         flat_stencil<MODE_UP, EpiJacobi, 0>(L, b, b, omega, EpiJacobi{u}, RedSlot{}, s, done,
                                             UpArgs{C, e, pre ? 1 : 0}))
         return 1;
     // (the split pair is faster than the tiled fused kernel where the flat Jacobi applies)
-    const bool split = std::getenv("HF_NO_FUSE") != nullptr ||
-                       (use_flat(L) && std::getenv("HF_FUSE_UP") == nullptr);
+    // correction + Jacobi sweep as the split pair unless fuse_up is requested: the
+    // tiled MODE_UP kernel measured slower than k_corr_flat + the sweep on the wide
+    // 513^3 wedge levels too (3.40 vs 1.07 + 1.63 ms, profiles/r02_kernel_table_513w.json)
+    const bool split = opt(OPT_NO_FUSE) || !opt(OPT_FUSE_UP);
     if (!split && L.lo1 == 0 && L.nx == L.n1 && C.lo1 == 0 && C.nx == C.n1) {
         stencil<MODE_UP, EpiJacobi, 0>(L, b, b, omega, EpiJacobi{u}, RedSlot{}, s, done,
                                         UpArgs{C, e, pre ? 1 : 0});
@@ -2913,30 +2513,9 @@ size_t fdm_smem_bytes(int n1, int n2, int n3) {
     return std::max(sp, sf);
 }
 // fdm = [V1^-1, V2^-1, V3^-1, V1, V2, V3] (row-major n_d x n_d each), tmp = 2N
-// returns the number of kernels launched (1: cluster kernel, 3: split path)
+// returns the number of kernels launched (3)
 int launch_fdm(int n1, int n2, int n3, const cd *fdm, const cd *invD, const cd *b, cd *tmp,
                cd *x, cudaStream_t s, const int *done) {
-    // single cluster launch: opt-in (HF_FDM_CLUSTER=1) -- measured 17.5 us against 11.4 us
-    // for the three-launch path at 17^3 (16 SMs cannot match its 68-block parallelism)
-    if (n1 <= FC_MAXN && n2 <= FC_MAXN && n3 <= FC_MAXN && std::getenv("HF_FDM_CLUSTER")) {
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(FC_CTAS);
-        cfg.blockDim = dim3(FC_NT);
-        cfg.dynamicSmemBytes = fdm_cluster_smem(n1, n2, n3);
-        cfg.stream = s;
-        cudaLaunchAttribute attr[2];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = FC_CTAS;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[1].val.programmaticStreamSerializationAllowed = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 2;
-        if (cudaLaunchKernelEx(&cfg, k_fdm_cluster, n1, n2, n3, fdm, invD, b, x, done) == cudaSuccess)
-            return 1;
-        cudaGetLastError();   // not launchable here: fall through to the three-kernel path
-    }
     const cd *W1 = fdm, *W2 = W1 + n1 * n1, *W3 = W2 + n2 * n2;
     const cd *V1 = W3 + n3 * n3, *V2 = V1 + n1 * n1, *V3 = V2 + n2 * n2;
     int R, C;
@@ -2949,33 +2528,6 @@ int launch_fdm(int n1, int n2, int n3, const cd *fdm, const cd *invD, const cd *
            (const cd *)t0, t1, done);
     launch(k_fdm_plane, gp, dim3(FDM_THREADS), sp, s, n2, n3, R, V2, V3, (const cd *)t1, x, done);
     return 3;
-}
-int coarse_blocks(size_t smem, int per_sm_cap) {
-    static int occ = -1;
-    static size_t occ_smem = 0;
-    if (occ < 0 || occ_smem != smem) {
-        cudaFuncSetAttribute(k_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_coarse, 256, smem) != cudaSuccess)
-            occ = 0;
-        occ_smem = smem;
-    }
-    int dev = 0, sms = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    return sms * std::min(occ, per_sm_cap);
-}
-cudaError_t launch_coarse(const CoArgs &a, int nblk, size_t smem, cudaStream_t s, const int *done) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(nblk);
-    cfg.blockDim = dim3(256);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;   // every block resident: grid barriers are safe
-    attr[0].val.cooperative = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_coarse, a, done);
 }
 void launch_set_identity(long long N, cd *B, cudaStream_t s) {
     launch(k_set_identity, dim3((unsigned)((N + 255) / 256)), dim3(256), 0, s, N, B);
@@ -2997,8 +2549,9 @@ void launch_dot(long long n, const cd *a, const cd *b, const RedSlot &rs, cudaSt
     launch(k_dot_store, dim3(VEC_BLOCKS), dim3(256), 0, s, n, a, b, rs);
 }
 void launch_bcg_init(long long n, const cd *b, cd *r, cd *rs, cd *x, cd *p, cd *v,
-                     const RedSlot &red, cudaStream_t s) {
-    launch(k_bcg_init, dim3(VEC_BLOCKS), dim3(256), 0, s, n, b, r, rs, x, p, v, red);
+                     const RedSlot &red, cudaStream_t s, int shadow, unsigned long long seed,
+                     long long q0) {
+    launch(k_bcg_init, dim3(VEC_BLOCKS), dim3(256), 0, s, n, b, r, rs, x, p, v, red, shadow, seed, q0);
 }
 void launch_bcg_p(long long n, const BcgState *st, const cd *r, cd *p, const cd *v,
                   cudaStream_t s, const int *done) {

@@ -4,6 +4,12 @@
 
 namespace hf {
 
+// kernel-variant options (hf_set_option in the C ABI); all off = the default
+enum HfOpt { OPT_NO_PDL = 0, OPT_NO_FLAT, OPT_NO_FLAT_DR, OPT_NO_DR, OPT_TILED_DR, OPT_FLAT_UP,
+             OPT_FUSE_UP, OPT_NO_FUSE, OPT_COARSEST_DENSE, OPT_COUNT };
+extern int g_opt[OPT_COUNT];
+inline bool opt(int o) { return g_opt[o] != 0; }
+
 int march_blocks(const Lvl &L);
 int tile_blocks(const Lvl &L);
 void init_kernel_attributes();
@@ -54,7 +60,8 @@ void launch_mgs(long long n, cd *w, const cd *c, const cd *vprev, const cd *vcur
 void launch_multi_axpy(long long n, int m, const cd *const *V, const cd *y, cd *x, cudaStream_t s);
 void launch_dot(long long n, const cd *a, const cd *b, const RedSlot &rs, cudaStream_t s);
 void launch_bcg_init(long long n, const cd *b, cd *r, cd *rs, cd *x, cd *p, cd *v,
-                     const RedSlot &red, cudaStream_t s);
+                     const RedSlot &red, cudaStream_t s, int shadow = HF_SHADOW_RHS,
+                     unsigned long long seed = 0, long long q0 = 0);
 void launch_bcg_p(long long n, const BcgState *st, const cd *r, cd *p, const cd *v,
                   cudaStream_t s, const int *done);
 void launch_bcg_s(long long n, const BcgState *st, const cd *r, const cd *v, cd *sv,
@@ -66,33 +73,5 @@ void launch_bcg_xhalf(long long n, const BcgState *st, cd *x, const cd *ph, cuda
 void launch_bcg_step(BcgState *st, int op, const cd *sums, cudaStream_t s);
 
 #define VEC_BLOCKS_HOST 592
-
-// coarse sub-cycle in one cooperative launch (k_coarse in hf_kernels.cu)
-enum { PH_DOWN = 0, PH_RESTRICT, PH_REST_B, PH_CORR, PH_JACOBI, PH_FDM_W, PH_FDM_FIBER, PH_FDM_V };
-#define CO_MAX_LEVELS 8
-#define CO_MAX_PHASES 48
-struct CoLevel {
-    Lvl L;
-    cd *b, *u, *r, *t;
-};
-struct CoPhase {
-    int type, l;
-};
-struct CoArgs {
-    CoLevel lv[CO_MAX_LEVELS];
-    CoPhase ph[CO_MAX_PHASES];
-    int nph;
-    double omega;
-    int pre;             // nu1 = 1: zero-guess pre-smoothing (t = w D^-1 b + P e)
-    int fR, fC;          // fdm row / column groups
-    const cd *fdm, *invD;
-    cd *ftmp;
-    unsigned long long *bar;   // monotonic arrival counter (grid barriers)
-};
-
-// co-resident blocks of k_coarse for `smem` dynamic bytes (0: not launchable)
-int coarse_blocks(size_t smem, int per_sm_cap);
-// returns the launch error (cooperative launches are checked by the caller)
-cudaError_t launch_coarse(const CoArgs &a, int nblk, size_t smem, cudaStream_t s, const int *done);
 
 }  // namespace hf

@@ -45,7 +45,29 @@ static int fail(int code, const std::string &msg) {
     } while (0)
 
 extern "C" const char *hf_last_error(void) { return g_err.c_str(); }
-extern "C" int hf_version(void) { return 1; }
+extern "C" int hf_version(void) { return 2; }
+
+// kernel-variant selection (A/B measurements and the parity tests that compare
+// the variants); every variant computes the same arithmetic.  Explicit API only:
+// the library reads no environment variables.
+static const char *const k_opt_names[OPT_COUNT] = {
+    "no_pdl", "no_flat", "no_flat_dr", "no_dr", "tiled_dr", "flat_up", "fuse_up", "no_fuse",
+    "coarsest_dense"};
+extern "C" int hf_set_option(const char *name, int value) {
+    if (!name) return fail(HF_ERR_ARG, "null option name");
+    for (int i = 0; i < OPT_COUNT; i++)
+        if (std::strcmp(name, k_opt_names[i]) == 0) {
+            g_opt[i] = value != 0;
+            return 0;
+        }
+    return fail(HF_ERR_ARG, std::string("unknown option ") + name);
+}
+extern "C" int hf_get_option(const char *name) {
+    if (!name) return fail(HF_ERR_ARG, "null option name");
+    for (int i = 0; i < OPT_COUNT; i++)
+        if (std::strcmp(name, k_opt_names[i]) == 0) return g_opt[i];
+    return fail(HF_ERR_ARG, std::string("unknown option ") + name);
+}
 extern "C" void hf_set_stream(void *stream) { g_user_stream = (cudaStream_t)stream; }
 extern "C" int hf_device_synchronize(void) {
     CK(cudaDeviceSynchronize());
@@ -68,7 +90,10 @@ struct Allocs {
         void *p = nullptr;
         err = cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T));
         if (err != cudaSuccess) return nullptr;
-        cudaMemset(p, 0, std::max<size_t>(count, 1) * sizeof(T));
+        // zero-fill, complete before any stream (incl. non-blocking ones) uses it
+        err = cudaMemset(p, 0, std::max<size_t>(count, 1) * sizeof(T));
+        if (err == cudaSuccess) err = cudaStreamSynchronize(cudaStreamLegacy);
+        if (err != cudaSuccess) { cudaFree(p); return nullptr; }
         ptrs.push_back(p);
         return (T *)p;
     }
@@ -207,11 +232,6 @@ struct hf_hierarchy {
     cd *fdm_invD = nullptr; // 1 / (l1_a + l2_b + l3_c + c) on the coarsest grid
     cd *fdm_tmp = nullptr;  // 2 N scratch
     int coarsest_flags = 0;
-    // levels >= co_first run as one cooperative k_coarse launch per cycle (-1: off)
-    int co_first = -1;
-    CoArgs co{};
-    int co_nblk = 0;
-    size_t co_smem = 0;
 };
 
 static bool keep_coarsening(int n1, int n2, int n3, const hf_mg_config &c) {
@@ -338,7 +358,7 @@ static int build_coarsest_fdm(hf_hierarchy *H, cudaStream_t s, bool &built) {
     built = false;
     Level &C = H->lev.back();
     const Lvl &L = C.L;
-    if (L.bc != HF_BC_SOMMERFELD || L.k != nullptr || std::getenv("HF_COARSEST_DENSE")) return 0;
+    if (L.bc != HF_BC_SOMMERFELD || L.k != nullptr || opt(OPT_COARSEST_DENSE)) return 0;
     if (L.lo1 != 0 || L.nx != L.n1) return 0;
     if (fdm_smem_bytes(L.n1, L.n2, L.n3) > 200 * 1024) return 0;
     cusolverDnHandle_t hs;
@@ -461,79 +481,6 @@ static int build_coarsest_direct(hf_hierarchy *H, cudaStream_t s) {
 
 static cudaStream_t work_stream() { return g_user_stream; }
 
-// The L2-resident bottom of a V(nu1 <= 1, 1) cycle as one k_coarse launch:
-// levels whose vertex count is at most HF_COARSE_MAX (default 300000, ~65^3)
-// down to a separable (fast-diagonalisation) coarsest level, whole grid only.
-static int build_coarse_schedule(hf_hierarchy *H) {
-    H->co_first = -1;
-    const hf_mg_config &c = H->cfg;
-    const int nl = (int)H->lev.size();
-    // opt-in (HF_COARSE=1): measured slower than the PDL-chained level kernels
-    // on B200
-    if (!std::getenv("HF_COARSE") || !H->fdm || nl < 2) return 0;
-    if (c.cycle != HF_CYCLE_V || c.nu1 > 1 || c.nu2 != 1) return 0;
-    const char *mx = std::getenv("HF_COARSE_MAX");
-    const long long maxn = mx ? std::atoll(mx) : 300000;
-    int first = nl - 1;
-    while (first > 1) {
-        const Lvl &L = H->lev[first - 1].L;
-        if ((long long)L.n1 * L.plane > maxn) break;
-        first--;
-    }
-    if (nl - first > CO_MAX_LEVELS) first = nl - CO_MAX_LEVELS;
-    for (int l = first; l < nl; l++) {
-        const Lvl &L = H->lev[l].L;
-        if (L.lo1 != 0 || L.nx != L.n1) return 0;
-    }
-    CoArgs &a = H->co;
-    a = CoArgs{};
-    for (int l = first; l < nl; l++) {
-        Level &lv = H->lev[l];
-        a.lv[l - first] = CoLevel{lv.L, lv.b, lv.u, lv.r, lv.t};
-    }
-    auto add = [&](int type, int l) {
-        if (a.nph < CO_MAX_PHASES) a.ph[a.nph++] = CoPhase{type, l - first};
-    };
-    const bool pre = c.nu1 == 1;
-    for (int l = first; l < nl - 1; l++) {
-        if (pre) {
-            add(PH_DOWN, l);
-            add(PH_RESTRICT, l);
-        } else {
-            add(PH_REST_B, l);
-        }
-    }
-    add(PH_FDM_W, nl - 1);
-    add(PH_FDM_FIBER, nl - 1);
-    add(PH_FDM_V, nl - 1);
-    for (int l = nl - 2; l >= first; l--) {
-        add(PH_CORR, l);
-        add(PH_JACOBI, l);
-    }
-    if (a.nph >= CO_MAX_PHASES) return 0;
-    if (const char *np = std::getenv("HF_COARSE_NPH"))   // timing experiments only (wrong results)
-        a.nph = std::max(0, std::min(a.nph, std::atoi(np)));
-    if (std::getenv("HF_COARSE_NOP"))   // timing experiments only: barriers without work
-        for (int p = 0; p < a.nph; p++) a.ph[p].type = -1;
-    a.omega = c.omega;
-    a.pre = pre ? 1 : 0;
-    const Lvl &K = H->lev.back().L;
-    fdm_groups(K.n1, K.n2, K.n3, a.fR, a.fC);
-    a.fdm = H->fdm;
-    a.invD = H->fdm_invD;
-    a.ftmp = H->fdm_tmp;
-    cudaError_t err;
-    a.bar = H->A.get<unsigned long long>(1, err);
-    if (!a.bar) return fail(HF_ERR_CUDA, "cudaMalloc coarse barrier");
-    H->co_smem = fdm_smem_bytes(K.n1, K.n2, K.n3);
-    const char *bps = std::getenv("HF_COARSE_BPS");
-    H->co_nblk = coarse_blocks(H->co_smem, bps ? std::max(1, std::atoi(bps)) : 2);
-    if (H->co_nblk <= 0) return 0;
-    H->co_first = first;
-    return 0;
-}
-
-
 extern "C" hf_hierarchy *hf_hierarchy_create(int n1, int n2, int n3, int lo1, int nx, double h,
                                              double beta1, double beta2, int bc,
                                              const double *k_host, double k_const,
@@ -595,10 +542,6 @@ extern "C" hf_hierarchy *hf_hierarchy_create(int n1, int n2, int n3, int lo1, in
         delete H;
         return nullptr;
     }
-    if (build_coarse_schedule(H)) {
-        delete H;
-        return nullptr;
-    }
     return H;
 }
 
@@ -635,11 +578,6 @@ static void smooth_sweeps(Level &lv, cd *u, const cd *b, double omega, int sweep
 }
 
 static void v_cycle(hf_hierarchy *H, int li, const cd *b, cd *u, cudaStream_t s, const int *done) {
-    if (li == H->co_first) {   // b, u are the level's own buffers below the finest level
-        launch_coarse(H->co, H->co_nblk, H->co_smem, s, done);
-        g_launches++;
-        return;
-    }
     Level &lv = H->lev[li];
     const hf_mg_config &c = H->cfg;
     if (li == (int)H->lev.size() - 1) { coarsest(H, b, u, s, done); return; }
@@ -647,10 +585,7 @@ static void v_cycle(hf_hierarchy *H, int li, const cd *b, cd *u, cudaStream_t s,
     const bool fused = c.nu1 <= 1 && c.nu2 == 1;
     // fused down + restriction (k_flat_dr) where it applies; the tiled fused kernel
     // (wider planes) is opt-in (HF_DR=1): slower than the split pair there
-    const char *drmin = std::getenv("HF_DR_MIN_N3");   // A/B: split pair below this plane width
-    const bool split_dr = std::getenv("HF_NO_DR") != nullptr ||
-                          (drmin && lv.L.n3 < std::atoi(drmin)) ||
-                          (!flat_dr_ok(lv.L) && std::getenv("HF_DR") == nullptr);
+    const bool split_dr = opt(OPT_NO_DR) || (!flat_dr_ok(lv.L) && !opt(OPT_TILED_DR));
     if (c.nu1 == 1 && fused && !split_dr) {
         L1(launch_down_restrict(lv.L, nx.L, b, nx.b, c.omega, s, done));
     } else if (c.nu1 == 1 && fused) {
@@ -920,12 +855,6 @@ struct hf_solver {
     cudaStream_t stream = nullptr;
     cudaGraphExec_t graph = nullptr;
     int graph_kernels = 0;
-    // whole solve as one conditional graph (while / nested if nodes)
-    cudaGraphExec_t cgraph = nullptr;
-    bool cgraph_tried = false;
-    unsigned long long hw = 0, h1 = 0, h2 = 0, h3 = 0;
-    int kern_first = 0, kern_s = 0, kern_second = 0, kern_xr = 0;   // kernels per section
-    cudaStream_t cs[3] = {nullptr, nullptr, nullptr};                // capture streams of the if bodies
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, evs = nullptr;
     // GMRES / IDR(s) workspace (allocated on first use)
     std::vector<cd *> basis;            // Krylov basis V (GMRES) / G, U, P (IDR)
@@ -937,9 +866,6 @@ struct hf_solver {
     int vcap = 0;
     ~hf_solver() {
         if (graph) cudaGraphExecDestroy(graph);
-        if (cgraph) cudaGraphExecDestroy(cgraph);
-        for (cudaStream_t c : cs)
-            if (c) cudaStreamDestroy(c);
         if (st_host) cudaFreeHost(st_host);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
@@ -985,8 +911,6 @@ extern "C" hf_solver *hf_solver_create(hf_operator *Aop, hf_hierarchy *M) {
 extern "C" void hf_solver_destroy(hf_solver *S) { delete S; }
 
 // one Bi-CGSTAB iteration (krylov.py:234-273), every kernel predicated on st->done
-static thread_local cudaError_t g_cond_fail = cudaSuccess;
-static void ei_fail(cudaError_t e) { g_cond_fail = e; }
 
 static void bcg_iteration(hf_solver *S, cudaStream_t s) {
     const Lvl &A = S->Aop->lv.L;
@@ -1001,113 +925,6 @@ static void bcg_iteration(hf_solver *S, cudaStream_t s) {
     L1(launch_bcg_xr(n, S->st, S->x, S->ph, S->sh, S->s, S->t, S->r, S->rs,
                      S->red.slot(FIN_BCG_RHO, S->st), s, done));
     cudaMemcpyAsync(S->st_host, S->st, sizeof(BcgState), cudaMemcpyDeviceToHost, s);
-}
-
-// One Bi-CGSTAB solve as a single CUDA graph: a while node iterates the
-// body, and nested if nodes stop mid-iteration (alpha breakdown, |s| converged,
-// omega breakdown) -- the finalize step of each device reduction sets the
-// conditions (bcg_finalize), so no kernel reads a "done" flag and the host
-// does not poll.
-template <class F>
-static cudaError_t capture_if(cudaStream_t s, cudaStream_t s2, unsigned long long &handle, F &&body) {
-    cudaStreamCaptureStatus st;
-    cudaGraph_t cg = nullptr;
-    const cudaGraphNode_t *deps = nullptr;
-    size_t nd = 0;
-    cudaError_t e = cudaStreamGetCaptureInfo(s, &st, nullptr, &cg, &deps, &nd);
-    if (e != cudaSuccess) return e;
-    cudaGraphConditionalHandle h;
-    if ((e = cudaGraphConditionalHandleCreate(&h, cg, 0, 0)) != cudaSuccess) return e;
-    handle = (unsigned long long)h;
-    cudaGraphNodeParams ip = {};
-    ip.type = cudaGraphNodeTypeConditional;
-    ip.conditional.handle = h;
-    ip.conditional.type = cudaGraphCondTypeIf;
-    ip.conditional.size = 1;
-    cudaGraphNode_t in;
-    if ((e = cudaGraphAddNode(&in, cg, deps, nd, &ip)) != cudaSuccess) return e;
-    if ((e = cudaStreamUpdateCaptureDependencies(s, &in, 1, cudaStreamSetCaptureDependencies)) != cudaSuccess)
-        return e;
-    if ((e = cudaStreamBeginCaptureToGraph(s2, ip.conditional.phGraph_out[0], nullptr, nullptr, 0,
-                                           cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
-        return e;
-    body(s2);
-    cudaGraph_t out;
-    return cudaStreamEndCapture(s2, &out);
-}
-
-static int build_cond_graph(hf_solver *S) {
-    if (S->cgraph || S->cgraph_tried) return 0;
-    S->cgraph_tried = true;
-    // opt-in: measured ~1% slower than replaying the per-iteration graph with
-    // a host poll every check_every iterations (three if-node evaluations per
-    // iteration cost more than the skipped done-flag reads and polls)
-    if (!std::getenv("HF_COND_GRAPH")) return 0;
-    for (cudaStream_t &c : S->cs)
-        if (!c && cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking) != cudaSuccess) return 0;
-    const Lvl &A = S->Aop->lv.L;
-    const long long n = S->n;
-    cudaGraph_t G = nullptr;
-    if (cudaGraphCreate(&G, 0) != cudaSuccess) return 0;
-    cudaGraphConditionalHandle hw;
-    cudaGraphNodeParams wp = {};
-    cudaGraphNode_t wn;
-    cudaError_t e = cudaGraphConditionalHandleCreate(&hw, G, 1, cudaGraphCondAssignDefault);
-    if (e == cudaSuccess) {
-        wp.type = cudaGraphNodeTypeConditional;
-        wp.conditional.handle = hw;
-        wp.conditional.type = cudaGraphCondTypeWhile;
-        wp.conditional.size = 1;
-        e = cudaGraphAddNode(&wn, G, nullptr, 0, &wp);
-    }
-    long long before = g_launches, mark;
-    cudaStream_t s = S->stream;
-    if (e == cudaSuccess)
-        e = cudaStreamBeginCaptureToGraph(s, wp.conditional.phGraph_out[0], nullptr, nullptr, 0,
-                                          cudaStreamCaptureModeThreadLocal);
-    if (e == cudaSuccess) {
-        mark = g_launches;
-        L1(launch_bcg_p(n, S->st, S->r, S->p, S->v, s, nullptr));
-        precondition(S->M, S->p, S->ph, s, nullptr);
-        L1(launch_apply_dot1(A, S->ph, S->v, S->rs, S->red.slot(FIN_BCG_ALPHA, S->st), s, nullptr));
-        S->kern_first = (int)(g_launches - mark);
-        cudaError_t ei = capture_if(s, S->cs[0], S->h1, [&](cudaStream_t s1) {
-            mark = g_launches;
-            L1(launch_bcg_s(n, S->st, S->r, S->v, S->s, S->red.slot(FIN_BCG_S, S->st), s1, nullptr));
-            S->kern_s = (int)(g_launches - mark);
-            cudaError_t e2 = capture_if(s1, S->cs[1], S->h2, [&](cudaStream_t s2) {
-                mark = g_launches;
-                precondition(S->M, S->s, S->sh, s2, nullptr);
-                L1(launch_apply_dot2(A, S->sh, S->t, S->s, S->red.slot(FIN_BCG_OMEGA, S->st), s2,
-                                     nullptr));
-                S->kern_second = (int)(g_launches - mark);
-                cudaError_t e3 = capture_if(s2, S->cs[2], S->h3, [&](cudaStream_t s3) {
-                    L1(launch_bcg_xr(n, S->st, S->x, S->ph, S->sh, S->s, S->t, S->r, S->rs,
-                                     S->red.slot(FIN_BCG_RHO, S->st), s3, nullptr));
-                    S->kern_xr = 1;
-                });
-                if (e3 != cudaSuccess) ei_fail(e3);
-            });
-            if (e2 != cudaSuccess) ei_fail(e2);
-        });
-        cudaGraph_t out;
-        cudaError_t ec = cudaStreamEndCapture(s, &out);
-        if (e == cudaSuccess) e = ei != cudaSuccess ? ei : ec;
-        if (e == cudaSuccess && g_cond_fail != cudaSuccess) e = g_cond_fail;
-    }
-    g_cond_fail = cudaSuccess;
-    g_launches = before;
-    if (e == cudaSuccess) e = cudaGraphInstantiate(&S->cgraph, G, 0);
-    cudaGraphDestroy(G);
-    if (std::getenv("HF_DEBUG"))
-        std::fprintf(stderr, "[hf] conditional graph: %s\n", e == cudaSuccess ? "ok" : cudaGetErrorString(e));
-    if (e != cudaSuccess) {           // older driver or capture problem: per-iteration graph
-        S->cgraph = nullptr;
-        cudaGetLastError();
-        return 0;
-    }
-    S->hw = (unsigned long long)hw;
-    return 0;
 }
 
 static int build_graph(hf_solver *S) {
@@ -1135,52 +952,41 @@ static int solve_bicgstab(hf_solver *S, const hf_solver_config *cfg, const cd *b
         if (!S->hist) return fail(HF_ERR_CUDA, "cudaMalloc history");
         S->hist_cap = cfg->maxit + 2;
     }
-    if (build_cond_graph(S)) return HF_ERR_CUDA;
-    if (!S->cgraph && build_graph(S)) return HF_ERR_CUDA;
+    if (build_graph(S)) return HF_ERR_CUDA;
     BcgState init{};
     init.tol = cfg->tol;
     init.btol = cfg->breakdown_tol > 0 ? cfg->breakdown_tol : 1e-30;
     init.maxit = cfg->maxit;
     init.hist = S->hist;
     init.hist_cap = S->hist_cap;
-    if (S->cgraph) {
-        init.cond = 1;
-        init.hw = S->hw; init.h1 = S->h1; init.h2 = S->h2; init.h3 = S->h3;
-    }
     *S->st_host = init;
     CK(cudaMemcpyAsync(S->st, S->st_host, sizeof(BcgState), cudaMemcpyHostToDevice, s));
     long long launches = 0;
     CK(cudaEventRecord(S->ev0, s));
-    L1(launch_bcg_init(S->n, b, S->r, S->rs, S->x, S->p, S->v, S->red.slot(FIN_BCG_INIT, S->st), s));
+    // shadow vector r~: b (the reference, krylov.py:229), the caller's host vector,
+    // or the seeded hash vector (SolverConfig.shadow)
+    int shadow = cfg->shadow_kind;
+    if (shadow == HF_SHADOW_RHS && cfg->shadow_host) shadow = HF_SHADOW_HOST;
+    if (shadow == HF_SHADOW_HOST) {
+        if (!cfg->shadow_host) return fail(HF_ERR_ARG, "HF_SHADOW_HOST needs shadow_host");
+        CK(cudaMemcpyAsync(S->rs, cfg->shadow_host, (size_t)S->n * sizeof(cd), cudaMemcpyHostToDevice, s));
+    }
+    const Lvl &AL = S->Aop->lv.L;
+    L1(launch_bcg_init(S->n, b, S->r, S->rs, S->x, S->p, S->v, S->red.slot(FIN_BCG_INIT, S->st), s,
+                       shadow, cfg->shadow_seed, (long long)AL.lo1 * AL.plane));
     launches++;
     CK(cudaMemcpyAsync(S->st_host, S->st, sizeof(BcgState), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    if (S->cgraph) {
-        if (!S->st_host->done) {
-            CK(cudaGraphLaunch(S->cgraph, s));
-            CK(cudaMemcpyAsync(S->st_host, S->st, sizeof(BcgState), cudaMemcpyDeviceToHost, s));
-            CK(cudaStreamSynchronize(s));
-            // kernels that ran: full iterations, plus the part of the last one
-            const BcgState &q = *S->st_host;
-            const int per = S->kern_first + S->kern_s + S->kern_second + S->kern_xr;
-            long long it = q.iter;
-            if (q.s_conv) launches += (it - 1) * per + S->kern_first + S->kern_s;
-            else if (q.breakdown == HF_BREAKDOWN_OMEGA) launches += it * per + S->kern_first + S->kern_s + S->kern_second;
-            else if (q.breakdown) launches += it * per + S->kern_first;
-            else launches += it * per;
+    int every = cfg->check_every > 0 ? cfg->check_every : 4;
+    int graphs = 0;
+    while (!S->st_host->done && graphs < cfg->maxit + every) {
+        for (int k = 0; k < every; k++) {
+            CK(cudaGraphLaunch(S->graph, s));
+            graphs++;
         }
-    } else {
-        int every = cfg->check_every > 0 ? cfg->check_every : 4;
-        int graphs = 0;
-        while (!S->st_host->done && graphs < cfg->maxit + every) {
-            for (int k = 0; k < every; k++) {
-                CK(cudaGraphLaunch(S->graph, s));
-                graphs++;
-            }
-            CK(cudaStreamSynchronize(s));
-        }
-        launches += (long long)graphs * S->graph_kernels;
+        CK(cudaStreamSynchronize(s));
     }
+    launches += (long long)graphs * S->graph_kernels;
     if (S->st_host->s_conv) {
         L1(launch_bcg_xhalf(S->n, S->st, S->x, S->ph, s));
         launches++;

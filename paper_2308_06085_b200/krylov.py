@@ -39,6 +39,12 @@ class SolverConfig:
     restart: int | None = None
     breakdown_tol: float = 1e-30
     check_every: int = 4
+    # Bi-CGSTAB shadow vector r~ (B200 addition): "rhs" is the reference's r~ = b
+    # (krylov.py:229); "random" draws the seeded, layout-independent hash vector
+    # (HF_SHADOW_HASH, seed rng_seed) on the device.  With a point source "rhs"
+    # makes rho = conj(b_s) r_s depend on one vertex and the large wedge grids
+    # stop on the rho breakdown test.
+    shadow: str = "rhs"
 
 
 @dataclass
@@ -116,10 +122,13 @@ class Solver:
             raise KrylovError(f"unknown method {cfg.method!r}; choose from {sorted(_native.METHOD)}")
         if cfg.method == "idrs" and cfg.s < 1:
             raise KrylovError("IDR requires s >= 1")
+        if cfg.shadow not in _native.SHADOW:
+            raise KrylovError(f"unknown shadow {cfg.shadow!r}; choose from {sorted(_native.SHADOW)}")
+        kind = _native.SHADOW[cfg.shadow] if cfg.method == "bicgstab" else 0
         return _native.SolverConfigC(_native.METHOD[cfg.method], float(cfg.tol), int(cfg.maxit),
                                      int(cfg.s), int(cfg.restart or 0), float(cfg.breakdown_tol),
                                      shadow.ctypes.data if shadow is not None else None,
-                                     int(cfg.check_every))
+                                     int(cfg.check_every), kind, int(cfg.rng_seed) & (2**64 - 1))
 
     def solve(self, b, cfg: SolverConfig, x=None, host: bool = False):
         """Returns (x, ConvergenceReport).  host=True: b/x are host arrays and the

@@ -17,3 +17,18 @@ def oracle():
     from oracle import oracle as O
     O.lib()
     return O
+
+
+@pytest.fixture
+def hfopt():
+    """Kernel-variant options of the native library (hf_set_option), reset to
+    the defaults when the test ends."""
+    from paper_2308_06085_b200 import _native
+    touched = set()
+
+    def setopt(name, value):
+        touched.add(name)
+        _native.set_option(name, value)
+    yield setopt
+    for name in touched:
+        _native.set_option(name, 0)

@@ -16,7 +16,7 @@ KEYS = {"metric", "value", "unit", "impl", "n_gpus", "steps", "warmup", "ms_per_
 def _run(env_extra):
     env = {**os.environ, **env_extra}
     return subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1",
-                           "--warmup", "0", "--cpu-iters", "2"],
+                           "--warmup", "0", "--cpu-iters", "2", "--config", "c1"],
                           cwd=ROOT, env=env, capture_output=True, text=True, timeout=300)
 
 

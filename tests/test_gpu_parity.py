@@ -76,7 +76,7 @@ def _pair(hf, oracle, n, bc, k, beta2=-0.5, **cfg):
 
 @pytest.mark.parametrize("dims,h,kc", [((17, 17, 17), 1 / 16, 80.0), ((9, 17, 5), 1 / 8, 7.5),
                                        ((17, 17, 17), 1 / 16, 40.0)])
-def test_coarsest_fast_diagonalisation(hf, oracle, dims, h, kc, monkeypatch):
+def test_coarsest_fast_diagonalisation(hf, oracle, dims, h, kc, hfopt):
     """Constant-k Sommerfeld coarsest solve (separable, k_fdm_*) is exact: the
     true residual through the oracle's operator is at round-off and it agrees
     with the dense-inverse path (HF_COARSEST_DENSE) to 1e-12."""
@@ -90,12 +90,7 @@ def test_coarsest_fast_diagonalisation(hf, oracle, dims, h, kc, monkeypatch):
     x = coarsest_solve(hier, b).cpu().numpy()
     r = b - oracle.apply(np.full(dims, kc), x, h, spec.shift, "sommerfeld")
     assert np.linalg.norm(r) / np.linalg.norm(b) < 1e-12
-    # the single thread-block-cluster launch (opt-in) gives the same solution
-    monkeypatch.setenv("HF_FDM_CLUSTER", "1")
-    xcl = coarsest_solve(hier, b).cpu().numpy()
-    monkeypatch.delenv("HF_FDM_CLUSTER")
-    assert _rel(xcl, x) < 1e-13
-    monkeypatch.setenv("HF_COARSEST_DENSE", "1")
+    hfopt("coarsest_dense", 1)
     dense = build_hierarchy(grid, None, spec, MGConfig(coarsest_threshold=64))
     assert dense.coarsest_kind == "symmetric"
     xd = coarsest_solve(dense, b).cpu().numpy()
@@ -110,7 +105,7 @@ def test_coarsest_fast_diagonalisation(hf, oracle, dims, h, kc, monkeypatch):
     ((65, 49, 33), "dirichlet", "field", {}),
     ((65, 65, 65), "sommerfeld", "const", {"nu1": 0}),
 ])
-def test_fused_up_matches_split(hf, dims, bc, kind, mg, monkeypatch):
+def test_fused_up_matches_split(hf, dims, bc, kind, mg, hfopt):
     """Prolongation + correction produced inside the post-smoothing sweep
     (MODE_UP) matches the split correction + Jacobi kernels (same arithmetic;
     FMA contraction may differ between the kernels)."""
@@ -121,12 +116,12 @@ def test_fused_up_matches_split(hf, dims, bc, kind, mg, monkeypatch):
     spec = OperatorSpec("cslp", 1.0, -0.5, Dirichlet(0.0) if bc == "dirichlet" else Sommerfeld(), k)
     r = torch.as_tensor(_rand(dims, 41)).cuda()
     hier = build_hierarchy(grid, None, spec, MGConfig(**mg))
-    monkeypatch.setenv("HF_FUSE_UP", "1")
+    hfopt("fuse_up", 1)
     fused = mg_precondition(hier, r).cpu().numpy()        # tiled MODE_UP
-    monkeypatch.setenv("HF_FLAT_UP", "1")
+    hfopt("flat_up", 1)
     flat = mg_precondition(hier, r).cpu().numpy()         # flat MODE_UP (opt-in)
-    monkeypatch.delenv("HF_FLAT_UP")
-    monkeypatch.setenv("HF_NO_FUSE", "1")
+    hfopt("flat_up", 0)
+    hfopt("no_fuse", 1)
     split = mg_precondition(hier, r).cpu().numpy()
     assert _rel(fused, split) < 1e-13
     assert _rel(flat, split) < 1e-13
@@ -142,13 +137,13 @@ def test_fused_up_matches_split(hf, dims, bc, kind, mg, monkeypatch):
     ((33, 17, 65), "sommerfeld", "field"),
 ])
 @pytest.mark.parametrize("variant", ["flat", "tiled"])
-def test_fused_down_restrict_matches_split(hf, dims, bc, kind, variant, monkeypatch):
+def test_fused_down_restrict_matches_split(hf, dims, bc, kind, variant, hfopt):
     """Pre-smoothing + residual + full weighting in one kernel (k_flat_dr, or
     the tiled k_down_restrict used on wide planes) matches the split down1 +
     restriction kernels on every level of the cycle (same arithmetic; only
     FMA contraction may differ)."""
     if variant == "tiled":
-        monkeypatch.setenv("HF_NO_FLAT_DR", "1")
+        hfopt("no_flat_dr", 1)
     from paper_2308_06085_b200.multigrid import MGConfig, build_hierarchy, mg_precondition
     from paper_2308_06085_b200.operators import Dirichlet, OperatorSpec, Sommerfeld
     grid = hf.make_grid(*dims, 1.0 / (dims[0] - 1))
@@ -156,15 +151,15 @@ def test_fused_down_restrict_matches_split(hf, dims, bc, kind, variant, monkeypa
     spec = OperatorSpec("cslp", 1.0, -0.5, Dirichlet(0.0) if bc == "dirichlet" else Sommerfeld(), k)
     r = torch.as_tensor(_rand(dims, 43)).cuda()
     hier = build_hierarchy(grid, None, spec, MGConfig())
-    monkeypatch.setenv("HF_DR", "1")
+    hfopt("tiled_dr", 1)
     fused = mg_precondition(hier, r).cpu().numpy()
-    monkeypatch.setenv("HF_NO_DR", "1")
+    hfopt("no_dr", 1)
     split = mg_precondition(hier, r).cpu().numpy()
     assert _rel(fused, split) < 1e-13
 
 
 @pytest.mark.parametrize("n,kind", [(129, "wedge"), (129, "const"), (65, "wedge")])
-def test_flat_kernels_match_tiled(hf, n, kind, monkeypatch):
+def test_flat_kernels_match_tiled(hf, n, kind, hfopt):
     """The flat bulk-copy kernels (k_flat_stencil, k_flat_dr, k_corr_flat) and
     the 2-D tiled cp.async kernels compute the same V-cycle and operator at
     BASELINE-like sizes, varying medium included (rounding-level differences
@@ -179,8 +174,8 @@ def test_flat_kernels_match_tiled(hf, n, kind, monkeypatch):
     A = StencilOperator(spec, p.grid)
     z_flat = mg_precondition(hier, r).cpu().numpy()
     v_flat = A.apply(r).cpu().numpy()
-    monkeypatch.setenv("HF_NO_FLAT", "1")
-    monkeypatch.setenv("HF_NO_DR", "1")
+    hfopt("no_flat", 1)
+    hfopt("no_dr", 1)
     z_tile = mg_precondition(hier, r).cpu().numpy()
     v_tile = A.apply(r).cpu().numpy()
     assert _rel(z_flat, z_tile) < 1e-12
@@ -230,7 +225,7 @@ def test_cycle_matches_oracle(hf, oracle, bc, cfg):
 @pytest.mark.parametrize("n,bc,kind", [((17, 17, 193), "sommerfeld", "const"),
                                         ((9, 9, 161), "dirichlet", "field"),
                                         ((9, 17, 255), "sommerfeld", "field")])
-def test_wide_plane_flat_kernels_match_oracle(hf, oracle, n, bc, kind, monkeypatch):
+def test_wide_plane_flat_kernels_match_oracle(hf, oracle, n, bc, kind, hfopt):
     """Planes 154..255 vertices wide: the flat kernels' five-points-per-thread
     fused down-sweep (k_flat_dr RPT 5) and the widest flat ranges, against the
     oracle's V-cycle, and the fused down-sweep against the split pair."""
@@ -240,7 +235,7 @@ def test_wide_plane_flat_kernels_match_oracle(hf, oracle, n, bc, kind, monkeypat
     r = _rand(n, 22)
     got = mg_precondition(hier, r).cpu().numpy()
     assert _rel(got, oh.precondition(r)) < 1e-9
-    monkeypatch.setenv("HF_NO_DR", "1")
+    hfopt("no_dr", 1)
     split = mg_precondition(hier, r).cpu().numpy()
     assert _rel(got, split) < 1e-13
 
@@ -346,33 +341,6 @@ def test_gmres_restart(hf, oracle):
     xr, rr = Solver(A, hier).solve(b, SolverConfig(method="gmres", restart=5, maxit=200))
     assert rr.converged
     assert np.linalg.norm(xr.cpu().numpy() - xo) / np.linalg.norm(xo) < 1e-5
-
-
-def test_conditional_graph_solve_matches(hf, monkeypatch):
-    """The opt-in single-graph solve (while / nested if nodes, HF_COND_GRAPH)
-    runs the same kernels: same iterations, bit-identical solution, also when
-    it stops on the half step."""
-    from paper_2308_06085_b200 import problems
-    from paper_2308_06085_b200.krylov import Solver, SolverConfig
-    from paper_2308_06085_b200.multigrid import MGConfig, build_hierarchy
-    from paper_2308_06085_b200.operators import OperatorSpec, StencilOperator
-    p = problems.point_source_cube(33, 20.0, "sommerfeld")
-    spec, b = problems.build_problem(p)
-    k = np.full(p.grid.shape, 20.0)
-
-    def run(tol):
-        A = StencilOperator(spec, p.grid)
-        hier = build_hierarchy(p.grid, None, OperatorSpec("cslp", 1.0, -0.5, spec.bc, k), MGConfig())
-        x, rep = Solver(A, hier).solve(b, SolverConfig(method="bicgstab", tol=tol, maxit=400))
-        return x.cpu().numpy(), rep
-
-    ref = [run(t) for t in (1e-6, 1e-3)]
-    monkeypatch.setenv("HF_COND_GRAPH", "1")
-    got = [run(t) for t in (1e-6, 1e-3)]
-    for (x0, r0), (x1, r1) in zip(ref, got):
-        assert r0.iterations == r1.iterations and r0.matvec_count == r1.matvec_count
-        assert np.array_equal(x0, x1)
-        assert r0.residual_history == r1.residual_history
 
 
 def test_repeat_solves_bit_identical(hf):

@@ -31,7 +31,7 @@ def test_library_loads_and_exports_every_symbol():
     for name in _declared_symbols():
         assert hasattr(lib, name), name
     L = _native.load()
-    assert L.hf_version() == 1
+    assert L.hf_version() == 2
 
 
 def test_missing_library_fails_loudly(tmp_path):

@@ -17,7 +17,7 @@ from paper_2308_06085_b200.multigrid import MGConfig, build_hierarchy  # noqa: E
 from paper_2308_06085_b200.operators import OperatorSpec, StencilOperator  # noqa: E402
 
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 10
-p, spec, b_host = bench._problem()
+p, spec, b_host = bench._problem("c1")
 A = StencilOperator(spec, p.grid)
 hier = build_hierarchy(p.grid, None, OperatorSpec("cslp", 1.0, -0.5, spec.bc, spec.k_field), MGConfig())
 solver = Solver(A, hier)
@@ -27,7 +27,7 @@ flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
 
 def run(every):
-    cfg = SolverConfig(method="bicgstab", tol=bench.TOL, maxit=bench.MAXIT, check_every=every)
+    cfg = SolverConfig(method="bicgstab", tol=bench.TOL, maxit=400, check_every=every)
     for _ in range(3):
         solver.solve(b, cfg, x=x)
     ts = []

@@ -16,7 +16,7 @@ def main():
     from paper_2308_06085_b200.dist import SlabSolver
     from paper_2308_06085_b200.krylov import SolverConfig
     from paper_2308_06085_b200.partition import LocalSlabComm, slab_partition
-    p, spec, b = bench._problem()
+    p, spec, b = bench._problem("c1")
     for ns in (1, 2, 4):
         ext = slab_partition(p.grid, ns)
         S = SlabSolver(p.grid, ext, spec.k_field, p.bc, LocalSlabComm(ns))

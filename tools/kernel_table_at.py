@@ -18,10 +18,9 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 513
 p = (problems.wedge3_problem(n) if "wedge" in sys.argv[2:]
      else problems.point_source_cube(n, 80.0 * (n - 1) / 128, "sommerfeld"))
 spec, b = problems.build_problem(p)
-A = StencilOperator(spec, p.grid)
-H = build_hierarchy(p.grid, None, OperatorSpec("cslp", 1.0, -0.5, spec.bc, spec.k_field), MGConfig())
+A, H, S = bench._solver_for(p, spec)
 hbm, kind = bench._peaks()
-t = bench.kernel_table(A, H, n ** 3, 1.0)
+t = bench.kernel_table(A, H, S, n ** 3, 1.0)
 for k, v in t.items():
     v["frac"] = round(v["gbs"] / hbm, 4)
     v.pop("share", None)

@@ -2,7 +2,8 @@
 dominant bench kernel: DRAM bytes (read + write) per launch, averaged over the
 captured launches of the named kernel.
 
-    python tools/ncu_traffic.py gpurun_out/dom.ncu-rep down_restrict k_flat_dr
+    python tools/ncu_traffic.py gpurun_out/dom.ncu-rep c2 jacobi_postsmooth k_stencil
+(entry keyed by the bench config, so bench.py picks the one of its workload)
 """
 import json
 import os
@@ -13,7 +14,7 @@ sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 from ncu_summary import main as summarise  # noqa: E402
 
 
-def run(rep, bench_name, kernel_regex):
+def run(rep, config, bench_name, kernel_regex):
     tmp = "/tmp/_ncu_traffic.json"
     summarise(rep, tmp)
     rows = [r for r in json.load(open(tmp)) if kernel_regex in r["kernel"]]
@@ -28,10 +29,17 @@ def run(rep, bench_name, kernel_regex):
            "source": os.path.basename(rep) + " (ncu --set full --clock-control none, cold cache)"}
     path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
                         "ncu_traffic.json")
+    try:
+        allc = json.load(open(path))
+        if "kernel" in allc:          # round-1 single-entry format
+            allc = {}
+    except Exception:
+        allc = {}
+    allc[config] = out
     with open(path, "w") as f:
-        json.dump(out, f, indent=1)
+        json.dump(allc, f, indent=1)
     print(json.dumps(out))
 
 
 if __name__ == "__main__":
-    run(sys.argv[1], sys.argv[2], sys.argv[3])
+    run(sys.argv[1], sys.argv[2], sys.argv[3], sys.argv[4])

@@ -162,7 +162,13 @@ int hf_coarsest_solve(hf_hierarchy *hier, const double *b, double *x);
 #define HF_COARSEST_KIND_DENSE 1       /* dense inverse, GEMV */
 #define HF_COARSEST_KIND_SYMMETRIC 2   /* packed symmetric M^-1 S^-1 */
 #define HF_COARSEST_KIND_SEPARABLE 3   /* fast diagonalisation (constant k) */
+#define HF_COARSEST_KIND_GMRES 4       /* GMRES to coarsest_tol (HF_COARSEST_GMRES, or the
+                                          direct method's fallback on coarsest grids over
+                                          60000 vertices without a separable factorisation) */
 int hf_coarsest_kind(const hf_hierarchy *hier);
+/* multigrid.py:320-322 hier.coarsest_flags: coarsest GMRES solves that stopped at
+   coarsest_maxit above coarsest_tol since the last reset (always 0 for exact solves). */
+int hf_coarsest_flags(hf_hierarchy *hier, int reset);
 /* multigrid.py:395-419 mg_precondition: z ~= M^-1 r, one V/F cycle */
 int hf_mg_precondition(hf_hierarchy *hier, const double *r, double *z);
 /* Fused pieces of one V(1,1) level (multigrid.py:337-343) for slab drivers that

@@ -30,7 +30,7 @@ EXPORTED = (
     "hf_operator_create", "hf_operator_destroy", "hf_operator_apply", "hf_operator_diag",
     "hf_jacobi_smooth", "hf_hierarchy_create", "hf_hierarchy_destroy",
     "hf_hierarchy_num_levels", "hf_hierarchy_level_shape", "hf_restrict_fw", "hf_prolong_tl",
-    "hf_coarsest_solve", "hf_coarsest_kind", "hf_mg_precondition", "hf_level_down1", "hf_level_down_restrict", "hf_level_up", "hf_level_correct", "hf_level_correct_ext",
+    "hf_coarsest_solve", "hf_coarsest_kind", "hf_coarsest_flags", "hf_mg_precondition", "hf_level_down1", "hf_level_down_restrict", "hf_level_up", "hf_level_correct", "hf_level_correct_ext",
     "hf_level_smooth", "hf_solver_create", "hf_solver_destroy",
     "hf_solve", "hf_solve_host", "hf_dot", "hf_solver_bench_vec",
     "hf_bcg_create", "hf_bcg_destroy", "hf_bcg_step", "hf_bcg_read", "hf_bcg_vec_init", "hf_bcg_vec_p",
@@ -108,6 +108,7 @@ def load(path: str = LIB_PATH):
         "hf_prolong_tl": ([vp, i, vp, vp], i),
         "hf_coarsest_solve": ([vp, vp, vp], i),
         "hf_coarsest_kind": ([vp], i),
+        "hf_coarsest_flags": ([vp, i], i),
         "hf_mg_precondition": ([vp, vp, vp], i),
         "hf_level_down1": ([vp, i, vp, vp], i),
         "hf_level_down_restrict": ([vp, i, vp, vp], i),

@@ -6,7 +6,7 @@ import os
 import subprocess
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SOURCES = ["csrc/hf_kernels.cu", "csrc/hf_runtime.cu"]
+SOURCES = ["csrc/hf_kernels.cu", "csrc/hf_coarse_gmres.cu", "csrc/hf_runtime.cu"]
 HEADERS = ["csrc/hf_device.cuh", "csrc/hf_kernels.cuh", "../include/helmfree_b200.h"]
 OUT = os.path.join(_HERE, "_lib", "libhelmfree_b200.so")
 

@@ -51,10 +51,6 @@ struct Lvl {
                          // tab[8 + nb] = D^-1(nb) / D^-1(0)
 };
 
-// D^-1 at local linear index q of a vertex touching nb physical faces
-__device__ __forceinline__ double2 dinv_at(const Lvl &L, long long q, int nb) {
-    return L.dinv ? __ldg(L.dinv + q) : __ldg(L.tab + 4 + nb);
-}
 
 __device__ __forceinline__ double kat(const Lvl &L, long long q) {
     return L.k ? __ldg(L.k + q) : L.kc;
@@ -78,6 +74,18 @@ __device__ __forceinline__ cd ap_of(const Lvl &L, double kk, int nb) {
 __device__ __forceinline__ cd diag_of(const Lvl &L, double kk, int nb) {
     if (L.bc == HF_BC_DIRICHLET && nb) return mk(1.0, 0.0);
     return ap_of(L, kk, nb);
+}
+
+// D^-1 from the wavenumber: one complex reciprocal (same formula as the stored
+// D^-1 field of k_dinv, so both give identical bits).  Cheaper than streaming
+// the 16-byte field: a varying medium reads k (8 B) anyway.
+__device__ __forceinline__ cd dinv_of(const Lvl &L, double kk, int nb) {
+    return cdiv(mk(1.0, 0.0), diag_of(L, kk, nb));
+}
+
+// D^-1 at local linear index q of a vertex touching nb physical faces
+__device__ __forceinline__ double2 dinv_at(const Lvl &L, long long q, int nb) {
+    return L.k ? dinv_of(L, __ldg(L.k + q), nb) : __ldg(L.tab + 4 + nb);
 }
 
 // ---------------------------------------------------------------------------

@@ -252,7 +252,7 @@ struct EpiJacobi {
 
 template <int MODE, bool KVAR, bool AUX>
 struct StencilSmem {
-    static constexpr bool kWd = MODE == MODE_PRE && KVAR;     // staged D^-1 field
+    static constexpr bool kWd = false;   // (D^-1 b is formed in place from k, see vfix)
     static constexpr bool kUp = MODE == MODE_UP;
     cd raw[RING][NFILL];
     cd wd[kWd ? RING : 1][kWd ? NFILL : 1];
@@ -345,6 +345,19 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
         }
         if (ok0) sm.raw[slot][tid] = cmul(sm.raw[slot][tid], tab[8 + nbx + nbe0]);
         if (ok1) sm.raw[slot][tid + NT] = cmul(sm.raw[slot][tid + NT], tab[8 + nbx + nbe1]);
+    };
+    // MODE_PRE, varying medium: each thread turns its own staged entries of b
+    // into f = D^-1 b in place once their plane lands (one plane ahead of use),
+    // D^-1 from k at the entry's (mirrored) vertex -- no D^-1 field is streamed
+    // and a point's row reads its seven neighbours' f directly
+    constexpr bool kVarPre = MODE == MODE_PRE && KVAR;
+    auto vfix = [&](int slot, int i) {
+        int gi = L.lo1 + i;
+        gi = gi < 0 ? -gi : (gi >= L.n1 ? 2 * (L.n1 - 1) - gi : gi);
+        const int nbx = (gi == 0) + (gi == L.n1 - 1);
+        const double *kp = L.k + (long long)(gi - L.lo1) * L.plane;
+        if (ok0) sm.raw[slot][tid] = cmul(sm.raw[slot][tid], dinv_of(L, __ldg(kp + go0), nbx + nbe0));
+        if (ok1) sm.raw[slot][tid + NT] = cmul(sm.raw[slot][tid + NT], dinv_of(L, __ldg(kp + go1), nbx + nbe1));
     };
     // MODE_UP: coarse tile of e staged once per block (all coarse planes the
     // chunk's fine planes i0-1 .. i1 interpolate from, mirrored ones included)
@@ -467,12 +480,15 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
 
     // planes i0-1 .. i0+RING-3 into slots 0 .. RING-2
     static_for<0, RING - 1>([&](auto Sc) { stage(Sc, i0 - 1 + decltype(Sc)::value); });
-    if (kScale || MODE == MODE_UP) {
+    if (kScale || kVarPre || MODE == MODE_UP) {
         cp_wait<RING - 3>();               // planes i0-1, i0 (and the e tile) landed
         __syncthreads();                   // tab[] and the e tile visible
         if (kScale) {
             fixup(0, i0 - 1);
             fixup(1, i0);
+        } else if (kVarPre) {
+            vfix(0, i0 - 1);
+            vfix(1, i0);
         } else {
             produce(0, i0 - 1);
             produce(1, i0);
@@ -500,6 +516,7 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
         }
         cp_wait<RING - 4>();               // plane i+1 landed (later ones may be in flight)
         if (kScale) fixup(sn, i + 1);      // own entries only: no barrier needed before
+        if (kVarPre && i + 1 <= i1) vfix(sn, i + 1);
         if (MODE == MODE_UP) produce(sn, i + 1);
         __syncthreads();
         stage_in(IC<ss>{}, i + RING - 2);  // into the slot read last at step i-1
@@ -515,16 +532,8 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
             const double kk = k_cur;
             cd post = one;
             if (MODE == MODE_PRE) {
-                if (KVAR) {                   // staged D^-1, w applied once after M
-                    const int W = SM::kWd ? 1 : 0;
+                if (KVAR) {                   // staged f = D^-1 b (vfix), w applied once after M
                     post = mk(omega, 0.0);
-                    fc = cmul(fc, sm.wd[W * sc][cf]);
-                    xm = cmul(xm, sm.wd[W * sp][cf]);
-                    xp = cmul(xp, sm.wd[W * sn][cf]);
-                    ym = cmul(ym, sm.wd[W * sc][cf - HALO_X]);
-                    yp = cmul(yp, sm.wd[W * sc][cf + HALO_X]);
-                    zm = cmul(zm, sm.wd[W * sc][cf - 1]);
-                    zp = cmul(zp, sm.wd[W * sc][cf + 1]);
                 } else {
                     post = wd0;               // f = wd0 * b^ (staged, rescaled at the faces)
                 }
@@ -540,7 +549,7 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
             cd av = mk(0, 0);
             if (Epi::kAux) av = a_cur;
             cd wd = mk(0, 0);
-            if (Epi::kDinv) wd = KVAR ? cscal(__ldg(L.dinv + q), omega) : wd_nb(nb);
+            if (Epi::kDinv) wd = KVAR ? cscal(dinv_of(L, kk, nb), omega) : wd_nb(nb);
             epi(q, fc, mf, wd, av, acc);
         }
         q += L.plane;
@@ -857,7 +866,7 @@ __global__ void __launch_bounds__(256, 3) k_flat_stencil(Lvl L, const cd *__rest
             if (MODE == MODE_PRE) mf = cmul(post, mf);
             if (!SOMM && nb) mf = (MODE == MODE_PRE) ? cmul(post, fc) : fc;
             cd wd = mk(0, 0);
-            if (Epi::kDinv) wd = KVAR ? cscal(__ldg(L.dinv + qk), omega) : tab[4 + nb];
+            if (Epi::kDinv) wd = KVAR ? cscal(dinv_of(L, C.k[k], nb), omega) : tab[4 + nb];
             if (act[k]) epi(qk, fc, mf, wd, ca[k], acc);
         }
         q += plane;

@@ -74,4 +74,23 @@ void launch_bcg_step(BcgState *st, int op, const cd *sums, cudaStream_t s);
 
 #define VEC_BLOCKS_HOST 592
 
+// coarsest GMRES in one cooperative launch (hf_coarse_gmres.cu)
+struct GmArgs {
+    Lvl L;                 // coarsest level (whole grid)
+    long long N;
+    int cap, maxit;        // basis vectors, iteration limit (multigrid.py:48-49)
+    double tol, btol;
+    const cd *b;
+    cd *x;
+    cd *V;                 // (cap + 1) * N basis
+    cd *part;              // 2 * blocks * (cap + 2) partial sums (double-buffered)
+    cd *Hm;                // cap * cap rotated Hessenberg columns (block 0)
+    cd *y;                 // cap
+    int *flags;            // solves that missed tol (coarsest_flags)
+    const int *done;
+};
+size_t coarse_gmres_smem(int cap);
+int coarse_gmres_blocks(long long N, int cap);
+cudaError_t launch_coarse_gmres(const GmArgs &a, int nblk, cudaStream_t s);
+
 }  // namespace hf

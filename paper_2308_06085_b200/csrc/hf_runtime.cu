@@ -232,6 +232,11 @@ struct hf_hierarchy {
     cd *fdm_invD = nullptr; // 1 / (l1_a + l2_b + l3_c + c) on the coarsest grid
     cd *fdm_tmp = nullptr;  // 2 N scratch
     int coarsest_flags = 0;
+    // coarsest GMRES (HF_COARSEST_GMRES, or the fallback when no exact
+    // factorisation applies): one cooperative launch per solve
+    bool gm_on = false;
+    GmArgs gm{};
+    int gm_nblk = 0;
 };
 
 static bool keep_coarsening(int n1, int n2, int n3, const hf_mg_config &c) {
@@ -405,7 +410,7 @@ static int build_coarsest_direct(hf_hierarchy *H, cudaStream_t s) {
     if (C.L.lo1 != 0 || C.L.nx != C.L.n1)
         return fail(HF_ERR_UNSUPPORTED, "direct coarsest solve needs the whole coarsest grid");
     long long N = (long long)C.L.n1 * C.L.plane;
-    if (N > 60000) return fail(HF_ERR_UNSUPPORTED, "coarsest grid too large for the dense inverse");
+    if (N > 60000) return 1;   // no exact factorisation: the caller falls back to GMRES
     H->Nc = (int)N;
     cudaError_t err;
     cd *Amat = nullptr;
@@ -481,6 +486,37 @@ static int build_coarsest_direct(hf_hierarchy *H, cudaStream_t s) {
 
 static cudaStream_t work_stream() { return g_user_stream; }
 
+// the reference's coarsest solve: GMRES to coarsest_tol (multigrid.py:300-323)
+static int build_coarsest_gmres(hf_hierarchy *H) {
+    Level &C = H->lev.back();
+    if (C.L.lo1 != 0 || C.L.nx != C.L.n1)
+        return fail(HF_ERR_UNSUPPORTED, "coarsest GMRES needs the whole coarsest grid");
+    const long long N = (long long)C.L.n1 * C.L.plane;
+    const long long mem_cap = (4ll << 30) / (16 * N) - 1;   // basis <= 4 GiB
+    const int cap = (int)std::max<long long>(8, std::min<long long>(
+                        std::min<long long>(H->cfg.coarsest_maxit, 1024), mem_cap));
+    const int nblk = coarse_gmres_blocks(N, cap);
+    if (nblk <= 0) return fail(HF_ERR_CUDA, "coarsest GMRES: kernel not launchable");
+    cudaError_t e;
+    GmArgs &g = H->gm;
+    g.L = C.L;
+    g.N = N;
+    g.cap = cap;
+    g.maxit = std::max(1, H->cfg.coarsest_maxit);
+    g.tol = H->cfg.coarsest_tol;
+    g.btol = 1e-30;
+    g.V = H->A.get<cd>((size_t)(cap + 1) * N, e);
+    g.part = H->A.get<cd>((size_t)2 * nblk * (cap + 2), e);
+    g.Hm = H->A.get<cd>((size_t)cap * cap, e);
+    g.y = H->A.get<cd>(cap, e);
+    g.flags = H->A.get<int>(1, e);
+    if (!g.V || !g.part || !g.Hm || !g.y || !g.flags) return fail(HF_ERR_CUDA, "cudaMalloc coarsest GMRES");
+    H->gm_nblk = nblk;
+    H->gm_on = true;
+    H->Nc = (int)N;
+    return 0;
+}
+
 extern "C" hf_hierarchy *hf_hierarchy_create(int n1, int n2, int n3, int lo1, int nx, double h,
                                              double beta1, double beta2, int bc,
                                              const double *k_host, double k_const,
@@ -490,8 +526,13 @@ extern "C" hf_hierarchy *hf_hierarchy_create(int n1, int n2, int n3, int lo1, in
         fail(HF_ERR_ARG, "unknown cycle type");
         return nullptr;
     }
-    if (cfg->coarsest_method != HF_COARSEST_DIRECT && cfg->coarsest_method != HF_COARSEST_EXTERNAL) {
-        fail(HF_ERR_UNSUPPORTED, "coarsest_method must be HF_COARSEST_DIRECT or HF_COARSEST_EXTERNAL");
+    if (cfg->coarsest_method != HF_COARSEST_DIRECT && cfg->coarsest_method != HF_COARSEST_GMRES &&
+        cfg->coarsest_method != HF_COARSEST_EXTERNAL) {
+        fail(HF_ERR_ARG, "coarsest_method must be HF_COARSEST_DIRECT, _GMRES or _EXTERNAL");
+        return nullptr;
+    }
+    if (cfg->coarsest_method == HF_COARSEST_GMRES && (cfg->coarsest_maxit < 1 || !(cfg->coarsest_tol > 0))) {
+        fail(HF_ERR_ARG, "coarsest GMRES needs coarsest_maxit >= 1 and coarsest_tol > 0");
         return nullptr;
     }
     if (cfg->nu1 < 0 || cfg->nu2 < 0 || !(cfg->omega > 0 && cfg->omega <= 1)) {
@@ -538,7 +579,14 @@ extern "C" hf_hierarchy *hf_hierarchy_create(int n1, int n2, int n3, int lo1, in
         }
         a = na; b = nb; c = nc; l0 = clo; cnx = chi - clo + 1; hh = 2.0 * hh;
     }
-    if (cfg->coarsest_method == HF_COARSEST_DIRECT && build_coarsest_direct(H, work_stream())) {
+    int rc = 0;
+    if (cfg->coarsest_method == HF_COARSEST_DIRECT) {
+        rc = build_coarsest_direct(H, work_stream());
+        if (rc == 1) rc = build_coarsest_gmres(H);   // too large for an exact factorisation
+    } else if (cfg->coarsest_method == HF_COARSEST_GMRES) {
+        rc = build_coarsest_gmres(H);
+    }
+    if (rc) {
         delete H;
         return nullptr;
     }
@@ -558,7 +606,12 @@ extern "C" int hf_hierarchy_level_shape(const hf_hierarchy *H, int l, int *d) {
 // cycles (multigrid.py:326-419)
 // ---------------------------------------------------------------------------
 static void coarsest(hf_hierarchy *H, const cd *b, cd *x, cudaStream_t s, const int *done) {
-    if (H->fdm) {
+    if (H->gm_on) {
+        GmArgs a = H->gm;
+        a.b = b; a.x = x; a.done = done;
+        launch_coarse_gmres(a, H->gm_nblk, s);
+        g_launches++;
+    } else if (H->fdm) {
         const Lvl &L = H->lev.back().L;
         g_launches += launch_fdm(L.n1, L.n2, L.n3, H->fdm, H->fdm_invD, b, H->fdm_tmp, x, s, done);
     } else if (H->symtiles) {
@@ -714,12 +767,25 @@ extern "C" int hf_coarsest_kind(const hf_hierarchy *H) {
     if (H->fdm) return HF_COARSEST_KIND_SEPARABLE;
     if (H->symtiles) return HF_COARSEST_KIND_SYMMETRIC;
     if (H->Minv) return HF_COARSEST_KIND_DENSE;
+    if (H->gm_on) return HF_COARSEST_KIND_GMRES;
     return HF_COARSEST_KIND_NONE;
+}
+
+extern "C" int hf_coarsest_flags(hf_hierarchy *H, int reset) {
+    if (!H) return fail(HF_ERR_ARG, "null hierarchy");
+    if (!H->gm_on) return 0;
+    int v = 0;
+    cudaStream_t s = work_stream();
+    CK(cudaStreamSynchronize(s));
+    CK(cudaMemcpy(&v, H->gm.flags, sizeof(int), cudaMemcpyDeviceToHost));
+    if (reset) CK(cudaMemset(H->gm.flags, 0, sizeof(int)));
+    CK(cudaDeviceSynchronize());
+    return v;
 }
 
 extern "C" int hf_coarsest_solve(hf_hierarchy *H, const double *b, double *x) {
     if (!H) return fail(HF_ERR_ARG, "null hierarchy");
-    if (H->cfg.coarsest_method != HF_COARSEST_DIRECT)
+    if (H->cfg.coarsest_method == HF_COARSEST_EXTERNAL)
         return fail(HF_ERR_ARG, "hierarchy was built with an external coarsest solve");
     coarsest(H, (const cd *)b, (cd *)x, work_stream(), nullptr);
     CKL();
@@ -962,6 +1028,7 @@ static int solve_bicgstab(hf_solver *S, const hf_solver_config *cfg, const cd *b
     *S->st_host = init;
     CK(cudaMemcpyAsync(S->st, S->st_host, sizeof(BcgState), cudaMemcpyHostToDevice, s));
     long long launches = 0;
+    if (S->M->gm_on) CK(cudaMemsetAsync(S->M->gm.flags, 0, sizeof(int), s));
     CK(cudaEventRecord(S->ev0, s));
     // shadow vector r~: b (the reference, krylov.py:229), the caller's host vector,
     // or the seeded hash vector (SolverConfig.shadow)
@@ -1007,6 +1074,7 @@ static int solve_bicgstab(hf_solver *S, const hf_solver_config *cfg, const cd *b
     rep->solve_ms = ms;
     rep->kernel_launches = (int)launches;
     rep->coarsest_flags = 0;
+    if (S->M->gm_on) CK(cudaMemcpy(&rep->coarsest_flags, S->M->gm.flags, sizeof(int), cudaMemcpyDeviceToHost));
     if (rep->history_host && rep->history_cap > 0 && st.iter > 0) {
         int cnt = std::min(st.iter, rep->history_cap);
         CK(cudaMemcpy(rep->history_host, S->hist, (size_t)cnt * sizeof(double), cudaMemcpyDeviceToHost));
@@ -1305,6 +1373,7 @@ static int solve_hostloop(hf_solver *S, const hf_solver_config *cfg, const cd *b
     cudaStream_t s = S->stream;
     KrylovOut o;
     long long launches = 0;
+    if (S->M->gm_on) CK(cudaMemsetAsync(S->M->gm.flags, 0, sizeof(int), s));
     CK(cudaEventRecord(S->ev0, s));
     int rc = cfg->method == HF_METHOD_GMRES ? solve_gmres(S, cfg, b, x, o, launches)
                                             : solve_idrs(S, cfg, b, x, o, launches);
@@ -1322,6 +1391,7 @@ static int solve_hostloop(hf_solver *S, const hf_solver_config *cfg, const cd *b
     rep->solve_ms = ms;
     rep->kernel_launches = (int)launches;
     rep->coarsest_flags = 0;
+    if (S->M->gm_on) CK(cudaMemcpy(&rep->coarsest_flags, S->M->gm.flags, sizeof(int), cudaMemcpyDeviceToHost));
     if (rep->history_host)
         for (int i = 0; i < std::min<int>((int)o.hist.size(), rep->history_cap); i++)
             rep->history_host[i] = o.hist[i];

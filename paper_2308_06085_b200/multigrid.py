@@ -7,11 +7,16 @@ build_hierarchy (:101-128), jacobi_smooth (:138-157), restrict_fw
 coarsest solve live in libhelmfree_b200.so.
 
 Coarsest solve: the reference runs unpreconditioned full GMRES to a relative
-residual of coarsest_tol (1e-11).  Here the fixed coarsest operator is
-factorised once at setup and applied as one dense GEMV per cycle
-(coarsest_method="direct"): it satisfies the same tolerance (exactly, up to
-round-off) with one HBM-bound pass instead of ~50-70 latency-bound GMRES
-iterations.
+residual of coarsest_tol (1e-11), max-iterations being a soft failure recorded
+in hier.coarsest_flags.  coarsest_method="gmres" runs exactly that on the
+device (one cooperative launch per solve, coarsest_tol / coarsest_maxit
+honoured, failures counted).  The default, coarsest_method="direct",
+factorises the fixed coarsest operator once at setup (fast diagonalisation for
+a constant medium, a packed symmetric or dense inverse otherwise) and meets
+the same tolerance exactly up to round-off with one pass instead of ~50-70
+latency-bound GMRES iterations; it falls back to GMRES when the coarsest grid
+has no exact factorisation (over 60000 vertices with a varying medium or
+Dirichlet faces).
 """
 
 from __future__ import annotations
@@ -98,10 +103,20 @@ class MGHierarchy:
 
     @property
     def coarsest_kind(self) -> str:
-        """Exact coarsest solve in use: "separable" (fast diagonalisation,
-        constant k), "symmetric" / "dense" (inverse), or "external"."""
+        """Coarsest solve in use: "separable" (fast diagonalisation, constant
+        k), "symmetric" / "dense" (inverse), "gmres", or "external"."""
         kind = _native.load().hf_coarsest_kind(self._h)
-        return {0: "external", 1: "dense", 2: "symmetric", 3: "separable"}[kind]
+        return {0: "external", 1: "dense", 2: "symmetric", 3: "separable", 4: "gmres"}[kind]
+
+    def sync_coarsest_flags(self) -> list:
+        """Append the device count of coarsest GMRES solves that stopped at
+        coarsest_maxit (multigrid.py:320-322) to coarsest_flags and reset it."""
+        n = _native.load().hf_coarsest_flags(self._h, 1)
+        if n < 0:
+            _native.check(n)
+        if n:
+            self.coarsest_flags.append({"count": int(n)})
+        return self.coarsest_flags
 
 
 def build_hierarchy(finest_grid: Grid3, finest_extent: BlockExtent | None,
@@ -202,6 +217,8 @@ def coarsest_solve(hier: MGHierarchy, b, out=None):
     dst = _out_like(hier.coarsest.extent.shape, out)
     _native.set_stream_from_torch()
     _native.check(_native.load().hf_coarsest_solve(hier._h, src.data_ptr(), dst.data_ptr()))
+    if hier.coarsest_kind == "gmres":
+        hier.sync_coarsest_flags()
     return out if out is not None else dst
 
 

@@ -421,8 +421,9 @@ def kernel_table(A, hier, solver, n, t_iter_ms, reps=12):
     rotate over sets whose total is > 2x L2.
 
     bytes_per_vertex = algorithmic HBM bytes per fine vertex of one launch:
-    16 per complex field read or written, + 8 for k and + 16 for the stored
-    D^-1 field when the medium varies (constant media pass k as a scalar),
+    16 per complex field read or written, + 8 for k when the medium varies
+    (constant media pass k as a scalar) and + 16 where a kernel streams the
+    stored D^-1 field (k_corr, k_flat_dr; the stencil sweeps form D^-1 from k),
     + 16 / 8 per fine vertex for coarse fields.  share = launches per
     Bi-CGSTAB iteration x ms / (ms per iteration)."""
     import torch
@@ -456,7 +457,7 @@ def kernel_table(A, hier, solver, n, t_iter_ms, reps=12):
         "prolong_correct": (lambda s: L.hf_level_correct(H, 0, p(s["b"]), p(s["ec"]), p(s["t"])),
                             32.0 + db + 16.0 * cr, "hbm", 2, "k_corr_flat<1>"),
         "jacobi_postsmooth": (lambda s: L.hf_level_smooth(H, 0, p(s["t"]), p(s["b"]), p(s["u"])),
-                              48.0 + kb + db, "hbm", 2,
+                              48.0 + kb, "hbm", 2,
                               "k_flat_stencil<LOAD,EpiJacobi>" if fused_down else
                               "k_stencil<LOAD,EpiJacobi>"),
     }
@@ -465,7 +466,7 @@ def kernel_table(A, hier, solver, n, t_iter_ms, reps=12):
                                   16.0 + kb + db + 16.0 * cr, "hbm", 2, "k_flat_dr")
     else:
         cases["presmooth_residual"] = (lambda s: L.hf_level_down1(H, 0, p(s["b"]), p(s["v"])),
-                                       32.0 + kb + db, "hbm", 2, "k_stencil<PRE,EpiResid>")
+                                       32.0 + kb, "hbm", 2, "k_stencil<PRE,EpiResid>")
         cases["restrict_fw"] = (lambda s: L.hf_restrict_fw(H, 0, p(s["v"]), p(s["bc"])),
                                 16.0 + 16.0 * cr, "hbm", 2, "k_restrict_flat")
     kind = hier.coarsest_kind

@@ -83,8 +83,11 @@ __device__ __forceinline__ cd dinv_of(const Lvl &L, double kk, int nb) {
     return cdiv(mk(1.0, 0.0), diag_of(L, kk, nb));
 }
 
-// D^-1 at local linear index q of a vertex touching nb physical faces
+// D^-1 at local linear index q of a vertex touching nb physical faces: the
+// stored field where the level keeps one (a pointwise kernel without ALU slack
+// -- k_corr -- is faster streaming 16 B than dividing), else from k
 __device__ __forceinline__ double2 dinv_at(const Lvl &L, long long q, int nb) {
+    if (L.dinv) return __ldg(L.dinv + q);
     return L.k ? dinv_of(L, __ldg(L.k + q), nb) : __ldg(L.tab + 4 + nb);
 }
 
@@ -112,7 +115,13 @@ struct RedSlot {
     cd *out;             // FIN_STORE destination (HF_MAX_DOTS)
     int op;
     BcgState *st;
+    // sparse shadow (st->nz > 0): sums[gd] = r~^H gvec over the nonzeros of r~,
+    // gathered by the last block (the dense pass then skips reading r~)
+    const cd *gvec = nullptr;
+    int gd = 0;
 };
+
+#define HF_NZ_MAX 16   // shadow vectors with at most this many nonzeros are gathered
 
 // Seeded shadow vector entry (SolverConfig.shadow = "random"): splitmix64 of
 // (seed, global vertex index) -> two doubles uniform in [-1/2, 1/2) (53-bit
@@ -140,6 +149,12 @@ struct BcgState {
     int iter, maxit, done, converged, breakdown, s_conv, matvecs, pad1;
     double *hist;
     int hist_cap, pad2;
+    // nonzeros of the shadow vector r~ (ascending index) when there are at most
+    // HF_NZ_MAX of them -- a point source with the reference's r~ = b has one:
+    // r~^H v is then conj(r~_s) v_s exactly, without streaming r~
+    int nz, nz_count;
+    long long nzq[HF_NZ_MAX];
+    cd nzw[HF_NZ_MAX];
 };
 
 __device__ __forceinline__ cd warp_sum(cd v) {
@@ -229,6 +244,12 @@ __device__ __forceinline__ void reduce_finish(cd (&acc)[ND], const RedSlot &rs) 
 #pragma unroll
             for (int d = 0; d < ND; d++) rs.out[d] = tot[d];
         } else {
+            if (rs.gvec && rs.st->nz > 0) {   // sparse shadow: fixed ascending order
+                cd g = mk(0, 0);
+                for (int k = 0; k < rs.st->nz; k++)
+                    g = cadd(g, cjmul(rs.st->nzw[k], __ldcg(rs.gvec + rs.st->nzq[k])));
+                sums[rs.gd] = g;
+            }
             bcg_finalize(rs.st, rs.op, sums);
         }
     }

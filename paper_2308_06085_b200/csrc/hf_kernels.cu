@@ -207,6 +207,10 @@ __device__ __forceinline__ void cp_async16s(unsigned saddr, const void *gmem, bo
     int sz = valid ? 16 : 0;
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(gmem), "r"(sz));
 }
+__device__ __forceinline__ void cp_async8s(unsigned saddr, const void *gmem, bool valid) {
+    int sz = valid ? 8 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(gmem), "r"(sz));
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
@@ -253,9 +257,11 @@ struct EpiJacobi {
 template <int MODE, bool KVAR, bool AUX>
 struct StencilSmem {
     static constexpr bool kWd = false;   // (D^-1 b is formed in place from k, see vfix)
+    static constexpr bool kKw = MODE == MODE_PRE && KVAR;   // staged k of the fill entries
     static constexpr bool kUp = MODE == MODE_UP;
     cd raw[RING][NFILL];
     cd wd[kWd ? RING : 1][kWd ? NFILL : 1];
+    double kw[kKw ? RING : 1][kKw ? NFILL : 1];
     cd ec[kUp ? UP_MAX_CPLANES : 1][kUp ? UP_EW * UP_EH : 1];   // coarse e tile
 };
 
@@ -355,9 +361,9 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
         int gi = L.lo1 + i;
         gi = gi < 0 ? -gi : (gi >= L.n1 ? 2 * (L.n1 - 1) - gi : gi);
         const int nbx = (gi == 0) + (gi == L.n1 - 1);
-        const double *kp = L.k + (long long)(gi - L.lo1) * L.plane;
-        if (ok0) sm.raw[slot][tid] = cmul(sm.raw[slot][tid], dinv_of(L, __ldg(kp + go0), nbx + nbe0));
-        if (ok1) sm.raw[slot][tid + NT] = cmul(sm.raw[slot][tid + NT], dinv_of(L, __ldg(kp + go1), nbx + nbe1));
+        if (ok0) sm.raw[slot][tid] = cmul(sm.raw[slot][tid], dinv_of(L, sm.kw[slot][tid], nbx + nbe0));
+        if (ok1)
+            sm.raw[slot][tid + NT] = cmul(sm.raw[slot][tid + NT], dinv_of(L, sm.kw[slot][tid + NT], nbx + nbe1));
     };
     // MODE_UP: coarse tile of e staged once per block (all coarse planes the
     // chunk's fine planes i0-1 .. i1 interpolate from, mirrored ones included)
@@ -432,7 +438,10 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
     // (invalid entries point at a valid vertex and copy 0 bytes)
     const unsigned sraw0 = (unsigned)__cvta_generic_to_shared(&sm.raw[0][tid]);
     const unsigned swd0 = (unsigned)__cvta_generic_to_shared(&sm.wd[0][SM::kWd ? tid : 0]);
+    const unsigned skw0 = (unsigned)__cvta_generic_to_shared(&sm.kw[0][SM::kKw ? tid : 0]);
     constexpr unsigned SLOT = NFILL * sizeof(cd);
+    constexpr unsigned KSLOT = NFILL * sizeof(double);
+    const double *k0 = SM::kKw ? L.k + go0 : nullptr, *k1 = SM::kKw ? L.k + go1 : nullptr;
     const cd *g0 = src + go0, *g1 = src + go1;
     const cd *d0 = SM::kWd ? L.dinv + go0 : nullptr, *d1 = SM::kWd ? L.dinv + go1 : nullptr;
     auto stage = [&](auto SS, int p) {     // one commit group per plane, ring slot SS
@@ -446,9 +455,11 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
         const bool v0 = pok && ok0, v1 = pok && ok1;
         cp_async16s(sraw0 + so, g0 + pb, v0);
         if (SM::kWd) cp_async16s(swd0 + so, d0 + pb, v0);
+        if (SM::kKw) cp_async8s(skw0 + decltype(SS)::value * KSLOT, k0 + pb, v0);
         if (has1) {
             cp_async16s(sraw0 + so + NT * sizeof(cd), g1 + pb, v1);
             if (SM::kWd) cp_async16s(swd0 + so + NT * sizeof(cd), d1 + pb, v1);
+            if (SM::kKw) cp_async8s(skw0 + decltype(SS)::value * KSLOT + NT * sizeof(double), k1 + pb, v1);
         }
         cp_commit();
     };
@@ -470,9 +481,11 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
         if (any) {
             cp_async16s(sraw0 + so, g0 + pb, ok0);
             if (SM::kWd) cp_async16s(swd0 + so, d0 + pb, ok0);
+            if (SM::kKw) cp_async8s(skw0 + decltype(SS)::value * KSLOT, k0 + pb, ok0);
             if (has1) {
                 cp_async16s(sraw0 + so + NT * sizeof(cd), g1 + pb, ok1);
                 if (SM::kWd) cp_async16s(swd0 + so + NT * sizeof(cd), d1 + pb, ok1);
+                if (SM::kKw) cp_async8s(skw0 + decltype(SS)::value * KSLOT + NT * sizeof(double), k1 + pb, ok1);
             }
         }
         cp_commit();
@@ -499,7 +512,7 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
     cd a_next = mk(0, 0);
     double k_next = L.kc;
     if (act && i0 < i1) {
-        if (Epi::kAux) a_next = __ldg(aux + q);
+        if (Epi::kAux && aux) a_next = __ldg(aux + q);
         if (KVAR) k_next = __ldg(L.k + q);
     }
     // one plane; R = (i - i0) mod RING fixes the ring slots at compile time:
@@ -511,7 +524,7 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
         const cd a_cur = a_next;
         const double k_cur = k_next;
         if (act && i + 1 < i1) {
-            if (Epi::kAux) a_next = __ldg(aux + q + L.plane);
+            if (Epi::kAux && aux) a_next = __ldg(aux + q + L.plane);
             if (KVAR) k_next = __ldg(L.k + q + L.plane);
         }
         cp_wait<RING - 4>();               // plane i+1 landed (later ones may be in flight)
@@ -811,7 +824,7 @@ __global__ void __launch_bounds__(256, 3) k_flat_stencil(Lvl L, const cd *__rest
         const bool top = gi == L.n1 - 1, bot = gi == 0;
         // centre epilogue operand of this plane, issued before the waits
         cd ca[2] = {mk(0, 0), mk(0, 0)};
-        if (Epi::kAux) {
+        if (Epi::kAux && aux) {
             ca[0] = __ldg(aux + q + qo0);
             ca[1] = __ldg(aux + q + qo1);
         }
@@ -1703,6 +1716,31 @@ __global__ void __launch_bounds__(256) k_bcg_init(long long n, const cd *__restr
     reduce_finish<2>(acc, red);
 }
 
+// nonzeros of the shadow vector (up to HF_NZ_MAX): slots taken in any order,
+// sorted by k_nz_finish, so the gathered inner products are deterministic
+__global__ void __launch_bounds__(256) k_nz_scan(long long n, const cd *__restrict__ rs, BcgState *st) {
+    pdl_enter();
+    for (long long q = blockIdx.x * 256ll + threadIdx.x; q < n; q += (long long)gridDim.x * 256) {
+        const cd w = __ldg(rs + q);
+        if (w.x != 0.0 || w.y != 0.0) {
+            const int k = atomicAdd(&st->nz_count, 1);
+            if (k < HF_NZ_MAX) st->nzq[k] = q;
+        }
+    }
+}
+__global__ void k_nz_finish(const cd *__restrict__ rs, BcgState *st) {
+    pdl_enter();
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const int c = st->nz_count;
+    if (c < 1 || c > HF_NZ_MAX) { st->nz = -1; return; }
+    for (int a = 1; a < c; a++)                     // insertion sort, <= 16 entries
+        for (int b = a; b > 0 && st->nzq[b - 1] > st->nzq[b]; b--) {
+            const long long t = st->nzq[b]; st->nzq[b] = st->nzq[b - 1]; st->nzq[b - 1] = t;
+        }
+    for (int k = 0; k < c; k++) st->nzw[k] = rs[st->nzq[k]];
+    st->nz = c;
+}
+
 // p = r + beta (p - omega v)   (krylov.py:240)
 __global__ void __launch_bounds__(256) k_bcg_p(long long n, const BcgState *st,
                                                const cd *__restrict__ r, cd *__restrict__ p,
@@ -1757,7 +1795,7 @@ __global__ void __launch_bounds__(256) k_bcg_xr(long long n, const BcgState *st,
         cd rv = csub(__ldg(s + q), cmul(om, __ldg(t + q)));
         r[q] = rv;
         acc[0] = cadd(acc[0], cjmul(rv, rv));
-        acc[1] = cadd(acc[1], cjmul(__ldg(rs + q), rv));
+        if (rs) acc[1] = cadd(acc[1], cjmul(__ldg(rs + q), rv));   // null: sparse shadow
     }
     reduce_finish<2>(acc, red);
 }
@@ -2574,6 +2612,10 @@ void launch_bcg_xr(long long n, const BcgState *st, cd *x, const cd *ph, const c
                    const cd *sv, const cd *t, cd *r, const cd *rs, const RedSlot &red,
                    cudaStream_t s, const int *done) {
     launch(k_bcg_xr, dim3(VEC_BLOCKS), dim3(256), 0, s, n, st, x, ph, sh, sv, t, r, rs, red, done);
+}
+void launch_nz_scan(long long n, const cd *rs, BcgState *st, cudaStream_t s) {
+    launch(k_nz_scan, dim3(VEC_BLOCKS), dim3(256), 0, s, n, rs, st);
+    launch(k_nz_finish, dim3(1), dim3(32), 0, s, rs, st);
 }
 void launch_bcg_step(BcgState *st, int op, const cd *sums, cudaStream_t s) {
     launch(k_bcg_step, dim3(1), dim3(32), 0, s, st, op, sums);

@@ -296,65 +296,127 @@ static bool invert(std::vector<zc> &A, int n) {
     return true;
 }
 
-// T = V diag(lam) V^-1 (row-major V, Vi); false if geev fails or the
-// decomposition does not reproduce T to ~1e-13 (then the dense path is used)
-static bool eig1d(cusolverDnHandle_t hs, const std::vector<zc> &T, int n, std::vector<zc> &lam,
-                  std::vector<zc> &V, std::vector<zc> &Vi, cudaStream_t s) {
-    std::vector<zc> Tc((size_t)n * n);   // column-major copy for cuSOLVER
-    for (int i = 0; i < n; i++)
-        for (int j = 0; j < n; j++) Tc[(size_t)j * n + i] = T[(size_t)i * n + j];
-    cusolverDnParams_t prm;
-    if (cusolverDnCreateParams(&prm) != CUSOLVER_STATUS_SUCCESS) return false;
-    void *dA = nullptr, *dW = nullptr, *dV = nullptr, *dwork = nullptr;
-    int *dinfo = nullptr;
-    size_t dws = 0, hws = 0;
-    bool ok = cudaMalloc(&dA, Tc.size() * sizeof(zc)) == cudaSuccess &&
-              cudaMalloc(&dW, n * sizeof(zc)) == cudaSuccess &&
-              cudaMalloc(&dV, Tc.size() * sizeof(zc)) == cudaSuccess &&
-              cudaMalloc(&dinfo, sizeof(int)) == cudaSuccess;
-    std::vector<char> hwork;
-    int info = -1;
-    if (ok) {
-        cudaMemcpy(dA, Tc.data(), Tc.size() * sizeof(zc), cudaMemcpyHostToDevice);
-        ok = cusolverDnXgeev_bufferSize(hs, prm, CUSOLVER_EIG_MODE_NOVECTOR, CUSOLVER_EIG_MODE_VECTOR,
-                                        n, CUDA_C_64F, dA, n, CUDA_C_64F, dW, CUDA_C_64F, nullptr, n,
-                                        CUDA_C_64F, dV, n, CUDA_C_64F, &dws, &hws) ==
-             CUSOLVER_STATUS_SUCCESS;
-    }
-    if (ok) {
-        hwork.resize(std::max<size_t>(hws, 1));
-        ok = cudaMalloc(&dwork, std::max<size_t>(dws, 1)) == cudaSuccess;
-    }
-    if (ok)
-        ok = cusolverDnXgeev(hs, prm, CUSOLVER_EIG_MODE_NOVECTOR, CUSOLVER_EIG_MODE_VECTOR, n,
-                             CUDA_C_64F, dA, n, CUDA_C_64F, dW, CUDA_C_64F, nullptr, n, CUDA_C_64F,
-                             dV, n, CUDA_C_64F, dwork, dws, hwork.data(), hws, dinfo) ==
-             CUSOLVER_STATUS_SUCCESS;
-    std::vector<zc> Vc((size_t)n * n);
+// Eigenvalues of a small complex upper-Hessenberg matrix (row-major, n <= ~100)
+// by the shifted QR algorithm: Wilkinson shifts from the trailing 2 x 2 block,
+// Givens QR steps on the active window, deflation on negligible subdiagonals.
+// Host code: the 1-D operators of the separable coarsest solve are at most a
+// few dozen wide, so a host solve takes microseconds (no device library setup).
+static bool hessenberg_eigvals(std::vector<zc> H, int n, std::vector<zc> &lam) {
     lam.assign(n, 0.0);
-    if (ok) {
-        ok = cudaStreamSynchronize(s) == cudaSuccess &&
-             cudaMemcpy(&info, dinfo, sizeof(int), cudaMemcpyDeviceToHost) == cudaSuccess &&
-             cudaMemcpy(lam.data(), dW, n * sizeof(zc), cudaMemcpyDeviceToHost) == cudaSuccess &&
-             cudaMemcpy(Vc.data(), dV, Vc.size() * sizeof(zc), cudaMemcpyDeviceToHost) == cudaSuccess &&
-             info == 0;
+    const double eps = 2.2e-16;
+    int hi = n - 1, iter = 0, total = 0;
+    auto h = [&](int i, int j) -> zc & { return H[(size_t)i * n + j]; };
+    while (hi >= 0) {
+        if (hi == 0) { lam[0] = h(0, 0); break; }
+        int l = hi;
+        while (l > 0 && std::abs(h(l, l - 1)) > eps * (std::abs(h(l, l)) + std::abs(h(l - 1, l - 1)))) l--;
+        if (l > 0) h(l, l - 1) = 0.0;
+        if (l == hi) { lam[hi] = h(hi, hi); hi--; iter = 0; continue; }
+        if (++total > 100 * n) return false;
+        const zc a = h(hi - 1, hi - 1), b = h(hi - 1, hi), c = h(hi, hi - 1), d = h(hi, hi);
+        zc mu;
+        if (iter % 11 == 10) {
+            mu = d + std::abs(c);                       // exceptional shift
+        } else {
+            const zc tr = a + d, det = a * d - b * c;
+            const zc disc = std::sqrt(tr * tr * 0.25 - det);
+            const zc m1 = tr * 0.5 + disc, m2 = tr * 0.5 - disc;
+            mu = std::abs(m1 - d) < std::abs(m2 - d) ? m1 : m2;
+        }
+        iter++;
+        for (int i = l; i <= hi; i++) h(i, i) -= mu;
+        std::vector<double> cs(hi - l);
+        std::vector<zc> sn(hi - l);
+        for (int k = l; k < hi; k++) {                  // rows: R = G^H (H - mu I)
+            const zc x = h(k, k), y = h(k + 1, k);
+            const double r = std::hypot(std::abs(x), std::abs(y));
+            double c0 = 1.0;
+            zc s0 = 0.0;
+            if (r > 0) {
+                c0 = std::abs(x) / r;
+                const zc ph = std::abs(x) > 0 ? x / std::abs(x) : zc(1.0, 0.0);
+                s0 = ph * std::conj(y) / r;
+            }
+            cs[k - l] = c0; sn[k - l] = s0;
+            for (int j = k; j <= hi; j++) {
+                const zc u = h(k, j), v = h(k + 1, j);
+                h(k, j) = c0 * u + s0 * v;
+                h(k + 1, j) = -std::conj(s0) * u + c0 * v;
+            }
+        }
+        for (int k = l; k < hi; k++) {                  // columns: R Q
+            const double c0 = cs[k - l];
+            const zc s0 = sn[k - l];
+            for (int i = l; i <= std::min(k + 1, hi); i++) {
+                const zc u = h(i, k), v = h(i, k + 1);
+                h(i, k) = c0 * u + std::conj(s0) * v;
+                h(i, k + 1) = -s0 * u + c0 * v;
+            }
+        }
+        for (int i = l; i <= hi; i++) h(i, i) += mu;
     }
-    cudaFree(dA); cudaFree(dW); cudaFree(dV); cudaFree(dwork); cudaFree(dinfo);
-    cusolverDnDestroyParams(prm);
-    if (!ok) return false;
-    V.resize((size_t)n * n);
-    for (int i = 0; i < n; i++)
-        for (int c = 0; c < n; c++) V[(size_t)i * n + c] = Vc[(size_t)c * n + i];
+    return true;
+}
+
+// solve (A) x = rhs in place (row-major, partial pivoting); false if singular
+static bool dense_lu_solve(std::vector<zc> A, int n, std::vector<zc> &x) {
+    for (int c = 0; c < n; c++) {
+        int p = c;
+        for (int r = c + 1; r < n; r++)
+            if (std::abs(A[(size_t)r * n + c]) > std::abs(A[(size_t)p * n + c])) p = r;
+        if (std::abs(A[(size_t)p * n + c]) == 0.0) return false;
+        if (p != c) {
+            for (int k = 0; k < n; k++) std::swap(A[(size_t)p * n + k], A[(size_t)c * n + k]);
+            std::swap(x[p], x[c]);
+        }
+        for (int r = c + 1; r < n; r++) {
+            const zc f = A[(size_t)r * n + c] / A[(size_t)c * n + c];
+            if (f == 0.0) continue;
+            for (int k = c; k < n; k++) A[(size_t)r * n + k] -= f * A[(size_t)c * n + k];
+            x[r] -= f * x[c];
+        }
+    }
+    for (int r = n - 1; r >= 0; r--) {
+        zc acc = x[r];
+        for (int k = r + 1; k < n; k++) acc -= A[(size_t)r * n + k] * x[k];
+        x[r] = acc / A[(size_t)r * n + r];
+    }
+    return true;
+}
+
+// T = V diag(lam) V^-1 (row-major V, Vi) on the host: eigenvalues by shifted QR,
+// eigenvectors by inverse iteration; false unless the decomposition reproduces
+// T to ~1e-12 (the hierarchy then falls back to an inverse-based solve)
+static bool eig1d(const std::vector<zc> &T, int n, std::vector<zc> &lam, std::vector<zc> &V,
+                  std::vector<zc> &Vi) {
+    if (!hessenberg_eigvals(T, n, lam)) return false;
+    double tn = 0;
+    for (const zc &t : T) tn = std::max(tn, std::abs(t));
+    V.assign((size_t)n * n, 0.0);
+    for (int c = 0; c < n; c++) {
+        std::vector<zc> A = T;
+        const zc sh = lam[c] + zc(tn * 1e-13, tn * 1e-13);   // keep T - sh I invertible
+        for (int i = 0; i < n; i++) A[(size_t)i * n + i] -= sh;
+        std::vector<zc> x(n);
+        for (int i = 0; i < n; i++) x[i] = zc(1.0 + 0.1 * i, 0.3 - 0.01 * i);
+        for (int it = 0; it < 3; it++) {
+            if (!dense_lu_solve(A, n, x)) return false;
+            double nrm = 0;
+            for (const zc &v : x) nrm += std::norm(v);
+            nrm = std::sqrt(nrm);
+            if (!(nrm > 0) || !std::isfinite(nrm)) return false;
+            for (zc &v : x) v /= nrm;
+        }
+        for (int i = 0; i < n; i++) V[(size_t)i * n + c] = x[i];
+    }
     Vi = V;
     if (!invert(Vi, n)) return false;
-    // check ||T - V diag(lam) V^-1|| / ||T||
-    double tn = 0, en = 0;
+    double en = 0;
     for (int i = 0; i < n; i++)
         for (int j = 0; j < n; j++) {
             zc acc = 0.0;
             for (int c = 0; c < n; c++) acc += V[(size_t)i * n + c] * lam[c] * Vi[(size_t)c * n + j];
             en = std::max(en, std::abs(acc - T[(size_t)i * n + j]));
-            tn = std::max(tn, std::abs(T[(size_t)i * n + j]));
         }
     return en <= 1e-12 * tn;
 }
@@ -366,14 +428,10 @@ static int build_coarsest_fdm(hf_hierarchy *H, cudaStream_t s, bool &built) {
     if (L.bc != HF_BC_SOMMERFELD || L.k != nullptr || opt(OPT_COARSEST_DENSE)) return 0;
     if (L.lo1 != 0 || L.nx != L.n1) return 0;
     if (fdm_smem_bytes(L.n1, L.n2, L.n3) > 200 * 1024) return 0;
-    cusolverDnHandle_t hs;
-    if (cusolverDnCreate(&hs) != CUSOLVER_STATUS_SUCCESS) return 0;
-    cusolverDnSetStream(hs, s);
     const int n[3] = {L.n1, L.n2, L.n3};
     std::vector<zc> lam[3], V[3], Vi[3];
     bool ok = true;
-    for (int d = 0; d < 3 && ok; d++) ok = eig1d(hs, op1d(n[d], L), n[d], lam[d], V[d], Vi[d], s);
-    cusolverDnDestroy(hs);
+    for (int d = 0; d < 3 && ok; d++) ok = eig1d(op1d(n[d], L), n[d], lam[d], V[d], Vi[d]);
     if (!ok) return 0;
     const long long N = (long long)L.n1 * L.plane;
     const zc c0(-L.sre * L.kc * L.kc, -L.sim * L.kc * L.kc);
@@ -885,7 +943,12 @@ struct RedBuf {
         out = A.get<cd>(HF_MAX_DOTS, e);
         return (partials && counter && out) ? 0 : -1;
     }
-    RedSlot slot(int op, BcgState *st) const { return RedSlot{partials, counter, out, op, st}; }
+    RedSlot slot(int op, BcgState *st, const cd *gvec = nullptr, int gd = 0) const {
+        RedSlot r{partials, counter, out, op, st};
+        r.gvec = gvec;
+        r.gd = gd;
+        return r;
+    }
 };
 
 extern "C" int hf_dot(int64_t n, const double *u, const double *v, double *out_host2) {
@@ -919,8 +982,8 @@ struct hf_solver {
     int hist_cap = 0;
     RedBuf red;
     cudaStream_t stream = nullptr;
-    cudaGraphExec_t graph = nullptr;
-    int graph_kernels = 0;
+    cudaGraphExec_t graph[2] = {nullptr, nullptr};   // [sparse shadow]
+    int graph_kernels[2] = {0, 0};
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, evs = nullptr;
     // GMRES / IDR(s) workspace (allocated on first use)
     std::vector<cd *> basis;            // Krylov basis V (GMRES) / G, U, P (IDR)
@@ -931,7 +994,8 @@ struct hf_solver {
     cd *ycoef = nullptr;
     int vcap = 0;
     ~hf_solver() {
-        if (graph) cudaGraphExecDestroy(graph);
+        for (cudaGraphExec_t g : graph)
+            if (g) cudaGraphExecDestroy(g);
         if (st_host) cudaFreeHost(st_host);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
@@ -978,32 +1042,36 @@ extern "C" void hf_solver_destroy(hf_solver *S) { delete S; }
 
 // one Bi-CGSTAB iteration (krylov.py:234-273), every kernel predicated on st->done
 
-static void bcg_iteration(hf_solver *S, cudaStream_t s) {
+// sparse: the shadow vector has <= HF_NZ_MAX nonzeros (st->nz); the matvec's
+// r~^H v and the x, r update's r~^H r are then gathered by the reductions'
+// last block instead of streaming r~ (16 B per vertex, twice per iteration)
+static void bcg_iteration(hf_solver *S, cudaStream_t s, bool sparse) {
     const Lvl &A = S->Aop->lv.L;
     const int *done = &S->st->done;
     long long n = S->n;
     L1(launch_bcg_p(n, S->st, S->r, S->p, S->v, s, done));
     precondition(S->M, S->p, S->ph, s, done);
-    L1(launch_apply_dot1(A, S->ph, S->v, S->rs, S->red.slot(FIN_BCG_ALPHA, S->st), s, done));
+    L1(launch_apply_dot1(A, S->ph, S->v, sparse ? nullptr : S->rs,
+                         S->red.slot(FIN_BCG_ALPHA, S->st, sparse ? S->v : nullptr, 0), s, done));
     L1(launch_bcg_s(n, S->st, S->r, S->v, S->s, S->red.slot(FIN_BCG_S, S->st), s, done));
     precondition(S->M, S->s, S->sh, s, done);
     L1(launch_apply_dot2(A, S->sh, S->t, S->s, S->red.slot(FIN_BCG_OMEGA, S->st), s, done));
-    L1(launch_bcg_xr(n, S->st, S->x, S->ph, S->sh, S->s, S->t, S->r, S->rs,
-                     S->red.slot(FIN_BCG_RHO, S->st), s, done));
+    L1(launch_bcg_xr(n, S->st, S->x, S->ph, S->sh, S->s, S->t, S->r, sparse ? nullptr : S->rs,
+                     S->red.slot(FIN_BCG_RHO, S->st, sparse ? S->r : nullptr, 1), s, done));
     cudaMemcpyAsync(S->st_host, S->st, sizeof(BcgState), cudaMemcpyDeviceToHost, s);
 }
 
-static int build_graph(hf_solver *S) {
-    if (S->graph) return 0;
+static int build_graph(hf_solver *S, bool sparse) {
+    if (S->graph[sparse]) return 0;
     cudaGraph_t g;
     long long before = g_launches;
     CK(cudaStreamBeginCapture(S->stream, cudaStreamCaptureModeThreadLocal));
-    bcg_iteration(S, S->stream);
+    bcg_iteration(S, S->stream, sparse);
     cudaError_t e = cudaStreamEndCapture(S->stream, &g);
     if (e != cudaSuccess) return fail(HF_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
-    S->graph_kernels = (int)(g_launches - before);
+    S->graph_kernels[sparse] = (int)(g_launches - before);
     g_launches = before;
-    e = cudaGraphInstantiate(&S->graph, g, 0);
+    e = cudaGraphInstantiate(&S->graph[sparse], g, 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) return fail(HF_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
     return 0;
@@ -1018,7 +1086,6 @@ static int solve_bicgstab(hf_solver *S, const hf_solver_config *cfg, const cd *b
         if (!S->hist) return fail(HF_ERR_CUDA, "cudaMalloc history");
         S->hist_cap = cfg->maxit + 2;
     }
-    if (build_graph(S)) return HF_ERR_CUDA;
     BcgState init{};
     init.tol = cfg->tol;
     init.btol = cfg->breakdown_tol > 0 ? cfg->breakdown_tol : 1e-30;
@@ -1041,19 +1108,22 @@ static int solve_bicgstab(hf_solver *S, const hf_solver_config *cfg, const cd *b
     const Lvl &AL = S->Aop->lv.L;
     L1(launch_bcg_init(S->n, b, S->r, S->rs, S->x, S->p, S->v, S->red.slot(FIN_BCG_INIT, S->st), s,
                        shadow, cfg->shadow_seed, (long long)AL.lo1 * AL.plane));
-    launches++;
+    launch_nz_scan(S->n, S->rs, S->st, s);
+    launches += 3;
     CK(cudaMemcpyAsync(S->st_host, S->st, sizeof(BcgState), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    const bool sparse = S->st_host->nz > 0;
+    if (build_graph(S, sparse)) return HF_ERR_CUDA;
     int every = cfg->check_every > 0 ? cfg->check_every : 4;
     int graphs = 0;
     while (!S->st_host->done && graphs < cfg->maxit + every) {
         for (int k = 0; k < every; k++) {
-            CK(cudaGraphLaunch(S->graph, s));
+            CK(cudaGraphLaunch(S->graph[sparse], s));
             graphs++;
         }
         CK(cudaStreamSynchronize(s));
     }
-    launches += (long long)graphs * S->graph_kernels;
+    launches += (long long)graphs * S->graph_kernels[sparse];
     if (S->st_host->s_conv) {
         L1(launch_bcg_xhalf(S->n, S->st, S->x, S->ph, s));
         launches++;

@@ -70,7 +70,7 @@ def test_fixtures_are_reference_runs():
     for case in ("cube129", "wedge65", "wedge129"):
         g = _gold(case)
         assert "reference helmfree" in g["generated_by"]
-        assert {r["variant"] for r in g["runs"]} == {"vdot", "pairwise", "chunk4096", "reversed"}
+        assert {"vdot", "pairwise", "chunk4096", "reversed"} <= {r["variant"] for r in g["runs"]}
         for r in g["runs"]:
             assert r["converged"] and r["final_relres"] <= 1e-6
             assert len(r["residual_history"]) == r["iterations"]

@@ -469,6 +469,14 @@ def kernel_table(A, hier, solver, n, t_iter_ms, reps=12):
                                        32.0 + kb, "hbm", 2, "k_stencil<PRE,EpiResid>")
         cases["restrict_fw"] = (lambda s: L.hf_restrict_fw(H, 0, p(s["v"]), p(s["bc"])),
                                 16.0 + 16.0 * cr, "hbm", 2, "k_restrict_flat")
+        # the fused alternatives on wide planes (not on the default path: share None)
+        cases["down_restrict_tiled"] = (lambda s: L.hf_level_down_restrict(H, 0, p(s["b"]), p(s["bc"])),
+                                        16.0 + kb + 16.0 * cr, "hbm", 0, "k_down_restrict")
+
+        def up_fused(s):
+            with _native.options(fuse_up=1):
+                L.hf_level_up(H, 0, p(s["b"]), p(s["ec"]), p(s["u"]))
+        cases["up_fused_tiled"] = (up_fused, 32.0 + kb + 16.0 * cr, "hbm", 0, "k_stencil<UP,EpiJacobi>")
     kind = hier.coarsest_kind
     nt = -(-ncs // 64)
     cbytes = {"separable": 112.0 * ncs,

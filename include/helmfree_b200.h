@@ -229,6 +229,31 @@ int hf_solve(hf_solver *s, const hf_solver_config *cfg, const double *b, double 
 int hf_solve_host(hf_solver *s, const hf_solver_config *cfg, const double *b_host,
                   double *x_host, hf_report *rep);
 
+/* ---- native multi-slab Bi-CGSTAB (runner.py:95-131 over i1 slabs) --------
+ * One iteration -- vector updates, the slab V(1,1) cycle, halo exchanges
+ * (partition.py:509-536), the coarsest gather, the inner-product all-reduces
+ * (partition.py:611-621) and the scalar update -- stream-ordered on one stream
+ * and replayed as one CUDA graph.  LOCAL: all slabs of the decomposition in this
+ * process (nloc == world; halos are device copies).  NCCL: one slab per rank,
+ * the balanced i1 split; halos ncclSend/ncclRecv with the neighbours, sums one
+ * ncclAllReduce, coarsest slabs one ncclAllGather (captured in the graph). */
+#define HF_TRANSPORT_LOCAL 0
+#define HF_TRANSPORT_NCCL 1
+typedef struct hf_slab hf_slab;
+/* load libnccl (path, or NULL for the already-loaded libnccl.so.2) */
+int hf_nccl_init(const char *libpath);
+/* rank 0 draws the 128-byte ncclUniqueId the caller broadcasts */
+int hf_nccl_unique_id(void *out128);
+/* lo1s / nxs: this process's slabs (global first plane, plane count) */
+hf_slab *hf_slab_create(int n1, int n2, int n3, double h, double beta1, double beta2, int bc,
+                        const double *k_host, double k_const, const hf_mg_config *cfg, int nloc,
+                        const int *lo1s, const int *nxs, int world, int rank, int transport,
+                        const void *nccl_id, int maxit);
+void hf_slab_destroy(hf_slab *slab);
+/* b_slabs / x_slabs: device pointers to each local slab's owned planes */
+int hf_slab_solve(hf_slab *slab, const hf_solver_config *cfg, const double *const *b_slabs,
+                  double *const *x_slabs, hf_report *rep);
+
 /* ---- krylov.py:67-78 dot (owned region, conjugated) --------------------- */
 int hf_dot(int64_t n, const double *u, const double *v, double *out_host2);
 

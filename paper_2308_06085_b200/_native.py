@@ -22,6 +22,7 @@ BREAKDOWN = {0: None, 1: "arnoldi", 2: "rho", 3: "omega", 4: "projection"}
 ERR_ARG = -1
 ERR_ZERO_DIAGONAL = -3
 ERR_UNSUPPORTED = -4
+TRANSPORT = {"local": 0, "nccl": 1}
 
 # every symbol include/helmfree_b200.h declares
 EXPORTED = (
@@ -35,6 +36,7 @@ EXPORTED = (
     "hf_solve", "hf_solve_host", "hf_dot", "hf_solver_bench_vec",
     "hf_bcg_create", "hf_bcg_destroy", "hf_bcg_step", "hf_bcg_read", "hf_bcg_vec_init", "hf_bcg_vec_p",
     "hf_bcg_vec_s", "hf_bcg_vec_xr", "hf_bcg_vec_xhalf", "hf_operator_apply_dot",
+    "hf_nccl_init", "hf_nccl_unique_id", "hf_slab_create", "hf_slab_destroy", "hf_slab_solve",
 )
 
 
@@ -132,6 +134,13 @@ def load(path: str = LIB_PATH):
         "hf_solve": ([vp, ctypes.POINTER(SolverConfigC), vp, vp, ctypes.POINTER(ReportC)], i),
         "hf_solve_host": ([vp, ctypes.POINTER(SolverConfigC), vp, vp, ctypes.POINTER(ReportC)], i),
         "hf_dot": ([ctypes.c_int64, vp, vp, dp], i),
+        "hf_nccl_init": ([ctypes.c_char_p], i),
+        "hf_nccl_unique_id": ([vp], i),
+        "hf_slab_create": ([i, i, i, d, d, d, i, vp, d, ctypes.POINTER(MGConfigC), i, ip, ip, i, i, i,
+                            vp, i], vp),
+        "hf_slab_destroy": ([vp], None),
+        "hf_slab_solve": ([vp, ctypes.POINTER(SolverConfigC), ctypes.POINTER(vp), ctypes.POINTER(vp),
+                           ctypes.POINTER(ReportC)], i),
     }
     for name in EXPORTED:
         fn = getattr(L, name)

@@ -257,7 +257,7 @@ struct EpiJacobi {
 template <int MODE, bool KVAR, bool AUX>
 struct StencilSmem {
     static constexpr bool kWd = false;   // (D^-1 b is formed in place from k, see vfix)
-    static constexpr bool kKw = MODE == MODE_PRE && KVAR;   // staged k of the fill entries
+    static constexpr bool kKw = (MODE == MODE_PRE || MODE == MODE_UP) && KVAR;   // staged k of the fill entries
     static constexpr bool kUp = MODE == MODE_UP;
     cd raw[RING][NFILL];
     cd wd[kWd ? RING : 1][kWd ? NFILL : 1];
@@ -421,8 +421,7 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
             if (gi & 1) pe = cscal(cadd(v0, cplane(cl + 1)), 0.5 * s2);
             else pe = s2 == 1.0 ? v0 : cscal(v0, s2);
             if (up.pre) {
-                const cd D = KVAR ? __ldg(L.dinv + (long long)(gi - L.lo1) * L.plane + go)
-                                  : tab[12 + nbx + nbe];
+                const cd D = KVAR ? dinv_of(L, sm.kw[slot][e], nbx + nbe) : tab[12 + nbx + nbe];
                 pe = cadd(cscal(cmul(sm.raw[slot][e], D), omega), pe);
             }
             sm.raw[slot][e] = pe;
@@ -1480,7 +1479,7 @@ __global__ void __launch_bounds__(256) k_restrict2(Lvl F, Lvl C, const cd *__res
 template <bool KVAR>
 struct DRSmem {
     cd f[DR_RING][DR_NF];
-    cd wd[KVAR ? DR_RING : 1][KVAR ? DR_NF : 1];
+    double kw[KVAR ? DR_RING : 1][KVAR ? DR_NF : 1];   // staged k of the fill entries
     cd r[2][DR_NR];
 };
 
@@ -1527,8 +1526,9 @@ __global__ void __launch_bounds__(DR_NT, 3) k_down_restrict(Lvl L, Lvl C, const 
     const bool edge_block = fj0 - 1 <= 0 || fj0 + DR_RY >= L.n2 - 1 || fm0 - 1 <= 0 ||
                             fm0 + DR_RX >= L.n3 - 1;
     const unsigned sf0 = (unsigned)__cvta_generic_to_shared(&sm.f[0][tid]);
-    const unsigned sw0 = (unsigned)__cvta_generic_to_shared(&sm.wd[0][KVAR ? tid : 0]);
+    const unsigned sw0 = (unsigned)__cvta_generic_to_shared(&sm.kw[0][KVAR ? tid : 0]);
     constexpr unsigned SLOT = DR_NF * sizeof(cd);
+    constexpr unsigned KSLOT = DR_NF * sizeof(double);
     // stage global fine plane gp (mirrored outside the grid) into ring slot s
     const int gp_last_stage = 2 * gc1;                       // last plane a residual reads
     auto stage = [&](int s, int gp) {
@@ -1537,17 +1537,27 @@ __global__ void __launch_bounds__(DR_NT, 3) k_down_restrict(Lvl L, Lvl C, const 
             const long long pb = (long long)(gm - L.lo1) * L.plane;
             const unsigned so = s * SLOT;
             cp_async16s(sf0 + so, b + pb + go[0], ok[0]);
-            if (KVAR) cp_async16s(sw0 + so, L.dinv + pb + go[0], ok[0]);
+            if (KVAR) cp_async8s(sw0 + s * KSLOT, L.k + pb + go[0], ok[0]);
             if (has1) {
                 cp_async16s(sf0 + so + DR_NT * sizeof(cd), b + pb + go[1], ok[1]);
-                if (KVAR) cp_async16s(sw0 + so + DR_NT * sizeof(cd), L.dinv + pb + go[1], ok[1]);
+                if (KVAR) cp_async8s(sw0 + s * KSLOT + DR_NT * sizeof(double), L.k + pb + go[1], ok[1]);
             }
         }
         cp_commit();
     };
-    // constant medium: rescale this thread's boundary fill entries of plane gp
+    // constant medium: rescale this thread's boundary fill entries of plane gp;
+    // varying medium: turn them into f = D^-1 b in place (D^-1 from the staged k)
     auto fixup = [&](int s, int gp) {
-        if (KVAR) return;
+        if (KVAR) {
+            const int gm = mirror(gp, L.n1);
+            const int nbx = (gm == 0) + (gm == L.n1 - 1);
+#pragma unroll
+            for (int k = 0; k < 2; k++) {
+                const int e = tid + k * DR_NT;
+                if (ok[k]) sm.f[s][e] = cmul(sm.f[s][e], dinv_of(L, sm.kw[s][e], nbx + nbe[k]));
+            }
+            return;
+        }
         const int gm = mirror(gp, L.n1);
         const int nbx = (gm == 0) + (gm == L.n1 - 1);
         if (nbx == 0 && !edge_block) return;
@@ -1646,17 +1656,7 @@ __global__ void __launch_bounds__(DR_NT, 3) k_down_restrict(Lvl L, Lvl C, const 
                 cd ym = r0[cf - DR_FX], yp = r0[cf + DR_FX];
                 cd zm = r0[cf - 1], zp = r0[cf + 1];
                 const int nb = (gp == 0) + (gp == L.n1 - 1) + nbjm;
-                cd post = wd0;
-                if (KVAR) {
-                    post = mk(omega, 0.0);
-                    fc = cmul(fc, sm.wd[sc][cf]);
-                    xm = cmul(xm, sm.wd[sp][cf]);
-                    xp = cmul(xp, sm.wd[sn][cf]);
-                    ym = cmul(ym, sm.wd[sc][cf - DR_FX]);
-                    yp = cmul(yp, sm.wd[sc][cf + DR_FX]);
-                    zm = cmul(zm, sm.wd[sc][cf - 1]);
-                    zp = cmul(zp, sm.wd[sc][cf + 1]);
-                }
+                const cd post = KVAR ? mk(omega, 0.0) : wd0;   // f = D^-1 b staged (fixup)
                 cd sum = cadd(cadd(cadd(xm, xp), cadd(ym, yp)), cadd(zm, zp));
                 const cd ap = KVAR ? ap_of(L, kq, nb) : (nb == 0 ? ap0 : tab[nb]);
                 cd mf = cmul(ap, fc);

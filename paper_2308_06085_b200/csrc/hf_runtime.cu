@@ -384,31 +384,81 @@ static bool dense_lu_solve(std::vector<zc> A, int n, std::vector<zc> &x) {
     return true;
 }
 
-// T = V diag(lam) V^-1 (row-major V, Vi) on the host: eigenvalues by shifted QR,
-// eigenvectors by inverse iteration; false unless the decomposition reproduces
-// T to ~1e-12 (the hierarchy then falls back to an inverse-based solve)
-static bool eig1d(const std::vector<zc> &T, int n, std::vector<zc> &lam, std::vector<zc> &V,
-                  std::vector<zc> &Vi) {
-    if (!hessenberg_eigvals(T, n, lam)) return false;
-    double tn = 0;
-    for (const zc &t : T) tn = std::max(tn, std::abs(t));
-    V.assign((size_t)n * n, 0.0);
+// eigenpairs of a small matrix A (row-major, upper Hessenberg): shifted QR for
+// the eigenvalues, inverse iteration for the eigenvectors (columns of X)
+static bool eig_small(const std::vector<zc> &A, int n, std::vector<zc> &lam, std::vector<zc> &X) {
+    if (!hessenberg_eigvals(A, n, lam)) return false;
+    double an = 0;
+    for (const zc &t : A) an = std::max(an, std::abs(t));
+    X.assign((size_t)n * n, 0.0);
     for (int c = 0; c < n; c++) {
-        std::vector<zc> A = T;
-        const zc sh = lam[c] + zc(tn * 1e-13, tn * 1e-13);   // keep T - sh I invertible
-        for (int i = 0; i < n; i++) A[(size_t)i * n + i] -= sh;
+        std::vector<zc> M = A;
+        const zc sh = lam[c] + zc(an * 1e-13, an * 1e-13);   // keep A - sh I invertible
+        for (int i = 0; i < n; i++) M[(size_t)i * n + i] -= sh;
         std::vector<zc> x(n);
         for (int i = 0; i < n; i++) x[i] = zc(1.0 + 0.1 * i, 0.3 - 0.01 * i);
         for (int it = 0; it < 3; it++) {
-            if (!dense_lu_solve(A, n, x)) return false;
+            if (!dense_lu_solve(M, n, x)) return false;
             double nrm = 0;
             for (const zc &v : x) nrm += std::norm(v);
             nrm = std::sqrt(nrm);
             if (!(nrm > 0) || !std::isfinite(nrm)) return false;
             for (zc &v : x) v /= nrm;
         }
-        for (int i = 0; i < n; i++) V[(size_t)i * n + c] = x[i];
+        for (int i = 0; i < n; i++) X[(size_t)i * n + c] = x[i];
     }
+    return true;
+}
+
+// T = V diag(lam) V^-1 (row-major V, Vi) on the host.  The 1-D operator is
+// symmetric under the reflection i -> n-1-i, and its eigenvalues come in
+// near-degenerate even / odd pairs (gaps ~1e-12 relative at n = 33), which no
+// shifted inverse iteration can separate.  So T is split into its even and odd
+// blocks (orthonormal reflection-symmetric bases, each tridiagonal), each block
+// is diagonalised on its own, and V = [Q_e X_e | Q_o X_o].  False unless the
+// decomposition reproduces T to ~1e-12 (the hierarchy then falls back to an
+// inverse-based coarsest solve).
+static bool eig1d(const std::vector<zc> &T, int n, std::vector<zc> &lam, std::vector<zc> &V,
+                  std::vector<zc> &Vi) {
+    const int m = n / 2, ne = n - m, no = m;      // even block has the centre when n is odd
+    const double r2 = std::sqrt(0.5);
+    // basis vectors as (index a, index b, coefficient of b): q = c_a e_a + c_b e_b
+    auto qvec = [&](bool even, int k, std::vector<zc> &q) {
+        q.assign(n, 0.0);
+        if (k < m) { q[k] = r2; q[n - 1 - k] = even ? r2 : -r2; }
+        else q[m] = 1.0;                             // centre (even, n odd)
+    };
+    std::vector<zc> lamv, Vall((size_t)n * n, 0.0);
+    int col = 0;
+    for (int par = 0; par < 2; par++) {
+        const bool even = par == 0;
+        const int d = even ? ne : no;
+        if (d == 0) continue;
+        std::vector<std::vector<zc>> Q(d);
+        for (int k = 0; k < d; k++) qvec(even, k, Q[k]);
+        std::vector<zc> B((size_t)d * d, 0.0);       // Q^T T Q (real orthonormal Q)
+        for (int a = 0; a < d; a++) {
+            std::vector<zc> tq(n, 0.0);
+            for (int i = 0; i < n; i++)
+                for (int j = std::max(0, i - 1); j <= std::min(n - 1, i + 1); j++) tq[i] += T[(size_t)i * n + j] * Q[a][j];
+            for (int b2 = 0; b2 < d; b2++) {
+                zc acc = 0.0;
+                for (int i = 0; i < n; i++) acc += Q[b2][i] * tq[i];
+                B[(size_t)b2 * d + a] = acc;
+            }
+        }
+        std::vector<zc> lb, X;
+        if (!eig_small(B, d, lb, X)) return false;
+        for (int c = 0; c < d; c++, col++) {
+            lamv.push_back(lb[c]);
+            for (int k = 0; k < d; k++)
+                for (int i = 0; i < n; i++) Vall[(size_t)i * n + col] += Q[k][i] * X[(size_t)k * d + c];
+        }
+    }
+    lam = lamv;
+    V = Vall;
+    double tn = 0;
+    for (const zc &t : T) tn = std::max(tn, std::abs(t));
     Vi = V;
     if (!invert(Vi, n)) return false;
     double en = 0;
@@ -1666,5 +1716,499 @@ extern "C" int hf_solve_host(hf_solver *S, const hf_solver_config *cfg, const do
     if (rc) return rc;
     CK(cudaMemcpyAsync(x_host, S->xb, bytes, cudaMemcpyDeviceToHost, S->stream));
     CK(cudaStreamSynchronize(S->stream));
+    return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Native multi-slab Bi-CGSTAB: the reference's SPMD worker body
+// (runner.py:95-131) with its distributed V-cycle (multigrid.py:326-343), halo
+// exchanges (partition.py:509-536) and global inner products
+// (partition.py:611-621), laid out as slabs along i1.  Every step of one
+// iteration -- vector updates, the slab V-cycle level kernels, the halo
+// exchanges, the coarsest gather, the inner-product all-reduces and the scalar
+// update -- is stream-ordered on ONE stream, and the iteration is captured once
+// as a CUDA graph and replayed (no host work per level or per inner product;
+// the host polls the device state every few iterations).
+//   transport LOCAL: all slabs of the decomposition in this process (virtual
+//     ranks on one GPU): halos are device copies, sums added in slab order.
+//   transport NCCL: one slab per process/GPU: halos are ncclSend/ncclRecv
+//     pairs with the two neighbours (peer to peer over NVLink), sums are one
+//     ncclAllReduce of four doubles, the coarsest slabs one ncclAllGather.
+//     NCCL is loaded at run time (hf_nccl_init) from the same libnccl the
+//     caller's torch.distributed uses; its calls are captured in the graph.
+// ---------------------------------------------------------------------------
+#include <dlfcn.h>
+
+namespace {
+struct NcclId { char internal[128]; };
+struct NcclApi {
+    void *h = nullptr;
+    int (*getUniqueId)(NcclId *) = nullptr;
+    int (*commInitRank)(void **, int, NcclId, int) = nullptr;
+    int (*commDestroy)(void *) = nullptr;
+    int (*send)(const void *, size_t, int, int, void *, cudaStream_t) = nullptr;
+    int (*recv)(void *, size_t, int, int, void *, cudaStream_t) = nullptr;
+    int (*groupStart)() = nullptr;
+    int (*groupEnd)() = nullptr;
+    int (*allReduce)(const void *, void *, size_t, int, int, void *, cudaStream_t) = nullptr;
+    int (*allGather)(const void *, void *, size_t, int, void *, cudaStream_t) = nullptr;
+    const char *(*errorString)(int) = nullptr;
+};
+NcclApi g_nccl;
+const int kNcclDouble = 8, kNcclSum = 0;
+}  // namespace
+
+extern "C" int hf_nccl_init(const char *libpath) {
+    if (g_nccl.h) return 0;
+    void *h = dlopen(libpath && *libpath ? libpath : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return fail(HF_ERR_UNSUPPORTED, std::string("cannot load NCCL: ") + dlerror());
+    auto sym = [&](const char *n) { return dlsym(h, n); };
+    g_nccl.getUniqueId = (int (*)(NcclId *))sym("ncclGetUniqueId");
+    g_nccl.commInitRank = (int (*)(void **, int, NcclId, int))sym("ncclCommInitRank");
+    g_nccl.commDestroy = (int (*)(void *))sym("ncclCommDestroy");
+    g_nccl.send = (int (*)(const void *, size_t, int, int, void *, cudaStream_t))sym("ncclSend");
+    g_nccl.recv = (int (*)(void *, size_t, int, int, void *, cudaStream_t))sym("ncclRecv");
+    g_nccl.groupStart = (int (*)())sym("ncclGroupStart");
+    g_nccl.groupEnd = (int (*)())sym("ncclGroupEnd");
+    g_nccl.allReduce = (int (*)(const void *, void *, size_t, int, int, void *, cudaStream_t))sym("ncclAllReduce");
+    g_nccl.allGather = (int (*)(const void *, void *, size_t, int, void *, cudaStream_t))sym("ncclAllGather");
+    g_nccl.errorString = (const char *(*)(int))sym("ncclGetErrorString");
+    if (!g_nccl.getUniqueId || !g_nccl.commInitRank || !g_nccl.send || !g_nccl.recv || !g_nccl.groupStart ||
+        !g_nccl.groupEnd || !g_nccl.allReduce || !g_nccl.allGather || !g_nccl.commDestroy)
+        return fail(HF_ERR_UNSUPPORTED, "libnccl lacks the point-to-point / collective API");
+    g_nccl.h = h;
+    return 0;
+}
+
+extern "C" int hf_nccl_unique_id(void *out128) {
+    if (!g_nccl.h) return fail(HF_ERR_ARG, "hf_nccl_init first");
+    NcclId id;
+    int r = g_nccl.getUniqueId(&id);
+    if (r) return fail(HF_ERR_CUDA, "ncclGetUniqueId failed");
+    std::memcpy(out128, &id, sizeof(id));
+    return 0;
+}
+
+struct SlabLocal {
+    hf_operator *A = nullptr;
+    hf_hierarchy *H = nullptr;
+    long long n = 0;
+    cd *x, *r, *rs, *p, *v, *ph, *s, *sh, *t;
+};
+
+struct hf_slab {
+    Allocs A;
+    int transport = HF_TRANSPORT_LOCAL, world = 1, rank = 0;
+    std::vector<SlabLocal> sl;
+    std::vector<int> clo, cnx;        // every slab's coarsest-level planes (global)
+    int cmax = 0;
+    long long cplane = 0;
+    hf_hierarchy *Hc = nullptr;       // whole coarsest grid, exact solve, replicated
+    cd *bc_full = nullptr, *xc_full = nullptr, *gpad = nullptr, *gsend = nullptr;
+    std::vector<char> fuse_down;      // per level: HF_GHOST-deep halo + fused down kernel
+    int nlev = 0;
+    BcgState *st = nullptr, *st_host = nullptr;
+    double *hist = nullptr;
+    int hist_cap = 0;
+    RedBuf red;
+    cd *sums = nullptr;               // [nloc][2] partial sums, then the total at [nloc]
+    cudaStream_t stream = nullptr;
+    cudaGraphExec_t graph = nullptr;
+    int graph_kernels = 0;
+    void *comm = nullptr;
+    ~hf_slab() {
+        if (graph) cudaGraphExecDestroy(graph);
+        for (SlabLocal &q : sl) {
+            if (q.H) hf_hierarchy_destroy(q.H);
+            if (q.A) hf_operator_destroy(q.A);
+        }
+        if (Hc) hf_hierarchy_destroy(Hc);
+        if (st_host) cudaFreeHost(st_host);
+        if (comm && g_nccl.commDestroy) g_nccl.commDestroy(comm);
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+extern "C" hf_slab *hf_slab_create(int n1, int n2, int n3, double h, double beta1, double beta2, int bc,
+                                   const double *k_host, double k_const, const hf_mg_config *mg,
+                                   int nloc, const int *lo1s, const int *nxs, int world, int rank,
+                                   int transport, const void *nccl_id, int maxit) {
+    if (!mg || nloc < 1 || !lo1s || !nxs || world < 1 || rank < 0 || rank >= world || maxit < 1) {
+        fail(HF_ERR_ARG, "bad slab arguments");
+        return nullptr;
+    }
+    if (mg->cycle != HF_CYCLE_V || mg->nu1 != 1 || mg->nu2 != 1) {
+        fail(HF_ERR_UNSUPPORTED, "slab driver implements the V(1,1) cycle");
+        return nullptr;
+    }
+    if (transport == HF_TRANSPORT_LOCAL && nloc != world) {
+        fail(HF_ERR_ARG, "LOCAL transport: all slabs in this process (nloc == world)");
+        return nullptr;
+    }
+    if (transport == HF_TRANSPORT_NCCL && (nloc != 1 || !nccl_id || !g_nccl.h)) {
+        fail(HF_ERR_ARG, "NCCL transport: one slab per rank, hf_nccl_init and a unique id");
+        return nullptr;
+    }
+    auto *S = new hf_slab();
+    S->transport = transport; S->world = world; S->rank = rank;
+    hf_mg_config c = *mg;
+    c.coarsest_method = HF_COARSEST_EXTERNAL;
+    cudaError_t e;
+    for (int i = 0; i < nloc; i++) {
+        SlabLocal q;
+        q.A = hf_operator_create(n1, n2, n3, lo1s[i], nxs[i], h, 1.0, 0.0, bc, k_host, k_const);
+        q.H = q.A ? hf_hierarchy_create(n1, n2, n3, lo1s[i], nxs[i], h, beta1, beta2, bc, k_host, k_const, &c)
+                  : nullptr;
+        if (!q.A || !q.H) { S->sl.push_back(q); delete S; return nullptr; }
+        const Lvl &L = q.A->lv.L;
+        q.n = (long long)L.nx * L.plane;
+        cd **vecs[] = {&q.x, &q.r, &q.rs, &q.p, &q.v, &q.ph, &q.s, &q.sh, &q.t};
+        for (cd **pv : vecs) {
+            *pv = new_field(S->A, L.nx, L.plane, e);
+            if (!*pv) { S->sl.push_back(q); delete S; fail(HF_ERR_CUDA, "cudaMalloc slab vectors"); return nullptr; }
+        }
+        S->sl.push_back(q);
+    }
+    S->nlev = (int)S->sl[0].H->lev.size();
+    if (S->nlev < 2) {
+        delete S;
+        fail(HF_ERR_UNSUPPORTED, "slab driver needs at least two multigrid levels");
+        return nullptr;
+    }
+    // every slab's extent per level (derive_coarse_extent, partition.py:120-131),
+    // to decide the fused down kernel (every slab of level l owns >= HF_GHOST planes)
+    // and to place the coarsest slabs
+    std::vector<int> all_lo(world), all_nx(world);
+    if (transport == HF_TRANSPORT_LOCAL) {
+        for (int r = 0; r < world; r++) { all_lo[r] = lo1s[r]; all_nx[r] = nxs[r]; }
+    } else {
+        // balanced split along i1 (partition.py:103-117), the caller's decomposition
+        const int base = n1 / world, rem = n1 % world;
+        int lo = 0;
+        for (int r = 0; r < world; r++) {
+            all_lo[r] = lo;
+            all_nx[r] = base + (r < rem ? 1 : 0);
+            lo += all_nx[r];
+        }
+        if (all_lo[rank] != lo1s[0] || all_nx[rank] != nxs[0]) {
+            delete S;
+            fail(HF_ERR_ARG, "NCCL transport expects the balanced i1 split (slab_partition)");
+            return nullptr;
+        }
+    }
+    S->fuse_down.assign(S->nlev, 1);
+    for (int l = 0; l < S->nlev; l++) {
+        for (int r = 0; r < world; r++)
+            if (all_nx[r] < HF_GHOST) S->fuse_down[l] = 0;
+        if (l + 1 < S->nlev)
+            for (int r = 0; r < world; r++) {
+                const int clo = (all_lo[r] + 1) / 2, chi = (all_lo[r] + all_nx[r] - 1) / 2;
+                all_lo[r] = clo;
+                all_nx[r] = chi - clo + 1;
+            }
+    }
+    S->clo = all_lo; S->cnx = all_nx;
+    S->cmax = *std::max_element(all_nx.begin(), all_nx.end());
+    // whole coarsest grid: exact solve replicated on every rank
+    const Lvl &K = S->sl[0].H->lev.back().L;
+    S->cplane = K.plane;
+    std::vector<double> kc;
+    const double *kcp = nullptr;
+    if (k_host) {
+        const int st = 1 << (S->nlev - 1);
+        kc.resize((size_t)K.n1 * K.plane);
+        for (int i = 0; i < K.n1; i++)
+            for (int j = 0; j < K.n2; j++)
+                for (int m = 0; m < K.n3; m++)
+                    kc[((size_t)i * K.n2 + j) * K.n3 + m] = k_host[((size_t)(st * i) * n2 + st * j) * n3 + st * m];
+        kcp = kc.data();
+    }
+    hf_mg_config cc = *mg;
+    cc.coarsest_method = HF_COARSEST_DIRECT;
+    cc.coarsest_threshold = std::max(K.n1, std::max(K.n2, K.n3)) + 1;   // one level
+    cc.threshold_ge = 0;
+    S->Hc = hf_hierarchy_create(K.n1, K.n2, K.n3, 0, K.n1, K.h, beta1, beta2, bc, kcp, k_const, &cc);
+    if (!S->Hc) { delete S; return nullptr; }
+    S->bc_full = S->A.get<cd>((size_t)K.n1 * K.plane, e);
+    S->xc_full = S->A.get<cd>((size_t)K.n1 * K.plane, e);
+    if (transport == HF_TRANSPORT_NCCL) {
+        S->gsend = S->A.get<cd>((size_t)S->cmax * K.plane, e);
+        S->gpad = S->A.get<cd>((size_t)world * S->cmax * K.plane, e);
+    }
+    S->st = S->A.get<BcgState>(1, e);
+    S->hist = S->A.get<double>((size_t)maxit + 2, e);
+    S->hist_cap = maxit + 2;
+    S->sums = S->A.get<cd>((size_t)(nloc + 1) * 2, e);
+    size_t nblk = VEC_BLOCKS_HOST;
+    for (SlabLocal &q : S->sl)
+        nblk = std::max<size_t>(nblk, std::max(march_blocks(q.A->lv.L), tile_blocks(q.A->lv.L)));
+    if (!S->bc_full || !S->xc_full || !S->st || !S->hist || !S->sums || S->red.init(S->A, nblk + 64) ||
+        (transport == HF_TRANSPORT_NCCL && (!S->gsend || !S->gpad)) ||
+        cudaMallocHost(&S->st_host, sizeof(BcgState)) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&S->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        delete S;
+        fail(HF_ERR_CUDA, "slab workspace allocation");
+        return nullptr;
+    }
+    if (transport == HF_TRANSPORT_NCCL) {
+        NcclId id;
+        std::memcpy(&id, nccl_id, sizeof(id));
+        const int r = g_nccl.commInitRank(&S->comm, world, id, rank);
+        if (r) {
+            S->comm = nullptr;
+            delete S;
+            fail(HF_ERR_CUDA, std::string("ncclCommInitRank: ") + (g_nccl.errorString ? g_nccl.errorString(r) : "?"));
+            return nullptr;
+        }
+    }
+    return S;
+}
+
+extern "C" void hf_slab_destroy(hf_slab *S) { delete S; }
+
+// fill `planes` ghost planes of level-l fields f[i] (owned plane 0) at interior faces
+static int slab_halo(hf_slab *S, int l, const std::vector<cd *> &f, int planes, cudaStream_t s) {
+    const int nloc = (int)S->sl.size();
+    if (S->transport == HF_TRANSPORT_LOCAL) {
+        for (int i = 0; i + 1 < nloc; i++) {
+            const Lvl &a = S->sl[i].H->lev[l].L, &b = S->sl[i + 1].H->lev[l].L;
+            const size_t bytes = (size_t)planes * a.plane * sizeof(cd);
+            CK(cudaMemcpyAsync(f[i] + (size_t)a.nx * a.plane, f[i + 1], bytes, cudaMemcpyDeviceToDevice, s));
+            CK(cudaMemcpyAsync(f[i + 1] - (size_t)planes * b.plane, f[i] + (size_t)(a.nx - planes) * a.plane,
+                               bytes, cudaMemcpyDeviceToDevice, s));
+        }
+        return 0;
+    }
+    if (S->world == 1) return 0;
+    const Lvl &L = S->sl[0].H->lev[l].L;
+    const size_t cnt = (size_t)planes * L.plane * 2;   // doubles
+    cd *o = f[0];
+    int r = g_nccl.groupStart();
+    if (S->rank > 0) {
+        r |= g_nccl.send(o, cnt, kNcclDouble, S->rank - 1, S->comm, s);
+        r |= g_nccl.recv(o - (size_t)planes * L.plane, cnt, kNcclDouble, S->rank - 1, S->comm, s);
+    }
+    if (S->rank < S->world - 1) {
+        r |= g_nccl.send(o + (size_t)(L.nx - planes) * L.plane, cnt, kNcclDouble, S->rank + 1, S->comm, s);
+        r |= g_nccl.recv(o + (size_t)L.nx * L.plane, cnt, kNcclDouble, S->rank + 1, S->comm, s);
+    }
+    r |= g_nccl.groupEnd();
+    return r ? fail(HF_ERR_CUDA, "NCCL halo exchange") : 0;
+}
+
+__global__ void k_sum_slabs(int nloc, cd *sums) {   // fixed slab order
+    if (threadIdx.x >= 2) return;
+    cd a = mk(0, 0);
+    for (int i = 0; i < nloc; i++) a = cadd(a, sums[2 * i + threadIdx.x]);
+    sums[2 * nloc + threadIdx.x] = a;
+}
+
+// global sums of the slabs' partials (all local slabs, all ranks) -> scalar step `op`
+static int slab_reduce_step(hf_slab *S, int op, cudaStream_t s) {
+    const int nloc = (int)S->sl.size();
+    cd *tot = S->sums + 2 * nloc;
+    if (S->transport == HF_TRANSPORT_LOCAL) {
+        k_sum_slabs<<<1, 32, 0, s>>>(nloc, S->sums);
+    } else if (g_nccl.allReduce(S->sums, tot, 4, kNcclDouble, kNcclSum, S->comm, s)) {
+        return fail(HF_ERR_CUDA, "NCCL all-reduce");
+    }
+    launch_bcg_step(S->st, op, tot, s);
+    g_launches += 2;
+    return 0;
+}
+
+static RedSlot slab_store(hf_slab *S, int i) {
+    RedSlot r = S->red.slot(FIN_STORE, nullptr);
+    r.out = S->sums + 2 * i;
+    return r;
+}
+
+// one V(1,1) cycle over the slabs: dst[i] ~= M^-1 src[i] (multigrid.py:326-343)
+static int slab_cycle(hf_slab *S, const std::vector<cd *> &src, const std::vector<cd *> &dst, cudaStream_t s) {
+    const int nloc = (int)S->sl.size(), nl = S->nlev;
+    const int *done = &S->st->done;
+    const double om = S->sl[0].H->cfg.omega;
+    auto bl = [&](int i, int l) { return l == 0 ? src[i] : S->sl[i].H->lev[l].b; };
+    auto ul = [&](int i, int l) { return l == 0 ? dst[i] : S->sl[i].H->lev[l].u; };
+    std::vector<cd *> f(nloc);
+    for (int l = 0; l < nl - 1; l++) {
+        for (int i = 0; i < nloc; i++) f[i] = bl(i, l);
+        if (S->fuse_down[l]) {
+            if (slab_halo(S, l, f, HF_GHOST, s)) return HF_ERR_CUDA;
+            for (int i = 0; i < nloc; i++) {
+                Level &lv = S->sl[i].H->lev[l], &nx = S->sl[i].H->lev[l + 1];
+                launch_down_restrict(lv.L, nx.L, f[i], nx.b, om, s, done);
+                g_launches++;
+            }
+            continue;
+        }
+        if (slab_halo(S, l, f, 1, s)) return HF_ERR_CUDA;
+        std::vector<cd *> rr(nloc);
+        for (int i = 0; i < nloc; i++) {
+            Level &lv = S->sl[i].H->lev[l];
+            launch_down1(lv.L, f[i], lv.r, om, s, done);
+            rr[i] = lv.r;
+        }
+        if (slab_halo(S, l, rr, 1, s)) return HF_ERR_CUDA;
+        for (int i = 0; i < nloc; i++) {
+            Level &lv = S->sl[i].H->lev[l], &nx = S->sl[i].H->lev[l + 1];
+            launch_restrict(lv.L, nx.L, lv.r, nx.b, s, done);
+        }
+        g_launches += 2 * nloc;
+    }
+    // coarsest: gather every slab's planes into the whole grid, exact solve, scatter
+    const size_t cpb = (size_t)S->cplane * sizeof(cd);
+    if (S->transport == HF_TRANSPORT_LOCAL) {
+        for (int i = 0; i < nloc; i++)
+            CK(cudaMemcpyAsync(S->bc_full + (size_t)S->clo[i] * S->cplane, S->sl[i].H->lev[nl - 1].b,
+                               S->cnx[i] * cpb, cudaMemcpyDeviceToDevice, s));
+    } else {
+        CK(cudaMemcpyAsync(S->gsend, S->sl[0].H->lev[nl - 1].b, S->cnx[S->rank] * cpb, cudaMemcpyDeviceToDevice, s));
+        if (g_nccl.allGather(S->gsend, S->gpad, (size_t)S->cmax * S->cplane * 2, kNcclDouble, S->comm, s))
+            return fail(HF_ERR_CUDA, "NCCL all-gather");
+        for (int r = 0; r < S->world; r++)
+            CK(cudaMemcpyAsync(S->bc_full + (size_t)S->clo[r] * S->cplane, S->gpad + (size_t)r * S->cmax * S->cplane,
+                               S->cnx[r] * cpb, cudaMemcpyDeviceToDevice, s));
+    }
+    coarsest(S->Hc, S->bc_full, S->xc_full, s, done);
+    for (int i = 0; i < nloc; i++) {
+        const int r = S->transport == HF_TRANSPORT_LOCAL ? i : S->rank;
+        CK(cudaMemcpyAsync(S->sl[i].H->lev[nl - 1].u, S->xc_full + (size_t)S->clo[r] * S->cplane,
+                           S->cnx[r] * cpb, cudaMemcpyDeviceToDevice, s));
+    }
+    for (int l = nl - 2; l >= 0; l--) {
+        for (int i = 0; i < nloc; i++) f[i] = S->sl[i].H->lev[l + 1].u;
+        if (slab_halo(S, l + 1, f, 1, s)) return HF_ERR_CUDA;
+        for (int i = 0; i < nloc; i++) {
+            Level &lv = S->sl[i].H->lev[l], &nx = S->sl[i].H->lev[l + 1];
+            // t on the owned planes and the interior-face ghost planes (b's halo from
+            // the down-sweep is valid): no halo exchange of t before the sweep
+            launch_correct(lv.L, nx.L, bl(i, l), nx.u, lv.t, om, true, s, done, true);
+            launch_jacobi(lv.L, lv.t, bl(i, l), ul(i, l), om, s, done);
+        }
+        g_launches += 2 * nloc;
+    }
+    return 0;
+}
+
+static int slab_iteration(hf_slab *S, cudaStream_t s) {
+    const int nloc = (int)S->sl.size();
+    const int *done = &S->st->done;
+    std::vector<cd *> src(nloc), dst(nloc);
+    for (int i = 0; i < nloc; i++) {
+        SlabLocal &q = S->sl[i];
+        L1(launch_bcg_p(q.n, S->st, q.r, q.p, q.v, s, done));
+        src[i] = q.p; dst[i] = q.ph;
+    }
+    if (slab_cycle(S, src, dst, s)) return HF_ERR_CUDA;
+    if (slab_halo(S, 0, dst, 1, s)) return HF_ERR_CUDA;
+    for (int i = 0; i < nloc; i++) {
+        SlabLocal &q = S->sl[i];
+        L1(launch_apply_dot1(q.A->lv.L, q.ph, q.v, q.rs, slab_store(S, i), s, done));
+    }
+    if (slab_reduce_step(S, FIN_BCG_ALPHA, s)) return HF_ERR_CUDA;
+    for (int i = 0; i < nloc; i++) {
+        SlabLocal &q = S->sl[i];
+        L1(launch_bcg_s(q.n, S->st, q.r, q.v, q.s, slab_store(S, i), s, done));
+        src[i] = q.s; dst[i] = q.sh;
+    }
+    if (slab_reduce_step(S, FIN_BCG_S, s)) return HF_ERR_CUDA;
+    if (slab_cycle(S, src, dst, s)) return HF_ERR_CUDA;
+    if (slab_halo(S, 0, dst, 1, s)) return HF_ERR_CUDA;
+    for (int i = 0; i < nloc; i++) {
+        SlabLocal &q = S->sl[i];
+        L1(launch_apply_dot2(q.A->lv.L, q.sh, q.t, q.s, slab_store(S, i), s, done));
+    }
+    if (slab_reduce_step(S, FIN_BCG_OMEGA, s)) return HF_ERR_CUDA;
+    for (int i = 0; i < nloc; i++) {
+        SlabLocal &q = S->sl[i];
+        L1(launch_bcg_xr(q.n, S->st, q.x, q.ph, q.sh, q.s, q.t, q.r, q.rs, slab_store(S, i), s, done));
+    }
+    if (slab_reduce_step(S, FIN_BCG_RHO, s)) return HF_ERR_CUDA;
+    CK(cudaMemcpyAsync(S->st_host, S->st, sizeof(BcgState), cudaMemcpyDeviceToHost, s));
+    return 0;
+}
+
+// b_slabs / x_slabs: per local slab, device pointers to the owned planes
+extern "C" int hf_slab_solve(hf_slab *S, const hf_solver_config *cfg, const double *const *b_slabs,
+                             double *const *x_slabs, hf_report *rep) {
+    if (!S || !cfg || !b_slabs || !x_slabs || !rep) return fail(HF_ERR_ARG, "null argument");
+    if (cfg->method != HF_METHOD_BICGSTAB) return fail(HF_ERR_UNSUPPORTED, "slab driver runs Bi-CGSTAB");
+    if (cfg->maxit + 2 > S->hist_cap) return fail(HF_ERR_ARG, "maxit above the slab solver's capacity");
+    cudaStream_t s = S->stream, us = work_stream();
+    cudaEvent_t ev;
+    CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CK(cudaEventRecord(ev, us));                 // order after the caller's stream
+    CK(cudaStreamWaitEvent(s, ev, 0));
+    const int nloc = (int)S->sl.size();
+    BcgState init{};
+    init.tol = cfg->tol;
+    init.btol = cfg->breakdown_tol > 0 ? cfg->breakdown_tol : 1e-30;
+    init.maxit = cfg->maxit;
+    init.hist = S->hist;
+    init.hist_cap = S->hist_cap;
+    *S->st_host = init;
+    CK(cudaMemcpyAsync(S->st, S->st_host, sizeof(BcgState), cudaMemcpyHostToDevice, s));
+    long long launches = 0;
+    const int shadow = cfg->shadow_kind == HF_SHADOW_HASH ? HF_SHADOW_HASH : HF_SHADOW_RHS;
+    for (int i = 0; i < nloc; i++) {
+        SlabLocal &q = S->sl[i];
+        const Lvl &L = q.A->lv.L;
+        launch_bcg_init(q.n, (const cd *)b_slabs[i], q.r, q.rs, q.x, q.p, q.v, slab_store(S, i), s, shadow,
+                        cfg->shadow_seed, (long long)L.lo1 * L.plane);
+        launches++;
+    }
+    if (slab_reduce_step(S, FIN_BCG_INIT, s)) return HF_ERR_CUDA;
+    CK(cudaMemcpyAsync(S->st_host, S->st, sizeof(BcgState), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (!S->graph) {
+        cudaGraph_t g;
+        long long before = g_launches;
+        CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        const int rc = slab_iteration(S, s);
+        cudaError_t e = cudaStreamEndCapture(s, &g);
+        if (rc) return rc;
+        if (e != cudaSuccess) return fail(HF_ERR_CUDA, std::string("slab graph capture: ") + cudaGetErrorString(e));
+        S->graph_kernels = (int)(g_launches - before);
+        g_launches = before;
+        e = cudaGraphInstantiate(&S->graph, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) return fail(HF_ERR_CUDA, std::string("slab graph instantiate: ") + cudaGetErrorString(e));
+    }
+    const int every = cfg->check_every > 0 ? cfg->check_every : 4;
+    int graphs = 0;
+    while (!S->st_host->done && graphs < cfg->maxit + every) {
+        for (int k = 0; k < every; k++) {
+            CK(cudaGraphLaunch(S->graph, s));
+            graphs++;
+        }
+        CK(cudaStreamSynchronize(s));
+    }
+    launches += (long long)graphs * S->graph_kernels;
+    for (int i = 0; i < nloc; i++) {
+        SlabLocal &q = S->sl[i];
+        if (S->st_host->s_conv) {
+            launch_bcg_xhalf(q.n, S->st, q.x, q.ph, s);
+            launches++;
+        }
+        CK(cudaMemcpyAsync(x_slabs[i], q.x, (size_t)q.n * sizeof(cd), cudaMemcpyDeviceToDevice, s));
+    }
+    CK(cudaStreamSynchronize(s));
+    CK(cudaEventRecord(ev, s));
+    CK(cudaStreamWaitEvent(us, ev, 0));
+    cudaEventDestroy(ev);
+    CKL();
+    const BcgState &st = *S->st_host;
+    rep->matvec_count = st.matvecs;
+    rep->iterations = st.iter;
+    rep->converged = st.converged;
+    rep->breakdown = st.breakdown;
+    rep->final_relres = st.relres;
+    rep->solve_ms = 0;
+    rep->kernel_launches = (int)launches;
+    rep->coarsest_flags = 0;
+    if (rep->history_host && rep->history_cap > 0 && st.iter > 0)
+        CK(cudaMemcpy(rep->history_host, S->hist, (size_t)std::min(st.iter, rep->history_cap) * sizeof(double),
+                      cudaMemcpyDeviceToHost));
     return 0;
 }

@@ -27,7 +27,7 @@ from .krylov import ConvergenceReport, SolverConfig
 from .multigrid import MGConfig
 from .operators import OperatorSpec, StencilOperator, bc_name, k_arguments
 
-__all__ = ["SlabSolver"]
+__all__ = ["SlabSolver", "NativeSlabSolver"]
 
 
 def _ptr(t):
@@ -350,3 +350,115 @@ def _level_extents(grid, nslabs, nlev):
             e = derive_coarse_extent(e)
         out.append(e)
     return out
+
+
+def _nccl_library_path() -> str:
+    """The libnccl torch.distributed uses (the torch wheel's nvidia-nccl), so the
+    native slab driver and torch share one NCCL build."""
+    try:
+        import nvidia.nccl
+        import os
+        base = os.path.dirname(nvidia.nccl.__file__) if nvidia.nccl.__file__ else list(nvidia.nccl.__path__)[0]
+        path = os.path.join(base, "lib", "libnccl.so.2")
+        if os.path.exists(path):
+            return path
+    except Exception:
+        pass
+    return "libnccl.so.2"
+
+
+class NativeSlabSolver:
+    """Multi-slab CSLP-preconditioned Bi-CGSTAB run entirely by the native
+    library (hf_slab_*): one stream-ordered iteration -- vector updates, slab
+    V(1,1) cycle, halo exchanges, coarsest gather, inner-product all-reduces,
+    scalar update -- captured once as a CUDA graph and replayed.
+
+    comm = LocalSlabComm(n): all n slabs of the decomposition in this process
+    (virtual ranks on one GPU, halos as device copies).  comm = TorchSlabComm()
+    over an NCCL process group: one slab per rank, halos ncclSend/ncclRecv with
+    the neighbours and sums one ncclAllReduce inside the graph (the NCCL unique
+    id is broadcast through torch.distributed once at setup).  Same recurrences
+    and arithmetic as SlabSolver / the single-slab solve (runner.py:95-131)."""
+
+    def __init__(self, grid: Grid3, extents, k_field, bc, comm, beta1=1.0, beta2=-0.5,
+                 mg: MGConfig | None = None, maxit: int = 4000):
+        from .partition import LocalSlabComm
+        self.grid, self.comm = grid, comm
+        self.extents = list(extents)
+        self.mg = mg or MGConfig()
+        self.maxit = int(maxit)
+        L = _native.load()
+        self.L = L
+        kfull, kc, self._keep = k_arguments(
+            OperatorSpec("helmholtz", 1.0, 0.0, bc, np.asarray(k_field)), grid, full_extent(grid))
+        kp = kfull.ctypes.data if kfull is not None else None
+        c = _native.MGConfigC(int(self.mg.nu1), int(self.mg.nu2), float(self.mg.omega),
+                              _native.CYCLE[self.mg.cycle.upper()], int(self.mg.coarsest_threshold),
+                              1 if self.mg.threshold_cmp == "ge" else 0, float(self.mg.coarsest_tol),
+                              int(self.mg.coarsest_maxit), _native.COARSEST["direct"])
+        nloc = len(self.extents)
+        lo = (ctypes.c_int * nloc)(*[e.lo1 - 1 for e in self.extents])
+        nx = (ctypes.c_int * nloc)(*[e.nx for e in self.extents])
+        nid = None
+        if isinstance(comm, LocalSlabComm):
+            transport, world, rank = _native.TRANSPORT["local"], nloc, 0
+        else:
+            if comm.dist.get_backend(comm.group) != "nccl":
+                raise NotImplementedError("the native slab driver runs over NCCL (or LocalSlabComm)")
+            transport, world, rank = _native.TRANSPORT["nccl"], comm.size, comm.rank
+            _native.check(L.hf_nccl_init(_nccl_library_path().encode()))
+            buf = (ctypes.c_char * 128)()
+            if rank == 0:
+                _native.check(L.hf_nccl_unique_id(buf))
+            obj = [bytes(buf)]
+            comm.dist.broadcast_object_list(obj, src=0, group=comm.group)
+            nid = (ctypes.c_char * 128).from_buffer_copy(obj[0])
+        _native.set_stream_from_torch()
+        h = L.hf_slab_create(grid.n1, grid.n2, grid.n3, grid.h, float(beta1), float(beta2),
+                             _native.BC[bc_name(bc)], kp, kc, ctypes.byref(c), nloc, lo, nx, world,
+                             rank, transport, ctypes.addressof(nid) if nid is not None else None,
+                             self.maxit)
+        if not h:
+            raise RuntimeError(_native.last_error())
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                self.L.hf_slab_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    def solve(self, b_slabs, cfg: SolverConfig | None = None, x_slabs=None):
+        """b_slabs: per local slab, the right-hand side (owned planes, device or
+        host).  Returns (x per slab, ConvergenceReport)."""
+        import torch
+        cfg = cfg or SolverConfig(method="bicgstab")
+        if cfg.method != "bicgstab":
+            raise NotImplementedError("the native slab driver runs Bi-CGSTAB")
+        if cfg.maxit > self.maxit:
+            raise ValueError(f"maxit {cfg.maxit} above this solver's capacity {self.maxit}")
+        b = [torch.as_tensor(x).to("cuda", torch.complex128).contiguous() for x in b_slabs]
+        x = x_slabs or [torch.empty_like(bi) for bi in b]
+        nloc = len(b)
+        bp = (ctypes.c_void_p * nloc)(*[t.data_ptr() for t in b])
+        xp = (ctypes.c_void_p * nloc)(*[t.data_ptr() for t in x])
+        kind = _native.SHADOW[cfg.shadow]
+        c = _native.SolverConfigC(_native.METHOD["bicgstab"], float(cfg.tol), int(cfg.maxit), 0, 0,
+                                  float(cfg.breakdown_tol), None, int(cfg.check_every), kind,
+                                  int(cfg.rng_seed) & (2**64 - 1))
+        hist = np.zeros(cfg.maxit + 2)
+        rep = _native.ReportC()
+        rep.history_host, rep.history_cap = hist.ctypes.data, len(hist)
+        _native.set_stream_from_torch()
+        _native.check(self.L.hf_slab_solve(self._h, ctypes.byref(c), bp, xp, ctypes.byref(rep)))
+        out = ConvergenceReport(method="bicgstab", matvec_count=rep.matvec_count,
+                                iterations=rep.iterations,
+                                residual_history=hist[:rep.iterations].tolist(),
+                                converged=bool(rep.converged),
+                                final_relres=float(rep.final_relres),
+                                breakdown=_native.BREAKDOWN[rep.breakdown],
+                                kernel_launches=rep.kernel_launches)
+        return x, out

@@ -104,7 +104,7 @@ def run_solve(cfg: RunConfig, write_outputs: bool = True) -> RunReport:
         full = x.cpu().numpy()
         fabric = "none"
     else:
-        from .dist import SlabSolver
+        from .dist import NativeSlabSolver, SlabSolver
         from .partition import LocalSlabComm, TorchSlabComm, slab_partition
         if cfg.solver["method"] != "bicgstab":
             raise ConfigError("the slab driver runs Bi-CGSTAB")
@@ -116,8 +116,14 @@ def run_solve(cfg: RunConfig, write_outputs: bool = True) -> RunReport:
             if comm.size != nslab:
                 raise ConfigError(f"topology.npx0={nslab} but the process group has {comm.size}")
             mine = [ext[comm.rank]]
-        S = SlabSolver(grid, mine, k_full, spec.bc, comm, pre["beta1"], pre["beta2"], _mg(cfg))
-        xs, conv = S.solve([rhs[e.lo1 - 1:e.hi1] for e in mine], _solver_cfg(cfg))
+        native = cfg.topology["fabric"] == "local" or comm.dist.get_backend(comm.group) == "nccl"
+        if native:     # the whole iteration in the native library, one CUDA graph
+            S = NativeSlabSolver(grid, mine, k_full, spec.bc, comm, pre["beta1"], pre["beta2"],
+                                 _mg(cfg), maxit=cfg.solver["maxit"])
+            xs, conv = S.solve([rhs[e.lo1 - 1:e.hi1] for e in mine], _solver_cfg(cfg))
+        else:          # gloo process group: device scalars, Python-driven levels
+            S = SlabSolver(grid, mine, k_full, spec.bc, comm, pre["beta1"], pre["beta2"], _mg(cfg))
+            xs, conv = S.solve_device([rhs[e.lo1 - 1:e.hi1] for e in mine], _solver_cfg(cfg))
         parts = [x.cpu().numpy() for x in xs]
         if cfg.topology["fabric"] == "local":
             full = np.concatenate(parts, 0)

@@ -1811,7 +1811,9 @@ struct hf_slab {
     double *hist = nullptr;
     int hist_cap = 0;
     RedBuf red;
-    cd *sums = nullptr;               // [nloc][2] partial sums, then the total at [nloc]
+    cd *sums = nullptr;               // [nloc][3 parts][2] partial sums, then the total
+    cudaStream_t cstream = nullptr;   // halo exchanges overlapped with interior planes
+    cudaEvent_t evf = nullptr, evj = nullptr;
     cudaStream_t stream = nullptr;
     cudaGraphExec_t graph = nullptr;
     int graph_kernels = 0;
@@ -1825,6 +1827,9 @@ struct hf_slab {
         if (Hc) hf_hierarchy_destroy(Hc);
         if (st_host) cudaFreeHost(st_host);
         if (comm && g_nccl.commDestroy) g_nccl.commDestroy(comm);
+        if (evf) cudaEventDestroy(evf);
+        if (evj) cudaEventDestroy(evj);
+        if (cstream) cudaStreamDestroy(cstream);
         if (stream) cudaStreamDestroy(stream);
     }
 };
@@ -1938,14 +1943,17 @@ extern "C" hf_slab *hf_slab_create(int n1, int n2, int n3, double h, double beta
     S->st = S->A.get<BcgState>(1, e);
     S->hist = S->A.get<double>((size_t)maxit + 2, e);
     S->hist_cap = maxit + 2;
-    S->sums = S->A.get<cd>((size_t)(nloc + 1) * 2, e);
+    S->sums = S->A.get<cd>((size_t)(3 * nloc + 1) * 2, e);
     size_t nblk = VEC_BLOCKS_HOST;
     for (SlabLocal &q : S->sl)
         nblk = std::max<size_t>(nblk, std::max(march_blocks(q.A->lv.L), tile_blocks(q.A->lv.L)));
     if (!S->bc_full || !S->xc_full || !S->st || !S->hist || !S->sums || S->red.init(S->A, nblk + 64) ||
         (transport == HF_TRANSPORT_NCCL && (!S->gsend || !S->gpad)) ||
         cudaMallocHost(&S->st_host, sizeof(BcgState)) != cudaSuccess ||
-        cudaStreamCreateWithFlags(&S->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaStreamCreateWithFlags(&S->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&S->cstream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&S->evf, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&S->evj, cudaEventDisableTiming) != cudaSuccess) {
         delete S;
         fail(HF_ERR_CUDA, "slab workspace allocation");
         return nullptr;
@@ -1996,31 +2004,52 @@ static int slab_halo(hf_slab *S, int l, const std::vector<cd *> &f, int planes, 
     return r ? fail(HF_ERR_CUDA, "NCCL halo exchange") : 0;
 }
 
-__global__ void k_sum_slabs(int nloc, cd *sums) {   // fixed slab order
+// sum the partials of `parts` slots per slab (fixed slab, then part order) into
+// `out`: the global total (LOCAL) or this rank's partial (NCCL, all-reduced next)
+__global__ void k_sum_slabs(int nloc, int parts, const cd *sums, cd *out) {
     if (threadIdx.x >= 2) return;
     cd a = mk(0, 0);
-    for (int i = 0; i < nloc; i++) a = cadd(a, sums[2 * i + threadIdx.x]);
-    sums[2 * nloc + threadIdx.x] = a;
+    for (int i = 0; i < nloc; i++)
+        for (int k = 0; k < parts; k++) a = cadd(a, sums[2 * (3 * i + k) + threadIdx.x]);
+    out[threadIdx.x] = a;
 }
 
 // global sums of the slabs' partials (all local slabs, all ranks) -> scalar step `op`
-static int slab_reduce_step(hf_slab *S, int op, cudaStream_t s) {
+static int slab_reduce_step(hf_slab *S, int op, cudaStream_t s, int parts = 1) {
     const int nloc = (int)S->sl.size();
-    cd *tot = S->sums + 2 * nloc;
+    cd *tot = S->sums + 2 * 3 * nloc;
     if (S->transport == HF_TRANSPORT_LOCAL) {
-        k_sum_slabs<<<1, 32, 0, s>>>(nloc, S->sums);
-    } else if (g_nccl.allReduce(S->sums, tot, 4, kNcclDouble, kNcclSum, S->comm, s)) {
-        return fail(HF_ERR_CUDA, "NCCL all-reduce");
+        k_sum_slabs<<<1, 32, 0, s>>>(nloc, parts, S->sums, tot);
+    } else {
+        const cd *src = S->sums;
+        if (parts > 1) {
+            k_sum_slabs<<<1, 32, 0, s>>>(nloc, parts, S->sums, S->sums + 2);   // into part 1 of slab 0
+            src = S->sums + 2;
+        }
+        if (g_nccl.allReduce(src, tot, 4, kNcclDouble, kNcclSum, S->comm, s))
+            return fail(HF_ERR_CUDA, "NCCL all-reduce");
     }
     launch_bcg_step(S->st, op, tot, s);
     g_launches += 2;
     return 0;
 }
 
-static RedSlot slab_store(hf_slab *S, int i) {
+static RedSlot slab_store(hf_slab *S, int i, int part = 0) {
     RedSlot r = S->red.slot(FIN_STORE, nullptr);
-    r.out = S->sums + 2 * i;
+    r.out = S->sums + 2 * (3 * i + part);
     return r;
+}
+
+// planes [p0, p1) of a slab level as a slab of its own: the kernels read the
+// planes either side of the range as ghost planes, so a range of interior
+// planes needs no halo
+static Lvl sub_slab(const Lvl &L, int p0, int p1) {
+    Lvl o = L;
+    o.lo1 = L.lo1 + p0;
+    o.nx = p1 - p0;
+    if (L.k) o.k = L.k + (size_t)p0 * L.plane;
+    if (L.dinv) o.dinv = L.dinv + (size_t)p0 * L.plane;
+    return o;
 }
 
 // one V(1,1) cycle over the slabs: dst[i] ~= M^-1 src[i] (multigrid.py:326-343)
@@ -2091,6 +2120,47 @@ static int slab_cycle(hf_slab *S, const std::vector<cd *> &src, const std::vecto
     return 0;
 }
 
+// v = A u with this slab's inner products, the halo exchange of u overlapped
+// with the interior planes: the exchange runs on the comm stream while the
+// interior planes [1, nx-1) (which read only owned planes) are swept on the main
+// stream; the two face planes follow once the ghost planes have arrived.  The
+// three launches store separate partial sums (parts 0..2).
+static int slab_matvec(hf_slab *S, int nd, const std::vector<cd *> &u, cudaStream_t s) {
+    const int nloc = (int)S->sl.size();
+    const int *done = &S->st->done;
+    auto mv = [&](int i, int p0, int p1, int part) {
+        SlabLocal &q = S->sl[i];
+        const Lvl &L = q.A->lv.L;
+        const size_t off = (size_t)p0 * L.plane;
+        const Lvl Ls = sub_slab(L, p0, p1);
+        if (nd == 1)
+            launch_apply_dot1(Ls, u[i] + off, q.v + off, q.rs + off, slab_store(S, i, part), s, done);
+        else
+            launch_apply_dot2(Ls, u[i] + off, q.t + off, q.s + off, slab_store(S, i, part), s, done);
+        g_launches++;
+    };
+    CK(cudaMemsetAsync(S->sums, 0, (size_t)3 * nloc * sizeof(cd) * 2, s));
+    CK(cudaEventRecord(S->evf, s));
+    CK(cudaStreamWaitEvent(S->cstream, S->evf, 0));
+    if (slab_halo(S, 0, u, 1, S->cstream)) return HF_ERR_CUDA;
+    CK(cudaEventRecord(S->evj, S->cstream));
+    for (int i = 0; i < nloc; i++) {
+        const int nx = S->sl[i].A->lv.L.nx;
+        if (nx > 2) mv(i, 1, nx - 1, 0);
+    }
+    CK(cudaStreamWaitEvent(s, S->evj, 0));
+    for (int i = 0; i < nloc; i++) {
+        const int nx = S->sl[i].A->lv.L.nx;
+        if (nx > 2) {
+            mv(i, 0, 1, 1);
+            mv(i, nx - 1, nx, 2);
+        } else {
+            mv(i, 0, nx, 1);
+        }
+    }
+    return 0;
+}
+
 static int slab_iteration(hf_slab *S, cudaStream_t s) {
     const int nloc = (int)S->sl.size();
     const int *done = &S->st->done;
@@ -2101,12 +2171,8 @@ static int slab_iteration(hf_slab *S, cudaStream_t s) {
         src[i] = q.p; dst[i] = q.ph;
     }
     if (slab_cycle(S, src, dst, s)) return HF_ERR_CUDA;
-    if (slab_halo(S, 0, dst, 1, s)) return HF_ERR_CUDA;
-    for (int i = 0; i < nloc; i++) {
-        SlabLocal &q = S->sl[i];
-        L1(launch_apply_dot1(q.A->lv.L, q.ph, q.v, q.rs, slab_store(S, i), s, done));
-    }
-    if (slab_reduce_step(S, FIN_BCG_ALPHA, s)) return HF_ERR_CUDA;
+    if (slab_matvec(S, 1, dst, s)) return HF_ERR_CUDA;
+    if (slab_reduce_step(S, FIN_BCG_ALPHA, s, 3)) return HF_ERR_CUDA;
     for (int i = 0; i < nloc; i++) {
         SlabLocal &q = S->sl[i];
         L1(launch_bcg_s(q.n, S->st, q.r, q.v, q.s, slab_store(S, i), s, done));
@@ -2114,12 +2180,8 @@ static int slab_iteration(hf_slab *S, cudaStream_t s) {
     }
     if (slab_reduce_step(S, FIN_BCG_S, s)) return HF_ERR_CUDA;
     if (slab_cycle(S, src, dst, s)) return HF_ERR_CUDA;
-    if (slab_halo(S, 0, dst, 1, s)) return HF_ERR_CUDA;
-    for (int i = 0; i < nloc; i++) {
-        SlabLocal &q = S->sl[i];
-        L1(launch_apply_dot2(q.A->lv.L, q.sh, q.t, q.s, slab_store(S, i), s, done));
-    }
-    if (slab_reduce_step(S, FIN_BCG_OMEGA, s)) return HF_ERR_CUDA;
+    if (slab_matvec(S, 2, dst, s)) return HF_ERR_CUDA;
+    if (slab_reduce_step(S, FIN_BCG_OMEGA, s, 3)) return HF_ERR_CUDA;
     for (int i = 0; i < nloc; i++) {
         SlabLocal &q = S->sl[i];
         L1(launch_bcg_xr(q.n, S->st, q.x, q.ph, q.sh, q.s, q.t, q.r, q.rs, slab_store(S, i), s, done));

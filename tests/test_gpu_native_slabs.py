@@ -66,7 +66,8 @@ def test_native_slabs_match_single(kind, nslabs):
 
 def test_native_slabs_match_python_slab_driver():
     """Same decomposition through the Python-driven device path
-    (SlabSolver.solve_device): same kernels and reduction order."""
+    (SlabSolver.solve_device): same kernels; the native matvec sums its
+    interior and face planes separately (overlapped halo), so rounding only."""
     from paper_2308_06085_b200.dist import NativeSlabSolver, SlabSolver
     from paper_2308_06085_b200.krylov import SolverConfig
     from paper_2308_06085_b200.partition import LocalSlabComm, slab_partition
@@ -75,10 +76,10 @@ def test_native_slabs_match_python_slab_driver():
     parts = [b[e.lo1 - 1:e.hi1] for e in ext]
     xn, rn = NativeSlabSolver(p.grid, ext, k, p.bc, LocalSlabComm(3)).solve(parts)
     xp, rp = SlabSolver(p.grid, ext, k, p.bc, LocalSlabComm(3)).solve_device(parts)
-    assert rn.iterations == rp.iterations
+    assert abs(rn.iterations - rp.iterations) <= 1
     x1 = np.concatenate([t.cpu().numpy() for t in xn], 0)
     x2 = np.concatenate([t.cpu().numpy() for t in xp], 0)
-    assert _rel(x1, x2) < 1e-12
+    assert _rel(x1, x2) < 1e-9
 
 
 def test_native_slabs_random_shadow_layout_independent():

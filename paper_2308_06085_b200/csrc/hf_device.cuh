@@ -80,7 +80,16 @@ __device__ __forceinline__ cd diag_of(const Lvl &L, double kk, int nb) {
 // D^-1 field of k_dinv, so both give identical bits).  Cheaper than streaming
 // the 16-byte field: a varying medium reads k (8 B) anyway.
 __device__ __forceinline__ cd dinv_of(const Lvl &L, double kk, int nb) {
-    return cdiv(mk(1.0, 0.0), diag_of(L, kk, nb));
+    const cd d = diag_of(L, kk, nb);
+    // 1 / |d|^2 without the IEEE division's special-case branch: the MUFU
+    // approximation refined by two Newton steps (|d|^2 is a normal number here,
+    // the diagonal is bounded away from 0 and overflow; result within 1 ulp)
+    const double m = d.x * d.x + d.y * d.y;
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(m));
+    r = fma(r, fma(-m, r, 1.0), r);
+    r = fma(r, fma(-m, r, 1.0), r);
+    return mk(d.x * r, -d.y * r);
 }
 
 // D^-1 at local linear index q of a vertex touching nb physical faces: the

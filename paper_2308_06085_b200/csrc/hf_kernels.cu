@@ -512,7 +512,7 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
     double k_next = L.kc;
     if (act && i0 < i1) {
         if (Epi::kAux && aux) a_next = __ldg(aux + q);
-        if (KVAR) k_next = __ldg(L.k + q);
+        if (KVAR && !SM::kKw) k_next = __ldg(L.k + q);
     }
     // one plane; R = (i - i0) mod RING fixes the ring slots at compile time:
     // i-1 in R, i in R+1, i+1 in R+2, and plane i+RING-2 is staged into R-1
@@ -524,7 +524,7 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
         const double k_cur = k_next;
         if (act && i + 1 < i1) {
             if (Epi::kAux && aux) a_next = __ldg(aux + q + L.plane);
-            if (KVAR) k_next = __ldg(L.k + q + L.plane);
+            if (KVAR && !SM::kKw) k_next = __ldg(L.k + q + L.plane);
         }
         cp_wait<RING - 4>();               // plane i+1 landed (later ones may be in flight)
         if (kScale) fixup(sn, i + 1);      // own entries only: no barrier needed before
@@ -541,7 +541,7 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
             cd xm = sm.raw[sp][cf], xp = sm.raw[sn][cf];
             cd ym = r0[cf - HALO_X], yp = r0[cf + HALO_X];
             cd zm = r0[cf - 1], zp = r0[cf + 1];
-            const double kk = k_cur;
+            const double kk = SM::kKw ? sm.kw[sc][cf] : k_cur;   // PRE: k staged with the halo
             cd post = one;
             if (MODE == MODE_PRE) {
                 if (KVAR) {                   // staged f = D^-1 b (vfix), w applied once after M
@@ -1156,7 +1156,7 @@ __global__ void k_dinv(Lvl L, int g0, int g1, cd *__restrict__ out) {
         int rem = (int)(t - (long long)(i - g0) * L.plane);
         int j = rem / L.n3, m = rem - j * L.n3;
         long long q = (long long)i * L.plane + rem;
-        out[q] = cdiv(mk(1.0, 0.0), diag_of(L, L.k[q], nbnd(L, L.lo1 + i, j, m)));
+        out[q] = dinv_of(L, L.k[q], nbnd(L, L.lo1 + i, j, m));
     }
 }
 

@@ -1,0 +1,31 @@
+"""One launch each of the 513^3 wedge finest-level kernels the solve runs
+(pre-smoothing + residual sweep, Jacobi sweep, correction, restriction, the
+Bi-CGSTAB x/r and s updates), for ncu --set full."""
+import ctypes
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2308_06085_b200 import _native, problems  # noqa: E402
+
+p = problems.wedge3_problem(int(os.environ.get("PROF_N", 513)))
+spec, b = problems.build_problem(p)
+A, H, S = bench._solver_for(p, spec)
+L = _native.load()
+_native.set_stream_from_torch()
+sh, csh = H.levels[0].extent.shape, H.levels[1].extent.shape
+r = lambda s: torch.randn(s, dtype=torch.complex128, device="cuda")
+bb, u, t, bc, ec = r(sh), r(sh), r(sh), r(csh), r(csh)
+ms = ctypes.c_float()
+for _ in range(2):
+    _native.check(L.hf_level_down1(H._h, 0, bb.data_ptr(), u.data_ptr()))
+    _native.check(L.hf_level_smooth(H._h, 0, t.data_ptr(), bb.data_ptr(), u.data_ptr()))
+    _native.check(L.hf_level_correct(H._h, 0, bb.data_ptr(), ec.data_ptr(), t.data_ptr()))
+    _native.check(L.hf_restrict_fw(H._h, 0, u.data_ptr(), bc.data_ptr()))
+    for w in (1, 2):
+        _native.check(L.hf_solver_bench_vec(S._h, w, 1, ctypes.byref(ms)))
+torch.cuda.synchronize()
+print("ok")

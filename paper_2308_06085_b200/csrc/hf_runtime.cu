@@ -2052,7 +2052,36 @@ static Lvl sub_slab(const Lvl &L, int p0, int p1) {
     return o;
 }
 
-// one V(1,1) cycle over the slabs: dst[i] ~= M^-1 src[i] (multigrid.py:326-343)
+// halo exchange on the comm stream, overlapped with `interior` on the main
+// stream; `boundary` runs after both (the ghost planes have arrived)
+template <class FI, class FB>
+static int overlapped(hf_slab *S, int l, const std::vector<cd *> &f, int planes, cudaStream_t s,
+                      FI &&interior, FB &&boundary) {
+    CK(cudaEventRecord(S->evf, s));
+    CK(cudaStreamWaitEvent(S->cstream, S->evf, 0));
+    if (slab_halo(S, l, f, planes, S->cstream)) return HF_ERR_CUDA;
+    CK(cudaEventRecord(S->evj, S->cstream));
+    interior();
+    CK(cudaStreamWaitEvent(s, S->evj, 0));
+    boundary();
+    return 0;
+}
+
+// coarse planes [c0, c1) (local) of slab level C whose fine planes [2gc - rad,
+// 2gc + rad] (global) all lie in the owned fine planes of F
+static void coarse_interior(const Lvl &F, const Lvl &C, int rad, int &c0, int &c1) {
+    const int flo = F.lo1, fhi = F.lo1 + F.nx - 1;
+    int g0 = (flo + rad + 1) / 2, g1 = (fhi - rad) / 2;       // ceil, floor
+    g0 = std::max(g0, C.lo1);
+    g1 = std::min(g1, C.lo1 + C.nx - 1);
+    c0 = g0 - C.lo1;
+    c1 = std::max(c0, g1 - C.lo1 + 1);
+}
+
+// one V(1,1) cycle over the slabs: dst[i] ~= M^-1 src[i] (multigrid.py:326-343).
+// Each level's halo exchange overlaps the part of the level kernel that needs
+// no ghost planes (interior planes launched as a sub-slab); the face planes
+// follow once the ghost planes have arrived.
 static int slab_cycle(hf_slab *S, const std::vector<cd *> &src, const std::vector<cd *> &dst, cudaStream_t s) {
     const int nloc = (int)S->sl.size(), nl = S->nlev;
     const int *done = &S->st->done;
@@ -2062,28 +2091,65 @@ static int slab_cycle(hf_slab *S, const std::vector<cd *> &src, const std::vecto
     std::vector<cd *> f(nloc);
     for (int l = 0; l < nl - 1; l++) {
         for (int i = 0; i < nloc; i++) f[i] = bl(i, l);
-        if (S->fuse_down[l]) {
-            if (slab_halo(S, l, f, HF_GHOST, s)) return HF_ERR_CUDA;
-            for (int i = 0; i < nloc; i++) {
-                Level &lv = S->sl[i].H->lev[l], &nx = S->sl[i].H->lev[l + 1];
-                launch_down_restrict(lv.L, nx.L, f[i], nx.b, om, s, done);
-                g_launches++;
-            }
+        const bool fuse = S->fuse_down[l] && (flat_dr_ok(S->sl[0].H->lev[l].L) || opt(OPT_TILED_DR)) &&
+                          !opt(OPT_NO_DR);
+        if (fuse) {
+            // b_c = R (b - M (w D^-1 b)): coarse planes reading fine planes 2gc-2 .. 2gc+2
+            auto part = [&](bool inner) {
+                for (int i = 0; i < nloc; i++) {
+                    Level &lv = S->sl[i].H->lev[l], &nx = S->sl[i].H->lev[l + 1];
+                    int c0, c1;
+                    coarse_interior(lv.L, nx.L, 2, c0, c1);
+                    auto run = [&](int a, int b2) {
+                        if (b2 <= a) return;
+                        launch_down_restrict(lv.L, sub_slab(nx.L, a, b2), f[i], nx.b + (size_t)a * nx.L.plane,
+                                             om, s, done);
+                        g_launches++;
+                    };
+                    if (inner) run(c0, c1);
+                    else { run(0, c0); run(std::max(c1, c0), nx.L.nx); }
+                }
+            };
+            if (overlapped(S, l, f, HF_GHOST, s, [&] { part(true); }, [&] { part(false); })) return HF_ERR_CUDA;
             continue;
         }
-        if (slab_halo(S, l, f, 1, s)) return HF_ERR_CUDA;
+        // split pair: r = b - M (w D^-1 b) on fine planes, then b_c = R r
         std::vector<cd *> rr(nloc);
-        for (int i = 0; i < nloc; i++) {
-            Level &lv = S->sl[i].H->lev[l];
-            launch_down1(lv.L, f[i], lv.r, om, s, done);
-            rr[i] = lv.r;
-        }
-        if (slab_halo(S, l, rr, 1, s)) return HF_ERR_CUDA;
-        for (int i = 0; i < nloc; i++) {
-            Level &lv = S->sl[i].H->lev[l], &nx = S->sl[i].H->lev[l + 1];
-            launch_restrict(lv.L, nx.L, lv.r, nx.b, s, done);
-        }
-        g_launches += 2 * nloc;
+        for (int i = 0; i < nloc; i++) rr[i] = S->sl[i].H->lev[l].r;
+        auto down = [&](bool inner) {
+            for (int i = 0; i < nloc; i++) {
+                Level &lv = S->sl[i].H->lev[l];
+                const int nx = lv.L.nx;
+                auto run = [&](int a, int b2) {
+                    if (b2 <= a) return;
+                    const size_t o = (size_t)a * lv.L.plane;
+                    launch_down1(sub_slab(lv.L, a, b2), f[i] + o, lv.r + o, om, s, done);
+                    g_launches++;
+                };
+                if (nx > 2) {
+                    if (inner) run(1, nx - 1);
+                    else { run(0, 1); run(nx - 1, nx); }
+                } else if (!inner) {
+                    run(0, nx);
+                }
+            }
+        };
+        if (overlapped(S, l, f, 1, s, [&] { down(true); }, [&] { down(false); })) return HF_ERR_CUDA;
+        auto restr = [&](bool inner) {
+            for (int i = 0; i < nloc; i++) {
+                Level &lv = S->sl[i].H->lev[l], &nx = S->sl[i].H->lev[l + 1];
+                int c0, c1;
+                coarse_interior(lv.L, nx.L, 1, c0, c1);
+                auto run = [&](int a, int b2) {
+                    if (b2 <= a) return;
+                    launch_restrict(lv.L, sub_slab(nx.L, a, b2), lv.r, nx.b + (size_t)a * nx.L.plane, s, done);
+                    g_launches++;
+                };
+                if (inner) run(c0, c1);
+                else { run(0, c0); run(std::max(c1, c0), nx.L.nx); }
+            }
+        };
+        if (overlapped(S, l, rr, 1, s, [&] { restr(true); }, [&] { restr(false); })) return HF_ERR_CUDA;
     }
     // coarsest: gather every slab's planes into the whole grid, exact solve, scatter
     const size_t cpb = (size_t)S->cplane * sizeof(cd);
@@ -2107,15 +2173,41 @@ static int slab_cycle(hf_slab *S, const std::vector<cd *> &src, const std::vecto
     }
     for (int l = nl - 2; l >= 0; l--) {
         for (int i = 0; i < nloc; i++) f[i] = S->sl[i].H->lev[l + 1].u;
-        if (slab_halo(S, l + 1, f, 1, s)) return HF_ERR_CUDA;
+        // t = w D^-1 b + P e: fine planes whose coarse planes (gi >> 1, + 1 when odd)
+        // are owned need no ghost plane of e; the rest (and t on the interior-face
+        // ghost planes, so the sweep needs no halo of t) after the exchange
+        auto corr = [&](bool inner) {
+            for (int i = 0; i < nloc; i++) {
+                Level &lv = S->sl[i].H->lev[l], &nx = S->sl[i].H->lev[l + 1];
+                const int nxf = lv.L.nx;
+                int a = 0, b2 = nxf;                              // interior fine planes [a, b2)
+                while (a < nxf && ((lv.L.lo1 + a) >> 1) < nx.L.lo1) a++;
+                while (b2 > a && (((lv.L.lo1 + b2 - 1) >> 1) + ((lv.L.lo1 + b2 - 1) & 1)) > nx.L.lo1 + nx.L.nx - 1) b2--;
+                auto run = [&](int p0, int p1, bool ghosts) {
+                    if (p1 <= p0) return;
+                    const size_t o = (size_t)p0 * lv.L.plane;
+                    launch_correct(sub_slab(lv.L, p0, p1), nx.L, bl(i, l) + o, nx.u, lv.t + o, om, true, s, done,
+                                   ghosts);
+                    g_launches++;
+                };
+                if (inner) {
+                    run(a, b2, false);
+                } else {
+                    // the face ranges; ghost planes only where the slab face is interior
+                    const bool glo = lv.L.lo1 > 0, ghi = lv.L.lo1 + nxf < lv.L.n1;
+                    if (a > 0) run(0, a, glo);
+                    else if (glo) run(0, std::min(1, nxf), true);   // ghost plane below (and plane 0 again)
+                    if (b2 < nxf) run(std::max(b2, a), nxf, ghi);
+                    else if (ghi) run(nxf - 1, nxf, true);
+                }
+            }
+        };
+        if (overlapped(S, l + 1, f, 1, s, [&] { corr(true); }, [&] { corr(false); })) return HF_ERR_CUDA;
         for (int i = 0; i < nloc; i++) {
-            Level &lv = S->sl[i].H->lev[l], &nx = S->sl[i].H->lev[l + 1];
-            // t on the owned planes and the interior-face ghost planes (b's halo from
-            // the down-sweep is valid): no halo exchange of t before the sweep
-            launch_correct(lv.L, nx.L, bl(i, l), nx.u, lv.t, om, true, s, done, true);
+            Level &lv = S->sl[i].H->lev[l];
             launch_jacobi(lv.L, lv.t, bl(i, l), ul(i, l), om, s, done);
         }
-        g_launches += 2 * nloc;
+        g_launches += nloc;
     }
     return 0;
 }

@@ -6,7 +6,8 @@ at sizes the C oracle solves in seconds.
   within +-1 iteration and 1e-8;
 * SolverConfig.shadow = "random" (HF_SHADOW_HASH, the B200 addition that
   converges where the reference's r~ = b stops on the rho test): native vs the
-  oracle's restatement of the same hash vector, +-1 iteration and 1e-8, on the
+  oracle's restatement of the same hash vector: identical early residual
+  histories (1e-8), +-1 iteration, solutions within the tolerance band, on the
   wedge and the random medium.
 """
 
@@ -57,8 +58,12 @@ def test_random_shadow_matches_oracle(oracle, name):
     p, k, b = _case(name)
     x, rep = _native(p, k, b, shadow="random")
     xo, ro = oracle.solve(k, b, p.grid.h, maxit=600, shadow="random", rng_seed=1234)
+    # the same shadow vector drives both: the residual histories coincide until
+    # rounding amplification sets in
+    np.testing.assert_allclose(rep.residual_history[:10], ro["residual_history"][:10], rtol=1e-8)
     assert rep.converged and ro["converged"]
     assert abs(rep.iterations - ro["iterations"]) <= 1
-    assert _rel(x, xo) < 1e-8
-    # the first residuals coincide: the same shadow vector drives both
-    np.testing.assert_allclose(rep.residual_history[:10], ro["residual_history"][:10], rtol=1e-8)
+    # with a dense random shadow the end of the solve is rounding-sensitive
+    # (measured: 6.8e-7 relative at 65^3, both at relres <= 1e-6): the solutions
+    # agree to the tolerance band, not to 1e-8 as with r~ = b at this size
+    assert _rel(x, xo) < 1e-5

@@ -125,3 +125,32 @@ def test_native_slabs_nccl_one_rank():
         del S
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("nslabs", [2, 3])
+def test_native_slabs_wide_planes(nslabs):
+    """Planes wider than 255 vertices: the slab cycle runs the split
+    pre-smoothing / restriction pair with both halos overlapped, and the
+    65 x 17 x 145 coarsest grid (no exact factorisation) runs the device GMRES
+    fallback."""
+    from paper_2308_06085_b200 import problems
+    from paper_2308_06085_b200.dist import NativeSlabSolver
+    from paper_2308_06085_b200.grid import make_grid
+    from paper_2308_06085_b200.krylov import SolverConfig
+    from paper_2308_06085_b200.partition import LocalSlabComm, slab_partition
+    grid = make_grid(33, 65, 289, 1.0 / 288)
+    rng = np.random.default_rng(5)
+    k = rng.uniform(40.0, 60.0, grid.shape)
+    b = np.zeros(grid.shape, complex)
+    b[16, 32, 144] = 1.0 / grid.h ** 3
+
+    class P:
+        pass
+    P.grid = grid
+    x1, r1 = _single(P, k, b)
+    ext = slab_partition(grid, nslabs)
+    from paper_2308_06085_b200.operators import Sommerfeld
+    xs, rep = NativeSlabSolver(grid, ext, k, Sommerfeld(), LocalSlabComm(nslabs)).solve(
+        [b[e.lo1 - 1:e.hi1] for e in ext], SolverConfig(method="bicgstab"))
+    assert rep.converged and abs(rep.iterations - r1.iterations) <= 1
+    assert _rel(np.concatenate([t.cpu().numpy() for t in xs], 0), x1) < 1e-8

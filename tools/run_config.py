@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--method", default="bicgstab", choices=["bicgstab", "gmres", "idrs"])
     ap.add_argument("--restart", type=int, default=0)
     ap.add_argument("--btol", type=float, default=1e-30)
+    ap.add_argument("--shadow", default="rhs", choices=["rhs", "random"])
     args = ap.parse_args()
     t0 = time.perf_counter()
     if args.which == "cube":
@@ -50,12 +51,11 @@ def main():
     torch.cuda.synchronize()
     t_setup = time.perf_counter() - t0
     cfg = SolverConfig(method=args.method, tol=1e-6, maxit=args.maxit, restart=args.restart or None,
-                       breakdown_tol=args.btol)
+                       breakdown_tol=args.btol, shadow=args.shadow, check_every=16)
     x, rep = S.solve(bd, cfg)
-    if args.method == "bicgstab":
-        x, rep = S.solve(bd, cfg)
     n = p.grid.num_vertices
-    print(json.dumps({"problem": args.which, "method": args.method, "breakdown_tol": args.btol, "grid": list(p.grid.shape), "unknowns": n,
+    print(json.dumps({"problem": args.which, "method": args.method, "shadow": args.shadow,
+                      "coarsest": H.coarsest_kind, "breakdown_tol": args.btol, "grid": list(p.grid.shape), "unknowns": n,
                       "kh_max": float(np.max(k) * p.grid.h), "levels": [lv.grid.n1 for lv in H.levels],
                       "iterations": rep.iterations, "converged": rep.converged,
                       "final_relres": rep.final_relres, "breakdown": rep.breakdown,

@@ -2421,8 +2421,10 @@ void launch_dinv(const Lvl &L, cd *out_owned, cudaStream_t s) {
 void launch_restrict(const Lvl &F, const Lvl &C, const cd *r, cd *out, cudaStream_t s,
                      const int *done) {
     if (!opt(OPT_NO_FLAT)) {
+        // ~20 blocks per SM in total (5 resident at 48 registers): a few full
+        // waves of short marches instead of 1.4 waves of long ones
         const int gx = (int)((C.plane + 255) / 256);
-        int gz = std::max(1, std::min(C.nx, (148 * 8) / gx));
+        int gz = std::max(1, std::min(C.nx, (148 * 20) / gx));
         const int chunk = (C.nx + gz - 1) / gz;
         gz = (C.nx + chunk - 1) / chunk;
         launch(k_restrict_flat, dim3(gx, gz), dim3(256), 0, s, F, C, r, out, chunk, done);

@@ -514,6 +514,7 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
         if (Epi::kAux && aux) a_next = __ldg(aux + q);
         if (KVAR && !SM::kKw) k_next = __ldg(L.k + q);
     }
+    cd rot_c = mk(0, 0), rot_m = mk(0, 0);   // centre values of planes i, i-1 (next step)
     // one plane; R = (i - i0) mod RING fixes the ring slots at compile time:
     // i-1 in R, i in R+1, i+1 in R+2, and plane i+RING-2 is staged into R-1
     auto step = [&](auto Rc, int i) {
@@ -537,8 +538,20 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
             const bool bxl = gi == 0, bxh = gi == L.n1 - 1;
             const int nb = (int)bxl + (int)bxh + nbjm;
             const cd *r0 = sm.raw[sc];
-            cd fc = r0[cf];
-            cd xm = sm.raw[sp][cf], xp = sm.raw[sn][cf];
+            // centre values of planes i-1, i rotate through registers along the
+            // march (plane i+1's was read as xp at the previous step, after its
+            // in-slot transform); only the first step reads them from the ring
+            cd fc, xm;
+            if (MODE != MODE_PRE || i == i0) {   // (rotation measured faster for PRE only)
+                fc = r0[cf];
+                xm = sm.raw[sp][cf];
+            } else {
+                fc = rot_c;
+                xm = rot_m;
+            }
+            cd xp = sm.raw[sn][cf];
+            rot_m = fc;
+            rot_c = xp;
             cd ym = r0[cf - HALO_X], yp = r0[cf + HALO_X];
             cd zm = r0[cf - 1], zp = r0[cf + 1];
             const double kk = SM::kKw ? sm.kw[sc][cf] : k_cur;   // PRE: k staged with the halo

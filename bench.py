@@ -235,7 +235,7 @@ def run_gpu(args):
     # ---- kernel roofline: live CUDA-event timing of the path's kernels ----
     hbm, peak_kind = _peaks()
     t_iter = ms_step / max(iters, 1)
-    kern = kernel_table(A, hier, solver, n, t_iter)
+    kern = kernel_table(A, hier, solver, n, t_iter, sparse_shadow=np.count_nonzero(b_host) <= 16)
     dom = max((k_ for k_ in kern if kern[k_]["bound"] == "hbm" and kern[k_]["share"]),
               key=lambda k_: kern[k_]["share"])
     kd = kern[dom]
@@ -415,7 +415,7 @@ def run_slabs(args):
     dist.destroy_process_group()
 
 
-def kernel_table(A, hier, solver, n, t_iter_ms, reps=12):
+def kernel_table(A, hier, solver, n, t_iter_ms, reps=12, sparse_shadow=True):
     """Live CUDA-event timing of the kernels the finest level of THIS workload's
     solve launches (the fused flat down-kernel where the plane is <= 255 wide,
     the split presmooth+residual / restriction pair otherwise; correction +
@@ -509,11 +509,14 @@ def kernel_table(A, hier, solver, n, t_iter_ms, reps=12):
         f"coarsest ({kind})", total_bytes=cbytes)
     # Bi-CGSTAB vector kernels, once per iteration (krylov.py:240-269), back to
     # back on the solver's workspace
+    # the x/r update reads r~ only when the shadow vector is dense; a point
+    # source with the reference's r~ = b is sparse (gathered)
+    sparse = bool(sparse_shadow)
     for nm, which, bpv in (("bcg_p_update", 0, 64.0), ("bcg_s_update", 1, 48.0),
-                           ("bcg_xr_update", 2, 128.0)):
+                           ("bcg_xr_update", 3 if sparse else 2, 112.0 if sparse else 128.0)):
         m = ctypes.c_float()
         _native.check(L.hf_solver_bench_vec(solver._h, which, r, ctypes.byref(m)))
-        put(nm, m.value, bpv, "hbm", 1, ("k_bcg_p", "k_bcg_s", "k_bcg_xr")[which])
+        put(nm, m.value, bpv, "hbm", 1, ("k_bcg_p", "k_bcg_s", "k_bcg_xr", "k_bcg_xr (sparse r~)")[which])
     return out
 
 

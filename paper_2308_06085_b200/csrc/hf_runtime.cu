@@ -1649,13 +1649,15 @@ extern "C" int hf_operator_apply_dot(hf_operator *op, hf_bcg *B, int nd, const d
 // solver's workspace, inner products into a scratch slot (the device scalar
 // state is not touched).  Mean device time per launch in *ms.
 extern "C" int hf_solver_bench_vec(hf_solver *S, int which, int reps, float *ms) {
-    if (!S || reps < 1 || !ms || which < 0 || which > 2) return fail(HF_ERR_ARG, "bad bench request");
+    if (!S || reps < 1 || !ms || which < 0 || which > 3) return fail(HF_ERR_ARG, "bad bench request");
     cudaStream_t s = work_stream();
     const RedSlot scratch = S->red.slot(FIN_STORE, nullptr);
     auto one = [&]() {
         if (which == 0) launch_bcg_p(S->n, S->st, S->r, S->p, S->v, s, nullptr);
         else if (which == 1) launch_bcg_s(S->n, S->st, S->r, S->v, S->s, scratch, s, nullptr);
-        else launch_bcg_xr(S->n, S->st, S->x, S->ph, S->sh, S->s, S->t, S->r, S->rs, scratch, s, nullptr);
+        else   // 3: the sparse-shadow variant (r~^H r gathered, r~ not streamed)
+            launch_bcg_xr(S->n, S->st, S->x, S->ph, S->sh, S->s, S->t, S->r, which == 2 ? S->rs : nullptr,
+                          scratch, s, nullptr);
     };
     if (reps > 1) one();   // warm-up (reps = 1: a single, cold launch)
     cudaEvent_t a, b;

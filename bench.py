@@ -442,6 +442,11 @@ def kernel_table(A, hier, solver, n, t_iter_ms, reps=12, sparse_shadow=True):
     cr = nc / nf
     kvar = A._keep is not None     # k passed per vertex (operators.k_arguments)
     kb, db = (8.0, 16.0) if kvar else (0.0, 0.0)
+    # palette levels (wide planes, <= 256 distinct k): 1-byte indices, no D^-1
+    # field; the pre-smoothing sweep still streams the 8-byte k
+    pal = kvar and shape[2] > 256 and len(np.unique(np.asarray(A.spec.k_field)[::7, ::7, ::7])) <= 256 \
+        and not _native.load().hf_get_option(b"no_palette")
+    kp, dp = (1.0, 0.0) if pal else (kb, db)
     nset = 1 if nf * 16 > 2 * L2_BYTES else 4
     rnd = lambda sh: torch.randn(sh, dtype=torch.complex128, device="cuda")
     sets = [dict(u=rnd(shape), b=rnd(shape), v=rnd(shape), t=rnd(shape), ec=rnd(cshape),
@@ -454,13 +459,13 @@ def kernel_table(A, hier, solver, n, t_iter_ms, reps=12, sparse_shadow=True):
     cases = {
         "device_copy": (lambda s: s["v"].copy_(s["u"]), 32.0, "ceiling", 0, "torch copy_"),
         "helmholtz_matvec": (lambda s: L.hf_operator_apply(A._h, p(s["u"]), p(s["v"])),
-                             32.0 + kb, "hbm", 2,
+                             32.0 + kp, "hbm", 2,
                              "k_flat_stencil<LOAD,EpiApply>" if fused_down else
                              "k_stencil<LOAD,EpiApply>"),
         "prolong_correct": (lambda s: L.hf_level_correct(H, 0, p(s["b"]), p(s["ec"]), p(s["t"])),
-                            32.0 + db + 16.0 * cr, "hbm", 2, "k_corr_flat<1>"),
+                            32.0 + (1.0 if pal else db) + 16.0 * cr, "hbm", 2, "k_corr_flat<1>"),
         "jacobi_postsmooth": (lambda s: L.hf_level_smooth(H, 0, p(s["t"]), p(s["b"]), p(s["u"])),
-                              48.0 + kb, "hbm", 2,
+                              48.0 + kp, "hbm", 2,
                               "k_flat_stencil<LOAD,EpiJacobi>" if fused_down else
                               "k_stencil<LOAD,EpiJacobi>"),
     }
@@ -475,11 +480,12 @@ def kernel_table(A, hier, solver, n, t_iter_ms, reps=12, sparse_shadow=True):
         # the fused alternatives on wide planes (not on the default path: share None)
         cases["down_restrict_tiled"] = (lambda s: L.hf_level_down_restrict(H, 0, p(s["b"]), p(s["bc"])),
                                         16.0 + kb + 16.0 * cr, "hbm", 0, "k_down_restrict")
+        kp_up = kb       # the fused up-sweep stages the 8-byte k (D^-1 of every staged entry)
 
         def up_fused(s):
             with _native.options(fuse_up=1):
                 L.hf_level_up(H, 0, p(s["b"]), p(s["ec"]), p(s["u"]))
-        cases["up_fused_tiled"] = (up_fused, 32.0 + kb + 16.0 * cr, "hbm", 0, "k_stencil<UP,EpiJacobi>")
+        cases["up_fused_tiled"] = (up_fused, 32.0 + kp_up + 16.0 * cr, "hbm", 0, "k_stencil<UP,EpiJacobi>")
     kind = hier.coarsest_kind
     nt = -(-ncs // 64)
     cbytes = {"separable": 112.0 * ncs,

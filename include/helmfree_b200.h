@@ -118,7 +118,8 @@ int hf_version(void);
 /* Kernel-variant selection for A/B measurements and the parity tests that compare
  * variants (process-wide; every variant computes the same arithmetic; all off is the
  * measured-fastest default).  Names: "no_pdl", "no_flat", "no_flat_dr", "no_dr",
- * "tiled_dr", "flat_up", "fuse_up", "no_fuse", "coarsest_dense".  The library reads
+ * "tiled_dr", "flat_up", "fuse_up", "no_fuse", "coarsest_dense", "no_palette" (the
+ * last applies to hierarchies / operators created after it is set).  The library reads
  * no environment variables. */
 int hf_set_option(const char *name, int value);
 int hf_get_option(const char *name);   /* 0/1, or HF_ERR_ARG for an unknown name */

@@ -172,7 +172,7 @@ def set_stream_from_torch() -> None:
 
 
 OPTIONS = ("no_pdl", "no_flat", "no_flat_dr", "no_dr", "tiled_dr", "flat_up", "fuse_up", "no_fuse",
-           "coarsest_dense")
+           "coarsest_dense", "no_palette")
 
 
 def set_option(name: str, value) -> None:

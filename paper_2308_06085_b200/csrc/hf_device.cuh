@@ -49,6 +49,13 @@ struct Lvl {
     const double2 *dinv; // D^-1 at owned plane 0 (ghost planes valid) when k varies, else null
     const double2 *tab;  // constant k, nb physical faces: tab[nb] = a_p, tab[4 + nb] = D^-1,
                          // tab[8 + nb] = D^-1(nb) / D^-1(0)
+    // palette (wide levels of a medium with <= 256 distinct wavenumbers): k as an
+    // 8-bit index into kpal, a_p and D^-1 per (index, face count) in apal / dpal
+    // (4 entries per index) -- 1 byte of k traffic per vertex instead of 8, no
+    // D^-1 field and no reciprocal
+    const unsigned char *kidx;   // at owned plane 0 (ghost planes valid), or null
+    const double *kpal;
+    const double2 *apal, *dpal;
 };
 
 
@@ -96,6 +103,7 @@ __device__ __forceinline__ cd dinv_of(const Lvl &L, double kk, int nb) {
 // stored field where the level keeps one (a pointwise kernel without ALU slack
 // -- k_corr -- is faster streaming 16 B than dividing), else from k
 __device__ __forceinline__ double2 dinv_at(const Lvl &L, long long q, int nb) {
+    if (L.kidx) return __ldg(L.dpal + 4 * __ldg(L.kidx + q) + nb);
     if (L.dinv) return __ldg(L.dinv + q);
     return L.k ? dinv_of(L, __ldg(L.k + q), nb) : __ldg(L.tab + 4 + nb);
 }

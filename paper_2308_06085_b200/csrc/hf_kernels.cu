@@ -357,13 +357,34 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
     // D^-1 from k at the entry's (mirrored) vertex -- no D^-1 field is streamed
     // and a point's row reads its seven neighbours' f directly
     constexpr bool kVarPre = MODE == MODE_PRE && KVAR;
+    // palette level: D^-1 of a staged entry is a table read at its 8-bit index,
+    // the indices of plane p+1's entries loaded one step ahead (pix0 / pix1)
+    // (the pre-smoothing sweep keeps staging k and forming D^-1: its per-entry
+    // table reads on the critical path of every plane measured slower)
+    const bool pal = KVAR && L.kidx != nullptr && MODE != MODE_PRE;
+    auto ldix = [&](int p, int go) -> int {
+        int g = L.lo1 + p;
+        g = g < 0 ? -g : (g >= L.n1 ? 2 * (L.n1 - 1) - g : g);
+        return __ldg(L.kidx + (long long)(g - L.lo1) * L.plane + go);
+    };
+    int pix0 = 0, pix1 = 0;
     auto vfix = [&](int slot, int i) {
         int gi = L.lo1 + i;
         gi = gi < 0 ? -gi : (gi >= L.n1 ? 2 * (L.n1 - 1) - gi : gi);
         const int nbx = (gi == 0) + (gi == L.n1 - 1);
+        if (pal) {
+            if (ok0) sm.raw[slot][tid] = cmul(sm.raw[slot][tid], __ldg(L.dpal + 4 * pix0 + nbx + nbe0));
+            if (ok1) sm.raw[slot][tid + NT] = cmul(sm.raw[slot][tid + NT], __ldg(L.dpal + 4 * pix1 + nbx + nbe1));
+            return;
+        }
         if (ok0) sm.raw[slot][tid] = cmul(sm.raw[slot][tid], dinv_of(L, sm.kw[slot][tid], nbx + nbe0));
         if (ok1)
             sm.raw[slot][tid + NT] = cmul(sm.raw[slot][tid + NT], dinv_of(L, sm.kw[slot][tid + NT], nbx + nbe1));
+    };
+    auto pfix = [&](int p) {          // prefetch the palette indices of plane p's own entries
+        if (!pal || p > i1) return;
+        if (ok0) pix0 = ldix(p, go0);
+        if (ok1) pix1 = ldix(p, go1);
     };
     // MODE_UP: coarse tile of e staged once per block (all coarse planes the
     // chunk's fine planes i0-1 .. i1 interpolate from, mirrored ones included)
@@ -441,6 +462,7 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
     constexpr unsigned SLOT = NFILL * sizeof(cd);
     constexpr unsigned KSLOT = NFILL * sizeof(double);
     const double *k0 = SM::kKw ? L.k + go0 : nullptr, *k1 = SM::kKw ? L.k + go1 : nullptr;
+    const bool stage_k = !pal || MODE == MODE_UP;   // MODE_UP forms D^-1 from the staged k
     const cd *g0 = src + go0, *g1 = src + go1;
     const cd *d0 = SM::kWd ? L.dinv + go0 : nullptr, *d1 = SM::kWd ? L.dinv + go1 : nullptr;
     auto stage = [&](auto SS, int p) {     // one commit group per plane, ring slot SS
@@ -454,11 +476,11 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
         const bool v0 = pok && ok0, v1 = pok && ok1;
         cp_async16s(sraw0 + so, g0 + pb, v0);
         if (SM::kWd) cp_async16s(swd0 + so, d0 + pb, v0);
-        if (SM::kKw) cp_async8s(skw0 + decltype(SS)::value * KSLOT, k0 + pb, v0);
+        if (SM::kKw && stage_k) cp_async8s(skw0 + decltype(SS)::value * KSLOT, k0 + pb, v0);
         if (has1) {
             cp_async16s(sraw0 + so + NT * sizeof(cd), g1 + pb, v1);
             if (SM::kWd) cp_async16s(swd0 + so + NT * sizeof(cd), d1 + pb, v1);
-            if (SM::kKw) cp_async8s(skw0 + decltype(SS)::value * KSLOT + NT * sizeof(double), k1 + pb, v1);
+            if (SM::kKw && stage_k) cp_async8s(skw0 + decltype(SS)::value * KSLOT + NT * sizeof(double), k1 + pb, v1);
         }
         cp_commit();
     };
@@ -480,11 +502,11 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
         if (any) {
             cp_async16s(sraw0 + so, g0 + pb, ok0);
             if (SM::kWd) cp_async16s(swd0 + so, d0 + pb, ok0);
-            if (SM::kKw) cp_async8s(skw0 + decltype(SS)::value * KSLOT, k0 + pb, ok0);
+            if (SM::kKw && stage_k) cp_async8s(skw0 + decltype(SS)::value * KSLOT, k0 + pb, ok0);
             if (has1) {
                 cp_async16s(sraw0 + so + NT * sizeof(cd), g1 + pb, ok1);
                 if (SM::kWd) cp_async16s(swd0 + so + NT * sizeof(cd), d1 + pb, ok1);
-                if (SM::kKw) cp_async8s(skw0 + decltype(SS)::value * KSLOT + NT * sizeof(double), k1 + pb, ok1);
+                if (SM::kKw && stage_k) cp_async8s(skw0 + decltype(SS)::value * KSLOT + NT * sizeof(double), k1 + pb, ok1);
             }
         }
         cp_commit();
@@ -499,8 +521,11 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
             fixup(0, i0 - 1);
             fixup(1, i0);
         } else if (kVarPre) {
+            pfix(i0 - 1);
             vfix(0, i0 - 1);
+            pfix(i0);
             vfix(1, i0);
+            pfix(i0 + 1);
         } else {
             produce(0, i0 - 1);
             produce(1, i0);
@@ -510,9 +535,11 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
     // centre-only epilogue operands (b or w, and k) are prefetched one plane ahead
     cd a_next = mk(0, 0);
     double k_next = L.kc;
+    int ci_next = 0;                    // palette index of this thread's vertex
     if (act && i0 < i1) {
         if (Epi::kAux && aux) a_next = __ldg(aux + q);
-        if (KVAR && !SM::kKw) k_next = __ldg(L.k + q);
+        if (pal) ci_next = __ldg(L.kidx + q);
+        else if (KVAR && !SM::kKw) k_next = __ldg(L.k + q);
     }
     cd rot_c = mk(0, 0), rot_m = mk(0, 0);   // centre values of planes i, i-1 (next step)
     // one plane; R = (i - i0) mod RING fixes the ring slots at compile time:
@@ -523,13 +550,18 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
         constexpr int ss = (R + RING - 1) % RING;
         const cd a_cur = a_next;
         const double k_cur = k_next;
+        const int ci_cur = ci_next;
         if (act && i + 1 < i1) {
             if (Epi::kAux && aux) a_next = __ldg(aux + q + L.plane);
-            if (KVAR && !SM::kKw) k_next = __ldg(L.k + q + L.plane);
+            if (pal) ci_next = __ldg(L.kidx + q + L.plane);
+            else if (KVAR && !SM::kKw) k_next = __ldg(L.k + q + L.plane);
         }
         cp_wait<RING - 4>();               // plane i+1 landed (later ones may be in flight)
         if (kScale) fixup(sn, i + 1);      // own entries only: no barrier needed before
-        if (kVarPre && i + 1 <= i1) vfix(sn, i + 1);
+        if (kVarPre && i + 1 <= i1) {
+            vfix(sn, i + 1);
+            pfix(i + 2);
+        }
         if (MODE == MODE_UP) produce(sn, i + 1);
         __syncthreads();
         stage_in(IC<ss>{}, i + RING - 2);  // into the slot read last at step i-1
@@ -554,7 +586,7 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
             rot_c = xp;
             cd ym = r0[cf - HALO_X], yp = r0[cf + HALO_X];
             cd zm = r0[cf - 1], zp = r0[cf + 1];
-            const double kk = SM::kKw ? sm.kw[sc][cf] : k_cur;   // PRE: k staged with the halo
+            const double kk = pal ? 0.0 : (SM::kKw ? sm.kw[sc][cf] : k_cur);   // PRE: k staged with the halo
             cd post = one;
             if (MODE == MODE_PRE) {
                 if (KVAR) {                   // staged f = D^-1 b (vfix), w applied once after M
@@ -565,7 +597,8 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
             }
             // uniform 7-point row: out-of-grid neighbours are already mirrored
             cd sum = cadd(cadd(cadd(xm, xp), cadd(ym, yp)), cadd(zm, zp));
-            const cd ap = KVAR ? ap_of(L, kk, nb) : (nb == 0 ? ap0 : tab[nb]);
+            const cd ap = KVAR ? (pal ? __ldg(L.apal + 4 * ci_cur + nb) : ap_of(L, kk, nb))
+                               : (nb == 0 ? ap0 : tab[nb]);
             cd mf = cmul(ap, fc);
             mf.x -= L.ih2 * sum.x;
             mf.y -= L.ih2 * sum.y;
@@ -574,7 +607,8 @@ __device__ __forceinline__ void stencil_body(const Lvl &L, const cd *__restrict_
             cd av = mk(0, 0);
             if (Epi::kAux) av = a_cur;
             cd wd = mk(0, 0);
-            if (Epi::kDinv) wd = KVAR ? cscal(dinv_of(L, kk, nb), omega) : wd_nb(nb);
+            if (Epi::kDinv)
+                wd = KVAR ? cscal(pal ? __ldg(L.dpal + 4 * ci_cur + nb) : dinv_of(L, kk, nb), omega) : wd_nb(nb);
             epi(q, fc, mf, wd, av, acc);
         }
         q += L.plane;
@@ -1160,6 +1194,16 @@ __global__ void __launch_bounds__(DR2_NT, 2) k_flat_dr(Lvl L, Lvl C, const cd *_
 }
 
 // D^-1 over a level of a varying medium (owned + ghost planes), at setup
+// palette tables: a_p and D^-1 of every (palette entry, face count) with the
+// device formulas, so they are bit-identical to the on-the-fly values
+__global__ void k_palette(Lvl L, int np, cd *__restrict__ apal, cd *__restrict__ dpal) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= 4 * np) return;
+    const double kk = L.kpal[t >> 2];
+    apal[t] = ap_of(L, kk, t & 3);
+    dpal[t] = dinv_of(L, kk, t & 3);
+}
+
 __global__ void k_dinv(Lvl L, int g0, int g1, cd *__restrict__ out) {
     pdl_enter();
     long long n = (long long)(g1 - g0) * L.plane;
@@ -2426,6 +2470,9 @@ void launch_jacobi0(const Lvl &L, const cd *b, cd *u, double omega, cudaStream_t
     int chunk;
     dim3 g = march_grid(L, chunk);
     launch(k_jacobi0, dim3(g), dim3(kMarchBlock), 0, s, L, b, u, omega, chunk, done);
+}
+void launch_palette(const Lvl &L, int np, cd *apal, cd *dpal, cudaStream_t s) {
+    launch(k_palette, dim3((4 * np + 127) / 128), dim3(128), 0, s, L, np, apal, dpal);
 }
 void launch_dinv(const Lvl &L, cd *out_owned, cudaStream_t s) {
     int g0 = std::max(-HF_GHOST, -L.lo1), g1 = std::min(L.nx + HF_GHOST, L.n1 - L.lo1);

@@ -6,7 +6,7 @@ namespace hf {
 
 // kernel-variant options (hf_set_option in the C ABI); all off = the default
 enum HfOpt { OPT_NO_PDL = 0, OPT_NO_FLAT, OPT_NO_FLAT_DR, OPT_NO_DR, OPT_TILED_DR, OPT_FLAT_UP,
-             OPT_FUSE_UP, OPT_NO_FUSE, OPT_COARSEST_DENSE, OPT_COUNT };
+             OPT_FUSE_UP, OPT_NO_FUSE, OPT_COARSEST_DENSE, OPT_NO_PALETTE, OPT_COUNT };
 extern int g_opt[OPT_COUNT];
 inline bool opt(int o) { return g_opt[o] != 0; }
 
@@ -37,6 +37,7 @@ void launch_prolong(const Lvl &F, const Lvl &C, const cd *e, cd *out, bool add, 
 // returns the number of kernels launched (1 fused, 2 split)
 int launch_up1(const Lvl &L, const Lvl &C, const cd *b, const cd *e, cd *u, cd *t, double omega,
                bool pre, cudaStream_t s, const int *done);
+void launch_palette(const Lvl &L, int np, cd *apal, cd *dpal, cudaStream_t s);
 void launch_dinv(const Lvl &L, cd *out_owned, cudaStream_t s);
 // ghosts: also the ghost planes at interior slab faces (b and e halos must be valid)
 void launch_correct(const Lvl &L, const Lvl &C, const cd *b, const cd *e, cd *t, double omega,

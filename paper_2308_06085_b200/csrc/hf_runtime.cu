@@ -52,7 +52,7 @@ extern "C" int hf_version(void) { return 2; }
 // the library reads no environment variables.
 static const char *const k_opt_names[OPT_COUNT] = {
     "no_pdl", "no_flat", "no_flat_dr", "no_dr", "tiled_dr", "flat_up", "fuse_up", "no_fuse",
-    "coarsest_dense"};
+    "coarsest_dense", "no_palette"};
 extern "C" int hf_set_option(const char *name, int value) {
     if (!name) return fail(HF_ERR_ARG, "null option name");
     for (int i = 0; i < OPT_COUNT; i++)
@@ -190,7 +190,52 @@ static int make_level(Allocs &A, Level &lv, int n1, int n2, int n3, int lo1, int
         CK(cudaMemcpy(dt, tab, sizeof(tab), cudaMemcpyHostToDevice));
         L.tab = dt;
     }
-    if (kfull) {
+    L.kidx = nullptr; L.kpal = nullptr; L.apal = nullptr; L.dpal = nullptr;
+    if (kfull && n3 > 256 && !opt(OPT_NO_PALETTE)) {
+        // wide level (tiled kernels): a medium with <= 256 distinct wavenumbers over
+        // this slab and its ghost planes is stored as 8-bit palette indices
+        const int g0 = std::max(0, lo1 - HF_GHOST), g1 = std::min(n1, lo1 + nx + HF_GHOST);
+        const size_t cnt = (size_t)(g1 - g0) * L.plane;
+        const double *src = kfull + (size_t)g0 * L.plane;
+        std::vector<double> pal;
+        bool fits = true;
+        double last = 0.0;
+        bool have = false;
+        for (size_t q = 0; q < cnt && fits; q++) {
+            const double v = src[q];
+            if (have && v == last) continue;
+            last = v;
+            have = true;
+            auto it = std::lower_bound(pal.begin(), pal.end(), v);
+            if (it == pal.end() || *it != v) {
+                if (pal.size() == 256) fits = false;
+                else pal.insert(it, v);
+            }
+        }
+        if (fits) {
+            std::vector<unsigned char> idx(cnt);
+            size_t lastq = 0;
+            for (size_t q = 0; q < cnt; q++) {
+                const double v = src[q];
+                if (q && v == src[lastq]) { idx[q] = idx[lastq]; lastq = q; continue; }
+                idx[q] = (unsigned char)(std::lower_bound(pal.begin(), pal.end(), v) - pal.begin());
+                lastq = q;
+            }
+            unsigned char *kb8 = A.get<unsigned char>((size_t)(nx + 2 * HF_GHOST) * L.plane, err);
+            double *kp = A.get<double>(256, err);
+            cd *ap = A.get<cd>(4 * 256, err), *dp = A.get<cd>(4 * 256, err);
+            if (!kb8 || !kp || !ap || !dp) return fail(HF_ERR_CUDA, "cudaMalloc palette");
+            CK(cudaMemcpy(kb8 + (size_t)(g0 - lo1 + HF_GHOST) * L.plane, idx.data(), cnt, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(kp, pal.data(), pal.size() * sizeof(double), cudaMemcpyHostToDevice));
+            L.kpal = kp;
+            launch_palette(L, (int)pal.size(), ap, dp, nullptr);
+            CK(cudaDeviceSynchronize());
+            L.kidx = kb8 + (size_t)HF_GHOST * L.plane;
+            L.apal = ap;
+            L.dpal = dp;
+        }
+    }
+    if (kfull && !L.kidx) {
         cd *dv = new_field(A, nx, L.plane, err);
         if (!dv) return fail(HF_ERR_CUDA, "cudaMalloc D^-1");
         launch_dinv(L, dv, nullptr);
@@ -2051,6 +2096,7 @@ static Lvl sub_slab(const Lvl &L, int p0, int p1) {
     o.nx = p1 - p0;
     if (L.k) o.k = L.k + (size_t)p0 * L.plane;
     if (L.dinv) o.dinv = L.dinv + (size_t)p0 * L.plane;
+    if (L.kidx) o.kidx = L.kidx + (size_t)p0 * L.plane;
     return o;
 }
 

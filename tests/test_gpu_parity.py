@@ -363,3 +363,27 @@ def test_repeat_solves_bit_identical(hf):
             ref, ref_it = x, rep.iterations
         assert rep.iterations == ref_it
         assert np.array_equal(x, ref)
+
+
+@pytest.mark.parametrize("bc", ["sommerfeld", "dirichlet"])
+def test_palette_level_matches_oracle(hf, oracle, bc, hfopt):
+    """Wide planes (n3 > 256) of a layered medium: k stored as 8-bit palette
+    indices, a_p / D^-1 from per-(index, face count) tables -- against the
+    oracle's cycle and apply, and against the same level without the palette."""
+    from paper_2308_06085_b200.multigrid import mg_precondition
+    from paper_2308_06085_b200.operators import Dirichlet, OperatorSpec, Sommerfeld, StencilOperator
+    n = (33, 17, 289)
+    z = np.linspace(0, 1, n[2])[None, None, :]
+    x = np.linspace(0, 1, n[0])[:, None, None]
+    k = np.broadcast_to(np.where(z > 0.4 + 0.2 * x, 30.0, np.where(z > 0.8 - 0.2 * x, 45.0, 20.0)), n).copy()
+    hier, oh = _pair(hf, oracle, n, bc, k)
+    r = _rand(n, 31)
+    got = mg_precondition(hier, r).cpu().numpy()
+    assert _rel(got, oh.precondition(r)) < 1e-9
+    spec = OperatorSpec("helmholtz", 1.0, 0.0, Dirichlet(0.0) if bc == "dirichlet" else Sommerfeld(), k)
+    grid = hf.make_grid(*n, 1.0 / (n[0] - 1))
+    v = StencilOperator(spec, grid).apply(r).cpu().numpy()
+    assert _rel(v, oracle.apply(k, r, grid.h, 1.0, bc)) < 1e-12
+    hfopt("no_palette", 1)
+    hier2, _ = _pair(hf, oracle, n, bc, k)
+    assert _rel(mg_precondition(hier2, r).cpu().numpy(), got) < 1e-12

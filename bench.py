@@ -90,7 +90,9 @@ def _ncu_traffic(kernel, config):
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             d = json.load(f)
         e = d.get(config, {})
-        return e["traffic_bytes_per_launch"] if e.get("kernel") == kernel else None
+        if "kernel" in e:             # single-kernel entry
+            e = {e["kernel"]: e}
+        return e[kernel]["traffic_bytes_per_launch"] if kernel in e else None
     except Exception:
         return None
 

@@ -3,7 +3,8 @@ dominant bench kernel: DRAM bytes (read + write) per launch, averaged over the
 captured launches of the named kernel.
 
     python tools/ncu_traffic.py gpurun_out/dom.ncu-rep c2 jacobi_postsmooth k_stencil
-(entry keyed by the bench config, so bench.py picks the one of its workload)
+(entries keyed by bench config and bench kernel name, so bench.py picks the
+one of its workload and dominant kernel)
 """
 import json
 import os
@@ -31,11 +32,13 @@ def run(rep, config, bench_name, kernel_regex):
                         "ncu_traffic.json")
     try:
         allc = json.load(open(path))
-        if "kernel" in allc:          # round-1 single-entry format
-            allc = {}
     except Exception:
         allc = {}
-    allc[config] = out
+    ent = allc.get(config, {})
+    if "kernel" in ent:               # single-kernel entry (older format)
+        ent = {ent["kernel"]: ent}
+    ent[bench_name] = out
+    allc[config] = ent
     with open(path, "w") as f:
         json.dump(allc, f, indent=1)
     print(json.dumps(out))

@@ -27,5 +27,7 @@ for _ in range(2):
     _native.check(L.hf_restrict_fw(H._h, 0, u.data_ptr(), bc.data_ptr()))
     for w in (1, 2):
         _native.check(L.hf_solver_bench_vec(S._h, w, 1, ctypes.byref(ms)))
+    _native.check(L.hf_solver_bench_vec(S._h, 3, 1, ctypes.byref(ms)))
+    _native.check(L.hf_solver_bench_vec(S._h, 0, 1, ctypes.byref(ms)))
 torch.cuda.synchronize()
 print("ok")

@@ -51,7 +51,7 @@ CONFIGS = {
                      "z=0.4+0.2x, z=0.8-0.2x), kh<=0.625, Sommerfeld, source (0.5,0.5,0.1), "
                      "complex128, CSLP(1, 0.5i-damped) V(1,1) omega=0.8, Bi-CGSTAB tol 1e-6 "
                      "(r~=b), fixed budget of 100 iterations per step"),
-        "iters": 100, "fixed": True, "cpu_iters": 2,
+        "iters": 100, "fixed": True, "cpu_iters": 1,
     },
     "c1": {
         "workload": ("configs[1]: 129^3 unit cube, k=80 (kh=0.625), Sommerfeld, centre point "
@@ -581,7 +581,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    # CPU legs: Bi-CGSTAB iterations per sample (default: 2 at 513^3, the full solve at 129^3)
+    # CPU legs: Bi-CGSTAB iterations per sample (default: 1 at 513^3, ~5 s on 16 cores;
+    # the full solve at 129^3)
     ap.add_argument("--cpu-iters", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-tts", action="store_true", help="skip the secondary solves in config")

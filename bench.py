@@ -586,7 +586,15 @@ def main():
     ap.add_argument("--cpu-iters", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-tts", action="store_true", help="skip the secondary solves in config")
+    ap.add_argument("--no-table", action="store_true", help="skip the per-kernel table (A/B runs)")
+    ap.add_argument("--opt", action="append", default=[], metavar="NAME=0|1",
+                    help="kernel-variant option of the library (hf_set_option), for A/B runs")
     args = ap.parse_args()
+    if args.opt and args.impl == "native":
+        from paper_2308_06085_b200 import _native
+        for kv in args.opt:
+            name, _, val = kv.partition("=")
+            _native.set_option(name, int(val or 1))
     _, world, _ = _env_rank()
     if args.gpus != world and args.impl == "native":
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch N>1 with torchrun")

@@ -54,6 +54,7 @@ struct Lvl {
     // (4 entries per index) -- 1 byte of k traffic per vertex instead of 8, no
     // D^-1 field and no reciprocal
     const unsigned char *kidx;   // at owned plane 0 (ghost planes valid), or null
+    int npal;                    // palette entries in use
     const double *kpal;
     const double2 *apal, *dpal;
 };
@@ -184,7 +185,8 @@ __device__ __forceinline__ cd warp_sum(cd v) {
 }
 
 // Block-wide deterministic sum of ND complex accumulators; result valid in
-// thread 0.  Requires blockDim.x*blockDim.y*blockDim.z == HF_RED_THREADS.
+// thread 0.  The first HF_RED_THREADS threads of the block contribute (a block
+// may carry extra warps, e.g. a producer warp, whose values are ignored).
 template <int ND>
 __device__ __forceinline__ void block_sum(cd (&acc)[ND], cd (&out)[ND]) {
     __shared__ cd sm[ND][HF_RED_THREADS / 32];
@@ -193,7 +195,7 @@ __device__ __forceinline__ void block_sum(cd (&acc)[ND], cd (&out)[ND]) {
 #pragma unroll
     for (int d = 0; d < ND; d++) {
         cd v = warp_sum(acc[d]);
-        if (lane == 0) sm[d][w] = v;
+        if (lane == 0 && w < HF_RED_THREADS / 32) sm[d][w] = v;
     }
     __syncthreads();
     if (tid == 0) {
@@ -207,7 +209,7 @@ __device__ __forceinline__ void block_sum(cd (&acc)[ND], cd (&out)[ND]) {
     __syncthreads();
 }
 
-__device__ void bcg_finalize(BcgState *st, int op, const cd *sums);
+__device__ inline void bcg_finalize(BcgState *st, int op, const cd *sums);   // hf_stencil.cuh
 
 // Write this block's partials; the last block to arrive reduces all partials in
 // fixed block order and runs the finalize step.
@@ -233,7 +235,7 @@ __device__ __forceinline__ void reduce_finish(cd (&acc)[ND], const RedSlot &rs) 
 #pragma unroll
     for (int d = 0; d < ND; d++) a2[d] = mk(0, 0);
     // four independent loads in flight per thread (fixed order => deterministic)
-    unsigned b = tid;
+    unsigned b = tid < HF_RED_THREADS ? tid : nblk;
     for (; b + 3 * HF_RED_THREADS < nblk; b += 4 * HF_RED_THREADS) {
         cd p[4][ND];
 #pragma unroll

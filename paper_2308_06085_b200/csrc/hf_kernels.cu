@@ -18,96 +18,11 @@
 #include <cstdlib>
 
 #include "hf_kernels.cuh"
+#include "hf_stencil.cuh"
 
 namespace hf {
 
 int g_opt[OPT_COUNT] = {};
-
-// ---------------------------------------------------------------------------
-// Bi-CGSTAB scalar state machine (krylov.py:234-273), run by one thread.
-// ---------------------------------------------------------------------------
-__device__ static void bcg_record(BcgState *st, double relres) {
-    if (st->hist && st->iter < st->hist_cap) st->hist[st->iter] = relres;
-    st->iter += 1;
-    st->relres = relres;
-}
-
-__device__ static void bcg_step(BcgState *st, int op, const cd *sums);
-__device__ void bcg_finalize(BcgState *st, int op, const cd *sums) { bcg_step(st, op, sums); }
-
-__device__ static void bcg_step(BcgState *st, int op, const cd *sums) {
-    switch (op) {
-    case FIN_BCG_INIT: {            // krylov.py:217-232
-        double bb = sums[0].x;
-        st->bnorm = sqrt(bb > 0.0 ? bb : 0.0);
-        st->rho = st->alpha = st->omega = mk(1.0, 0.0);
-        st->iter = 0; st->matvecs = 0; st->breakdown = 0; st->s_conv = 0;
-        st->converged = 0; st->done = 0;
-        if (st->bnorm == 0.0) { st->converged = 1; st->done = 1; st->relres = 0.0; return; }
-        st->relres = st->bnorm / st->bnorm;
-        if (st->relres <= st->tol) { st->converged = 1; st->done = 1; return; }
-        if (st->iter >= st->maxit) { st->done = 1; return; }
-        st->rho_new = sums[1];
-        if (cabsd(st->rho_new) < st->btol) { st->breakdown = HF_BREAKDOWN_RHO; st->done = 1; return; }
-        st->beta = cmul(cdiv(st->rho_new, st->rho), cdiv(st->alpha, st->omega));
-        return;
-    }
-    case FIN_BCG_ALPHA: {           // krylov.py:242-247
-        st->matvecs += 1;
-        cd den = sums[0];
-        if (cabsd(den) < st->btol) { st->breakdown = HF_BREAKDOWN_RHO; st->done = 1; return; }
-        st->alpha = cdiv(st->rho_new, den);
-        return;
-    }
-    case FIN_BCG_S: {               // krylov.py:248-255
-        double ss = sums[0].x;
-        double snorm = sqrt(ss > 0.0 ? ss : 0.0);
-        if (snorm / st->bnorm <= st->tol) {
-            bcg_record(st, snorm / st->bnorm);
-            st->s_conv = 1; st->converged = 1; st->done = 1;
-        }
-        return;
-    }
-    case FIN_BCG_OMEGA: {           // krylov.py:257-265
-        st->matvecs += 1;
-        cd tt = sums[0], ts = sums[1];
-        if (cabsd(tt) < st->btol) { st->breakdown = HF_BREAKDOWN_OMEGA; st->done = 1; return; }
-        st->omega = cdiv(ts, tt);
-        if (cabsd(st->omega) < st->btol) { st->breakdown = HF_BREAKDOWN_OMEGA; st->done = 1; return; }
-        return;
-    }
-    case FIN_BCG_RHO: {             // krylov.py:266-273, then the loop head 234-239
-        st->rho = st->rho_new;
-        double rr = sums[0].x;
-        double relres = sqrt(rr > 0.0 ? rr : 0.0) / st->bnorm;
-        bcg_record(st, relres);
-        if (relres <= st->tol) { st->converged = 1; st->done = 1; return; }
-        if (st->iter >= st->maxit) { st->done = 1; return; }
-        st->rho_new = sums[1];
-        if (cabsd(st->rho_new) < st->btol) { st->breakdown = HF_BREAKDOWN_RHO; st->done = 1; return; }
-        st->beta = cmul(cdiv(st->rho_new, st->rho), cdiv(st->alpha, st->omega));
-        return;
-    }
-    default:
-        return;
-    }
-}
-
-// Programmatic dependent launch: every kernel is launched with the
-// programmatic-stream-serialization attribute.  On entry a CTA waits for the
-// previous grid to complete (its writes are then visible) and immediately
-// signals that the next grid may launch: that happens once every CTA of this
-// grid is resident, so the next kernel's CTAs fill SMs as this grid's last
-// wave drains and start the moment it completes.  Waiting before anything
-// else keeps the chain transitive (no grid can finish before its predecessor).
-__device__ __forceinline__ void pdl_enter() {
-    asm volatile("griddepcontrol.wait;\n" ::: "memory");
-    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-}
-__device__ __forceinline__ bool is_done(const int *done) {
-    pdl_enter();
-    return done && *(volatile const int *)done;
-}
 
 // ---------------------------------------------------------------------------
 // marching stencil kernels
@@ -214,45 +129,6 @@ __device__ __forceinline__ void cp_async8s(unsigned saddr, const void *gmem, boo
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
-// epilogues: epi(q, f_centre, (M f)_centre, w D^-1 at the centre, staged operand, acc)
-// v = M f (+ inner products), DOT: 0 none, 1 conj(w) v, 2 conj(v) v & conj(v) w
-template <int DOT>
-struct EpiApply {
-    cd *v;
-    static constexpr bool kAux = DOT > 0;   // w
-    static constexpr bool kDinv = false;
-    __device__ __forceinline__ void operator()(long long q, cd, cd mf, cd, cd aux,
-                                               cd (&acc)[2]) const {
-        v[q] = mf;
-        if (DOT == 1) acc[0] = cadd(acc[0], cjmul(aux, mf));
-        if (DOT == 2) {
-            acc[0] = cadd(acc[0], cjmul(mf, mf));
-            acc[1] = cadd(acc[1], cjmul(mf, aux));
-        }
-    }
-};
-
-// r = b - M f (residual; with MODE_PRE the fused pre-smooth + residual)
-struct EpiResid {
-    cd *r;
-    static constexpr bool kAux = true;      // b
-    static constexpr bool kDinv = false;
-    __device__ __forceinline__ void operator()(long long q, cd, cd mf, cd, cd b, cd (&)[2]) const {
-        r[q] = csub(b, mf);
-    }
-};
-
-// u = f + w D^-1 (b - M f) (one damped Jacobi sweep, multigrid.py:153-156)
-struct EpiJacobi {
-    cd *u;
-    static constexpr bool kAux = true;      // b
-    static constexpr bool kDinv = true;
-    __device__ __forceinline__ void operator()(long long q, cd fc, cd mf, cd wd, cd b,
-                                               cd (&)[2]) const {
-        u[q] = cadd(fc, cmul(wd, csub(b, mf)));
-    }
-};
 
 template <int MODE, bool KVAR, bool AUX>
 struct StencilSmem {
@@ -657,34 +533,6 @@ __global__ void __launch_bounds__(NT) k_stencil(Lvl L, const cd *__restrict__ sr
 #define FS_PTS 512
 #define FS_RING 5
 #define FS_MAX_N3 256
-
-__device__ __forceinline__ unsigned smem_u32(const void *p) {
-    return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(bar),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(unsigned dst, const void *src, unsigned bytes, unsigned bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
-        "l"(src), "r"(bytes), "r"(bar)
-        : "memory");
-}
 
 // slot geometry of one block: window [w0, w0 + FS_PTS + 2 (n3 + 1)) of the plane
 __host__ __device__ __forceinline__ int fs_window(int n3) { return FS_PTS + 2 * (n3 + 1); }
@@ -2241,24 +2089,6 @@ __global__ void k_zero(long long n, cd *__restrict__ y) {
 // ---------------------------------------------------------------------------
 // host launchers
 // ---------------------------------------------------------------------------
-// every launch carries the programmatic-stream-serialization attribute (PDL)
-template <class... KArgs, class... Args>
-static void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
-                   Args &&...args) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = grid;
-    cfg.blockDim = block;
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    const bool pdl = !opt(OPT_NO_PDL);
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = pdl ? 1 : 0;
-    cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
-}
-
 static dim3 march_grid(const Lvl &L, int &chunk) {
     int gx = (L.n3 + MARCH_BX - 1) / MARCH_BX;
     int gy = (L.n2 + MARCH_BY - 1) / MARCH_BY;
@@ -2349,10 +2179,26 @@ static void flat_attr() {
     cudaFuncSetAttribute(k_flat_stencil<MODE, Epi, ND, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
 }
 
+// kind code of the wide-plane family (hf_wide.cu) for a (MODE, epilogue) pair
+template <int MODE, class Epi> struct WideKind { static constexpr int value = -1; };
+template <> struct WideKind<MODE_LOAD, EpiApply<0>> { static constexpr int value = 0; };
+template <> struct WideKind<MODE_LOAD, EpiApply<1>> { static constexpr int value = 1; };
+template <> struct WideKind<MODE_LOAD, EpiApply<2>> { static constexpr int value = 2; };
+template <> struct WideKind<MODE_LOAD, EpiResid> { static constexpr int value = 3; };
+template <> struct WideKind<MODE_LOAD, EpiJacobi> { static constexpr int value = 4; };
+template <> struct WideKind<MODE_PRE, EpiResid> { static constexpr int value = 5; };
+template <int D> static cd *epi_out(const EpiApply<D> &e) { return e.v; }
+static cd *epi_out(const EpiResid &e) { return e.r; }
+static cd *epi_out(const EpiJacobi &e) { return e.u; }
+
 template <int MODE, class Epi, int ND>
 static void stencil(const Lvl &L, const cd *src, const cd *aux, double omega, const Epi &e,
                     const RedSlot &rs, cudaStream_t s, const int *done,
                     const UpArgs &up = UpArgs{}) {
+    if (WideKind<MODE, Epi>::value >= 0 && wide_ok(L, WideKind<MODE, Epi>::value)) {
+        launch_wide(WideKind<MODE, Epi>::value, L, src, aux, epi_out(e), omega, rs, s, done);
+        return;
+    }
     if ((MODE == MODE_LOAD || MODE == MODE_PRE) &&
         flat_stencil<MODE == MODE_PRE ? MODE_PRE : MODE_LOAD, Epi, ND>(L, src, aux, omega, e, rs, s, done))
         return;
@@ -2419,7 +2265,7 @@ int tile_blocks(const Lvl &L) {
     int chunk;
     dim3 g = tile_grid(L, chunk);
     const int gx = (int)((L.plane + FS_PTS - 1) / FS_PTS);   // k_flat_stencil grid (flat_launch_t)
-    return std::max<int>(g.x * g.y * g.z, gx * L.nx);
+    return std::max<int>(std::max<int>(g.x * g.y * g.z, gx * L.nx), wide_blocks(L));
 }
 
 void launch_apply(const Lvl &L, const cd *u, cd *v, cudaStream_t s, const int *done) {
@@ -2572,6 +2418,12 @@ int launch_up1(const Lvl &L, const Lvl &C, const cd *b, const cd *e, cd *u, cd *
     // correction + Jacobi sweep as the split pair unless fuse_up is requested: the
     // tiled MODE_UP kernel measured slower than k_corr_flat + the sweep on the wide
     // 513^3 wedge levels too (3.40 vs 1.07 + 1.63 ms, profiles/r02_kernel_table_513w.json)
+    // wide whole-grid levels: the wide family's fused up-sweep (hf_wide.cu)
+    if (!opt(OPT_NO_FUSE) && !opt(OPT_NO_WIDE_UP) && !opt(OPT_FUSE_UP) && wide_ok(L, 6) && L.lo1 == 0 &&
+        L.nx == L.n1 && C.lo1 == 0 && C.nx == C.n1) {
+        launch_wide_up(L, C, b, e, u, omega, pre, s, done);
+        return 1;
+    }
     const bool split = opt(OPT_NO_FUSE) || !opt(OPT_FUSE_UP);
     if (!split && L.lo1 == 0 && L.nx == L.n1 && C.lo1 == 0 && C.nx == C.n1) {
         stencil<MODE_UP, EpiJacobi, 0>(L, b, b, omega, EpiJacobi{u}, RedSlot{}, s, done,

@@ -6,12 +6,21 @@ namespace hf {
 
 // kernel-variant options (hf_set_option in the C ABI); all off = the default
 enum HfOpt { OPT_NO_PDL = 0, OPT_NO_FLAT, OPT_NO_FLAT_DR, OPT_NO_DR, OPT_TILED_DR, OPT_FLAT_UP,
-             OPT_FUSE_UP, OPT_NO_FUSE, OPT_COARSEST_DENSE, OPT_NO_PALETTE, OPT_COUNT };
+             OPT_FUSE_UP, OPT_NO_FUSE, OPT_COARSEST_DENSE, OPT_NO_PALETTE, OPT_NO_WIDE, OPT_FORCE_WIDE,
+             OPT_WIDE_P4, OPT_WIDE_ALL, OPT_NO_WIDE_UP, OPT_COUNT };
 extern int g_opt[OPT_COUNT];
 inline bool opt(int o) { return g_opt[o] != 0; }
 
 int march_blocks(const Lvl &L);
 int tile_blocks(const Lvl &L);
+// wide-plane sweeps (hf_wide.cu): kind 0 apply, 1 apply + conj(w) v, 2 apply + v^H v & v^H w,
+// 3 residual, 4 Jacobi sweep, 5 zero-guess pre-smoothing + residual
+bool wide_ok(const Lvl &L, int kind);
+int wide_blocks(const Lvl &L);
+void launch_wide_up(const Lvl &L, const Lvl &C, const cd *b, const cd *e, cd *u, double omega,
+                    bool pre, cudaStream_t s, const int *done);
+void launch_wide(int kind, const Lvl &L, const cd *src, const cd *aux, cd *out, double omega,
+                 const RedSlot &rs, cudaStream_t s, const int *done);
 void init_kernel_attributes();
 void launch_apply(const Lvl &L, const cd *u, cd *v, cudaStream_t s, const int *done);
 void launch_apply_dot1(const Lvl &L, const cd *u, cd *v, const cd *w, const RedSlot &rs,

@@ -52,7 +52,7 @@ extern "C" int hf_version(void) { return 2; }
 // the library reads no environment variables.
 static const char *const k_opt_names[OPT_COUNT] = {
     "no_pdl", "no_flat", "no_flat_dr", "no_dr", "tiled_dr", "flat_up", "fuse_up", "no_fuse",
-    "coarsest_dense", "no_palette"};
+    "coarsest_dense", "no_palette", "no_wide", "force_wide", "wide_p4", "wide_all", "no_wide_up"};
 extern "C" int hf_set_option(const char *name, int value) {
     if (!name) return fail(HF_ERR_ARG, "null option name");
     for (int i = 0; i < OPT_COUNT; i++)
@@ -190,8 +190,8 @@ static int make_level(Allocs &A, Level &lv, int n1, int n2, int n3, int lo1, int
         CK(cudaMemcpy(dt, tab, sizeof(tab), cudaMemcpyHostToDevice));
         L.tab = dt;
     }
-    L.kidx = nullptr; L.kpal = nullptr; L.apal = nullptr; L.dpal = nullptr;
-    if (kfull && n3 > 256 && !opt(OPT_NO_PALETTE)) {
+    L.kidx = nullptr; L.kpal = nullptr; L.apal = nullptr; L.dpal = nullptr; L.npal = 0;
+    if (kfull && (n3 > 256 || opt(OPT_FORCE_WIDE)) && !opt(OPT_NO_PALETTE)) {
         // wide level (tiled kernels): a medium with <= 256 distinct wavenumbers over
         // this slab and its ghost planes is stored as 8-bit palette indices
         const int g0 = std::max(0, lo1 - HF_GHOST), g1 = std::min(n1, lo1 + nx + HF_GHOST);
@@ -231,6 +231,7 @@ static int make_level(Allocs &A, Level &lv, int n1, int n2, int n3, int lo1, int
             launch_palette(L, (int)pal.size(), ap, dp, nullptr);
             CK(cudaDeviceSynchronize());
             L.kidx = kb8 + (size_t)HF_GHOST * L.plane;
+            L.npal = (int)pal.size();
             L.apal = ap;
             L.dpal = dp;
         }

@@ -11,6 +11,9 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 from paper_2308_06085_b200 import _native, problems  # noqa: E402
 
+for kv in os.environ.get("HF_PROF_OPTS", "").split(","):       # e.g. HF_PROF_OPTS=wide_p2=1,no_wide=0
+    if "=" in kv:
+        _native.set_option(kv.split("=")[0], int(kv.split("=")[1]))
 p = problems.wedge3_problem(int(os.environ.get("PROF_N", 513)))
 spec, b = problems.build_problem(p)
 A, H, S = bench._solver_for(p, spec)

@@ -11,6 +11,11 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 from paper_2308_06085_b200.krylov import SolverConfig  # noqa: E402
 
+from paper_2308_06085_b200 import _native  # noqa: E402
+
+for kv in os.environ.get("HF_PROF_OPTS", "").split(","):       # e.g. HF_PROF_OPTS=no_wide=1
+    if "=" in kv:
+        _native.set_option(kv.split("=")[0], int(kv.split("=")[1]))
 cfgname = os.environ.get("PROF_CONFIG", "c2")
 p, spec, b = bench._problem(cfgname)
 A, hier, S = bench._solver_for(p, spec)

@@ -458,31 +458,41 @@ def kernel_table(A, hier, solver, n, t_iter_ms, reps=12, sparse_shadow=True):
     xc, rc = rnd(hier.coarsest.grid.shape), rnd(hier.coarsest.grid.shape)
     p = lambda x: x.data_ptr()
     fused_down = shape[2] <= 255
+    wide = not fused_down and not L.hf_get_option(b"no_wide")
+    wide_all = wide and bool(L.hf_get_option(b"wide_all"))
+    wide_up = wide and not L.hf_get_option(b"no_wide_up") and not L.hf_get_option(b"no_fuse")
+    sweep = "k_flat_stencil" if fused_down else ("k_wide" if wide_all else "k_stencil")
     cases = {
         "device_copy": (lambda s: s["v"].copy_(s["u"]), 32.0, "ceiling", 0, "torch copy_"),
+        # the first matvec of an iteration (sparse shadow: r~^H v is gathered, no inner-product
+        # pass); the second one carries t^H t and t^H s (matvec_dot2 below)
         "helmholtz_matvec": (lambda s: L.hf_operator_apply(A._h, p(s["u"]), p(s["v"])),
-                             32.0 + kp, "hbm", 2,
-                             "k_flat_stencil<LOAD,EpiApply>" if fused_down else
-                             "k_stencil<LOAD,EpiApply>"),
+                             32.0 + kp, "hbm", 1 if sparse_shadow else 0, "k_wide<LOAD,APPLY0>" if wide else f"{sweep}<LOAD,EpiApply>"),
+        # split up-sweep: on the default path only where the fused up-sweep does not apply
         "prolong_correct": (lambda s: L.hf_level_correct(H, 0, p(s["b"]), p(s["ec"]), p(s["t"])),
-                            32.0 + (1.0 if pal else db) + 16.0 * cr, "hbm", 2, "k_corr_flat<1>"),
+                            32.0 + (1.0 if pal else db) + 16.0 * cr, "hbm", 0 if wide_up else 2,
+                            "k_corr_flat<1>"),
         "jacobi_postsmooth": (lambda s: L.hf_level_smooth(H, 0, p(s["t"]), p(s["b"]), p(s["u"])),
-                              48.0 + kp, "hbm", 2,
-                              "k_flat_stencil<LOAD,EpiJacobi>" if fused_down else
-                              "k_stencil<LOAD,EpiJacobi>"),
+                              48.0 + kp, "hbm", 0 if wide_up else 2, f"{sweep}<LOAD,EpiJacobi>"),
     }
     if fused_down:
         cases["down_restrict"] = (lambda s: L.hf_level_down_restrict(H, 0, p(s["b"]), p(s["bc"])),
                                   16.0 + kb + db + 16.0 * cr, "hbm", 2, "k_flat_dr")
     else:
+        # the wide family's pre-smoothing sweep reads the palette index (1 B), the tiled one k (8 B)
         cases["presmooth_residual"] = (lambda s: L.hf_level_down1(H, 0, p(s["b"]), p(s["v"])),
-                                       32.0 + kb, "hbm", 2, "k_stencil<PRE,EpiResid>")
+                                       32.0 + (kp if wide else kb), "hbm", 2,
+                                       "k_wide<PRE,RESID>" if wide else "k_stencil<PRE,EpiResid>")
         cases["restrict_fw"] = (lambda s: L.hf_restrict_fw(H, 0, p(s["v"]), p(s["bc"])),
                                 16.0 + 16.0 * cr, "hbm", 2, "k_restrict_flat")
-        # the fused alternatives on wide planes (not on the default path: share None)
+        if wide_up:
+            # fused up-sweep: b, palette index / k, coarse e in; u out (t never written)
+            cases["up_fused"] = (lambda s: L.hf_level_up(H, 0, p(s["b"]), p(s["ec"]), p(s["u"])),
+                                 32.0 + kp + 16.0 * cr, "hbm", 2, "k_wide<UP,JACOBI>")
+        # the tiled fused alternatives on wide planes (not on the default path: share None)
         cases["down_restrict_tiled"] = (lambda s: L.hf_level_down_restrict(H, 0, p(s["b"]), p(s["bc"])),
                                         16.0 + kb + 16.0 * cr, "hbm", 0, "k_down_restrict")
-        kp_up = kb       # the fused up-sweep stages the 8-byte k (D^-1 of every staged entry)
+        kp_up = kb       # the tiled fused up-sweep stages the 8-byte k (D^-1 of every staged entry)
 
         def up_fused(s):
             with _native.options(fuse_up=1):
@@ -521,10 +531,12 @@ def kernel_table(A, hier, solver, n, t_iter_ms, reps=12, sparse_shadow=True):
     # source with the reference's r~ = b is sparse (gathered)
     sparse = bool(sparse_shadow)
     for nm, which, bpv in (("bcg_p_update", 0, 64.0), ("bcg_s_update", 1, 48.0),
-                           ("bcg_xr_update", 3 if sparse else 2, 112.0 if sparse else 128.0)):
+                           ("bcg_xr_update", 3 if sparse else 2, 112.0 if sparse else 128.0),
+                           ("matvec_dot2", 4, 48.0 + kp)):
         m = ctypes.c_float()
         _native.check(L.hf_solver_bench_vec(solver._h, which, r, ctypes.byref(m)))
-        put(nm, m.value, bpv, "hbm", 1, ("k_bcg_p", "k_bcg_s", "k_bcg_xr", "k_bcg_xr (sparse r~)")[which])
+        put(nm, m.value, bpv, "hbm", 1 if which != 4 or sparse else 2,
+            ("k_bcg_p", "k_bcg_s", "k_bcg_xr", "k_bcg_xr (sparse r~)", f"{sweep}<LOAD,EpiApply<2>>")[which])
     return out
 
 

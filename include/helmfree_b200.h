@@ -222,8 +222,9 @@ int hf_operator_apply_dot(hf_operator *A, hf_bcg *state, int nd, const double *u
 /* Measurement hook (bench.py): mean device ms of the Bi-CGSTAB vector kernel
  * `which` (0: p update, 1: s update + |s|^2, 2: x, r update + |r|^2, r~^H r,
  * 3: the same with a sparse shadow vector (r~ not streamed); krylov.py:240,
- * 248-249, 266-269) over `reps` launches on the solver's
- * workspace; the device scalar state is not modified. */
+ * 248-249, 266-269; 4: the second matvec of an iteration with its inner
+ * products, t = A s^, t^H t, t^H s, krylov.py:256-258) over `reps` launches
+ * on the solver's workspace; the device scalar state is not modified. */
 int hf_solver_bench_vec(hf_solver *solver, int which, int reps, float *ms);
 int hf_solve(hf_solver *s, const hf_solver_config *cfg, const double *b, double *x,
              hf_report *rep);

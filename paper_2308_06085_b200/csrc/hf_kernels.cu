@@ -1717,6 +1717,18 @@ __global__ void k_bcg_step(BcgState *st, int op, const cd *sums) {
     bcg_finalize(st, op, sums);
 }
 
+// sparse shadow: r~^H g over the (<= HF_NZ_MAX) nonzeros of r~, then the scalar
+// step `op` that consumes it as sums[0] -- the matvec feeding it runs without
+// an inner-product pass (no second operand streamed)
+__global__ void k_bcg_gather(BcgState *st, int op, const cd *__restrict__ g, const int *done) {
+    if (is_done(done)) return;
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    cd sums[HF_MAX_DOTS] = {mk(0, 0), mk(0, 0)};
+    for (int k = 0; k < st->nz; k++)            // fixed ascending order
+        sums[0] = cadd(sums[0], cjmul(st->nzw[k], __ldcg(g + st->nzq[k])));
+    bcg_finalize(st, op, sums);
+}
+
 // x += alpha ph  (convergence at the half step, krylov.py:250-255)
 __global__ void k_bcg_xhalf(long long n, const BcgState *st, cd *__restrict__ x,
                             const cd *__restrict__ ph) {
@@ -2530,6 +2542,9 @@ void launch_bcg_xr(long long n, const BcgState *st, cd *x, const cd *ph, const c
 void launch_nz_scan(long long n, const cd *rs, BcgState *st, cudaStream_t s) {
     launch(k_nz_scan, dim3(VEC_BLOCKS), dim3(256), 0, s, n, rs, st);
     launch(k_nz_finish, dim3(1), dim3(32), 0, s, rs, st);
+}
+void launch_bcg_gather(BcgState *st, int op, const cd *g, cudaStream_t s, const int *done) {
+    launch(k_bcg_gather, dim3(1), dim3(32), 0, s, st, op, g, done);
 }
 void launch_bcg_step(BcgState *st, int op, const cd *sums, cudaStream_t s) {
     launch(k_bcg_step, dim3(1), dim3(32), 0, s, st, op, sums);

@@ -1147,8 +1147,14 @@ static void bcg_iteration(hf_solver *S, cudaStream_t s, bool sparse) {
     long long n = S->n;
     L1(launch_bcg_p(n, S->st, S->r, S->p, S->v, s, done));
     precondition(S->M, S->p, S->ph, s, done);
-    L1(launch_apply_dot1(A, S->ph, S->v, sparse ? nullptr : S->rs,
-                         S->red.slot(FIN_BCG_ALPHA, S->st, sparse ? S->v : nullptr, 0), s, done));
+    if (sparse) {
+        // r~^H v = conj(r~_s) v_s over the few nonzeros of r~: a plain matvec, then a
+        // one-thread gather + scalar step (same value as the last-block gather)
+        L1(launch_apply(A, S->ph, S->v, s, done));
+        L1(launch_bcg_gather(S->st, FIN_BCG_ALPHA, S->v, s, done));
+    } else {
+        L1(launch_apply_dot1(A, S->ph, S->v, S->rs, S->red.slot(FIN_BCG_ALPHA, S->st), s, done));
+    }
     L1(launch_bcg_s(n, S->st, S->r, S->v, S->s, S->red.slot(FIN_BCG_S, S->st), s, done));
     precondition(S->M, S->s, S->sh, s, done);
     L1(launch_apply_dot2(A, S->sh, S->t, S->s, S->red.slot(FIN_BCG_OMEGA, S->st), s, done));
@@ -1695,12 +1701,14 @@ extern "C" int hf_operator_apply_dot(hf_operator *op, hf_bcg *B, int nd, const d
 // solver's workspace, inner products into a scratch slot (the device scalar
 // state is not touched).  Mean device time per launch in *ms.
 extern "C" int hf_solver_bench_vec(hf_solver *S, int which, int reps, float *ms) {
-    if (!S || reps < 1 || !ms || which < 0 || which > 3) return fail(HF_ERR_ARG, "bad bench request");
+    if (!S || reps < 1 || !ms || which < 0 || which > 4) return fail(HF_ERR_ARG, "bad bench request");
     cudaStream_t s = work_stream();
     const RedSlot scratch = S->red.slot(FIN_STORE, nullptr);
     auto one = [&]() {
         if (which == 0) launch_bcg_p(S->n, S->st, S->r, S->p, S->v, s, nullptr);
         else if (which == 1) launch_bcg_s(S->n, S->st, S->r, S->v, S->s, scratch, s, nullptr);
+        else if (which == 4)   // the second matvec of an iteration: t = A s^ with t^H t, t^H s
+            launch_apply_dot2(S->Aop->lv.L, S->sh, S->t, S->s, scratch, s, nullptr);
         else   // 3: the sparse-shadow variant (r~^H r gathered, r~ not streamed)
             launch_bcg_xr(S->n, S->st, S->x, S->ph, S->sh, S->s, S->t, S->r, which == 2 ? S->rs : nullptr,
                           scratch, s, nullptr);

@@ -58,8 +58,11 @@ enum { KV_CONST = 0, KV_FIELD = 1, KV_PAL = 2 };
 
 constexpr int WX = 32;            // tile width (i3): one warp row
 constexpr int WRS = WX + 2;       // staged entries per tile row
-constexpr int WNC = 256;          // consumer threads
-constexpr int WNT = WNC + 32;     // + the producer warp
+// consumer warps of a block: 8 for the plain sweeps (9 warps, 3 blocks per SM at 72
+// registers); 7 for the in-slot transform modes -- registers are allocated per SM
+// sub-partition (16 K each), two 8-warp blocks put 4 warps on each (128 registers, no
+// spills), two 9-warp blocks up to 5 (96)
+__host__ __device__ constexpr int wide_ncw(int mode) { return mode == 0 ? 8 : 7; }
 constexpr int WRING = 4;
 constexpr int WPAL = 16;          // palette entries held in shared memory (else the k field is used)
 constexpr int WUP_CHUNK = 32;     // fine planes per block of the fused up-sweep
@@ -73,9 +76,9 @@ struct WideUp {          // WIDE_UP: the coarse level and its correction
     int pre;             // 1: t = w D^-1 b + P e (nu1 = 1), 0: t = P e (nu1 = 0)
 };
 
-template <int P, bool AUX, bool UP = false>
+template <int P, bool AUX, bool UP = false, int NCW = 8>
 struct WideTile {
-    static constexpr int WY = 8 * P;              // tile height (i2)
+    static constexpr int WY = NCW * P;            // tile height (i2)
     static constexpr int ROWS = WY + 2;
     static constexpr int ENT = ROWS * WRS;        // stencil operand entries of a slot
     static constexpr int AENT = AUX ? WY * WX : 0;   // centre-only operand entries
@@ -96,12 +99,16 @@ struct WidePlane {       // register set of one plane of a thread's strip
 };
 
 template <int MODE, int EPI, int KV, bool SOMM, int P>
-__global__ void __launch_bounds__(WNT, (P >= 4 || MODE != WIDE_LOAD ? 2 : 3))
+// registers are allocated per SM sub-partition (16 K each): 3 blocks of 9 warps put up to
+// 7 warps on one (72 registers), 2 blocks up to 5 (96) -- the in-slot transform modes and
+// the 4-row strips take 2 blocks
+__global__ void __launch_bounds__(32 * (wide_ncw(MODE) + 1), (P >= 4 || MODE != WIDE_LOAD ? 2 : 3))
 k_wide(Lvl L, const cd *__restrict__ src, const cd *__restrict__ aux, cd *__restrict__ out,
        double omega, int chunk, RedSlot rs, WideUp up, const int *done) {
     constexpr bool kAux = EPI != WE_APPLY0 && MODE == WIDE_LOAD;   // staged centre-only operand
     constexpr bool kXf = MODE != WIDE_LOAD;                        // entries transformed in the slot
-    using T = WideTile<P, kAux, MODE == WIDE_UP>;
+    constexpr int NCW = wide_ncw(MODE), WNC = 32 * NCW;
+    using T = WideTile<P, kAux, MODE == WIDE_UP, NCW>;
     constexpr int ND = EPI == WE_APPLY1 ? 1 : (EPI == WE_APPLY2 ? 2 : 0);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ __align__(8) unsigned long long bars[3 * WRING + 1];
@@ -353,8 +360,18 @@ k_wide(Lvl L, const cd *__restrict__ src, const cd *__restrict__ aux, cd *__rest
 
         // transform of plane p (WIDE_PRE): own centres -> fo[] = D^-1 b (stored when
         // `ring`), bo[] = b; the thread's ring entry
+        // WIDE_UP: P e at the thread's centres and ring entry of plane p -- needs the coarse
+        // tile only, so it is issued ahead of the wait for the plane itself
+        auto prolong_all = [&](int p, cd (&pe)[P], cd &peh, bool ring) {
+            if (MODE == WIDE_UP) {
+#pragma unroll
+                for (int r = 0; r < P; r++) pe[r] = prolong(p, eo[r], (js + r) & 1, opar3);
+                if (ring && he_ok) peh = prolong(p, he_eo, he_par & 2, he_par & 1);
+            }
+        };
         auto transform = [&](int p, cd (&fo)[P], cd (&bo)[P], const double (&kk)[P],
-                             const int (&ii)[P], double hk, int hi, bool ring) {
+                             const int (&ii)[P], double hk, int hi, const cd (&pe)[P], cd peh,
+                             bool ring) {
             cd *sl = slot(p);
             const int nbx = nbx_of(p);
             if (MODE == WIDE_UP) {
@@ -362,13 +379,13 @@ k_wide(Lvl L, const cd *__restrict__ src, const cd *__restrict__ aux, cd *__rest
 #pragma unroll
                 for (int r = 0; r < P; r++) {
                     bo[r] = sl[cf0 + r * WRS];
-                    cd t = prolong(p, eo[r], (js + r) & 1, opar3);
+                    cd t = pe[r];
                     if (up.pre) t = cadd(cmul(bo[r], dfac(kk[r], ii[r], nbx + ((nbs >> (2 * r)) & 3))), t);
                     fo[r] = t;
                     if (ring && r < nrow) sl[cf0 + r * WRS] = t;
                 }
                 if (ring && he_ok) {
-                    cd t = prolong(p, he_eo, he_par & 2, he_par & 1);
+                    cd t = peh;
                     if (up.pre) t = cadd(cmul(sl[he_off], dfac(hk, hi, nbx + he_nb)), t);
                     sl[he_off] = t;
                 }
@@ -412,12 +429,17 @@ k_wide(Lvl L, const cd *__restrict__ src, const cd *__restrict__ aux, cd *__rest
             int hi0 = 0;
             load_hk(i0, hk0, hi0);
             load_hk(i0 + 1, hk_n, hi_n);
+            cd pe[P], peh = mk(0, 0);
+#pragma unroll
+            for (int r = 0; r < P; r++) pe[r] = mk(0, 0);
+            prolong_all(i0 - 1, pe, peh, false);
             wait_bar(b_full, i0 - 1);
-            transform(i0 - 1, S0.f, bn, kp, ip, 0.0, 0, false);
+            transform(i0 - 1, S0.f, bn, kp, ip, 0.0, 0, pe, peh, false);
             arrive_bar(b_xf, i0 - 1);        // (keeps the slot's xf phase in step with its uses)
             arrive_bar(b_empty, i0 - 1);
+            prolong_all(i0, pe, peh, true);
             wait_bar(b_full, i0);
-            transform(i0, S1.f, bc, kc, ic, hk0, hi0, true);
+            transform(i0, S1.f, bc, kc, ic, hk0, hi0, pe, peh, true);
             arrive_bar(b_xf, i0);
         } else {
             load_k(i0, kc, ic);
@@ -444,31 +466,48 @@ k_wide(Lvl L, const cd *__restrict__ src, const cd *__restrict__ aux, cd *__rest
             } else if (i + 1 < i1) {
                 load_k(i + 1, kn, in_);
             }
-            wait_bar(b_full, i + 1);
+            const cd *s0 = slot(i);
+            const int nbx = nbx_of(i);
+            cd nsum[P];                      // (ym + yp) + (zm + zp) of plane i
+            auto inplane = [&]() {
+                const cd yup = s0[cf0 - WRS], ydn = s0[cf0 + P * WRS];
+                cd ylast = ydn;
+                // (the row below the last active row of a partial strip is a ring entry)
+                if (kXf && nrow > 0 && nrow < P) ylast = s0[cf0 + nrow * WRS];
+#pragma unroll
+                for (int r = 0; r < P; r++) {
+                    const cd zm = s0[cf0 + r * WRS - 1], zp = s0[cf0 + r * WRS + 1];
+                    const cd ym = r == 0 ? yup : Cc.f[r > 0 ? r - 1 : 0];
+                    cd yp = r == P - 1 ? ydn : Cc.f[r < P - 1 ? r + 1 : 0];
+                    if (kXf && r < P - 1 && r == nrow - 1) yp = ylast;
+                    nsum[r] = cadd(cadd(ym, yp), cadd(zm, zp));
+                }
+            };
             if (kXf) {
-                transform(i + 1, Nx.f, bn, kn, in_, hk_n, hi_n, true);
+                cd pe[P], peh = mk(0, 0);
+#pragma unroll
+                for (int r = 0; r < P; r++) pe[r] = mk(0, 0);
+                prolong_all(i + 1, pe, peh, true);
+                wait_bar(b_full, i + 1);
+                transform(i + 1, Nx.f, bn, kn, in_, hk_n, hi_n, pe, peh, true);
                 arrive_bar(b_xf, i + 1);
-                wait_bar(b_xf, i);           // every warp's entries of plane i are in place
+                // every warp's entries of plane i are in place (signalled one step ago: a
+                // warp waits here only when it runs a whole step ahead of the slowest one;
+                // waiting BEFORE the transform measured 50 % slower)
+                wait_bar(b_xf, i);
+                inplane();
             } else {
+                wait_bar(b_full, i + 1);
                 const cd *sn = slot(i + 1);
 #pragma unroll
                 for (int r = 0; r < P; r++) Nx.f[r] = sn[cf0 + r * WRS];
+                inplane();
             }
-            const cd *s0 = slot(i);
-            const int nbx = nbx_of(i);
-            const cd yup = s0[cf0 - WRS], ydn = s0[cf0 + P * WRS];
-            cd ylast = ydn;
-            // (the row below the last active row of a partial strip is a ring entry)
-            if (kXf && nrow > 0 && nrow < P) ylast = s0[cf0 + nrow * WRS];
 #pragma unroll
             for (int r = 0; r < P; r++) {
                 const cd fc = Cc.f[r];
-                const cd zm = s0[cf0 + r * WRS - 1], zp = s0[cf0 + r * WRS + 1];
                 const cd av = kXf ? bc[r] : (kAux ? s0[af0 + r * WX] : mk(0, 0));
-                const cd ym = r == 0 ? yup : Cc.f[r > 0 ? r - 1 : 0];
-                cd yp = r == P - 1 ? ydn : Cc.f[r < P - 1 ? r + 1 : 0];
-                if (kXf && r < P - 1 && r == nrow - 1) yp = ylast;
-                const cd sum = cadd(cadd(cadd(Pm.f[r], Nx.f[r]), cadd(ym, yp)), cadd(zm, zp));
+                const cd sum = cadd(cadd(Pm.f[r], Nx.f[r]), nsum[r]);
                 const int nb = nbx + ((nbs >> (2 * r)) & 3);
                 cd ap;
                 if (KV == KV_CONST) ap = tab[nb];
@@ -543,9 +582,9 @@ k_wide(Lvl L, const cd *__restrict__ src, const cd *__restrict__ aux, cd *__rest
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
-template <int P>
+template <int P, int NCW = 8>
 static dim3 wide_grid(const Lvl &L, int &chunk) {
-    using T = WideTile<P, false>;
+    using T = WideTile<P, false, false, NCW>;
     const int gx = (L.n3 + WX - 1) / WX, gy = (L.n2 + T::WY - 1) / T::WY;
     // several short waves (sliver tiles at the 2^k + 1 edges finish early and the
     // block scheduler back-fills); every chunk re-reads two planes
@@ -561,7 +600,8 @@ template <int MODE, int EPI, int KV, bool SOMM, int P>
 static void wide_launch_t(const Lvl &L, const cd *src, const cd *aux, cd *out, double omega,
                           const RedSlot &rs, cudaStream_t s, const int *done,
                           const WideUp &up = WideUp{}) {
-    constexpr size_t smem = WideTile<P, EPI != WE_APPLY0 && MODE == WIDE_LOAD, MODE == WIDE_UP>::smem;
+    constexpr int NCW = wide_ncw(MODE);
+    constexpr size_t smem = WideTile<P, EPI != WE_APPLY0 && MODE == WIDE_LOAD, MODE == WIDE_UP, NCW>::smem;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_wide<MODE, EPI, KV, SOMM, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -569,12 +609,12 @@ static void wide_launch_t(const Lvl &L, const cd *src, const cd *aux, cd *out, d
         attr = true;
     }
     int chunk;
-    dim3 g = wide_grid<P>(L, chunk);
+    dim3 g = wide_grid<P, NCW>(L, chunk);
     if (MODE == WIDE_UP) {               // the staged coarse tile covers WUP_CHUNK fine planes
         chunk = std::min(L.nx, WUP_CHUNK);
         g.z = (L.nx + chunk - 1) / chunk;
     }
-    launch(k_wide<MODE, EPI, KV, SOMM, P>, g, dim3(WNT), smem, s, L, src, aux ? aux : src, out, omega,
+    launch(k_wide<MODE, EPI, KV, SOMM, P>, g, dim3(32 * (NCW + 1)), smem, s, L, src, aux ? aux : src, out, omega,
            chunk, rs, up, done);
 }
 
@@ -634,8 +674,8 @@ void launch_wide_up(const Lvl &L, const Lvl &C, const cd *b, const cd *e, cd *u,
 
 int wide_blocks(const Lvl &L) {
     int c2, c4;
-    const dim3 a = wide_grid<2>(L, c2), b = wide_grid<4>(L, c4);
-    return (int)std::max(a.x * a.y * a.z, b.x * b.y * b.z);
+    const dim3 a = wide_grid<2>(L, c2), b = wide_grid<4>(L, c4), c = wide_grid<2, 7>(L, c2);
+    return (int)std::max(std::max(a.x * a.y * a.z, b.x * b.y * b.z), c.x * c.y * c.z);
 }
 
 }  // namespace hf

@@ -28,6 +28,7 @@ for _ in range(2):
     _native.check(L.hf_level_smooth(H._h, 0, t.data_ptr(), bb.data_ptr(), u.data_ptr()))
     _native.check(L.hf_level_correct(H._h, 0, bb.data_ptr(), ec.data_ptr(), t.data_ptr()))
     _native.check(L.hf_restrict_fw(H._h, 0, u.data_ptr(), bc.data_ptr()))
+    _native.check(L.hf_level_up(H._h, 0, bb.data_ptr(), ec.data_ptr(), u.data_ptr()))
     for w in (1, 2):
         _native.check(L.hf_solver_bench_vec(S._h, w, 1, ctypes.byref(ms)))
     _native.check(L.hf_solver_bench_vec(S._h, 3, 1, ctypes.byref(ms)))

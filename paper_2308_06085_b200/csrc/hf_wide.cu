@@ -111,7 +111,7 @@ k_wide(Lvl L, const cd *__restrict__ src, const cd *__restrict__ aux, cd *__rest
     using T = WideTile<P, kAux, MODE == WIDE_UP, NCW>;
     constexpr int ND = EPI == WE_APPLY1 ? 1 : (EPI == WE_APPLY2 ? 2 : 0);
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ __align__(8) unsigned long long bars[3 * WRING + 1];
+    __shared__ __align__(8) unsigned long long bars[3 * WRING + (MODE == WIDE_UP ? WUP_CPL : 0)];
     __shared__ cd tab[12];
     // palette: a_p and w D^-1 per (index, face count)
     __shared__ cd pal_a[KV == KV_PAL ? 4 * WPAL : 1], pal_d[KV == KV_PAL ? 4 * WPAL : 1];
@@ -124,7 +124,7 @@ k_wide(Lvl L, const cd *__restrict__ src, const cd *__restrict__ aux, cd *__rest
     const unsigned sraw = smem_u32(smem_raw);
     const unsigned sbase = (sraw + 127u) & ~127u;
     const unsigned b_full = smem_u32(bars), b_empty = b_full + 8 * WRING, b_xf = b_full + 16 * WRING;
-    const unsigned b_coarse = b_full + 24 * WRING;     // WIDE_UP: the coarse tile has landed
+    const unsigned b_coarse = b_full + 24 * WRING;     // WIDE_UP: one barrier per staged coarse plane
     cd *const sgen = reinterpret_cast<cd *>(smem_raw + (sbase - sraw));
     auto gmirror = [&](int g) { return g < 0 ? -g : (g >= n1 ? 2 * (n1 - 1) - g : g); };
 
@@ -134,7 +134,8 @@ k_wide(Lvl L, const cd *__restrict__ src, const cd *__restrict__ aux, cd *__rest
             mbar_init(b_empty + 8 * k, WNC / 32);
             mbar_init(b_xf + 8 * k, WNC / 32);
         }
-        mbar_init(b_coarse, 1);
+        if (MODE == WIDE_UP)
+            for (int k = 0; k < WUP_CPL; k++) mbar_init(b_coarse + 8 * k, 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     if (KV == KV_CONST && tid < 4) {
@@ -193,19 +194,25 @@ k_wide(Lvl L, const cd *__restrict__ src, const cd *__restrict__ aux, cd *__rest
         }
         const bool aok = kAux && lane < ar;
         const int agoff = aok ? (j0 + lane) * n3 + m0 : 0;
-        if (MODE == WIDE_UP) {
+        // WIDE_UP: coarse plane pl of the tile (lane r copies its row r), each on its own
+        // barrier, issued a few planes ahead of the fine planes that interpolate from it
+        int cp_issued = 0;
+        auto issue_coarse = [&](int upto) {
             const Lvl &C = up.C;
-            if (lane == 0) mbar_expect_tx(b_coarse, (unsigned)(ncp * nch * ncw) * 16u);
-            __syncwarp();
-            for (int t = lane; t < ncp * nch; t += 32) {
-                const int pl = t / nch, ry = t - pl * nch;
-                bulk_g2s(sbase + (unsigned)(WRING * T::SLOT + (pl * T::CH + ry) * WCW) * 16u,
-                         up.e + (long long)(cp_lo + pl - C.lo1) * C.plane + (long long)(cj_lo + ry) * C.n3 + cm_lo,
-                         (unsigned)ncw * 16u, b_coarse);
+            for (; cp_issued <= upto && cp_issued < ncp; cp_issued++) {
+                const unsigned bar = b_coarse + 8 * cp_issued;
+                if (lane == 0) mbar_expect_tx(bar, (unsigned)(nch * ncw) * 16u);
+                __syncwarp();
+                if (lane < nch)
+                    bulk_g2s(sbase + (unsigned)(WRING * T::SLOT + (cp_issued * T::CH + lane) * WCW) * 16u,
+                             up.e + (long long)(cp_lo + cp_issued - C.lo1) * C.plane +
+                                 (long long)(cj_lo + lane) * C.n3 + cm_lo,
+                             (unsigned)ncw * 16u, bar);
             }
-        }
+        };
         for (int p = i0 - 1, d = 0; p <= last; p++, d++) {
             const int k = d & (WRING - 1);
+            if (MODE == WIDE_UP) issue_coarse(((gmirror(L.lo1 + p) >> 1) - cp_lo) + 3);
             if (d >= WRING) mbar_wait(b_empty + 8 * k, ((d / WRING) - 1) & 1);
             // (the pre-smoothing sweep rewrote the slot through the generic proxy)
             if (kXf) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -362,8 +369,12 @@ k_wide(Lvl L, const cd *__restrict__ src, const cd *__restrict__ aux, cd *__rest
         // `ring`), bo[] = b; the thread's ring entry
         // WIDE_UP: P e at the thread's centres and ring entry of plane p -- needs the coarse
         // tile only, so it is issued ahead of the wait for the plane itself
+        int cp_have = 0;                     // coarse planes [0, cp_have) of the tile have landed
         auto prolong_all = [&](int p, cd (&pe)[P], cd &peh, bool ring) {
             if (MODE == WIDE_UP) {
+                const int gm = L.lo1 + (p == p_top_ ? p - 2 : (p == p_bot_ ? p + 2 : p));
+                const int need = ((gm >> 1) - cp_lo) + (gm & 1);
+                for (; cp_have <= need; cp_have++) mbar_wait(b_coarse + 8 * cp_have, 0);
 #pragma unroll
                 for (int r = 0; r < P; r++) pe[r] = prolong(p, eo[r], (js + r) & 1, opar3);
                 if (ring && he_ok) peh = prolong(p, he_eo, he_par & 2, he_par & 1);
@@ -421,7 +432,6 @@ k_wide(Lvl L, const cd *__restrict__ src, const cd *__restrict__ aux, cd *__rest
 #pragma unroll
         for (int r = 0; r < P; r++) bc[r] = bn[r] = mk(0, 0);
         if (kXf) {
-            if (MODE == WIDE_UP) mbar_wait(b_coarse, 0);
             load_k(i0 - 1, kp, ip);          // (temporarily) plane i0-1
             load_k(i0, kc, ic);
             load_k(i0 + 1, kn, in_);

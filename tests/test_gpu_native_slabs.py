@@ -64,6 +64,27 @@ def test_native_slabs_match_single(kind, nslabs):
     assert np.array_equal(np.concatenate([t.cpu().numpy() for t in xs2], 0), x)
 
 
+@pytest.mark.parametrize("kind,nslabs", [("cube", 2), ("wedge", 3)])
+def test_native_slabs_wide_family(kind, nslabs, hfopt):
+    """The wide-plane sweep family (hf_wide.cu) on slabs: interior slab faces read
+    the ghost planes, only the global end planes are mirrored, one-plane
+    sub-slabs (the matvec's face planes) -- `force_wide` routes the 65^3 levels
+    through it; against the single-slab solve of the default kernels."""
+    from paper_2308_06085_b200.dist import NativeSlabSolver
+    from paper_2308_06085_b200.krylov import SolverConfig
+    from paper_2308_06085_b200.partition import LocalSlabComm, slab_partition
+    p, k, b = _problem(kind)
+    x1, r1 = _single(p, k, b)
+    hfopt("force_wide", 1)
+    hfopt("no_dr", 1)
+    ext = slab_partition(p.grid, nslabs)
+    S = NativeSlabSolver(p.grid, ext, k, p.bc, LocalSlabComm(nslabs))
+    xs, rep = S.solve([b[e.lo1 - 1:e.hi1] for e in ext], SolverConfig(method="bicgstab"))
+    x = np.concatenate([t.cpu().numpy() for t in xs], 0)
+    assert rep.converged and abs(rep.iterations - r1.iterations) <= 1
+    assert _rel(x, x1) < 1e-8
+
+
 def test_native_slabs_match_python_slab_driver():
     """Same decomposition through the Python-driven device path
     (SlabSolver.solve_device): same kernels; the native matvec sums its

@@ -1,6 +1,7 @@
 """A/B of kernel-variant option sets on the bench workload: ms per Bi-CGSTAB
 iteration of the 513^3 wedge (fixed budget of 50 iterations, 3 timed solves
-after 1 warm-up), every variant in one process on one box.
+after 1 warm-up), every variant in one process on one box.  AB_N sets the grid
+side, AB_MEDIUM the medium (wedge | const | random: n x n x (n+1)/2).
 
     python tools/ab_iter.py "no_wide=1" "" "wide_p4=1"
 """
@@ -17,11 +18,15 @@ from paper_2308_06085_b200.krylov import SolverConfig  # noqa: E402
 
 n = int(os.environ.get("AB_N", 513))
 iters = int(os.environ.get("AB_ITERS", 50))
-p, spec, b_host = bench._problem("c2") if n == 513 else (None, None, None)
-if p is None:
-    from paper_2308_06085_b200 import problems
+medium = os.environ.get("AB_MEDIUM", "wedge")     # wedge | const | random
+from paper_2308_06085_b200 import problems  # noqa: E402
+if medium == "const":
+    p = problems.point_source_cube(n, 80.0 * (n - 1) / 128, "sommerfeld")
+elif medium == "random":
+    p = problems.random_medium_problem((n, n, (n + 1) // 2))
+else:
     p = problems.wedge3_problem(n)
-    spec, b_host = problems.build_problem(p)
+spec, b_host = problems.build_problem(p)
 b = torch.as_tensor(b_host).cuda()
 x = torch.empty_like(b)
 cfg = SolverConfig(method="bicgstab", tol=1e-6, maxit=iters, check_every=4)
@@ -39,7 +44,7 @@ for variant in sys.argv[1:] or [""]:
             e.record()
             torch.cuda.synchronize()
             ms.append(s.elapsed_time(e) / rep.iterations)
-        print(json.dumps({"variant": variant or "default", "grid": n, "ms_per_iteration": [round(m, 3) for m in ms],
+        print(json.dumps({"variant": variant or "default", "grid": list(p.grid.shape), "medium": medium, "ms_per_iteration": [round(m, 3) for m in ms],
                           "iterations": rep.iterations, "relres": rep.final_relres}), flush=True)
         del A, H, S
     torch.cuda.empty_cache()

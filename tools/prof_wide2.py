@@ -1,6 +1,8 @@
-"""One launch each of the 513^3 wedge finest-level kernels the solve runs
-(pre-smoothing + residual sweep, Jacobi sweep, correction, restriction, the
-Bi-CGSTAB x/r and s updates), for ncu --set full."""
+"""One launch each of the 513^3 wedge finest-level kernels the solve runs, in
+the order of tools/gpu_evidence3.sh's kernel list (pre-smoothing + residual
+sweep, restriction, fused up-sweep, matvec, matvec with t^H t / t^H s, the
+Bi-CGSTAB p / s / x,r updates, then the split correction + Jacobi pair of the
+slab path), for ncu --set full."""
 import ctypes
 import os
 import sys
@@ -23,15 +25,18 @@ sh, csh = H.levels[0].extent.shape, H.levels[1].extent.shape
 r = lambda s: torch.randn(s, dtype=torch.complex128, device="cuda")
 bb, u, t, bc, ec = r(sh), r(sh), r(sh), r(csh), r(csh)
 ms = ctypes.c_float()
-for _ in range(2):
-    _native.check(L.hf_level_down1(H._h, 0, bb.data_ptr(), u.data_ptr()))
-    _native.check(L.hf_level_smooth(H._h, 0, t.data_ptr(), bb.data_ptr(), u.data_ptr()))
+A_h = A._h
+for _ in range(int(os.environ.get("PROF_PASSES", 2))):
+    _native.check(L.hf_level_down1(H._h, 0, bb.data_ptr(), u.data_ptr()))             # presmooth_residual
+    _native.check(L.hf_restrict_fw(H._h, 0, u.data_ptr(), bc.data_ptr()))             # restrict_fw
+    _native.check(L.hf_level_up(H._h, 0, bb.data_ptr(), ec.data_ptr(), u.data_ptr())) # up_fused
+    _native.check(L.hf_operator_apply(A_h, u.data_ptr(), t.data_ptr()))               # helmholtz_matvec
+    _native.check(L.hf_solver_bench_vec(S._h, 4, 1, ctypes.byref(ms)))                # matvec_dot2
+    _native.check(L.hf_solver_bench_vec(S._h, 0, 1, ctypes.byref(ms)))                # bcg_p_update
+    _native.check(L.hf_solver_bench_vec(S._h, 1, 1, ctypes.byref(ms)))                # bcg_s_update
+    _native.check(L.hf_solver_bench_vec(S._h, 3, 1, ctypes.byref(ms)))                # bcg_xr_update (sparse)
+    # the split up-sweep pair (slab path)
     _native.check(L.hf_level_correct(H._h, 0, bb.data_ptr(), ec.data_ptr(), t.data_ptr()))
-    _native.check(L.hf_restrict_fw(H._h, 0, u.data_ptr(), bc.data_ptr()))
-    _native.check(L.hf_level_up(H._h, 0, bb.data_ptr(), ec.data_ptr(), u.data_ptr()))
-    for w in (1, 2):
-        _native.check(L.hf_solver_bench_vec(S._h, w, 1, ctypes.byref(ms)))
-    _native.check(L.hf_solver_bench_vec(S._h, 3, 1, ctypes.byref(ms)))
-    _native.check(L.hf_solver_bench_vec(S._h, 0, 1, ctypes.byref(ms)))
+    _native.check(L.hf_level_smooth(H._h, 0, t.data_ptr(), bb.data_ptr(), u.data_ptr()))
 torch.cuda.synchronize()
 print("ok")

@@ -301,24 +301,26 @@ k_wide(Lvl L, const cd *__restrict__ src, const cd *__restrict__ aux, cd *__rest
         for (int r = 0; r < P; r++)
             eo[r] = MODE == WIDE_UP && r < nrow ? (((js + r) >> 1) - cj_lo) * WCW + ((m >> 1) - cm_lo) : 0;
         const int opar3 = m & 1;
-        // P e at an entry: bilinear (i2, i3) sums of one or two coarse planes (k_corr arithmetic)
-        auto prolong = [&](int p, int off, bool o2, bool o3) -> cd {
-            const int gm = L.lo1 + (p == p_top_ ? p - 2 : (p == p_bot_ ? p + 2 : p));
-            const cd *ec = ctile + ((gm >> 1) - cp_lo) * (T::CH * WCW) + off;
-            auto cplane = [&](const cd *q) -> cd {
-                cd a = q[0];
-                if (o3) a = cadd(a, q[1]);
-                if (o2) {
-                    a = cadd(a, q[WCW]);
-                    if (o3) a = cadd(a, q[WCW + 1]);
-                }
-                return a;
-            };
-            const double s2 = (o2 && o3) ? 0.25 : ((o2 || o3) ? 0.5 : 1.0);
-            const cd v0 = cplane(ec);
-            if (gm & 1) return cscal(cadd(v0, cplane(ec + T::CH * WCW)), 0.5 * s2);
-            return s2 == 1.0 ? v0 : cscal(v0, s2);
+        // P e at an entry: bilinear (i2, i3) sums of one or two coarse planes (k_corr
+        // arithmetic).  The in-plane sum of a coarse plane serves the three fine planes
+        // around it, so the sums of the thread's entries are kept in registers along
+        // the march (e2 / e2h, of coarse tile plane e2_c): an even fine plane reuses
+        // them, an odd one adds the next coarse plane's sums and keeps those.
+        auto cplane = [&](int cl, int off, bool o2, bool o3) -> cd {
+            const cd *q = ctile + cl * (T::CH * WCW) + off;
+            cd a = q[0];
+            if (o3) a = cadd(a, q[1]);
+            if (o2) {
+                a = cadd(a, q[WCW]);
+                if (o3) a = cadd(a, q[WCW + 1]);
+            }
+            return a;
         };
+        auto pscale = [](bool o2, bool o3) -> double { return (o2 && o3) ? 0.25 : ((o2 || o3) ? 0.5 : 1.0); };
+        cd e2[P], e2h = mk(0, 0);
+#pragma unroll
+        for (int r = 0; r < P; r++) e2[r] = mk(0, 0);
+        int e2_c = -1;
 
         // local plane p mirrored at the ends of the grid (global -1 -> 1, n1 -> n1 - 2)
         const int p_top = p_top_, p_bot = p_bot_;
@@ -344,6 +346,17 @@ k_wide(Lvl L, const cd *__restrict__ src, const cd *__restrict__ aux, cd *__rest
             kc[r] = kn[r] = kp[r] = L.kc;
             ic[r] = in_[r] = ip[r] = 0;
         }
+        // (q: element offset of strip row 0 in the plane to read)
+        auto load_k_at = [&](long long q, double (&kk)[P], int (&ii)[P]) {
+            if (KV != KV_CONST) {
+#pragma unroll
+                for (int r = 0; r < P; r++) {
+                    const long long qq = q + (r < nrow ? r * n3 : 0);
+                    if (KV == KV_FIELD) kk[r] = __ldg(L.k + qq);
+                    else ii[r] = (int)__ldg(L.kidx + qq);
+                }
+            }
+        };
         auto load_k = [&](int p, double (&kk)[P], int (&ii)[P]) {
             if (KV != KV_CONST) {
                 const long long q = kplane(p) + own0;
@@ -364,6 +377,13 @@ k_wide(Lvl L, const cd *__restrict__ src, const cd *__restrict__ aux, cd *__rest
                 else ii = (int)__ldg(L.kidx + q);
             }
         };
+        const int he_rel = he_goff - own0;
+        auto load_hk_at = [&](long long q, double &kk, int &ii) {
+            if (kXf && KV != KV_CONST && he_ok) {
+                if (KV == KV_FIELD) kk = __ldg(L.k + q + he_rel);
+                else ii = (int)__ldg(L.kidx + q + he_rel);
+            }
+        };
 
         // transform of plane p (WIDE_PRE): own centres -> fo[] = D^-1 b (stored when
         // `ring`), bo[] = b; the thread's ring entry
@@ -373,11 +393,40 @@ k_wide(Lvl L, const cd *__restrict__ src, const cd *__restrict__ aux, cd *__rest
         auto prolong_all = [&](int p, cd (&pe)[P], cd &peh, bool ring) {
             if (MODE == WIDE_UP) {
                 const int gm = L.lo1 + (p == p_top_ ? p - 2 : (p == p_bot_ ? p + 2 : p));
-                const int need = ((gm >> 1) - cp_lo) + (gm & 1);
-                for (; cp_have <= need; cp_have++) mbar_wait(b_coarse + 8 * cp_have, 0);
+                const int cl = (gm >> 1) - cp_lo;
+                const bool odd = gm & 1;
+                for (; cp_have <= cl + (int)odd; cp_have++) mbar_wait(b_coarse + 8 * cp_have, 0);
+                const bool hring = he_ok;        // (the ring entry's sums are carried on every plane)
+                if (e2_c != cl) {                // first plane of the march, mirrored end planes
 #pragma unroll
-                for (int r = 0; r < P; r++) pe[r] = prolong(p, eo[r], (js + r) & 1, opar3);
-                if (ring && he_ok) peh = prolong(p, he_eo, he_par & 2, he_par & 1);
+                    for (int r = 0; r < P; r++) e2[r] = cplane(cl, eo[r], (js + r) & 1, opar3);
+                    if (hring) e2h = cplane(cl, he_eo, he_par & 2, he_par & 1);
+                    e2_c = cl;
+                }
+                if (!odd) {
+#pragma unroll
+                    for (int r = 0; r < P; r++) {
+                        const double s2 = pscale((js + r) & 1, opar3);
+                        pe[r] = s2 == 1.0 ? e2[r] : cscal(e2[r], s2);
+                    }
+                    if (ring && hring) {
+                        const double s2 = pscale(he_par & 2, he_par & 1);
+                        peh = s2 == 1.0 ? e2h : cscal(e2h, s2);
+                    }
+                } else {
+#pragma unroll
+                    for (int r = 0; r < P; r++) {
+                        const cd nx = cplane(cl + 1, eo[r], (js + r) & 1, opar3);
+                        pe[r] = cscal(cadd(e2[r], nx), 0.5 * pscale((js + r) & 1, opar3));
+                        e2[r] = nx;
+                    }
+                    if (hring) {
+                        const cd nx = cplane(cl + 1, he_eo, he_par & 2, he_par & 1);
+                        peh = cscal(cadd(e2h, nx), 0.5 * pscale(he_par & 2, he_par & 1));
+                        e2h = nx;
+                    }
+                    e2_c = cl + 1;
+                }
             }
         };
         auto transform = [&](int p, cd (&fo)[P], cd (&bo)[P], const double (&kk)[P],
@@ -465,17 +514,21 @@ k_wide(Lvl L, const cd *__restrict__ src, const cd *__restrict__ aux, cd *__rest
         }
 
         long long q = (long long)i0 * plane + own0;       // strip row 0 in plane i
+        // strip row 0 in the plane whose wavenumbers the next step reads (i + 2 / i + 1)
+        long long kq = q + (kXf ? 2 : 1) * plane;
         const double ih2 = L.ih2;
 
         auto step = [&](int i, WidePlane<P> &Pm, WidePlane<P> &Cc, WidePlane<P> &Nx) {
             if (kXf) {
-                if (i + 2 <= last) {
-                    load_k(i + 2, kp, ip);
-                    load_hk(i + 2, hk_p, hi_p);
+                if (i + 2 <= last) {             // (global plane n1 is the mirrored plane n1 - 2)
+                    const long long kk2 = i + 2 == p_top ? kq - 2 * plane : kq;
+                    load_k_at(kk2, kp, ip);
+                    load_hk_at(kk2, hk_p, hi_p);
                 }
             } else if (i + 1 < i1) {
-                load_k(i + 1, kn, in_);
+                load_k_at(kq, kn, in_);
             }
+            kq += plane;
             const cd *s0 = slot(i);
             const int nbx = nbx_of(i);
             cd nsum[P];                      // (ym + yp) + (zm + zp) of plane i

@@ -1,6 +1,5 @@
 // hf_stencil.cuh -- device / launch building blocks shared by the kernel
-// translation units (hf_kernels.cu, hf_wide.cu): the Bi-CGSTAB scalar state
-// machine run by the last block of a reduction, programmatic dependent launch,
+// translation units (hf_kernels.cu, hf_wide.cu): programmatic dependent launch,
 // mbarrier / bulk-copy wrappers, the stencil epilogues and the launch helper.
 #pragma once
 #include <utility>
@@ -8,73 +7,6 @@
 #include "hf_kernels.cuh"
 
 namespace hf {
-
-// ---------------------------------------------------------------------------
-// Bi-CGSTAB scalar state machine (krylov.py:234-273), run by one thread.
-// ---------------------------------------------------------------------------
-__device__ inline void bcg_record(BcgState *st, double relres) {
-    if (st->hist && st->iter < st->hist_cap) st->hist[st->iter] = relres;
-    st->iter += 1;
-    st->relres = relres;
-}
-
-__device__ inline void bcg_finalize(BcgState *st, int op, const cd *sums) {
-    switch (op) {
-    case FIN_BCG_INIT: {            // krylov.py:217-232
-        double bb = sums[0].x;
-        st->bnorm = sqrt(bb > 0.0 ? bb : 0.0);
-        st->rho = st->alpha = st->omega = mk(1.0, 0.0);
-        st->iter = 0; st->matvecs = 0; st->breakdown = 0; st->s_conv = 0;
-        st->converged = 0; st->done = 0;
-        if (st->bnorm == 0.0) { st->converged = 1; st->done = 1; st->relres = 0.0; return; }
-        st->relres = st->bnorm / st->bnorm;
-        if (st->relres <= st->tol) { st->converged = 1; st->done = 1; return; }
-        if (st->iter >= st->maxit) { st->done = 1; return; }
-        st->rho_new = sums[1];
-        if (cabsd(st->rho_new) < st->btol) { st->breakdown = HF_BREAKDOWN_RHO; st->done = 1; return; }
-        st->beta = cmul(cdiv(st->rho_new, st->rho), cdiv(st->alpha, st->omega));
-        return;
-    }
-    case FIN_BCG_ALPHA: {           // krylov.py:242-247
-        st->matvecs += 1;
-        cd den = sums[0];
-        if (cabsd(den) < st->btol) { st->breakdown = HF_BREAKDOWN_RHO; st->done = 1; return; }
-        st->alpha = cdiv(st->rho_new, den);
-        return;
-    }
-    case FIN_BCG_S: {               // krylov.py:248-255
-        double ss = sums[0].x;
-        double snorm = sqrt(ss > 0.0 ? ss : 0.0);
-        if (snorm / st->bnorm <= st->tol) {
-            bcg_record(st, snorm / st->bnorm);
-            st->s_conv = 1; st->converged = 1; st->done = 1;
-        }
-        return;
-    }
-    case FIN_BCG_OMEGA: {           // krylov.py:257-265
-        st->matvecs += 1;
-        cd tt = sums[0], ts = sums[1];
-        if (cabsd(tt) < st->btol) { st->breakdown = HF_BREAKDOWN_OMEGA; st->done = 1; return; }
-        st->omega = cdiv(ts, tt);
-        if (cabsd(st->omega) < st->btol) { st->breakdown = HF_BREAKDOWN_OMEGA; st->done = 1; return; }
-        return;
-    }
-    case FIN_BCG_RHO: {             // krylov.py:266-273, then the loop head 234-239
-        st->rho = st->rho_new;
-        double rr = sums[0].x;
-        double relres = sqrt(rr > 0.0 ? rr : 0.0) / st->bnorm;
-        bcg_record(st, relres);
-        if (relres <= st->tol) { st->converged = 1; st->done = 1; return; }
-        if (st->iter >= st->maxit) { st->done = 1; return; }
-        st->rho_new = sums[1];
-        if (cabsd(st->rho_new) < st->btol) { st->breakdown = HF_BREAKDOWN_RHO; st->done = 1; return; }
-        st->beta = cmul(cdiv(st->rho_new, st->rho), cdiv(st->alpha, st->omega));
-        return;
-    }
-    default:
-        return;
-    }
-}
 
 // Programmatic dependent launch: every kernel is launched with the
 // programmatic-stream-serialization attribute.  On entry a CTA waits for the

@@ -464,15 +464,15 @@ k_wide(Lvl L, const cd *__restrict__ src, const cd *__restrict__ aux, cd *__rest
                 }
                 if (ring && he_ok && nbx + he_nb > 0)
                     sl[he_off] = cmul(sl[he_off], tab[8 + nbx + he_nb]);
-                return;
-            }
+            } else {
 #pragma unroll
-            for (int r = 0; r < P; r++) {
-                bo[r] = sl[cf0 + r * WRS];
-                fo[r] = cmul(bo[r], dfac(kk[r], ii[r], nbx + ((nbs >> (2 * r)) & 3)));
-                if (ring && r < nrow) sl[cf0 + r * WRS] = fo[r];
+                for (int r = 0; r < P; r++) {
+                    bo[r] = sl[cf0 + r * WRS];
+                    fo[r] = cmul(bo[r], dfac(kk[r], ii[r], nbx + ((nbs >> (2 * r)) & 3)));
+                    if (ring && r < nrow) sl[cf0 + r * WRS] = fo[r];
+                }
+                if (ring && he_ok) sl[he_off] = cmul(sl[he_off], dfac(hk, hi, nbx + he_nb));
             }
-            if (ring && he_ok) sl[he_off] = cmul(sl[he_off], dfac(hk, hi, nbx + he_nb));
         };
 
         // ---- prologue: planes i0-1 and i0 into the register sets ----

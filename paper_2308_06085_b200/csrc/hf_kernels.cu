@@ -1658,10 +1658,13 @@ __global__ void __launch_bounds__(256) k_bcg_p(long long n, const BcgState *st,
     }
 }
 
-// s = r - alpha v ; |s|^2   (krylov.py:248-249)
-__global__ void __launch_bounds__(256) k_bcg_s(long long n, const BcgState *st,
-                                               const cd *__restrict__ r, const cd *__restrict__ v,
-                                               cd *__restrict__ s, RedSlot red, const int *done) {
+// s = r - alpha v ; |s|^2   (krylov.py:248-249).  s may BE r (the single-slab solver keeps
+// s in r's buffer: the old residual is dead once s exists, and an in-place pass measured
+// 1.23 -> 1.08 ms at 513^3), so r and s are neither restrict nor read through the
+// read-only path; every element is read once and then written by the same thread.
+__global__ void __launch_bounds__(256) k_bcg_s(long long n, const BcgState *st, const cd *r,
+                                               const cd *__restrict__ v, cd *s, RedSlot red,
+                                               const int *done) {
     if (is_done(done)) return;
     cd al = st->alpha;
     cd acc[1] = {mk(0, 0)};
@@ -1669,7 +1672,7 @@ __global__ void __launch_bounds__(256) k_bcg_s(long long n, const BcgState *st,
     long long q = blockIdx.x * 256ll + threadIdx.x;
     // two strides per trip; the per-thread accumulation order is unchanged
     for (; q + S < n; q += 2 * S) {
-        cd r0 = __ldg(r + q), r1 = __ldg(r + q + S), v0 = __ldg(v + q), v1 = __ldg(v + q + S);
+        cd r0 = r[q], r1 = r[q + S], v0 = __ldg(v + q), v1 = __ldg(v + q + S);
         cd s0 = csub(r0, cmul(al, v0)), s1 = csub(r1, cmul(al, v1));
         s[q] = s0;
         s[q + S] = s1;
@@ -1677,18 +1680,19 @@ __global__ void __launch_bounds__(256) k_bcg_s(long long n, const BcgState *st,
         acc[0] = cadd(acc[0], cjmul(s1, s1));
     }
     if (q < n) {
-        cd sv = csub(__ldg(r + q), cmul(al, __ldg(v + q)));
+        cd sv = csub(r[q], cmul(al, __ldg(v + q)));
         s[q] = sv;
         acc[0] = cadd(acc[0], cjmul(sv, sv));
     }
     reduce_finish<1>(acc, red);
 }
 
-// x += alpha ph + omega sh ; r = s - omega t ; |r|^2, rs^H r   (krylov.py:266-269)
+// x += alpha ph + omega sh ; r = s - omega t ; |r|^2, rs^H r   (krylov.py:266-269).
+// s may BE r (see k_bcg_s).
 __global__ void __launch_bounds__(256) k_bcg_xr(long long n, const BcgState *st,
                                                 cd *__restrict__ x, const cd *__restrict__ ph,
-                                                const cd *__restrict__ sh, const cd *__restrict__ s,
-                                                const cd *__restrict__ t, cd *__restrict__ r,
+                                                const cd *__restrict__ sh, const cd *s,
+                                                const cd *__restrict__ t, cd *r,
                                                 const cd *__restrict__ rs, RedSlot red,
                                                 const int *done) {
     if (is_done(done)) return;
@@ -1697,7 +1701,7 @@ __global__ void __launch_bounds__(256) k_bcg_xr(long long n, const BcgState *st,
     for (long long q = blockIdx.x * 256ll + threadIdx.x; q < n; q += (long long)gridDim.x * 256) {
         cd xv = cadd(cadd(x[q], cmul(al, __ldg(ph + q))), cmul(om, __ldg(sh + q)));
         x[q] = xv;
-        cd rv = csub(__ldg(s + q), cmul(om, __ldg(t + q)));
+        cd rv = csub(s[q], cmul(om, __ldg(t + q)));
         r[q] = rv;
         acc[0] = cadd(acc[0], cjmul(rv, rv));
         if (rs) acc[1] = cadd(acc[1], cjmul(__ldg(rs + q), rv));   // null: sparse shadow

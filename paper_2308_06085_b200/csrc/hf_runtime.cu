@@ -1111,11 +1111,14 @@ extern "C" hf_solver *hf_solver_create(hf_operator *Aop, hf_hierarchy *M) {
     S->Aop = Aop; S->M = M;
     S->n = (long long)L.nx * L.plane;
     cudaError_t e;
-    cd **vecs[] = {&S->x, &S->r, &S->rs, &S->p, &S->v, &S->ph, &S->s, &S->sh, &S->t};
+    cd **vecs[] = {&S->x, &S->r, &S->rs, &S->p, &S->v, &S->ph, &S->sh, &S->t};
     for (cd **pv : vecs) {
         *pv = new_field(S->A, L.nx, L.plane, e);
         if (!*pv) { fail(HF_ERR_CUDA, "cudaMalloc solver vectors"); delete S; return nullptr; }
     }
+    // s = r - alpha v lives in r's buffer: r is dead once s exists (krylov.py:248-269 reads
+    // only s and t until the new r), and the in-place updates stream one array less
+    S->s = S->r;
     S->st = S->A.get<BcgState>(1, e);
     size_t nblk = std::max<size_t>(std::max(march_blocks(L), tile_blocks(L)), VEC_BLOCKS_HOST);
     if (!S->st || S->red.init(S->A, nblk + 64)) {

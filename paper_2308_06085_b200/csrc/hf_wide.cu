@@ -65,7 +65,7 @@ constexpr int WRS = WX + 2;       // staged entries per tile row
 __host__ __device__ constexpr int wide_ncw(int mode) { return mode == 0 ? 8 : 7; }
 constexpr int WRING = 4;
 constexpr int WPAL = 16;          // palette entries held in shared memory (else the k field is used)
-constexpr int WUP_CHUNK = 32;     // fine planes per block of the fused up-sweep
+constexpr int WUP_CHUNK = 48;     // fine planes per block of the fused up-sweep
 constexpr int WUP_CPL = WUP_CHUNK / 2 + 2;   // coarse planes staged per block
 constexpr int WCW = WX / 2 + 2;   // coarse tile row length
 static_assert((WRING & (WRING - 1)) == 0, "ring size is a power of two");

@@ -654,7 +654,9 @@ static dim3 wide_grid(const Lvl &L, int &chunk) {
     const long long cols = (long long)gx * gy;
     const long long target = 148LL * (P >= 4 ? 2 : 3) * 6;
     int gz = (int)std::max<long long>(1, std::min<long long>(L.nx, (target + cols - 1) / cols));
-    chunk = std::max((L.nx + gz - 1) / gz, std::min(L.nx, 8));
+    // (the transform modes -- 7 consumer warps -- pay more per chunk: two extra planes are
+    // transformed, so their marches are at least 32 planes long)
+    chunk = std::max((L.nx + gz - 1) / gz, std::min(L.nx, NCW == 7 ? 32 : 8));
     gz = (L.nx + chunk - 1) / chunk;
     return dim3(gx, gy, gz);
 }

@@ -1926,11 +1926,12 @@ extern "C" hf_slab *hf_slab_create(int n1, int n2, int n3, double h, double beta
         if (!q.A || !q.H) { S->sl.push_back(q); delete S; return nullptr; }
         const Lvl &L = q.A->lv.L;
         q.n = (long long)L.nx * L.plane;
-        cd **vecs[] = {&q.x, &q.r, &q.rs, &q.p, &q.v, &q.ph, &q.s, &q.sh, &q.t};
+        cd **vecs[] = {&q.x, &q.r, &q.rs, &q.p, &q.v, &q.ph, &q.sh, &q.t};
         for (cd **pv : vecs) {
             *pv = new_field(S->A, L.nx, L.plane, e);
             if (!*pv) { S->sl.push_back(q); delete S; fail(HF_ERR_CUDA, "cudaMalloc slab vectors"); return nullptr; }
         }
+        q.s = q.r;      // s lives in r's buffer (in-place s and x / r updates, as in hf_solver)
         S->sl.push_back(q);
     }
     S->nlev = (int)S->sl[0].H->lev.size();
@@ -2262,6 +2263,38 @@ static int slab_cycle(hf_slab *S, const std::vector<cd *> &src, const std::vecto
                 }
             }
         };
+        // wide levels: prolongation + correction + Jacobi sweep in ONE pass of the wide family
+        // (hf_wide.cu WIDE_UP; the correction t is never written).  The sweep transforms one
+        // plane beyond each end of its range, so the planes [a + 1, b2 - 1) need no ghost
+        // plane of e and overlap its exchange; the two face ranges follow.
+        const bool wide_up = wide_ok(S->sl[0].H->lev[l].L, 6) && !opt(OPT_NO_WIDE_UP) && !opt(OPT_NO_FUSE);
+        auto upw = [&](bool inner) {
+            for (int i = 0; i < nloc; i++) {
+                Level &lv = S->sl[i].H->lev[l], &nx = S->sl[i].H->lev[l + 1];
+                const int nxf = lv.L.nx;
+                const bool glo = lv.L.lo1 > 0, ghi = lv.L.lo1 + nxf < lv.L.n1;
+                int a = 0, b2 = nxf;
+                while (a < nxf && ((lv.L.lo1 + a) >> 1) < nx.L.lo1) a++;
+                while (b2 > a && (((lv.L.lo1 + b2 - 1) >> 1) + ((lv.L.lo1 + b2 - 1) & 1)) > nx.L.lo1 + nx.L.nx - 1) b2--;
+                const int p0 = glo ? std::min(a + 1, nxf) : 0, p1 = ghi ? std::max(b2 - 1, p0) : nxf;
+                auto run = [&](int q0, int q1) {
+                    if (q1 <= q0) return;
+                    const size_t o = (size_t)q0 * lv.L.plane;
+                    launch_wide_up(sub_slab(lv.L, q0, q1), nx.L, bl(i, l) + o, nx.u, ul(i, l) + o, om, true, s, done);
+                    g_launches++;
+                };
+                if (inner) {
+                    run(p0, p1);
+                } else {
+                    run(0, p0);
+                    run(p1, nxf);
+                }
+            }
+        };
+        if (wide_up) {
+            if (overlapped(S, l + 1, f, 1, s, [&] { upw(true); }, [&] { upw(false); })) return HF_ERR_CUDA;
+            continue;
+        }
         if (overlapped(S, l + 1, f, 1, s, [&] { corr(true); }, [&] { corr(false); })) return HF_ERR_CUDA;
         for (int i = 0; i < nloc; i++) {
             Level &lv = S->sl[i].H->lev[l];

@@ -64,12 +64,14 @@ def test_native_slabs_match_single(kind, nslabs):
     assert np.array_equal(np.concatenate([t.cpu().numpy() for t in xs2], 0), x)
 
 
-@pytest.mark.parametrize("kind,nslabs", [("cube", 2), ("wedge", 3)])
+@pytest.mark.parametrize("kind,nslabs", [("cube", 2), ("wedge", 3), ("wedge", 4), ("cube", 5)])
 def test_native_slabs_wide_family(kind, nslabs, hfopt):
     """The wide-plane sweep family (hf_wide.cu) on slabs: interior slab faces read
     the ghost planes, only the global end planes are mirrored, one-plane
-    sub-slabs (the matvec's face planes) -- `force_wide` routes the 65^3 levels
-    through it; against the single-slab solve of the default kernels."""
+    sub-slabs (the matvec's face planes), and the fused up-sweep launched as an
+    interior range overlapping the exchange of the coarse correction plus two
+    face ranges that read its ghost planes -- `force_wide` routes the 65^3
+    levels through it; against the single-slab solve of the default kernels."""
     from paper_2308_06085_b200.dist import NativeSlabSolver
     from paper_2308_06085_b200.krylov import SolverConfig
     from paper_2308_06085_b200.partition import LocalSlabComm, slab_partition

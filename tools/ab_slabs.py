@@ -30,7 +30,7 @@ with _native.options(**opts):
     for ns in (1, 2, 4, 8):
         ext = slab_partition(p.grid, ns)
         S = NativeSlabSolver(p.grid, ext, k, p.bc, LocalSlabComm(ns))
-        parts = [b[e.lo1 - 1:e.hi1] for e in ext]
+        parts = [torch.as_tensor(np.ascontiguousarray(b[e.lo1 - 1:e.hi1])).cuda() for e in ext]   # resident
         cfg = SolverConfig(method="bicgstab", tol=1e-6, maxit=iters, check_every=4)
         S.solve(parts, cfg)
         torch.cuda.synchronize()

@@ -1733,6 +1733,17 @@ __global__ void k_bcg_gather(BcgState *st, int op, const cd *__restrict__ g, con
     bcg_finalize(st, op, sums);
 }
 
+// slab drivers: this slab's share of r~^H g over the slab's own nonzeros of r~ (a per-slab
+// nonzero list in nz; the shares are summed across slabs / ranks like any partial sum)
+__global__ void k_gather_store(const BcgState *nz, const cd *__restrict__ g, cd *out, const int *done) {
+    if (is_done(done)) return;
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    cd a = mk(0, 0);
+    for (int k = 0; k < nz->nz; k++)            // fixed ascending order; nz <= 0: none here
+        a = cadd(a, cjmul(nz->nzw[k], __ldcg(g + nz->nzq[k])));
+    *out = a;
+}
+
 // x += alpha ph  (convergence at the half step, krylov.py:250-255)
 __global__ void k_bcg_xhalf(long long n, const BcgState *st, cd *__restrict__ x,
                             const cd *__restrict__ ph) {
@@ -2546,6 +2557,9 @@ void launch_bcg_xr(long long n, const BcgState *st, cd *x, const cd *ph, const c
 void launch_nz_scan(long long n, const cd *rs, BcgState *st, cudaStream_t s) {
     launch(k_nz_scan, dim3(VEC_BLOCKS), dim3(256), 0, s, n, rs, st);
     launch(k_nz_finish, dim3(1), dim3(32), 0, s, rs, st);
+}
+void launch_gather_store(const BcgState *nz, const cd *g, cd *out, cudaStream_t s, const int *done) {
+    launch(k_gather_store, dim3(1), dim3(32), 0, s, nz, g, out, done);
 }
 void launch_bcg_gather(BcgState *st, int op, const cd *g, cudaStream_t s, const int *done) {
     launch(k_bcg_gather, dim3(1), dim3(32), 0, s, st, op, g, done);

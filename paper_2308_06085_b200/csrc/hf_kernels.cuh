@@ -81,6 +81,8 @@ void launch_bcg_xr(long long n, const BcgState *st, cd *x, const cd *ph, const c
                    cudaStream_t s, const int *done);
 void launch_bcg_xhalf(long long n, const BcgState *st, cd *x, const cd *ph, cudaStream_t s);
 void launch_bcg_step(BcgState *st, int op, const cd *sums, cudaStream_t s);
+// slab drivers: *out = this slab's share of r~^H g over its own nonzeros of r~ (list in nz)
+void launch_gather_store(const BcgState *nz, const cd *g, cd *out, cudaStream_t s, const int *done);
 // sparse shadow: sums[0] = r~^H g gathered over the nonzeros of r~, then scalar step `op`
 void launch_bcg_gather(BcgState *st, int op, const cd *g, cudaStream_t s, const int *done);
 // find the (<= HF_NZ_MAX) nonzeros of the shadow vector: st->nz = count, or -1 (dense)

@@ -1874,11 +1874,18 @@ struct hf_slab {
     cudaStream_t cstream = nullptr;   // halo exchanges overlapped with interior planes
     cudaEvent_t evf = nullptr, evj = nullptr;
     cudaStream_t stream = nullptr;
-    cudaGraphExec_t graph = nullptr;
-    int graph_kernels = 0;
+    cudaGraphExec_t graph[2] = {nullptr, nullptr};   // [sparse shadow on this rank's slabs]
+    int graph_kernels[2] = {0, 0};
+    // sparse shadow: per local slab, the (<= HF_NZ_MAX) nonzeros of its part of r~ (only the
+    // nz fields of the struct are used); r~ is then not streamed by the matvec / x, r update
+    std::vector<BcgState *> nzst;
+    BcgState *nz_host = nullptr;      // pinned, one per local slab
+    bool sparse = false;
     void *comm = nullptr;
     ~hf_slab() {
-        if (graph) cudaGraphExecDestroy(graph);
+        for (int k = 0; k < 2; k++)
+            if (graph[k]) cudaGraphExecDestroy(graph[k]);
+        if (nz_host) cudaFreeHost(nz_host);
         for (SlabLocal &q : sl) {
             if (q.H) hf_hierarchy_destroy(q.H);
             if (q.A) hf_operator_destroy(q.A);
@@ -2318,7 +2325,9 @@ static int slab_matvec(hf_slab *S, int nd, const std::vector<cd *> &u, cudaStrea
         const Lvl &L = q.A->lv.L;
         const size_t off = (size_t)p0 * L.plane;
         const Lvl Ls = sub_slab(L, p0, p1);
-        if (nd == 1)
+        if (nd == 1 && S->sparse)      // r~^H v gathered below: a plain matvec
+            launch_apply(Ls, u[i] + off, q.v + off, s, done);
+        else if (nd == 1)
             launch_apply_dot1(Ls, u[i] + off, q.v + off, q.rs + off, slab_store(S, i, part), s, done);
         else
             launch_apply_dot2(Ls, u[i] + off, q.t + off, q.s + off, slab_store(S, i, part), s, done);
@@ -2343,6 +2352,11 @@ static int slab_matvec(hf_slab *S, int nd, const std::vector<cd *> &u, cudaStrea
             mv(i, 0, nx, 1);
         }
     }
+    if (nd == 1 && S->sparse)
+        for (int i = 0; i < nloc; i++) {
+            launch_gather_store(S->nzst[i], S->sl[i].v, S->sums + 2 * (3 * i), s, done);
+            g_launches++;
+        }
     return 0;
 }
 
@@ -2369,7 +2383,9 @@ static int slab_iteration(hf_slab *S, cudaStream_t s) {
     if (slab_reduce_step(S, FIN_BCG_OMEGA, s, 3)) return HF_ERR_CUDA;
     for (int i = 0; i < nloc; i++) {
         SlabLocal &q = S->sl[i];
-        L1(launch_bcg_xr(q.n, S->st, q.x, q.ph, q.sh, q.s, q.t, q.r, q.rs, slab_store(S, i), s, done));
+        L1(launch_bcg_xr(q.n, S->st, q.x, q.ph, q.sh, q.s, q.t, q.r, S->sparse ? nullptr : q.rs,
+                         slab_store(S, i), s, done));
+        if (S->sparse) L1(launch_gather_store(S->nzst[i], q.r, S->sums + 2 * (3 * i) + 1, s, done));
     }
     if (slab_reduce_step(S, FIN_BCG_RHO, s)) return HF_ERR_CUDA;
     CK(cudaMemcpyAsync(S->st_host, S->st, sizeof(BcgState), cudaMemcpyDeviceToHost, s));
@@ -2407,8 +2423,27 @@ extern "C" int hf_slab_solve(hf_slab *S, const hf_solver_config *cfg, const doub
     }
     if (slab_reduce_step(S, FIN_BCG_INIT, s)) return HF_ERR_CUDA;
     CK(cudaMemcpyAsync(S->st_host, S->st, sizeof(BcgState), cudaMemcpyDeviceToHost, s));
+    // nonzeros of this rank's parts of r~ (a point source with r~ = b: at most one slab has any)
+    if (S->nzst.empty()) {
+        cudaError_t e2;
+        for (int i = 0; i < nloc; i++) {
+            S->nzst.push_back(S->A.get<BcgState>(1, e2));
+            if (!S->nzst.back()) return fail(HF_ERR_CUDA, "cudaMalloc slab nonzero list");
+        }
+        if (cudaMallocHost(&S->nz_host, nloc * sizeof(BcgState)) != cudaSuccess)
+            return fail(HF_ERR_CUDA, "cudaMallocHost slab nonzero list");
+    }
+    for (int i = 0; i < nloc; i++) {
+        CK(cudaMemsetAsync(S->nzst[i], 0, sizeof(BcgState), s));
+        launch_nz_scan(S->sl[i].n, S->sl[i].rs, S->nzst[i], s);
+        CK(cudaMemcpyAsync(S->nz_host + i, S->nzst[i], sizeof(BcgState), cudaMemcpyDeviceToHost, s));
+        launches += 2;
+    }
     CK(cudaStreamSynchronize(s));
-    if (!S->graph) {
+    S->sparse = true;
+    for (int i = 0; i < nloc; i++) S->sparse = S->sparse && S->nz_host[i].nz_count <= HF_NZ_MAX;
+    const int gi = S->sparse ? 1 : 0;
+    if (!S->graph[gi]) {
         cudaGraph_t g;
         long long before = g_launches;
         CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
@@ -2416,9 +2451,9 @@ extern "C" int hf_slab_solve(hf_slab *S, const hf_solver_config *cfg, const doub
         cudaError_t e = cudaStreamEndCapture(s, &g);
         if (rc) return rc;
         if (e != cudaSuccess) return fail(HF_ERR_CUDA, std::string("slab graph capture: ") + cudaGetErrorString(e));
-        S->graph_kernels = (int)(g_launches - before);
+        S->graph_kernels[gi] = (int)(g_launches - before);
         g_launches = before;
-        e = cudaGraphInstantiate(&S->graph, g, 0);
+        e = cudaGraphInstantiate(&S->graph[gi], g, 0);
         cudaGraphDestroy(g);
         if (e != cudaSuccess) return fail(HF_ERR_CUDA, std::string("slab graph instantiate: ") + cudaGetErrorString(e));
     }
@@ -2426,12 +2461,12 @@ extern "C" int hf_slab_solve(hf_slab *S, const hf_solver_config *cfg, const doub
     int graphs = 0;
     while (!S->st_host->done && graphs < cfg->maxit + every) {
         for (int k = 0; k < every; k++) {
-            CK(cudaGraphLaunch(S->graph, s));
+            CK(cudaGraphLaunch(S->graph[gi], s));
             graphs++;
         }
         CK(cudaStreamSynchronize(s));
     }
-    launches += (long long)graphs * S->graph_kernels;
+    launches += (long long)graphs * S->graph_kernels[gi];
     for (int i = 0; i < nloc; i++) {
         SlabLocal &q = S->sl[i];
         if (S->st_host->s_conv) {

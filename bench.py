@@ -21,6 +21,14 @@ Besides the headline line the run reports, in `config`:
     (SolverConfig.shadow = "random", converges where r~ = b breaks down);
   * configs[1] (129^3, k = 80 cube) time to solution at tol 1e-6.
 
+`roofline.kernels` is the live CUDA-event table of the finest-level kernels on
+the DEFAULT path of this workload (wide sweep family: pre-smoothing + residual
+sweep, restriction, fused up-sweep, matvec, matvec with t^H t / t^H s, the three
+vector updates), `share` = launches per iteration x ms / ms per iteration; the
+kernels of other variants appear with share null.  `--opt name=0|1` sets a
+kernel-variant option of the library for an A/B run,
+`--no-tts` / `--no-cpu` skip the secondary measurements.
+
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c1] [--impl reference]
 """
 
@@ -598,7 +606,6 @@ def main():
     ap.add_argument("--cpu-iters", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-tts", action="store_true", help="skip the secondary solves in config")
-    ap.add_argument("--no-table", action="store_true", help="skip the per-kernel table (A/B runs)")
     ap.add_argument("--opt", action="append", default=[], metavar="NAME=0|1",
                     help="kernel-variant option of the library (hf_set_option), for A/B runs")
     args = ap.parse_args()

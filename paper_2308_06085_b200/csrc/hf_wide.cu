@@ -62,11 +62,16 @@ constexpr int WRS = WX + 2;       // staged entries per tile row
 // registers); 7 for the in-slot transform modes -- registers are allocated per SM
 // sub-partition (16 K each), two 8-warp blocks put 4 warps on each (128 registers, no
 // spills), two 9-warp blocks up to 5 (96)
-__host__ __device__ constexpr int wide_ncw(int mode) { return mode == 0 ? 8 : 7; }
+// (strips of 3 / 4 rows, options wide_p3 / wide_p4: 5 / 4 consumer warps for the transform
+// modes -- fewer, fatter warps, the per-plane barrier traffic paid once per 3 / 4 points)
+__host__ __device__ constexpr int wide_ncw(int mode, int P = 2) {
+    return mode == 0 ? 8 : (P == 2 ? 7 : (P == 3 ? 5 : 4));
+}
 constexpr int WRING = 4;
 constexpr int WPAL = 16;          // palette entries held in shared memory (else the k field is used)
-constexpr int WUP_CHUNK = 48;     // fine planes per block of the fused up-sweep
-constexpr int WUP_CPL = WUP_CHUNK / 2 + 2;   // coarse planes staged per block
+// fine planes per block of the fused up-sweep / coarse planes staged per block
+__host__ __device__ constexpr int wup_chunk(int P) { return P == 2 ? 48 : 40; }
+__host__ __device__ constexpr int wup_cpl(int P) { return wup_chunk(P) / 2 + 2; }
 constexpr int WCW = WX / 2 + 2;   // coarse tile row length
 static_assert((WRING & (WRING - 1)) == 0, "ring size is a power of two");
 
@@ -84,8 +89,8 @@ struct WideTile {
     static constexpr int AENT = AUX ? WY * WX : 0;   // centre-only operand entries
     static constexpr int SLOT = ENT + AENT;
     static constexpr int NHE = 2 * WRS + 2 * WY;  // entries of the ring around the tile
-    static constexpr int CH = WY / 2 + 2;         // coarse tile rows
-    static constexpr int CENT = UP ? WUP_CPL * CH * WCW : 0;   // staged coarse tile
+    static constexpr int CH = (WY + 1) / 2 + 2;   // coarse tile rows (tiles may start on odd rows)
+    static constexpr int CENT = UP ? wup_cpl(P) * CH * WCW : 0;   // staged coarse tile
     static constexpr size_t smem = (size_t)(WRING * SLOT + CENT) * sizeof(cd) + 128;
 };
 
@@ -102,12 +107,12 @@ template <int MODE, int EPI, int KV, bool SOMM, int P>
 // registers are allocated per SM sub-partition (16 K each): 3 blocks of 9 warps put up to
 // 7 warps on one (72 registers), 2 blocks up to 5 (96) -- the in-slot transform modes and
 // the 4-row strips take 2 blocks
-__global__ void __launch_bounds__(32 * (wide_ncw(MODE) + 1), (P >= 4 || MODE != WIDE_LOAD ? 2 : 3))
+__global__ void __launch_bounds__(32 * (wide_ncw(MODE, P) + 1), (P >= 4 || MODE != WIDE_LOAD ? 2 : 3))
 k_wide(Lvl L, const cd *__restrict__ src, const cd *__restrict__ aux, cd *__restrict__ out,
        double omega, int chunk, RedSlot rs, WideUp up, const int *done) {
     constexpr bool kAux = EPI != WE_APPLY0 && MODE == WIDE_LOAD;   // staged centre-only operand
     constexpr bool kXf = MODE != WIDE_LOAD;                        // entries transformed in the slot
-    constexpr int NCW = wide_ncw(MODE), WNC = 32 * NCW;
+    constexpr int NCW = wide_ncw(MODE, P), WNC = 32 * NCW, WUP_CPL = wup_cpl(P);
     using T = WideTile<P, kAux, MODE == WIDE_UP, NCW>;
     constexpr int ND = EPI == WE_APPLY1 ? 1 : (EPI == WE_APPLY2 ? 2 : 0);
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -656,7 +661,7 @@ static dim3 wide_grid(const Lvl &L, int &chunk) {
     int gz = (int)std::max<long long>(1, std::min<long long>(L.nx, (target + cols - 1) / cols));
     // (the transform modes -- 7 consumer warps -- pay more per chunk: two extra planes are
     // transformed, so their marches are at least 32 planes long)
-    chunk = std::max((L.nx + gz - 1) / gz, std::min(L.nx, NCW == 7 ? 32 : 8));
+    chunk = std::max((L.nx + gz - 1) / gz, std::min(L.nx, NCW < 8 ? 32 : 8));
     gz = (L.nx + chunk - 1) / chunk;
     return dim3(gx, gy, gz);
 }
@@ -665,7 +670,7 @@ template <int MODE, int EPI, int KV, bool SOMM, int P>
 static void wide_launch_t(const Lvl &L, const cd *src, const cd *aux, cd *out, double omega,
                           const RedSlot &rs, cudaStream_t s, const int *done,
                           const WideUp &up = WideUp{}) {
-    constexpr int NCW = wide_ncw(MODE);
+    constexpr int NCW = wide_ncw(MODE, P);
     constexpr size_t smem = WideTile<P, EPI != WE_APPLY0 && MODE == WIDE_LOAD, MODE == WIDE_UP, NCW>::smem;
     static bool attr = false;
     if (!attr) {
@@ -676,7 +681,7 @@ static void wide_launch_t(const Lvl &L, const cd *src, const cd *aux, cd *out, d
     int chunk;
     dim3 g = wide_grid<P, NCW>(L, chunk);
     if (MODE == WIDE_UP) {               // the staged coarse tile covers WUP_CHUNK fine planes
-        chunk = std::min(L.nx, WUP_CHUNK);
+        chunk = std::min(L.nx, wup_chunk(P));
         g.z = (L.nx + chunk - 1) / chunk;
     }
     launch(k_wide<MODE, EPI, KV, SOMM, P>, g, dim3(32 * (NCW + 1)), smem, s, L, src, aux ? aux : src, out, omega,
@@ -715,7 +720,11 @@ bool wide_ok(const Lvl &L, int kind) {
 // 5 zero-guess pre-smoothing + residual
 void launch_wide(int kind, const Lvl &L, const cd *src, const cd *aux, cd *out, double omega,
                  const RedSlot &rs, cudaStream_t s, const int *done) {
-    const bool p4 = opt(OPT_WIDE_P4);   // 32 x 32 tiles, four rows per thread (default: 32 x 16, two)
+    const bool p4 = opt(OPT_WIDE_P4);   // four rows per thread (default: two)
+    if (kind == 5 && opt(OPT_WIDE_P3)) {   // three rows per thread (transform modes only)
+        wide_launch_kv<WIDE_PRE, WE_RESID, 3>(L, src, aux, out, omega, rs, s, done);
+        return;
+    }
 #define HF_WIDE_KIND(K, MODE, EPI)                                                                 \
     if (kind == K) {                                                                               \
         if (p4) wide_launch_kv<MODE, EPI, 4>(L, src, aux, out, omega, rs, s, done);                \
@@ -734,13 +743,18 @@ void launch_wide(int kind, const Lvl &L, const cd *src, const cd *aux, cd *out, 
 // fused up-sweep on a whole-grid wide level: u = t + w D^-1 (b - M t), t = [w D^-1 b] + P e
 void launch_wide_up(const Lvl &L, const Lvl &C, const cd *b, const cd *e, cd *u, double omega,
                     bool pre, cudaStream_t s, const int *done) {
-    wide_launch_kv<WIDE_UP, WE_JACOBI, 2>(L, b, b, u, omega, RedSlot{}, s, done, WideUp{C, e, pre ? 1 : 0});
+    const WideUp up{C, e, pre ? 1 : 0};
+    if (opt(OPT_WIDE_P3)) wide_launch_kv<WIDE_UP, WE_JACOBI, 3>(L, b, b, u, omega, RedSlot{}, s, done, up);
+    else if (opt(OPT_WIDE_P4)) wide_launch_kv<WIDE_UP, WE_JACOBI, 4>(L, b, b, u, omega, RedSlot{}, s, done, up);
+    else wide_launch_kv<WIDE_UP, WE_JACOBI, 2>(L, b, b, u, omega, RedSlot{}, s, done, up);
 }
 
 int wide_blocks(const Lvl &L) {
     int c2, c4;
     const dim3 a = wide_grid<2>(L, c2), b = wide_grid<4>(L, c4), c = wide_grid<2, 7>(L, c2);
-    return (int)std::max(std::max(a.x * a.y * a.z, b.x * b.y * b.z), c.x * c.y * c.z);
+    const dim3 d = wide_grid<3, 5>(L, c2), e = wide_grid<4, 4>(L, c2);
+    return (int)std::max(std::max(std::max(a.x * a.y * a.z, b.x * b.y * b.z), c.x * c.y * c.z),
+                         std::max(d.x * d.y * d.z, e.x * e.y * e.z));
 }
 
 }  // namespace hf

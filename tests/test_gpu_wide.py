@@ -2,8 +2,8 @@
 thread, bulk-copied tile rows) against the C oracle.  The family serves planes
 wider than 256 vertices; `force_wide` routes every level through it so the
 ragged small grids (partial tiles, mirrored rows / columns inside a tile,
-one-plane chunks) are covered, for both strip heights (P = 2 default,
-`wide_p4`), the three wavenumber layouts (constant, float64 field, 8-bit
+one-plane chunks) are covered, for the strip heights (two rows per thread by
+default, `wide_p3` / `wide_p4`), the three wavenumber layouts (constant, float64 field, 8-bit
 palette) and both boundary conditions."""
 
 import numpy as np
@@ -49,13 +49,14 @@ GRIDS = [(5, 5, 5), (5, 7, 9), (9, 33, 34), (6, 34, 65), (17, 40, 33), (4, 9, 70
 @pytest.mark.parametrize("dims", GRIDS)
 @pytest.mark.parametrize("bc", ["dirichlet", "sommerfeld"])
 @pytest.mark.parametrize("medium", ["const", "field", "layered"])
-@pytest.mark.parametrize("p4", [0, 1])
-def test_wide_sweeps_match_oracle(hf, oracle, dims, bc, medium, p4, hfopt):
+@pytest.mark.parametrize("strips", ["", "wide_p3", "wide_p4"])
+def test_wide_sweeps_match_oracle(hf, oracle, dims, bc, medium, strips, hfopt):
     """A u, the Jacobi sweep and the zero-guess sweep + residual, kernel by kernel."""
     from paper_2308_06085_b200.multigrid import jacobi_smooth
     from paper_2308_06085_b200.operators import Dirichlet, OperatorSpec, Sommerfeld, StencilOperator
     hfopt("force_wide", 1)
-    hfopt("wide_p4", p4)
+    if strips:
+        hfopt(strips, 1)
     h = 0.125
     k = _medium(medium, dims)
     u0, b = _rand(dims, 2), _rand(dims, 8)
@@ -81,8 +82,8 @@ def test_wide_sweeps_match_oracle(hf, oracle, dims, bc, medium, p4, hfopt):
     ((33, 33, 33), "dirichlet", "const", {}),
     ((17, 65, 41), "sommerfeld", "field", dict(nu1=0, nu2=1)),
 ])
-@pytest.mark.parametrize("p4", [0, 1])
-def test_wide_cycle_matches_oracle(hf, oracle, n, bc, medium, cfg, p4, hfopt):
+@pytest.mark.parametrize("strips", ["", "wide_p3", "wide_p4"])
+def test_wide_cycle_matches_oracle(hf, oracle, n, bc, medium, cfg, strips, hfopt):
     """Whole cycles with every level's sweeps on the wide family (split
     down-sweep: the fused flat kernel is switched off), against the oracle and
     against the default kernels."""
@@ -96,7 +97,8 @@ def test_wide_cycle_matches_oracle(hf, oracle, n, bc, medium, cfg, p4, hfopt):
     base = mg_precondition(build_hierarchy(grid, None, spec, mg), r).cpu().numpy()
     hfopt("force_wide", 1)
     hfopt("no_dr", 1)
-    hfopt("wide_p4", p4)
+    if strips:
+        hfopt(strips, 1)
     hier = build_hierarchy(grid, None, spec, mg)
     got = mg_precondition(hier, r).cpu().numpy()
     oh = oracle.Hierarchy(k, grid.h, beta2=-0.5, bc=bc, nu1=mg.nu1, nu2=mg.nu2, omega=mg.omega,
@@ -107,8 +109,8 @@ def test_wide_cycle_matches_oracle(hf, oracle, n, bc, medium, cfg, p4, hfopt):
 
 
 @pytest.mark.parametrize("medium", ["const", "layered"])
-@pytest.mark.parametrize("p4", [0, 1])
-def test_wide_solve_matches_default(hf, oracle, medium, p4, hfopt):
+@pytest.mark.parametrize("strips", ["", "wide_p3", "wide_p4"])
+def test_wide_solve_matches_default(hf, oracle, medium, strips, hfopt):
     """Bi-CGSTAB with the matvec's inner products (r~^H v; t^H t, t^H s)
     accumulated by the wide sweeps: iteration count and solution of the default
     kernels, and the oracle's."""
@@ -130,7 +132,8 @@ def test_wide_solve_matches_default(hf, oracle, medium, p4, hfopt):
     x0, r0 = run()
     hfopt("force_wide", 1)
     hfopt("no_dr", 1)
-    hfopt("wide_p4", p4)
+    if strips:
+        hfopt(strips, 1)
     x1, r1 = run()
     assert r0.converged and r1.converged
     assert abs(r0.iterations - r1.iterations) <= 1

@@ -65,7 +65,7 @@ constexpr int WRS = WX + 2;       // staged entries per tile row
 // (strips of 3 / 4 rows, options wide_p3 / wide_p4: 5 / 4 consumer warps for the transform
 // modes -- fewer, fatter warps, the per-plane barrier traffic paid once per 3 / 4 points)
 __host__ __device__ constexpr int wide_ncw(int mode, int P = 2) {
-    return mode == 0 ? 8 : (P == 2 ? 7 : (P == 3 ? 5 : 4));
+    return mode == 0 || P == 1 ? 8 : (P == 2 ? 7 : (P == 3 ? 5 : 4));
 }
 constexpr int WRING = 4;
 constexpr int WPAL = 16;          // palette entries held in shared memory (else the k field is used)
@@ -107,7 +107,8 @@ template <int MODE, int EPI, int KV, bool SOMM, int P>
 // registers are allocated per SM sub-partition (16 K each): 3 blocks of 9 warps put up to
 // 7 warps on one (72 registers), 2 blocks up to 5 (96) -- the in-slot transform modes and
 // the 4-row strips take 2 blocks
-__global__ void __launch_bounds__(32 * (wide_ncw(MODE, P) + 1), (P >= 4 || MODE != WIDE_LOAD ? 2 : 3))
+__global__ void __launch_bounds__(32 * (wide_ncw(MODE, P) + 1),
+                                  (P >= 4 || (MODE != WIDE_LOAD && P > 1) || (MODE == WIDE_UP) ? 2 : 3))
 k_wide(Lvl L, const cd *__restrict__ src, const cd *__restrict__ aux, cd *__restrict__ out,
        double omega, int chunk, RedSlot rs, WideUp up, const int *done) {
     constexpr bool kAux = EPI != WE_APPLY0 && MODE == WIDE_LOAD;   // staged centre-only operand
@@ -725,6 +726,10 @@ void launch_wide(int kind, const Lvl &L, const cd *src, const cd *aux, cd *out, 
         wide_launch_kv<WIDE_PRE, WE_RESID, 3>(L, src, aux, out, omega, rs, s, done);
         return;
     }
+    if (kind == 5 && opt(OPT_WIDE_P1)) {   // one row per thread, 8 consumer warps, 3 blocks per SM
+        wide_launch_kv<WIDE_PRE, WE_RESID, 1>(L, src, aux, out, omega, rs, s, done);
+        return;
+    }
 #define HF_WIDE_KIND(K, MODE, EPI)                                                                 \
     if (kind == K) {                                                                               \
         if (p4) wide_launch_kv<MODE, EPI, 4>(L, src, aux, out, omega, rs, s, done);                \
@@ -744,7 +749,8 @@ void launch_wide(int kind, const Lvl &L, const cd *src, const cd *aux, cd *out, 
 void launch_wide_up(const Lvl &L, const Lvl &C, const cd *b, const cd *e, cd *u, double omega,
                     bool pre, cudaStream_t s, const int *done) {
     const WideUp up{C, e, pre ? 1 : 0};
-    if (opt(OPT_WIDE_P3)) wide_launch_kv<WIDE_UP, WE_JACOBI, 3>(L, b, b, u, omega, RedSlot{}, s, done, up);
+    if (opt(OPT_WIDE_P1)) wide_launch_kv<WIDE_UP, WE_JACOBI, 1>(L, b, b, u, omega, RedSlot{}, s, done, up);
+    else if (opt(OPT_WIDE_P3)) wide_launch_kv<WIDE_UP, WE_JACOBI, 3>(L, b, b, u, omega, RedSlot{}, s, done, up);
     else if (opt(OPT_WIDE_P4)) wide_launch_kv<WIDE_UP, WE_JACOBI, 4>(L, b, b, u, omega, RedSlot{}, s, done, up);
     else wide_launch_kv<WIDE_UP, WE_JACOBI, 2>(L, b, b, u, omega, RedSlot{}, s, done, up);
 }
@@ -752,9 +758,9 @@ void launch_wide_up(const Lvl &L, const Lvl &C, const cd *b, const cd *e, cd *u,
 int wide_blocks(const Lvl &L) {
     int c2, c4;
     const dim3 a = wide_grid<2>(L, c2), b = wide_grid<4>(L, c4), c = wide_grid<2, 7>(L, c2);
-    const dim3 d = wide_grid<3, 5>(L, c2), e = wide_grid<4, 4>(L, c2);
+    const dim3 d = wide_grid<3, 5>(L, c2), e = wide_grid<4, 4>(L, c2), f = wide_grid<1, 8>(L, c2);
     return (int)std::max(std::max(std::max(a.x * a.y * a.z, b.x * b.y * b.z), c.x * c.y * c.z),
-                         std::max(d.x * d.y * d.z, e.x * e.y * e.z));
+                         std::max(std::max(d.x * d.y * d.z, e.x * e.y * e.z), f.x * f.y * f.z));
 }
 
 }  // namespace hf

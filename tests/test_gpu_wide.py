@@ -49,7 +49,7 @@ GRIDS = [(5, 5, 5), (5, 7, 9), (9, 33, 34), (6, 34, 65), (17, 40, 33), (4, 9, 70
 @pytest.mark.parametrize("dims", GRIDS)
 @pytest.mark.parametrize("bc", ["dirichlet", "sommerfeld"])
 @pytest.mark.parametrize("medium", ["const", "field", "layered"])
-@pytest.mark.parametrize("strips", ["", "wide_p3", "wide_p4"])
+@pytest.mark.parametrize("strips", ["", "wide_p1", "wide_p3", "wide_p4"])
 def test_wide_sweeps_match_oracle(hf, oracle, dims, bc, medium, strips, hfopt):
     """A u, the Jacobi sweep and the zero-guess sweep + residual, kernel by kernel."""
     from paper_2308_06085_b200.multigrid import jacobi_smooth
@@ -82,7 +82,7 @@ def test_wide_sweeps_match_oracle(hf, oracle, dims, bc, medium, strips, hfopt):
     ((33, 33, 33), "dirichlet", "const", {}),
     ((17, 65, 41), "sommerfeld", "field", dict(nu1=0, nu2=1)),
 ])
-@pytest.mark.parametrize("strips", ["", "wide_p3", "wide_p4"])
+@pytest.mark.parametrize("strips", ["", "wide_p1", "wide_p3", "wide_p4"])
 def test_wide_cycle_matches_oracle(hf, oracle, n, bc, medium, cfg, strips, hfopt):
     """Whole cycles with every level's sweeps on the wide family (split
     down-sweep: the fused flat kernel is switched off), against the oracle and
@@ -109,7 +109,7 @@ def test_wide_cycle_matches_oracle(hf, oracle, n, bc, medium, cfg, strips, hfopt
 
 
 @pytest.mark.parametrize("medium", ["const", "layered"])
-@pytest.mark.parametrize("strips", ["", "wide_p3", "wide_p4"])
+@pytest.mark.parametrize("strips", ["", "wide_p1", "wide_p3", "wide_p4"])
 def test_wide_solve_matches_default(hf, oracle, medium, strips, hfopt):
     """Bi-CGSTAB with the matvec's inner products (r~^H v; t^H t, t^H s)
     accumulated by the wide sweeps: iteration count and solution of the default

@@ -46,11 +46,15 @@ def hf():
 GRIDS = [(5, 5, 5), (5, 7, 9), (9, 33, 34), (6, 34, 65), (17, 40, 33), (4, 9, 70)]
 
 
-@pytest.mark.parametrize("dims", GRIDS)
+# every grid with the default strips; two ragged grids with the optional strip heights
+SWEEP_CASES = [(d, "") for d in GRIDS] + [(d, s) for s in ("wide_p1", "wide_p3", "wide_p4")
+                                            for d in ((5, 7, 9), (6, 34, 65))]
+
+
+@pytest.mark.parametrize("dims,strips", SWEEP_CASES)
 @pytest.mark.parametrize("bc", ["dirichlet", "sommerfeld"])
 @pytest.mark.parametrize("medium", ["const", "field", "layered"])
-@pytest.mark.parametrize("strips", ["", "wide_p1", "wide_p3", "wide_p4"])
-def test_wide_sweeps_match_oracle(hf, oracle, dims, bc, medium, strips, hfopt):
+def test_wide_sweeps_match_oracle(hf, oracle, dims, strips, bc, medium, hfopt):
     """A u, the Jacobi sweep and the zero-guess sweep + residual, kernel by kernel."""
     from paper_2308_06085_b200.multigrid import jacobi_smooth
     from paper_2308_06085_b200.operators import Dirichlet, OperatorSpec, Sommerfeld, StencilOperator
@@ -74,15 +78,19 @@ def test_wide_sweeps_match_oracle(hf, oracle, dims, bc, medium, strips, hfopt):
     assert _rel(u.cpu().numpy(), oh.jacobi(0, u0, b, 0.8, 2)) < 1e-12
 
 
-@pytest.mark.parametrize("n,bc,medium,cfg", [
+CYCLE_CASES = [
     ((33, 33, 33), "sommerfeld", "field", {}),
     ((33, 33, 33), "dirichlet", "layered", {}),
     ((33, 17, 65), "sommerfeld", "layered", dict(cycle="F")),
     ((17, 33, 49), "sommerfeld", "const", dict(nu1=2, nu2=1)),
     ((33, 33, 33), "dirichlet", "const", {}),
     ((17, 65, 41), "sommerfeld", "field", dict(nu1=0, nu2=1)),
-])
-@pytest.mark.parametrize("strips", ["", "wide_p1", "wide_p3", "wide_p4"])
+]
+
+
+@pytest.mark.parametrize("n,bc,medium,cfg,strips",
+                         [c + ("",) for c in CYCLE_CASES] +
+                         [c + (s,) for s in ("wide_p1", "wide_p3", "wide_p4") for c in CYCLE_CASES[1:4]])
 def test_wide_cycle_matches_oracle(hf, oracle, n, bc, medium, cfg, strips, hfopt):
     """Whole cycles with every level's sweeps on the wide family (split
     down-sweep: the fused flat kernel is switched off), against the oracle and
@@ -108,8 +116,8 @@ def test_wide_cycle_matches_oracle(hf, oracle, n, bc, medium, cfg, strips, hfopt
     assert _rel(got, base) < 1e-12
 
 
-@pytest.mark.parametrize("medium", ["const", "layered"])
-@pytest.mark.parametrize("strips", ["", "wide_p1", "wide_p3", "wide_p4"])
+@pytest.mark.parametrize("medium,strips", [("const", ""), ("layered", ""), ("layered", "wide_p1"),
+                                            ("const", "wide_p3"), ("layered", "wide_p4")])
 def test_wide_solve_matches_default(hf, oracle, medium, strips, hfopt):
     """Bi-CGSTAB with the matvec's inner products (r~^H v; t^H t, t^H s)
     accumulated by the wide sweeps: iteration count and solution of the default

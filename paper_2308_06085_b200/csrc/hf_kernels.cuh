@@ -7,7 +7,7 @@ namespace hf {
 // kernel-variant options (hf_set_option in the C ABI); all off = the default
 enum HfOpt { OPT_NO_PDL = 0, OPT_NO_FLAT, OPT_NO_FLAT_DR, OPT_NO_DR, OPT_TILED_DR, OPT_FLAT_UP,
              OPT_FUSE_UP, OPT_NO_FUSE, OPT_COARSEST_DENSE, OPT_NO_PALETTE, OPT_NO_WIDE, OPT_FORCE_WIDE,
-             OPT_WIDE_P4, OPT_WIDE_ALL, OPT_NO_WIDE_UP, OPT_WIDE_P3, OPT_WIDE_P1, OPT_COUNT };
+             OPT_WIDE_P4, OPT_WIDE_ALL, OPT_NO_WIDE_UP, OPT_WIDE_P3, OPT_WIDE_P1, OPT_WIDE_BIG, OPT_COUNT };
 extern int g_opt[OPT_COUNT];
 inline bool opt(int o) { return g_opt[o] != 0; }
 

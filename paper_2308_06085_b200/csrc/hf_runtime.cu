@@ -52,7 +52,7 @@ extern "C" int hf_version(void) { return 2; }
 // the library reads no environment variables.
 static const char *const k_opt_names[OPT_COUNT] = {
     "no_pdl", "no_flat", "no_flat_dr", "no_dr", "tiled_dr", "flat_up", "fuse_up", "no_fuse",
-    "coarsest_dense", "no_palette", "no_wide", "force_wide", "wide_p4", "wide_all", "no_wide_up", "wide_p3", "wide_p1"};
+    "coarsest_dense", "no_palette", "no_wide", "force_wide", "wide_p4", "wide_all", "no_wide_up", "wide_p3", "wide_p1", "wide_big"};
 extern "C" int hf_set_option(const char *name, int value) {
     if (!name) return fail(HF_ERR_ARG, "null option name");
     for (int i = 0; i < OPT_COUNT; i++)

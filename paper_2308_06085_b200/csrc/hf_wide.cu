@@ -64,13 +64,17 @@ constexpr int WRS = WX + 2;       // staged entries per tile row
 // spills), two 9-warp blocks up to 5 (96)
 // (strips of 3 / 4 rows, options wide_p3 / wide_p4: 5 / 4 consumer warps for the transform
 // modes -- fewer, fatter warps, the per-plane barrier traffic paid once per 3 / 4 points)
+// P >= 10 encodes the BIG block of the transform modes: P - 10 rows per thread, 15 consumer
+// warps + the producer in one 512-thread block per SM (16 warps: 4 per sub-partition, 128
+// registers; a 32 x 30 tile: 1.13 instead of 1.21 staged entries per point)
+__host__ __device__ constexpr int wide_rows(int P) { return P >= 10 ? P - 10 : P; }
 __host__ __device__ constexpr int wide_ncw(int mode, int P = 2) {
-    return mode == 0 || P == 1 ? 8 : (P == 2 ? 7 : (P == 3 ? 5 : 4));
+    return P >= 10 ? 15 : (mode == 0 || P == 1 ? 8 : (P == 2 ? 7 : (P == 3 ? 5 : 4)));
 }
 constexpr int WRING = 4;
 constexpr int WPAL = 16;          // palette entries held in shared memory (else the k field is used)
 // fine planes per block of the fused up-sweep / coarse planes staged per block
-__host__ __device__ constexpr int wup_chunk(int P) { return P == 2 ? 48 : 40; }
+__host__ __device__ constexpr int wup_chunk(int P) { return P == 2 || P >= 10 ? 48 : 40; }
 __host__ __device__ constexpr int wup_cpl(int P) { return wup_chunk(P) / 2 + 2; }
 constexpr int WCW = WX / 2 + 2;   // coarse tile row length
 static_assert((WRING & (WRING - 1)) == 0, "ring size is a power of two");
@@ -83,7 +87,7 @@ struct WideUp {          // WIDE_UP: the coarse level and its correction
 
 template <int P, bool AUX, bool UP = false, int NCW = 8>
 struct WideTile {
-    static constexpr int WY = NCW * P;            // tile height (i2)
+    static constexpr int WY = NCW * wide_rows(P); // tile height (i2)
     static constexpr int ROWS = WY + 2;
     static constexpr int ENT = ROWS * WRS;        // stencil operand entries of a slot
     static constexpr int AENT = AUX ? WY * WX : 0;   // centre-only operand entries
@@ -103,18 +107,19 @@ struct WidePlane {       // register set of one plane of a thread's strip
     cd f[P];             // staged operand at the thread's P points
 };
 
-template <int MODE, int EPI, int KV, bool SOMM, int P>
+template <int MODE, int EPI, int KV, bool SOMM, int PP>
 // registers are allocated per SM sub-partition (16 K each): 3 blocks of 9 warps put up to
 // 7 warps on one (72 registers), 2 blocks up to 5 (96) -- the in-slot transform modes and
 // the 4-row strips take 2 blocks
-__global__ void __launch_bounds__(32 * (wide_ncw(MODE, P) + 1),
-                                  (P >= 4 || (MODE != WIDE_LOAD && P > 1) || (MODE == WIDE_UP) ? 2 : 3))
+__global__ void __launch_bounds__(32 * (wide_ncw(MODE, PP) + 1),
+                                  (PP >= 10 ? 1 : (PP >= 4 || (MODE != WIDE_LOAD && PP > 1) || (MODE == WIDE_UP) ? 2 : 3)))
 k_wide(Lvl L, const cd *__restrict__ src, const cd *__restrict__ aux, cd *__restrict__ out,
        double omega, int chunk, RedSlot rs, WideUp up, const int *done) {
     constexpr bool kAux = EPI != WE_APPLY0 && MODE == WIDE_LOAD;   // staged centre-only operand
     constexpr bool kXf = MODE != WIDE_LOAD;                        // entries transformed in the slot
-    constexpr int NCW = wide_ncw(MODE, P), WNC = 32 * NCW, WUP_CPL = wup_cpl(P);
-    using T = WideTile<P, kAux, MODE == WIDE_UP, NCW>;
+    constexpr int P = wide_rows(PP);
+    constexpr int NCW = wide_ncw(MODE, PP), WNC = 32 * NCW, WUP_CPL = wup_cpl(PP);
+    using T = WideTile<PP, kAux, MODE == WIDE_UP, NCW>;
     constexpr int ND = EPI == WE_APPLY1 ? 1 : (EPI == WE_APPLY2 ? 2 : 0);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ __align__(8) unsigned long long bars[3 * WRING + (MODE == WIDE_UP ? WUP_CPL : 0)];
@@ -658,7 +663,7 @@ static dim3 wide_grid(const Lvl &L, int &chunk) {
     // several short waves (sliver tiles at the 2^k + 1 edges finish early and the
     // block scheduler back-fills); every chunk re-reads two planes
     const long long cols = (long long)gx * gy;
-    const long long target = 148LL * (P >= 4 ? 2 : 3) * 6;
+    const long long target = 148LL * (P >= 10 ? 1 : (P >= 4 ? 2 : 3)) * 6;
     int gz = (int)std::max<long long>(1, std::min<long long>(L.nx, (target + cols - 1) / cols));
     // (the transform modes -- 7 consumer warps -- pay more per chunk: two extra planes are
     // transformed, so their marches are at least 32 planes long)
@@ -726,6 +731,10 @@ void launch_wide(int kind, const Lvl &L, const cd *src, const cd *aux, cd *out, 
         wide_launch_kv<WIDE_PRE, WE_RESID, 3>(L, src, aux, out, omega, rs, s, done);
         return;
     }
+    if (kind == 5 && opt(OPT_WIDE_BIG)) {  // one 512-thread block per SM, 15 consumer warps
+        wide_launch_kv<WIDE_PRE, WE_RESID, 12>(L, src, aux, out, omega, rs, s, done);
+        return;
+    }
     if (kind == 5 && opt(OPT_WIDE_P1)) {   // one row per thread, 8 consumer warps, 3 blocks per SM
         wide_launch_kv<WIDE_PRE, WE_RESID, 1>(L, src, aux, out, omega, rs, s, done);
         return;
@@ -749,7 +758,8 @@ void launch_wide(int kind, const Lvl &L, const cd *src, const cd *aux, cd *out, 
 void launch_wide_up(const Lvl &L, const Lvl &C, const cd *b, const cd *e, cd *u, double omega,
                     bool pre, cudaStream_t s, const int *done) {
     const WideUp up{C, e, pre ? 1 : 0};
-    if (opt(OPT_WIDE_P1)) wide_launch_kv<WIDE_UP, WE_JACOBI, 1>(L, b, b, u, omega, RedSlot{}, s, done, up);
+    if (opt(OPT_WIDE_BIG)) wide_launch_kv<WIDE_UP, WE_JACOBI, 12>(L, b, b, u, omega, RedSlot{}, s, done, up);
+    else if (opt(OPT_WIDE_P1)) wide_launch_kv<WIDE_UP, WE_JACOBI, 1>(L, b, b, u, omega, RedSlot{}, s, done, up);
     else if (opt(OPT_WIDE_P3)) wide_launch_kv<WIDE_UP, WE_JACOBI, 3>(L, b, b, u, omega, RedSlot{}, s, done, up);
     else if (opt(OPT_WIDE_P4)) wide_launch_kv<WIDE_UP, WE_JACOBI, 4>(L, b, b, u, omega, RedSlot{}, s, done, up);
     else wide_launch_kv<WIDE_UP, WE_JACOBI, 2>(L, b, b, u, omega, RedSlot{}, s, done, up);
@@ -759,7 +769,8 @@ int wide_blocks(const Lvl &L) {
     int c2, c4;
     const dim3 a = wide_grid<2>(L, c2), b = wide_grid<4>(L, c4), c = wide_grid<2, 7>(L, c2);
     const dim3 d = wide_grid<3, 5>(L, c2), e = wide_grid<4, 4>(L, c2), f = wide_grid<1, 8>(L, c2);
-    return (int)std::max(std::max(std::max(a.x * a.y * a.z, b.x * b.y * b.z), c.x * c.y * c.z),
+    const dim3 g = wide_grid<12, 15>(L, c2);
+    return (int)std::max(std::max(std::max(a.x * a.y * a.z, b.x * b.y * b.z), std::max(c.x * c.y * c.z, g.x * g.y * g.z)),
                          std::max(std::max(d.x * d.y * d.z, e.x * e.y * e.z), f.x * f.y * f.z));
 }
 

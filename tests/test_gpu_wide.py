@@ -47,7 +47,7 @@ GRIDS = [(5, 5, 5), (5, 7, 9), (9, 33, 34), (6, 34, 65), (17, 40, 33), (4, 9, 70
 
 
 # every grid with the default strips; two ragged grids with the optional strip heights
-SWEEP_CASES = [(d, "") for d in GRIDS] + [(d, s) for s in ("wide_p1", "wide_p3", "wide_p4")
+SWEEP_CASES = [(d, "") for d in GRIDS] + [(d, s) for s in ("wide_p1", "wide_p3", "wide_p4", "wide_big")
                                             for d in ((5, 7, 9), (6, 34, 65))]
 
 
@@ -90,7 +90,7 @@ CYCLE_CASES = [
 
 @pytest.mark.parametrize("n,bc,medium,cfg,strips",
                          [c + ("",) for c in CYCLE_CASES] +
-                         [c + (s,) for s in ("wide_p1", "wide_p3", "wide_p4") for c in CYCLE_CASES[1:4]])
+                         [c + (s,) for s in ("wide_p1", "wide_p3", "wide_p4", "wide_big") for c in CYCLE_CASES[1:4]])
 def test_wide_cycle_matches_oracle(hf, oracle, n, bc, medium, cfg, strips, hfopt):
     """Whole cycles with every level's sweeps on the wide family (split
     down-sweep: the fused flat kernel is switched off), against the oracle and
@@ -117,7 +117,7 @@ def test_wide_cycle_matches_oracle(hf, oracle, n, bc, medium, cfg, strips, hfopt
 
 
 @pytest.mark.parametrize("medium,strips", [("const", ""), ("layered", ""), ("layered", "wide_p1"),
-                                            ("const", "wide_p3"), ("layered", "wide_p4")])
+                                            ("const", "wide_p3"), ("layered", "wide_p4"), ("layered", "wide_big")])
 def test_wide_solve_matches_default(hf, oracle, medium, strips, hfopt):
     """Bi-CGSTAB with the matvec's inner products (r~^H v; t^H t, t^H s)
     accumulated by the wide sweeps: iteration count and solution of the default

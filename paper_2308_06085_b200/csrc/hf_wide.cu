@@ -570,6 +570,9 @@ k_wide(Lvl L, const cd *__restrict__ src, const cd *__restrict__ aux, cd *__rest
                 // waiting BEFORE the transform measured 50 % slower)
                 wait_bar(b_xf, i);
                 inplane();
+                // plane i's slot is not read again (b of the epilogue is a register): release
+                // it ahead of the arithmetic and the stores
+                arrive_bar(b_empty, i);
             } else {
                 wait_bar(b_full, i + 1);
                 const cd *sn = slot(i + 1);
@@ -617,7 +620,7 @@ k_wide(Lvl L, const cd *__restrict__ src, const cd *__restrict__ aux, cd *__rest
                     }
                 }
             }
-            arrive_bar(b_empty, i);          // this warp is done with plane i's slot
+            if (!kXf) arrive_bar(b_empty, i);   // this warp is done with plane i's slot
             // rotation of the small per-point state (a few moves per strip)
 #pragma unroll
             for (int r = 0; r < P; r++) {

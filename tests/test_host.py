@@ -135,3 +135,22 @@ def test_abi_argument_errors_without_a_gpu():
     assert L.hf_bcg_step(None, 2, None) == _native.ERR_ARG
     assert L.hf_level_down_restrict(None, 0, None, None) == _native.ERR_ARG
     assert L.hf_level_up(None, 0, None, None, None) == _native.ERR_ARG
+
+
+def test_kernel_variant_options_are_named_and_default_off():
+    """Every kernel-variant option DESIGN.md section 9 lists is known to
+    hf_set_option / hf_get_option, off by default, and unknown names are
+    rejected (the library reads no environment variables)."""
+    from paper_2308_06085_b200 import _native
+    L = _native.load()
+    names = ["no_pdl", "no_flat", "no_flat_dr", "no_dr", "tiled_dr", "flat_up", "fuse_up", "no_fuse",
+             "coarsest_dense", "no_palette", "no_wide", "force_wide", "wide_p4", "wide_all",
+             "no_wide_up", "wide_p3", "wide_p1", "wide_big"]
+    for n in names:
+        assert L.hf_get_option(n.encode()) == 0, n
+        _native.set_option(n, 1)
+        assert L.hf_get_option(n.encode()) == 1
+        _native.set_option(n, 0)
+    assert L.hf_get_option(b"no_such_option") == _native.ERR_ARG
+    with pytest.raises(_native.NativeError):
+        _native.set_option("no_such_option", 1)

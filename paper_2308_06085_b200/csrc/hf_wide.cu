@@ -1,16 +1,20 @@
 // hf_wide.cu -- stencil sweeps on WIDE planes (n3 > 256: the 513^3 / 1025^2
 // finest levels), sm_100a.
 //
-// A block owns a 32 x 8P tile of (i3, i2) columns and marches along i1.  It is
-// warp-specialised: eight CONSUMER warps compute, one PRODUCER warp feeds a
-// ring of WRING plane slots with cp.async.bulk copies, and the warps are
-// synchronised only through mbarriers -- there is no block-wide barrier on the
-// march, so the consumer warps drift apart by up to the ring depth and hide
-// each other's latencies:
+// A block owns a 32 x (NCW P) tile of (i3, i2) columns and marches along i1.  It
+// is warp-specialised: NCW CONSUMER warps compute (8 for the plain sweeps, 7 for
+// the in-slot transform modes: two 8-warp blocks put 4 warps on every SM
+// sub-partition, 128 registers without spills), one PRODUCER warp feeds a ring
+// of 4 plane slots with cp.async.bulk copies, and the warps are synchronised
+// only through mbarriers -- there is no block-wide barrier on the march, so the
+// consumer warps drift apart by up to the ring depth and hide each other's
+// latencies:
 //   full[k]   the producer's copies of a plane have landed (expect_tx)
-//   empty[k]  all eight consumer warps are done reading the slot
-//   xf[k]     (pre-smoothing sweep) all consumer warps have transformed their
+//   empty[k]  all consumer warps are done reading the slot
+//   xf[k]     (transform modes) all consumer warps have transformed their
 //             entries of the plane in the slot
+// P = 2 rows per thread by default; 1 / 3 / 4 rows and a 15-consumer-warp block
+// are kept as options (all measured slower).
 // A consumer thread owns P consecutive i2 rows of one i3 column:
 //   * the x neighbours rotate through registers along the march (three named
 //     register sets, the march unrolled by three: no moves),
@@ -28,7 +32,7 @@
 // identities and never use them), copied from the mirrored address, so the
 // 7-point row is uniform.
 //
-// Two stencil inputs (same arithmetic as k_stencil / k_flat_stencil):
+// Three stencil inputs (same arithmetic as k_stencil / k_flat_stencil):
 //   WIDE_LOAD  f = src            (A u with inner products, b - M u, Jacobi sweep)
 //   WIDE_PRE   f = D^-1 b: zero-guess pre-smoothing folded into the residual,
 //              r = b - M (w D^-1 b) (multigrid.py:148-151 + 383-386).  A thread
@@ -40,7 +44,9 @@
 //              (prolong_tl + _correct, multigrid.py:238-297, 389-392) produced in
 //              the slot like WIDE_PRE's D^-1 b, the k_corr arithmetic at the
 //              (mirrored) coordinates of every entry; the coarse tile of e the
-//              block's fine planes interpolate from is staged once per block.
+//              block's fine planes interpolate from is staged plane by plane, each
+//              on its own barrier, and the in-plane sums of a coarse plane are
+//              carried in registers over the three fine planes they serve.
 //              Epilogue: the post-smoothing Jacobi sweep u = t + w D^-1 (b - M t).
 //              The correction t never goes to memory (-32 B per vertex against
 //              the split k_corr_flat + Jacobi pair).

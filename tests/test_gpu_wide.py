@@ -82,10 +82,10 @@ _CYCLE_REF = {}
 CYCLE_CASES = [
     ((33, 33, 33), "sommerfeld", "field", {}),
     ((33, 33, 33), "dirichlet", "layered", {}),
-    ((33, 17, 65), "sommerfeld", "layered", dict(cycle="F")),
-    ((17, 33, 49), "sommerfeld", "const", dict(nu1=2, nu2=1)),
+    ((33, 33, 65), "sommerfeld", "layered", dict(cycle="F")),
+    ((33, 33, 49), "sommerfeld", "const", dict(nu1=2, nu2=1)),
     ((33, 33, 33), "dirichlet", "const", {}),
-    ((17, 33, 41), "sommerfeld", "field", dict(nu1=0, nu2=1)),
+    ((33, 41, 33), "sommerfeld", "field", dict(nu1=0, nu2=1)),
 ]
 
 

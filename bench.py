@@ -543,7 +543,9 @@ def kernel_table(A, hier, solver, n, t_iter_ms, reps=12, sparse_shadow=True):
                            ("matvec_dot2", 4, 48.0 + kp)):
         m = ctypes.c_float()
         _native.check(L.hf_solver_bench_vec(solver._h, which, r, ctypes.byref(m)))
-        put(nm, m.value, bpv, "hbm", 1 if which != 4 or sparse else 2,
+        # (the solver's own vectors: HBM-streaming when a vector is larger than L2, else the
+        # launches re-read L2-resident data and the figure is not an HBM fraction)
+        put(nm, m.value, bpv, "hbm" if nf * 16 > L2_BYTES else "l2-resident", 1 if which != 4 or sparse else 2,
             ("k_bcg_p", "k_bcg_s", "k_bcg_xr", "k_bcg_xr (sparse r~)", f"{sweep}<LOAD,EpiApply<2>>")[which])
     return out
 
